@@ -1,0 +1,115 @@
+/*
+ * ttk_b200.h -- C ABI of the B200-native (sm_100a, fp64) TT-sGMRES hot path.
+ *
+ * Drop-in boundary for the reference package `ttkrylov` (arXiv 2409.09471
+ * companion code, /root/reference/pkg/src/ttkrylov).  The reference has no
+ * FFI: its boundary is the module-level Python API over lists of float64
+ * C-order cores (ttkrylov/__init__.py:3-69).  Each entry point below replaces
+ * the arithmetic of one reference function; the Python mirror in
+ * paper_2409_09471_b200/ binds them with ctypes.
+ *
+ * Conventions
+ *  - all double pointers are DEVICE pointers to fp64 C-order cores:
+ *      TT vector core k   : (r[k], n[k], r[k+1])         r[0] = r[d] = 1
+ *      TT operator core k : (rho[k], m[k], n[k], rho[k+1]) rho[0] = rho[d] = 1
+ *  - shape/rank arrays and pointer arrays are HOST arrays;
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream); all work is
+ *    stream-ordered; functions that return host-side results (ranks,
+ *    scalars) synchronise the stream before returning;
+ *  - `ws`/`ws_bytes` is caller-owned device scratch; size it with the
+ *    matching *_ws_bytes query (the library keeps no global device state);
+ *  - return 0 on success; nonzero status codes:
+ *      1 TTK_SHAPE_MISMATCH  (reference ShapeMismatch, tt.py:22-23)
+ *      2 TTK_INVALID_VALUE   (reference ValueError)
+ *      3 TTK_CUDA_ERROR
+ *      4 TTK_WORKSPACE       (workspace too small)
+ *      5 TTK_DEGENERATE      (reference DegenerateRecovery, streaming.py:20-21)
+ *    ttk_last_error() returns the message of the last failure on this thread.
+ */
+#ifndef TTK_B200_H_
+#define TTK_B200_H_
+
+#include <stddef.h>
+
+#define TTK_ABI_VERSION 1
+
+#define TTK_OK 0
+#define TTK_SHAPE_MISMATCH 1
+#define TTK_INVALID_VALUE 2
+#define TTK_CUDA_ERROR 3
+#define TTK_WORKSPACE 4
+#define TTK_DEGENERATE 5
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- library ------------------------------------------------------------ */
+const char* ttk_last_error(void);
+int ttk_version(void);
+int ttk_device_arch(void); /* compute capability of the current device, e.g. 100 */
+
+/* ---- dense building block ------------------------------------------------
+ * Strided batched fp64 GEMM on the DMMA tensor pipe:
+ *   C_b(m,n) = alpha * sum_k A_b(m,k) B_b(k,n) + beta * C_b(m,n)
+ *   A_b(m,k) = A[b*a_bs + m*a_ms + k*a_ks], B_b(k,n) = B[b*b_bs + k*b_ks + n*b_ns],
+ *   C_b(m,n) = C[b*c_bs + m*c_ms + n*c_ns].
+ * Replaces the np.tensordot / einsum contractions of the reference
+ * (tt.py:292-293,311,333,367; streaming.py:131,136,139). */
+int ttk_gemm_strided(int batch, int M, int N, int K, double alpha, const double* A,
+                     long long a_ms, long long a_ks, long long a_bs, const double* B,
+                     long long b_ks, long long b_ns, long long b_bs, double beta, double* C,
+                     long long c_ms, long long c_ns, long long c_bs, void* ws, size_t ws_bytes,
+                     void* stream);
+size_t ttk_gemm_strided_ws_bytes(int batch, int M, int N, int K);
+
+/* ---- tt_matvec (reference tt.py:302-314) -----------------------------------
+ * G_k[(a*rho[k]+al), i, (b*rho[k+1]+be)] = sum_j D_k[al,i,j,be] * C_k[a,j,b]
+ * One grouped launch over all d cores; G_k must hold r[k]*rho[k]*m[k]*r[k+1]*rho[k+1]. */
+int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
+               const double* const* D, const double* const* C, double* const* G, void* stream);
+
+/* ---- TT-axpy / concatenation (reference tt_add + tt_scale, tt.py:254-282) --
+ * out = sum_t coeff[t] * term_t as ONE block-diagonal concatenation: first core
+ * concatenated along axis 2, last along axis 0 (scaled by coeff[t], the factor
+ * the reference's tt_scale puts in the last core), interior cores block
+ * diagonal; d == 1 sums entrywise.  Equal to the explicit Arnoldi update
+ * tt_add(vt, tt_scale(v_i, -h_i)) chained left to right (solvers.py:361-366).
+ * ranks: nterms x (d+1); in: nterms x d (term-major); out: d, preallocated with
+ * ranks (1, sum_t r_t[1], ..., sum_t r_t[d-1], 1).  nterms <= 16, d <= 64. */
+int ttk_tt_concat(int d, int nterms, const double* coeff, const int* dims, const int* ranks,
+                  const double* const* in, double* const* out, void* stream);
+/* y[i] = alpha * x[i] (last-core scaling of tt_scale, tt.py:278-282) */
+int ttk_scale(double* y, const double* x, long long n, double alpha, void* stream);
+/* out_dev[0] = sum x[i]^2, fixed reduction order; ws >= 2048 bytes */
+int ttk_sumsq(const double* x, long long n, double* out_dev, void* ws, size_t ws_bytes,
+              void* stream);
+
+/* ---- tt_dot (reference tt.py:285-294), batched over p partners -----------
+ * out_dev[i] = <x, y_i>, left-to-right interface sweep, grouped DMMA GEMMs
+ * per core.  xr: d+1 ranks of x; yr: p x (d+1); y: p x d pointers. */
+int ttk_tt_dots(int d, const int* dims, const int* xr, const double* const* x, int p,
+                const int* yr, const double* const* y, double* out_dev, void* ws, size_t ws_bytes,
+                void* stream);
+size_t ttk_tt_dots_ws_bytes(int d, const int* dims, const int* xr, int p, const int* yr);
+
+/* ---- Khatri-Rao sketch (reference kr_apply, sketch.py:50-70) ---------------
+ * out[v, j - s_lo] = (row j of the Khatri-Rao product of F_1..F_d) . vec(x_v)
+ * for rows j in [s_lo, s_hi) and nvec TT vectors x_v (row-shardable: every GPU
+ * passes its own [s_lo, s_hi)).  F: d pointers to the full (s x n_k)
+ * row-major factors; ranks: nvec x (d+1); cores: nvec x d; out row-major
+ * nvec x (s_hi - s_lo). */
+int ttk_kr_sketch(int d, const int* n, int s_lo, int s_hi, const double* const* F, int nvec,
+                  const int* ranks, const double* const* cores, double* out, void* ws,
+                  size_t ws_bytes, void* stream);
+size_t ttk_kr_sketch_ws_bytes(int d, const int* n, int s_lo, int s_hi, int nvec, const int* ranks);
+/* same, forcing the fused (path 0) or two-phase (path 1) kernel; for tests */
+int ttk_kr_sketch_path(int path, int d, const int* n, int s_lo, int s_hi, const double* const* F,
+                       int nvec, const int* ranks, const double* const* cores, double* out,
+                       void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TTK_B200_H_ */

@@ -1,0 +1,35 @@
+"""B200-native (sm_100a, fp64) hot path of randomized TT-sGMRES (arXiv 2409.09471).
+
+Drop-in mirror of the reference package ``ttkrylov``'s TT core-list API for the
+path named by BASELINE.json: TT matvec, TT-axpy/concatenation, dot/norm,
+TT-SVD and randomize-then-orthogonalize rounding, the Khatri-Rao sketch, the
+streaming sketches and ``tt_sgmres``.  Cores are CUDA fp64 torch tensors; the
+arithmetic runs in libttk_b200.so (C ABI: include/ttk_b200.h).
+"""
+
+from .errors import DegenerateRecovery, ShapeMismatch, SizeLimit
+from .sketch import KhatriRaoSketch, kr_apply, kr_apply_batch, kr_apply_device, kr_apply_rows, kr_sketch_new
+from .tt import (
+    DENSE_CAP,
+    RoundSpec,
+    TTOperator,
+    TTVector,
+    attainable_ranks,
+    identity_operator,
+    kron_sum_operator,
+    max_rank,
+    tt_add,
+    tt_combine,
+    tt_dot,
+    tt_dots,
+    tt_matvec,
+    tt_norm,
+    tt_op_to_dense,
+    tt_random,
+    tt_rank_one,
+    tt_scale,
+    tt_to_dense,
+    tt_zero,
+)
+
+__version__ = "0.1.0"

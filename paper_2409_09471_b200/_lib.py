@@ -1,0 +1,112 @@
+"""ctypes binding of the C ABI declared in include/ttk_b200.h.
+
+The product path has no CPU fallback: if libttk_b200.so is missing or no CUDA
+device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from .errors import DegenerateRecovery, ShapeMismatch
+
+_PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG_DIR, "libttk_b200.so")
+
+c_int = ctypes.c_int
+c_ll = ctypes.c_longlong
+c_double = ctypes.c_double
+c_size = ctypes.c_size_t
+c_vp = ctypes.c_void_p
+P_int = ctypes.POINTER(ctypes.c_int)
+P_vp = ctypes.POINTER(ctypes.c_void_p)
+P_double = ctypes.POINTER(ctypes.c_double)
+
+# name -> (restype, argtypes); every symbol here is declared in include/ttk_b200.h
+SIGNATURES = {
+    "ttk_last_error": (ctypes.c_char_p, []),
+    "ttk_version": (c_int, []),
+    "ttk_device_arch": (c_int, []),
+    "ttk_gemm_strided": (c_int, [c_int, c_int, c_int, c_int, c_double, c_vp, c_ll, c_ll, c_ll,
+                                 c_vp, c_ll, c_ll, c_ll, c_double, c_vp, c_ll, c_ll, c_ll,
+                                 c_vp, c_size, c_vp]),
+    "ttk_gemm_strided_ws_bytes": (c_size, [c_int, c_int, c_int, c_int]),
+    "ttk_matvec": (c_int, [c_int, P_int, P_int, P_int, P_int, P_vp, P_vp, P_vp, c_vp]),
+    "ttk_tt_concat": (c_int, [c_int, c_int, P_double, P_int, P_int, P_vp, P_vp, c_vp]),
+    "ttk_scale": (c_int, [c_vp, c_vp, c_ll, c_double, c_vp]),
+    "ttk_sumsq": (c_int, [c_vp, c_ll, c_vp, c_vp, c_size, c_vp]),
+    "ttk_tt_dots": (c_int, [c_int, P_int, P_int, P_vp, c_int, P_int, P_vp, c_vp, c_vp, c_size, c_vp]),
+    "ttk_tt_dots_ws_bytes": (c_size, [c_int, P_int, P_int, c_int, P_int]),
+    "ttk_kr_sketch": (c_int, [c_int, P_int, c_int, c_int, P_vp, c_int, P_int, P_vp, c_vp, c_vp,
+                              c_size, c_vp]),
+    "ttk_kr_sketch_path": (c_int, [c_int, c_int, P_int, c_int, c_int, P_vp, c_int, P_int, P_vp, c_vp,
+                                   c_vp, c_size, c_vp]),
+    "ttk_kr_sketch_ws_bytes": (c_size, [c_int, P_int, c_int, c_int, c_int, P_int]),
+}
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the native library; raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"native library {LIB_PATH} is not built; run `python -m paper_2409_09471_b200.build` "
+            "or __graft_entry__.build() (there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name, None)
+        if fn is None:
+            continue  # reported by tests/test_abi.py
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status == 0:
+        return
+    msg = load().ttk_last_error().decode(errors="replace")
+    if status == 1:
+        raise ShapeMismatch(msg)
+    if status == 2:
+        raise ValueError(msg)
+    if status == 5:
+        raise DegenerateRecovery(msg)
+    raise RuntimeError(f"ttk native error {status}: {msg}")
+
+
+def require_cuda(t: torch.Tensor, what: str = "tensor"):
+    if not t.is_cuda:
+        raise RuntimeError(f"{what} must live on a CUDA device: the B200 path has no CPU fallback")
+
+
+def int_array(vals):
+    vals = [int(v) for v in vals]
+    return (ctypes.c_int * max(len(vals), 1))(*vals)
+
+
+def double_array(vals):
+    vals = [float(v) for v in vals]
+    return (ctypes.c_double * max(len(vals), 1))(*vals)
+
+
+def ptr_array(tensors):
+    ptrs = [t.data_ptr() if t is not None else 0 for t in tensors]
+    return (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """Caller-owned scratch from torch's caching allocator."""
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)

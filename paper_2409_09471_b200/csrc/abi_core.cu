@@ -1,0 +1,101 @@
+// C-ABI entry points: library info, error channel, grouped GEMM, TT matvec.
+#include "gemm.cuh"
+#include "../../include/ttk_b200.h"
+
+#include <string>
+#include <vector>
+
+namespace ttk {
+
+static thread_local char g_err[1024] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+const char* last_error() { return g_err; }
+
+}  // namespace ttk
+
+using namespace ttk;
+
+extern "C" {
+
+const char* ttk_last_error(void) { return ttk::last_error(); }
+
+int ttk_version(void) { return TTK_ABI_VERSION; }
+
+int ttk_device_arch(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major * 10 + minor;
+}
+
+int ttk_gemm_strided(int batch, int M, int N, int K, double alpha, const double* A,
+                     long long a_ms, long long a_ks, long long a_bs, const double* B,
+                     long long b_ks, long long b_ns, long long b_bs, double beta, double* C,
+                     long long c_ms, long long c_ns, long long c_bs, void* ws, size_t ws_bytes,
+                     void* stream) {
+  TTK_REQUIRE(batch >= 0 && M >= 0 && N >= 0 && K >= 0, kInvalidValue, "negative GEMM size");
+  if (batch == 0 || M == 0 || N == 0) return kOk;
+  std::vector<GemmProblem> probs(batch);
+  for (int b = 0; b < batch; ++b)
+    probs[b] = make_gemm(M, N, K, A + b * a_bs, a_ms, a_ks, B + b * b_bs, b_ks, b_ns, C + b * c_bs,
+                         c_ms, c_ns, alpha, beta);
+  return gemm_group_launch(probs.data(), batch, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t ttk_gemm_strided_ws_bytes(int batch, int M, int N, int K) {
+  if (batch <= 0 || M <= 0 || N <= 0) return 0;
+  std::vector<GemmProblem> probs(batch);
+  for (int b = 0; b < batch; ++b)
+    probs[b] = make_gemm(M, N, K, nullptr, 1, 1, nullptr, 1, 1, nullptr, 1, 1);
+  return gemm_group_ws_bytes(probs.data(), batch);
+}
+
+// tt_matvec: G_k[(a*rho0+al), i, (b*rho1+be)] = sum_j D_k[al,i,j,be] * C_k[a,j,b]
+// Reference: ttkrylov/tt.py:302-314 (tensordot over j, transpose (0,2,3,1,4),
+// reshape to (r0*rho0, m, r1*rho1): vector-rank major, operator-rank minor).
+int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
+               const double* const* D, const double* const* C, double* const* G, void* stream) {
+  TTK_REQUIRE(d >= 1, kInvalidValue, "d must be >= 1");
+  TTK_REQUIRE(rho[0] == 1 && rho[d] == 1 && r[0] == 1 && r[d] == 1, kShapeMismatch,
+              "boundary ranks must equal 1");
+  std::vector<GemmProblem> probs;
+  probs.reserve(64);
+  for (int k = 0; k < d; ++k) {
+    const int r0 = r[k], r1 = r[k + 1], p0 = rho[k], p1 = rho[k + 1];
+    const int mk = m[k], nk = n[k];
+    TTK_REQUIRE(r0 >= 0 && r1 >= 0 && p0 >= 1 && p1 >= 1 && mk >= 1 && nk >= 1, kShapeMismatch,
+                "bad shapes at core %d", k);
+    if (r0 == 0 || r1 == 0) continue;
+    const long long rr1 = (long long)r1 * p1;
+    for (int al = 0; al < p0; ++al) {
+      GemmProblem p{};
+      // rows  (a,b)   : A(p,j) = C[a, j, b]
+      // cols  (i,be)  : B(j,q) = D[al, i, j, be]
+      p.M = r0 * r1;
+      p.N = mk * p1;
+      p.K = nk;
+      p.A = C[k];
+      p.a_mdiv = r1; p.a_ms1 = (long long)nk * r1; p.a_ms0 = 1; p.a_ks = r1;
+      p.B = D[k] + (long long)al * mk * nk * p1;
+      p.b_ndiv = p1; p.b_ns1 = (long long)nk * p1; p.b_ns0 = 1; p.b_ks = p1;
+      p.C = G[k] + (long long)al * mk * rr1;
+      p.c_mdiv = r1; p.c_ms1 = (long long)p0 * mk * rr1; p.c_ms0 = p1;
+      p.c_ndiv = p1; p.c_ns1 = rr1; p.c_ns0 = 1;
+      p.alpha = 1.0; p.beta = 0.0; p.splits = 1;
+      probs.push_back(p);
+    }
+  }
+  if (probs.empty()) return kOk;
+  return gemm_group_launch(probs.data(), (int)probs.size(), nullptr, 0, (cudaStream_t)stream,
+                           /*allow_split=*/false);
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Shared device/host helpers for the TT-sGMRES B200 kernels (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstdarg>
+#include <cmath>
+
+namespace ttk {
+
+// ---------------------------------------------------------------------------
+// error reporting: every extern "C" entry point returns 0 on success and a
+// nonzero status otherwise; the message is kept per host thread.
+enum Status : int {
+  kOk = 0,
+  kShapeMismatch = 1,   // maps to ShapeMismatch (ValueError) on the Python side
+  kInvalidValue = 2,    // maps to ValueError
+  kCudaError = 3,       // maps to RuntimeError
+  kWorkspace = 4,       // caller-provided workspace too small
+  kDegenerate = 5,      // DegenerateRecovery
+};
+
+void set_error(const char* fmt, ...);
+const char* last_error();
+
+#define TTK_CHECK_CUDA(expr)                                                     \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::ttk::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr,            \
+                       cudaGetErrorString(_e));                                  \
+      return ::ttk::kCudaError;                                                  \
+    }                                                                            \
+  } while (0)
+
+#define TTK_CHECK_LAUNCH()                                                       \
+  do {                                                                           \
+    cudaError_t _e = cudaGetLastError();                                         \
+    if (_e != cudaSuccess) {                                                     \
+      ::ttk::set_error("%s:%d: launch failed -> %s", __FILE__, __LINE__,        \
+                       cudaGetErrorString(_e));                                  \
+      return ::ttk::kCudaError;                                                  \
+    }                                                                            \
+  } while (0)
+
+#define TTK_REQUIRE(cond, status, ...)                                           \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      ::ttk::set_error(__VA_ARGS__);                                             \
+      return (status);                                                           \
+    }                                                                            \
+  } while (0)
+
+#define TTK_TRY(expr)                                                            \
+  do {                                                                           \
+    int _s = (expr);                                                             \
+    if (_s != ::ttk::kOk) return _s;                                             \
+  } while (0)
+
+constexpr int kNumSMs = 148;
+
+inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// simple bump allocator over a caller-provided workspace
+struct Arena {
+  char* base;
+  size_t cap;
+  size_t used = 0;
+  Arena(void* b, size_t c) : base((char*)b), cap(c) {}
+  template <class T>
+  T* take(size_t count) {
+    size_t off = align_up(used, 256);
+    size_t bytes = count * sizeof(T);
+    if (base == nullptr || off + bytes > cap) { used = off + bytes; return nullptr; }
+    used = off + bytes;
+    return reinterpret_cast<T*>(base + off);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  // D(8x8) += A(8x4, row) * B(4x8, col); lane l holds A[l/4][l%4], B[l%4][l/4],
+  // and C[l/4][2*(l%4) + {0,1}].
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 8-byte async global->shared copy; src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src, bool valid) {
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src), "r"(sz));
+}
+
+// 16-byte async copy (both addresses 16B aligned)
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src, bool valid) {
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src), "r"(sz));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace ttk

@@ -1,0 +1,292 @@
+// Grouped fp64 GEMM on the FP64 tensor pipe (DMMA.8x8x4 via mma.sync.m8n8k4.f64).
+//
+// Every TT contraction on the hot path (matvec cores, RTO partial
+// contractions, projections, Gram/dot sweeps, stream-sketch sweeps) reduces to
+//   C(m,n) = alpha * sum_k A(m,k) B(k,n) + beta * C(m,n)
+// where the row/column index maps are *two-level affine*:
+//   A(m,k) = A[(m / a_mdiv) * a_ms1 + (m % a_mdiv) * a_ms0 + k * a_ks]
+//   B(k,n) = B[(n / b_ndiv) * b_ns1 + (n % b_ndiv) * b_ns0 + k * b_ks]
+//   C(m,n) = C[(m / c_mdiv) * c_ms1 + (m % c_mdiv) * c_ms0
+//              + (n / c_ndiv) * c_ns1 + (n % c_ndiv) * c_ns0]
+// which covers plain/transposed/strided GEMMs and the rank-merged
+// (vector-rank major, operator-rank minor) output layout of tt_matvec.
+// Operands are staged through a 3-stage cp.async shared-memory pipeline; the
+// per-row/column offsets are tabulated once per tile in shared memory.
+#pragma once
+#include "common.cuh"
+
+namespace ttk {
+
+struct GemmProblem {
+  const double* A;
+  const double* B;
+  double* C;
+  double* partial;  // split-K partials: splits * M * N (row-major), nullptr if splits == 1
+  long long a_ms0, a_ms1, a_ks;
+  long long b_ns0, b_ns1, b_ks;
+  long long c_ms0, c_ms1, c_ns0, c_ns1;
+  double alpha, beta;
+  int M, N, K;
+  int a_mdiv, b_ndiv, c_mdiv, c_ndiv;
+  int splits, k_per_split;
+  int tiles_m, tiles_n;
+  int tile_begin;  // first CTA index of this problem within the group launch
+};
+
+constexpr int kMaxGroup = 96;
+
+struct GemmGroup {
+  int count;
+  int total_tiles;
+  GemmProblem p[kMaxGroup];
+};
+
+__device__ __forceinline__ long long amap(const GemmProblem& P, int m) {
+  int q = m / P.a_mdiv;
+  return (long long)q * P.a_ms1 + (long long)(m - q * P.a_mdiv) * P.a_ms0;
+}
+__device__ __forceinline__ long long bmap(const GemmProblem& P, int n) {
+  int q = n / P.b_ndiv;
+  return (long long)q * P.b_ns1 + (long long)(n - q * P.b_ndiv) * P.b_ns0;
+}
+__device__ __forceinline__ long long cmap_m(const GemmProblem& P, int m) {
+  int q = m / P.c_mdiv;
+  return (long long)q * P.c_ms1 + (long long)(m - q * P.c_mdiv) * P.c_ms0;
+}
+__device__ __forceinline__ long long cmap_n(const GemmProblem& P, int n) {
+  int q = n / P.c_ndiv;
+  return (long long)q * P.c_ns1 + (long long)(n - q * P.c_ndiv) * P.c_ns0;
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+struct GemmCfg {
+  static constexpr int kThreads = 32 * WARPS_M * WARPS_N;
+  static constexpr int WM = BM / WARPS_M;  // rows per warp
+  static constexpr int WN = BN / WARPS_N;  // cols per warp
+  static constexpr int FM = WM / 8;        // 8x8 fragments per warp along m
+  static constexpr int FN = WN / 8;
+  static constexpr int SA = BM + 4;  // smem row stride (doubles) of the k-major A tile
+  static constexpr int SB = BN + 4;
+  static constexpr size_t kSmemBytes =
+      sizeof(double) * (size_t)STAGES * BK * (SA + SB) + sizeof(long long) * (BM + BN) * 2;
+  static_assert(BM % (8 * WARPS_M) == 0 && BN % (8 * WARPS_N) == 0, "tile");
+  static_assert(BK % 4 == 0, "bk");
+  static_assert(SA % 16 == 4 && SB % 16 == 4, "bank-conflict-free fragment loads");
+};
+
+template <class Cfg, int BM, int BN, int BK, int STAGES>
+__device__ __forceinline__ void gemm_load_stage(const GemmProblem& P, double* As, double* Bs,
+                                                const long long* rowA, const long long* colB,
+                                                int m0, int n0, int k0, int kend) {
+  const int tid = threadIdx.x;
+  // A tile: BM x BK, stored k-major (As[k][m]).  Map threads so that the
+  // contiguous global direction is the fast thread index.
+  if (P.a_ks == 1) {
+#pragma unroll 4
+    for (int e = tid; e < BM * BK; e += Cfg::kThreads) {
+      int k = e % BK, m = e / BK;
+      int gk = k0 + k;
+      bool ok = (m0 + m < P.M) && (gk < kend);
+      const double* src = ok ? P.A + rowA[m] + gk : P.A;
+      cp_async8(As + k * Cfg::SA + m, src, ok);
+    }
+  } else {
+#pragma unroll 4
+    for (int e = tid; e < BM * BK; e += Cfg::kThreads) {
+      int m = e % BM, k = e / BM;
+      int gk = k0 + k;
+      bool ok = (m0 + m < P.M) && (gk < kend);
+      const double* src = ok ? P.A + rowA[m] + (long long)gk * P.a_ks : P.A;
+      cp_async8(As + k * Cfg::SA + m, src, ok);
+    }
+  }
+  if (P.b_ks == 1) {
+#pragma unroll 4
+    for (int e = tid; e < BN * BK; e += Cfg::kThreads) {
+      int k = e % BK, n = e / BK;
+      int gk = k0 + k;
+      bool ok = (n0 + n < P.N) && (gk < kend);
+      const double* src = ok ? P.B + colB[n] + gk : P.B;
+      cp_async8(Bs + k * Cfg::SB + n, src, ok);
+    }
+  } else {
+#pragma unroll 4
+    for (int e = tid; e < BN * BK; e += Cfg::kThreads) {
+      int n = e % BN, k = e / BN;
+      int gk = k0 + k;
+      bool ok = (n0 + n < P.N) && (gk < kend);
+      const double* src = ok ? P.B + colB[n] + (long long)gk * P.b_ks : P.B;
+      cp_async8(Bs + k * Cfg::SB + n, src, ok);
+    }
+  }
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
+    gemm_group_kernel(const __grid_constant__ GemmGroup G) {
+  using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* As = reinterpret_cast<double*>(smem_raw);
+  double* Bs = As + STAGES * BK * Cfg::SA;
+  long long* rowA = reinterpret_cast<long long*>(Bs + STAGES * BK * Cfg::SB);
+  long long* colB = rowA + BM;
+  long long* rowC = colB + BN;
+  long long* colC = rowC + BM;
+
+  // locate the problem owning this CTA
+  int bid = blockIdx.x;
+  int pi = 0;
+  {
+    int lo = 0, hi = G.count - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (G.p[mid].tile_begin <= bid) lo = mid; else hi = mid - 1;
+    }
+    pi = lo;
+  }
+  const GemmProblem& P = G.p[pi];
+  int t = bid - P.tile_begin;
+  const int split = t % P.splits;
+  t /= P.splits;
+  const int tn = t % P.tiles_n;
+  const int tm = t / P.tiles_n;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int kbeg = split * P.k_per_split;
+  const int kend = min(P.K, kbeg + P.k_per_split);
+
+  for (int i = threadIdx.x; i < BM; i += Cfg::kThreads) {
+    int m = min(m0 + i, P.M - 1);
+    rowA[i] = amap(P, m);
+    rowC[i] = cmap_m(P, m);
+  }
+  for (int i = threadIdx.x; i < BN; i += Cfg::kThreads) {
+    int n = min(n0 + i, P.N - 1);
+    colB[i] = bmap(P, n);
+    colC[i] = cmap_n(P, n);
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm0 = (warp / WARPS_N) * Cfg::WM;
+  const int wn0 = (warp % WARPS_N) * Cfg::WN;
+
+  double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk)
+      gemm_load_stage<Cfg, BM, BN, BK, STAGES>(P, As + s * BK * Cfg::SA, Bs + s * BK * Cfg::SB, rowA,
+                                               colB, m0, n0, kbeg + s * BK, kend);
+    cp_async_commit();
+  }
+
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nxt = kt + STAGES - 1;
+      if (nxt < nk) {
+        int st = nxt % STAGES;
+        gemm_load_stage<Cfg, BM, BN, BK, STAGES>(P, As + st * BK * Cfg::SA, Bs + st * BK * Cfg::SB,
+                                                 rowA, colB, m0, n0, kbeg + nxt * BK, kend);
+      }
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * BK * Cfg::SA;
+    const double* bs = Bs + (kt % STAGES) * BK * Cfg::SB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(kk + fk) * Cfg::SA + wm0 + i * 8 + fr];
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[(kk + fk) * Cfg::SB + wn0 + j * 8 + fr];
+#pragma unroll
+      for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue
+  if (P.splits > 1) {
+    double* part = P.partial + (size_t)split * P.M * P.N;
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i) {
+      int ml = wm0 + i * 8 + fr;
+      int m = m0 + ml;
+      if (m >= P.M) continue;
+#pragma unroll
+      for (int j = 0; j < Cfg::FN; ++j) {
+        int nl = wn0 + j * 8 + 2 * fk;
+        int n = n0 + nl;
+        if (n < P.N) part[(size_t)m * P.N + n] = acc[i][j][0];
+        if (n + 1 < P.N) part[(size_t)m * P.N + n + 1] = acc[i][j][1];
+      }
+    }
+    return;
+  }
+  const double alpha = P.alpha, beta = P.beta;
+#pragma unroll
+  for (int i = 0; i < Cfg::FM; ++i) {
+    int ml = wm0 + i * 8 + fr;
+    if (m0 + ml >= P.M) continue;
+    long long ro = rowC[ml];
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+      int nl = wn0 + j * 8 + 2 * fk;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (n0 + nl + h < P.N) {
+          double* dst = P.C + ro + colC[nl + h];
+          double v = alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * *dst;
+          *dst = v;
+        }
+      }
+    }
+  }
+}
+
+// deterministic split-K reduction: C = alpha * sum_s partial[s] + beta * C
+__global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G);
+
+// Host-side helpers ----------------------------------------------------------
+
+// Fill tile bookkeeping of a problem; returns CTA count. split-K factor decided here.
+struct GemmPlan {
+  int bm, bn;
+  size_t partial_elems;  // total split-K workspace (doubles)
+};
+
+// Launch a group of problems (count <= kMaxGroup, same tile config chosen
+// internally). `ws` provides the split-K partial buffers (may be null when no
+// split is needed; query with gemm_group_ws_bytes).
+int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, cudaStream_t st,
+                      bool allow_split = true);
+size_t gemm_group_ws_bytes(const GemmProblem* probs, int count, bool allow_split = true);
+
+// Convenience: plain strided problem, C(m,n) = alpha*sum_k A(m,k)B(k,n) + beta*C
+inline GemmProblem make_gemm(int M, int N, int K, const double* A, long long a_ms, long long a_ks,
+                             const double* B, long long b_ks, long long b_ns, double* C,
+                             long long c_ms, long long c_ns, double alpha = 1.0, double beta = 0.0) {
+  GemmProblem p{};
+  p.A = A; p.B = B; p.C = C; p.partial = nullptr;
+  p.M = M; p.N = N; p.K = K;
+  p.a_ms0 = a_ms; p.a_ms1 = 0; p.a_mdiv = 1 << 30; p.a_ks = a_ks;
+  p.b_ns0 = b_ns; p.b_ns1 = 0; p.b_ndiv = 1 << 30; p.b_ks = b_ks;
+  p.c_ms0 = c_ms; p.c_ms1 = 0; p.c_mdiv = 1 << 30;
+  p.c_ns0 = c_ns; p.c_ns1 = 0; p.c_ndiv = 1 << 30;
+  p.alpha = alpha; p.beta = beta;
+  p.splits = 1;
+  return p;
+}
+
+}  // namespace ttk

@@ -1,0 +1,373 @@
+// Khatri-Rao structured sketch of TT vectors (reference kr_apply, sketch.py:50-70).
+//
+//   y_j = sum_{i_1..i_d} prod_k F_k[j, i_k] * v[i_1, ..., i_d]
+//
+// Per row j a running state s_j (1 x r_k) advances mode by mode:
+//   s_j <- sum_{a, i} s_j[a] F_k[j, i] C_k[a, i, :]
+// which is a GEMM with M = rows, K = r_{k-1} n_k, N = r_k whose A operand
+// A[j, (a,i)] = s_j[a] * F_k[j, i] is a Khatri-Rao product formed on the fly.
+//
+// Two device paths:
+//  * fused (many rows, ranks <= 128): one CTA owns 128 rows of one vector and
+//    runs all d modes with the state resident in shared memory; F and C_k tiles
+//    are staged by a 3-stage cp.async pipeline and contracted on the DMMA pipe.
+//  * two-phase (few rows, e.g. the solver's s = 2*maxit sketch of one vector):
+//    phase 1 computes every M_k = F_k x_2 C_k (s x r_{k-1} x r_k) for all modes
+//    at once with the grouped GEMM (all FLOPs, fully parallel); phase 2 walks
+//    the per-row state through the d small matrices (rows are independent).
+// Output rows stay in their fixed positions (SPEC: deterministic row order).
+#include "gemm.cuh"
+#include "../../include/ttk_b200.h"
+
+#include <algorithm>
+#include <vector>
+
+namespace ttk {
+
+constexpr int kKrMaxModes = 64;
+constexpr int kKrMaxSlots = 1536;  // (vector, mode) core pointers per launch
+
+struct KrParams {
+  int d;
+  int S;         // rows handled (s_hi - s_lo)
+  int nvec;
+  int rmax;
+  const double* F[kKrMaxModes];  // row s_lo of factor k, row stride ldF[k] = n_k
+  int n[kKrMaxModes];
+  double* out;                   // nvec x S
+  const double* core[kKrMaxSlots];   // vec * d + k
+  short rank[kKrMaxSlots + 64];      // vec * (d+1) + k
+};
+
+namespace kr {
+constexpr int WARPS = 8;
+constexpr int FM = 2;                 // 16 rows per warp
+constexpr int BM = WARPS * 8 * FM;    // 128 rows per CTA
+constexpr int BN = 128;               // max rank handled by the fused path
+constexpr int FNMAX = BN / 8;
+constexpr int BK = 16;
+constexpr int STAGES = 3;
+constexpr int SST = BN + 1;           // odd stride: conflict-free state reads
+constexpr int SF = BM + 4;
+constexpr int SB = BN + 4;
+constexpr size_t kSmem = sizeof(double) * ((size_t)BM * SST + (size_t)STAGES * BK * (SF + SB)) +
+                         sizeof(int) * STAGES * BK;
+}  // namespace kr
+
+__device__ __forceinline__ void kr_load_stage(const KrParams& P, const double* Fk, const double* Ck,
+                                              int n, int r1, int K, int k0, int j0, double* Fs,
+                                              double* Bs, int* r0tab) {
+  using namespace kr;
+  const int tid = threadIdx.x;
+  // F chunk: Fs[kk][row] = F[j0+row][i(k0+kk)]
+  for (int e = tid; e < BM * BK; e += WARPS * 32) {
+    int kk = e % BK, row = e / BK;
+    int k = k0 + kk;
+    bool ok = (k < K) && (j0 + row < P.S);
+    int a = ok ? k / n : 0;
+    int i = k - a * n;
+    const double* src = ok ? Fk + (long long)(j0 + row) * n + i : Fk;
+    cp_async8(Fs + kk * SF + row, src, ok);
+  }
+  // C chunk: Bs[kk][col] = C[(k0+kk), col]  (C as (r0*n) x r1 row-major)
+  for (int e = tid; e < BN * BK; e += WARPS * 32) {
+    int col = e % BN, kk = e / BN;
+    int k = k0 + kk;
+    bool ok = (k < K) && (col < r1);
+    const double* src = ok ? Ck + (long long)k * r1 + col : Ck;
+    cp_async8(Bs + kk * SB + col, src, ok);
+  }
+  if (tid < BK) {
+    int k = k0 + tid;
+    r0tab[tid] = (k < K) ? k / n : 0;
+  }
+}
+
+__global__ void __launch_bounds__(kr::WARPS * 32, 1)
+    kr_fused_kernel(const __grid_constant__ KrParams P) {
+  using namespace kr;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* St = reinterpret_cast<double*>(smem_raw);
+  double* Fs = St + BM * SST;
+  double* Bs = Fs + STAGES * BK * SF;
+  int* r0tab = reinterpret_cast<int*>(Bs + STAGES * BK * SB);
+
+  const int vec = blockIdx.y;
+  const int j0 = blockIdx.x * BM;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int wrow = warp * 8 * FM;
+
+  for (int e = threadIdx.x; e < BM; e += WARPS * 32) St[e * SST] = 1.0;
+  __syncthreads();
+
+  for (int k = 0; k < P.d; ++k) {
+    const int r0 = P.rank[vec * (P.d + 1) + k];
+    const int r1 = P.rank[vec * (P.d + 1) + k + 1];
+    const int n = P.n[k];
+    const int K = r0 * n;
+    const double* Fk = P.F[k];
+    const double* Ck = P.core[vec * P.d + k];
+    const int fn = (r1 + 7) / 8;
+
+    double acc[FM][FNMAX][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FNMAX; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int nk = (K + BK - 1) / BK;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nk)
+        kr_load_stage(P, Fk, Ck, n, r1, K, s * BK, j0, Fs + s * BK * SF, Bs + s * BK * SB,
+                      r0tab + s * BK);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        int nxt = kt + STAGES - 1;
+        if (nxt < nk) {
+          int st = nxt % STAGES;
+          kr_load_stage(P, Fk, Ck, n, r1, K, nxt * BK, j0, Fs + st * BK * SF, Bs + st * BK * SB,
+                        r0tab + st * BK);
+        }
+        cp_async_commit();
+      }
+      const int st = kt % STAGES;
+      const double* fs = Fs + st * BK * SF;
+      const double* bs = Bs + st * BK * SB;
+      const int* rt = r0tab + st * BK;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        const int a = rt[kk + fk];
+        double af[FM];
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          const int row = wrow + i * 8 + fr;
+          af[i] = fs[(kk + fk) * SF + row] * St[row * SST + a];
+        }
+#pragma unroll
+        for (int j = 0; j < FNMAX; ++j) {
+          if (j < fn) {
+            const double bf = bs[(kk + fk) * SB + j * 8 + fr];
+#pragma unroll
+            for (int i = 0; i < FM; ++i) dmma_8x8x4(acc[i][j], af[i], bf);
+          }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // every warp is done with the stage buffers and its old state rows
+    // new state (warp-private rows)
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const int row = wrow + i * 8 + fr;
+#pragma unroll
+      for (int j = 0; j < FNMAX; ++j) {
+        if (j < fn) {
+          const int col = j * 8 + 2 * fk;
+          if (col < r1) St[row * SST + col] = acc[i][j][0];
+          if (col + 1 < r1) St[row * SST + col + 1] = acc[i][j][1];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int row = threadIdx.x; row < BM; row += WARPS * 32)
+    if (j0 + row < P.S) P.out[(long long)vec * P.S + j0 + row] = St[row * SST];
+}
+
+// phase 2 of the two-phase path: per (vector, row) walk the state through
+// M_k[j] (r0 x r1), M stored as [vec][k] blocks of S x r0 x r1.
+struct KrChainParams {
+  int d, S, nvec, rmax;
+  const double* M;            // base of the M buffer
+  long long moff[kKrMaxSlots];  // offset of block (vec, k)
+  short rank[kKrMaxSlots + 64];
+  double* out;
+};
+
+__global__ void kr_chain_kernel(const __grid_constant__ KrChainParams P) {
+  extern __shared__ double sm[];
+  const int rows_per_cta = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = blockIdx.y;
+  const int j = blockIdx.x * rows_per_cta + warp;
+  double* st = sm + warp * 2 * P.rmax;
+  double* nx = st + P.rmax;
+  if (lane == 0) st[0] = 1.0;
+  __syncwarp();
+  for (int k = 0; k < P.d; ++k) {
+    const int r0 = P.rank[vec * (P.d + 1) + k];
+    const int r1 = P.rank[vec * (P.d + 1) + k + 1];
+    if (j < P.S) {
+      const double* Mk = P.M + P.moff[vec * P.d + k] + (long long)j * r0 * r1;
+      for (int b = lane; b < r1; b += 32) {
+        double s = 0.0;
+        for (int a = 0; a < r0; ++a) s += st[a] * Mk[(long long)a * r1 + b];
+        nx[b] = s;
+      }
+    }
+    __syncwarp();
+    double* t = st; st = nx; nx = t;
+  }
+  if (j < P.S && lane == 0) P.out[(long long)vec * P.S + j] = st[0];
+}
+
+}  // namespace ttk
+
+using namespace ttk;
+
+namespace {
+
+int kr_fused(int d, const int* n, int S, const double* const* F, int nvec, const int* ranks,
+             const double* const* cores, double* out, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    TTK_CHECK_CUDA(cudaFuncSetAttribute(kr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kr::kSmem));
+    attr = true;
+  }
+  const int per = std::max(1, std::min(kKrMaxSlots / d, 64));
+  for (int v0 = 0; v0 < nvec; v0 += per) {
+    int nv = std::min(per, nvec - v0);
+    static thread_local KrParams P;
+    P.d = d; P.S = S; P.nvec = nv; P.rmax = 0;
+    for (int k = 0; k < d; ++k) { P.F[k] = F[k]; P.n[k] = n[k]; }
+    P.out = out + (long long)v0 * S;
+    for (int v = 0; v < nv; ++v) {
+      for (int k = 0; k < d; ++k) P.core[v * d + k] = cores[(long long)(v0 + v) * d + k];
+      for (int k = 0; k <= d; ++k) P.rank[v * (d + 1) + k] = (short)ranks[(long long)(v0 + v) * (d + 1) + k];
+    }
+    dim3 grid(ceil_div(S, kr::BM), nv);
+    kr_fused_kernel<<<grid, kr::WARPS * 32, kr::kSmem, st>>>(P);
+    TTK_CHECK_LAUNCH();
+  }
+  return kOk;
+}
+
+size_t kr_two_phase_elems(int d, int S, int nvec, const int* ranks) {
+  size_t tot = 0;
+  for (int v = 0; v < nvec; ++v)
+    for (int k = 0; k < d; ++k)
+      tot += (size_t)S * ranks[v * (d + 1) + k] * ranks[v * (d + 1) + k + 1];
+  return tot;
+}
+
+int kr_two_phase(int d, const int* n, int S, const double* const* F, int nvec, const int* ranks,
+                 const double* const* cores, double* out, void* ws, size_t ws_bytes,
+                 cudaStream_t st) {
+  size_t melems = kr_two_phase_elems(d, S, nvec, ranks);
+  Arena ar(ws, ws_bytes);
+  double* M = ar.take<double>(melems);
+  std::vector<GemmProblem> probs;
+  probs.reserve((size_t)nvec * d);
+  std::vector<long long> moff((size_t)nvec * d);
+  long long off = 0;
+  int rmax = 1;
+  for (int v = 0; v < nvec; ++v) {
+    for (int k = 0; k < d; ++k) {
+      const int r0 = ranks[v * (d + 1) + k], r1 = ranks[v * (d + 1) + k + 1];
+      rmax = std::max(rmax, std::max(r0, r1));
+      moff[(size_t)v * d + k] = off;
+      GemmProblem p{};
+      p.M = S; p.N = r0 * r1; p.K = n[k];
+      p.A = F[k]; p.a_ms0 = n[k]; p.a_ms1 = 0; p.a_mdiv = 1 << 30; p.a_ks = 1;
+      p.B = cores[(size_t)v * d + k];
+      p.b_ndiv = r1; p.b_ns1 = (long long)n[k] * r1; p.b_ns0 = 1; p.b_ks = r1;
+      p.C = M ? M + off : nullptr;
+      p.c_mdiv = 1 << 30; p.c_ms0 = (long long)r0 * r1; p.c_ms1 = 0;
+      p.c_ndiv = 1 << 30; p.c_ns0 = 1; p.c_ns1 = 0;
+      p.alpha = 1.0; p.beta = 0.0; p.splits = 1;
+      probs.push_back(p);
+      off += (long long)S * r0 * r1;
+    }
+  }
+  TTK_REQUIRE(M != nullptr, kWorkspace, "kr_sketch: workspace too small (%zu bytes needed)",
+              ar.used);
+  TTK_TRY(gemm_group_launch(probs.data(), (int)probs.size(), nullptr, 0, st, false));
+  const int per = std::max(1, std::min(kKrMaxSlots / d, 1024));
+  for (int v0 = 0; v0 < nvec; v0 += per) {
+    int nv = std::min(per, nvec - v0);
+    static thread_local KrChainParams C;
+    C.d = d; C.S = S; C.nvec = nv; C.rmax = rmax; C.M = M;
+    C.out = out + (long long)v0 * S;
+    for (int v = 0; v < nv; ++v) {
+      for (int k = 0; k < d; ++k) C.moff[v * d + k] = moff[(size_t)(v0 + v) * d + k];
+      for (int k = 0; k <= d; ++k) C.rank[v * (d + 1) + k] = (short)ranks[(v0 + v) * (d + 1) + k];
+    }
+    const int rows_per_cta = 4;
+    dim3 grid(ceil_div(S, rows_per_cta), nv);
+    size_t smem = sizeof(double) * 2 * rmax * rows_per_cta;
+    if (smem > 48 * 1024)
+      TTK_CHECK_CUDA(cudaFuncSetAttribute(kr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+    kr_chain_kernel<<<grid, 32 * rows_per_cta, smem, st>>>(C);
+    TTK_CHECK_LAUNCH();
+  }
+  return kOk;
+}
+
+bool use_fused(int d, int S, int nvec, const int* ranks) {
+  for (int v = 0; v < nvec; ++v)
+    for (int k = 0; k <= d; ++k)
+      if (ranks[v * (d + 1) + k] > kr::BN) return false;
+  // the fused path needs enough (vector, row-block) CTAs to fill the machine
+  long ctas = (long)nvec * ceil_div(S, kr::BM);
+  return ctas >= kNumSMs / 2;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Sketch rows [s_lo, s_hi) of nvec TT vectors.  F: d device pointers to the
+// FULL factors (s_total x n_k row-major); out: nvec x (s_hi - s_lo) row-major.
+// ranks: nvec x (d+1); cores: nvec x d device pointers.
+size_t ttk_kr_sketch_ws_bytes(int d, const int* n, int s_lo, int s_hi, int nvec, const int* ranks) {
+  const int S = s_hi - s_lo;
+  if (S <= 0 || nvec <= 0) return 0;
+  if (use_fused(d, S, nvec, ranks)) return 0;
+  return kr_two_phase_elems(d, S, nvec, ranks) * sizeof(double) + 4096;
+}
+
+int ttk_kr_sketch(int d, const int* n, int s_lo, int s_hi, const double* const* F, int nvec,
+                  const int* ranks, const double* const* cores, double* out, void* ws,
+                  size_t ws_bytes, void* stream) {
+  TTK_REQUIRE(d >= 1 && d <= kKrMaxModes, kInvalidValue, "kr_sketch: d=%d out of range", d);
+  TTK_REQUIRE(s_hi >= s_lo && s_lo >= 0, kInvalidValue, "kr_sketch: bad row range");
+  const int S = s_hi - s_lo;
+  if (S == 0 || nvec == 0) return kOk;
+  for (int v = 0; v < nvec; ++v)
+    TTK_REQUIRE(ranks[v * (d + 1)] == 1 && ranks[v * (d + 1) + d] == 1, kShapeMismatch,
+                "kr_sketch: boundary ranks must equal 1");
+  std::vector<const double*> Fo(d);
+  for (int k = 0; k < d; ++k) Fo[k] = F[k] + (long long)s_lo * n[k];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (use_fused(d, S, nvec, ranks)) return kr_fused(d, n, S, Fo.data(), nvec, ranks, cores, out, st);
+  return kr_two_phase(d, n, S, Fo.data(), nvec, ranks, cores, out, ws, ws_bytes, st);
+}
+
+// Force a path (testing): path 0 = fused, 1 = two-phase.
+int ttk_kr_sketch_path(int path, int d, const int* n, int s_lo, int s_hi, const double* const* F,
+                       int nvec, const int* ranks, const double* const* cores, double* out,
+                       void* ws, size_t ws_bytes, void* stream) {
+  const int S = s_hi - s_lo;
+  if (S <= 0 || nvec == 0) return kOk;
+  std::vector<const double*> Fo(d);
+  for (int k = 0; k < d; ++k) Fo[k] = F[k] + (long long)s_lo * n[k];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (path == 0) {
+    for (int v = 0; v < nvec; ++v)
+      for (int k = 0; k <= d; ++k)
+        TTK_REQUIRE(ranks[v * (d + 1) + k] <= kr::BN, kInvalidValue, "fused path needs ranks <= %d",
+                    kr::BN);
+    return kr_fused(d, n, S, Fo.data(), nvec, ranks, cores, out, st);
+  }
+  return kr_two_phase(d, n, S, Fo.data(), nvec, ranks, cores, out, ws, ws_bytes, st);
+}
+
+}  // extern "C"

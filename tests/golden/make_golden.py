@@ -1,0 +1,291 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container only (needs /root/reference):
+    python tests/golden/make_golden.py
+Writes small .npz fixtures next to this script.  The GPU box never runs this
+script; tests load the committed fixtures.  Shapes and seeds follow the
+reference's own tests (pkg/tests/test_tt.py, test_sketch.py,
+test_streaming.py, test_solvers.py) plus one BASELINE-size solver history
+(config 1, with the reference's tt_round zero test bypassed -- quirk Q1).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+import ttkrylov  # noqa: E402
+import ttkrylov.solvers as rsolvers  # noqa: E402
+import ttkrylov.streaming as rstreaming  # noqa: E402
+from ttkrylov import tt as rtt  # noqa: E402
+from ttkrylov.problems import ConvectionDiffusionSpec, convection_diffusion  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def cores_dict(prefix, cores, out):
+    out[f"{prefix}__d"] = np.array(len(cores))
+    for k, c in enumerate(cores):
+        out[f"{prefix}__{k}"] = np.ascontiguousarray(c)
+
+
+def random_operator(row_dims, col_dims, ranks, seed):
+    # same construction as pkg/tests/test_tt.py:48-55
+    rng = np.random.default_rng(seed)
+    full = [1] + list(ranks) + [1]
+    return [rng.standard_normal((full[k], row_dims[k], col_dims[k], full[k + 1]))
+            for k in range(len(row_dims))]
+
+
+def gen_tt_ops():
+    out = {}
+    # matvec (test_tt.py:193-220)
+    cases = [
+        ("mv_identity", [np.eye(n).reshape(1, n, n, 1) for n in (3, 4, 5)],
+         ttkrylov.tt_random([3, 4, 5], [2, 3], seed=11)),
+        ("mv_rankprod", random_operator([3, 3, 3], [3, 3, 3], [2, 2], 12),
+         ttkrylov.tt_random([3, 3, 3], [3, 3], seed=13)),
+        ("mv_dense", random_operator([4, 4, 4], [4, 4, 4], [2, 3], 14),
+         ttkrylov.tt_random([4, 4, 4], [2, 2], seed=15)),
+        ("mv_rect", random_operator([2, 3], [4, 5], [2], 16),
+         ttkrylov.tt_random([4, 5], [3], seed=17)),
+        ("mv_mixed", random_operator([5, 3, 6, 2], [4, 7, 3, 5], [3, 1, 2], 18),
+         ttkrylov.tt_random([4, 7, 3, 5], [4, 5, 2], seed=19)),
+    ]
+    names = []
+    for name, op, v in cases:
+        res = ttkrylov.tt_matvec(ttkrylov.TTOperator(op), v)
+        cores_dict(name + "_op", op, out)
+        cores_dict(name + "_x", v.cores, out)
+        cores_dict(name + "_y", res.cores, out)
+        names.append(name)
+    out["mv_names"] = np.array(names)
+
+    # add / scale (test_tt.py:112-160)
+    a = ttkrylov.tt_random([3, 3, 3], [2, 3], seed=0)
+    b = ttkrylov.tt_random([3, 3, 3], [1, 2], seed=1)
+    cores_dict("add_a", a.cores, out)
+    cores_dict("add_b", b.cores, out)
+    cores_dict("add_y", ttkrylov.tt_add(a, b).cores, out)
+    a1 = ttkrylov.TTVector([np.array([[[1.0], [2.0]]])])
+    b1 = ttkrylov.TTVector([np.array([[[5.0], [7.0]]])])
+    cores_dict("add1_a", a1.cores, out)
+    cores_dict("add1_b", b1.cores, out)
+    cores_dict("add1_y", ttkrylov.tt_add(a1, b1).cores, out)
+    s = ttkrylov.tt_random([3, 4, 3], [2, 2], seed=6)
+    cores_dict("scale_a", s.cores, out)
+    cores_dict("scale_y", ttkrylov.tt_scale(s, -2.5).cores, out)
+    # a multi-term explicit Arnoldi update: vt - h1 v1 - h2 v2 (solvers.py:361-366)
+    vt = ttkrylov.tt_random([4, 5, 3, 4], [3, 4, 2], seed=40)
+    v1 = ttkrylov.tt_random([4, 5, 3, 4], [2, 2, 2], seed=41)
+    v2 = ttkrylov.tt_random([4, 5, 3, 4], [1, 3, 2], seed=42)
+    acc = vt
+    hs = [0.37, -1.25]
+    for h, vi in zip(hs, (v1, v2)):
+        acc = ttkrylov.tt_add(acc, ttkrylov.tt_scale(vi, -h))
+    for nm, v in (("axpy_vt", vt), ("axpy_v1", v1), ("axpy_v2", v2), ("axpy_y", acc)):
+        cores_dict(nm, v.cores, out)
+    out["axpy_h"] = np.array(hs)
+
+    # dot / norm (test_tt.py:163-190)
+    da = ttkrylov.tt_random([5, 5, 5], [3, 3], seed=8)
+    db = ttkrylov.tt_random([5, 5, 5], [2, 4], seed=9)
+    cores_dict("dot_a", da.cores, out)
+    cores_dict("dot_b", db.cores, out)
+    out["dot_ab"] = np.array(ttkrylov.tt_dot(da, db))
+    nn = ttkrylov.tt_random([4, 6, 3], [2, 5], seed=10)
+    cores_dict("norm_a", nn.cores, out)
+    out["norm_a_val"] = np.array(ttkrylov.tt_norm(nn))
+
+    # rounding (test_tt.py:228-275), reference tt_round as-is
+    rcases = []
+    a = ttkrylov.tt_random([4, 4, 4], [2, 2], seed=18)
+    rcases.append(("rd_minimal", a, 1e-14, None))
+    a = ttkrylov.tt_random([4, 4, 4], [2, 2], seed=19)
+    rcases.append(("rd_doubled", ttkrylov.tt_add(a, a), 1e-12, None))
+    for tol in (1e-2, 1e-6, 1e-10):
+        for seed in (0, 3, 7):
+            rcases.append((f"rd_contract_{tol:g}_{seed}",
+                           ttkrylov.tt_random([5, 6, 4, 5], [4, 6, 4], seed=seed), tol, None))
+    rcases.append(("rd_cap", ttkrylov.tt_random([6, 6, 6], [5, 5], seed=21), 0.0, 2))
+    a = ttkrylov.tt_random([3, 4, 3], [2, 2], seed=2)
+    rcases.append(("rd_cancel", ttkrylov.tt_add(a, ttkrylov.tt_scale(a, -1.0)), 1e-12, None))
+    a = ttkrylov.tt_add(ttkrylov.tt_random([4, 5, 4], [3, 3], seed=22),
+                        ttkrylov.tt_random([4, 5, 4], [2, 2], seed=23))
+    rcases.append(("rd_idem", a, 1e-3, None))
+    names = []
+    for name, v, tol, cap in rcases:
+        r = ttkrylov.tt_round(v, ttkrylov.RoundSpec(tol, cap))
+        cores_dict(name + "_x", v.cores, out)
+        out[name + "_dense"] = ttkrylov.tt_to_dense(r)
+        out[name + "_ranks"] = np.array(r.ranks)
+        out[name + "_spec"] = np.array([tol, -1 if cap is None else cap])
+        names.append(name)
+    out["rd_names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "tt_ops.npz"), **out)
+
+
+def gen_sketch():
+    out = {}
+    cases = [
+        ("kr_d1", ttkrylov.kr_sketch_new([6], 4, seed=7), ttkrylov.tt_random([6], [], seed=8)),
+        ("kr_dense", ttkrylov.kr_sketch_new([3, 4, 4], 7, seed=9),
+         ttkrylov.tt_random([3, 4, 4], [3, 2], seed=10)),
+        ("kr_lin", ttkrylov.kr_sketch_new([3, 3, 3], 9, seed=11),
+         ttkrylov.tt_random([3, 3, 3], [2, 2], seed=12)),
+        ("kr_chunk", ttkrylov.kr_sketch_new([3, 4], 50, seed=18),
+         ttkrylov.tt_random([3, 4], [3], seed=19)),
+        ("kr_wide", ttkrylov.kr_sketch_new([5, 8, 6, 7, 4], 33, seed=20),
+         ttkrylov.tt_random([5, 8, 6, 7, 4], [5, 17, 9, 3], seed=21)),
+    ]
+    names = []
+    for name, s, v in cases:
+        y = ttkrylov.kr_apply(s, v)
+        for k, f in enumerate(s.factors):
+            out[f"{name}_F__{k}"] = f
+        cores_dict(name + "_x", v.cores, out)
+        out[name + "_y"] = y
+        names.append(name)
+    out["kr_names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "sketch.npz"), **out)
+
+
+def gen_streaming():
+    out = {}
+    frame = rstreaming.StreamFrame.create([3, 4, 3], [2, 2], oversampling=3, seed=6)
+    t = ttkrylov.tt_random([3, 4, 3], [2, 3], seed=7)
+    pair = rstreaming.stream_sketch(t, frame)
+    cores_dict("ss_left", frame.left.cores, out)
+    cores_dict("ss_right", frame.right.cores, out)
+    cores_dict("ss_x", t.cores, out)
+    for k, p in enumerate(pair.psi):
+        out[f"ss_psi__{k}"] = p
+    for k, o in enumerate(pair.omega):
+        out[f"ss_omega__{k}"] = o
+    # 5-term combination + recovery (test_streaming.py:182-195)
+    dims = [4, 4, 4, 4]
+    frame = rstreaming.StreamFrame.create(dims, [4, 10, 4], oversampling=8, seed=22)
+    vs = [ttkrylov.tt_random(dims, [2, 2, 2], seed=200 + i) for i in range(5)]
+    ys = np.array([0.3, -1.1, 2.0, 0.7, -0.4])
+    comb = rstreaming.combine_pairs([rstreaming.stream_sketch(v, frame) for v in vs], ys)
+    got = rstreaming.stream_recover(comb, ttkrylov.RoundSpec(1e-12))
+    cores_dict("rc_left", frame.left.cores, out)
+    cores_dict("rc_right", frame.right.cores, out)
+    for i, v in enumerate(vs):
+        cores_dict(f"rc_v{i}", v.cores, out)
+    out["rc_y"] = ys
+    out["rc_dense"] = ttkrylov.tt_to_dense(got)
+    out["rc_ranks"] = np.array(got.ranks)
+    np.savez_compressed(os.path.join(HERE, "streaming.npz"), **out)
+
+
+def nozero_round(v, spec):
+    """Reference tt_round minus its zero test (tt.py:350-356), built from the
+    reference's own _right_orthogonalize/_truncation_rank (quirk Q1 bypass)."""
+    d = v.d
+    if d == 1:
+        return v.copy()
+    cores = rtt._right_orthogonalize([c.copy() for c in v.cores])
+    nrm = np.linalg.norm(cores[0])
+    if nrm == 0:
+        return rtt.tt_zero(v.dims)
+    budget = spec.rel_tol * nrm / np.sqrt(d - 1)
+    for k in range(d - 1):
+        c = cores[k]
+        r0, n, r1 = c.shape
+        u, sv, vt = np.linalg.svd(c.reshape(r0 * n, r1), full_matrices=False)
+        r = rtt._truncation_rank(sv, budget)
+        if spec.max_rank is not None:
+            r = min(r, spec.max_rank)
+        cores[k] = u[:, :r].reshape(r0, n, r)
+        cores[k + 1] = np.tensordot(sv[:r, None] * vt[:r], cores[k + 1], axes=([1], [0]))
+    return ttkrylov.TTVector(cores)
+
+
+def probe_sketch(x, nprobe=24, seed=777):
+    s = ttkrylov.kr_sketch_new(list(x.dims), nprobe, seed=seed)
+    return ttkrylov.kr_apply(s, x)
+
+
+def solver_case(name, op, b, cfg, sketch, out, frame=None):
+    x, rep = rsolvers.tt_sgmres(op, b, None, cfg, sketch, frame)
+    cores_dict(name + "_op", op.op_cores, out)
+    cores_dict(name + "_b", b.cores, out)
+    for k, f in enumerate(sketch.factors):
+        out[f"{name}_F__{k}"] = f
+    out[name + "_res"] = np.array(rep.res_sketched)
+    out[name + "_ranks"] = np.array(rep.basis_rank)
+    out[name + "_iters"] = np.array(rep.iterations)
+    out[name + "_conv"] = np.array(rep.converged)
+    out[name + "_xprobe"] = probe_sketch(x)
+    out[name + "_xnorm"] = np.array(ttkrylov.tt_norm(x))
+    out[name + "_cfg"] = np.array([cfg.maxit, cfg.tol, cfg.ell, cfg.eta,
+                                   -1 if cfg.max_rank is None else cfg.max_rank,
+                                   cfg.sketch_rows, cfg.oversampling,
+                                   -1 if cfg.solution_rank is None else cfg.solution_rank,
+                                   cfg.seed, 1 if cfg.combine_mode == "stta" else 0])
+    if frame is not None:
+        cores_dict(name + "_left", frame.left.cores, out)
+        cores_dict(name + "_right", frame.right.cores, out)
+    return x, rep
+
+
+def gen_solver_small():
+    out = {}
+    op, rhs = convection_diffusion(ConvectionDiffusionSpec(d=3, n=5))
+    cfg = rsolvers.SolverConfig(maxit=100, tol=1e-8, ell=1, eta=0.3, seed=6, solution_rank=10)
+    s = ttkrylov.kr_sketch_new(rhs.dims, cfg.sketch_rows, seed=7)
+    solver_case("sv_pde", op, rhs, cfg, s, out)
+    cfg = rsolvers.SolverConfig(maxit=60, tol=1e-8, ell=2, eta=0.3, seed=3, solution_rank=10)
+    s = ttkrylov.kr_sketch_new(rhs.dims, cfg.sketch_rows, seed=4)
+    solver_case("sv_ell2", op, rhs, cfg, s, out)
+    cfg = rsolvers.SolverConfig(maxit=100, tol=1e-7, ell=2, seed=14, combine_mode="stta",
+                                solution_rank=10)
+    s = ttkrylov.kr_sketch_new(rhs.dims, cfg.sketch_rows, seed=15)
+    solver_case("sv_stta", op, rhs, cfg, s, out)
+    out["sv_names"] = np.array(["sv_pde", "sv_ell2", "sv_stta"])
+    np.savez_compressed(os.path.join(HERE, "solver_small.npz"), **out)
+
+
+def gen_solver_cfg1():
+    """BASELINE config 1 with the Q1 zero test bypassed."""
+    out = {}
+    n, d = 32, 8
+    lap = (n + 1) ** 2 * (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1))
+    op = ttkrylov.kron_sum_operator([lap] * d)
+    rng = np.random.default_rng(0)
+    b = ttkrylov.tt_rank_one([rng.standard_normal(n) for _ in range(d)])
+    b = ttkrylov.tt_scale(b, 1.0 / ttkrylov.tt_norm(b))
+    cfg = rsolvers.SolverConfig(maxit=40, tol=1e-8, ell=2, eta=1.0, max_rank=30,
+                                sketch_rows=80, seed=0)
+    s = ttkrylov.kr_sketch_new(b.dims, 80, seed=0)
+    # StreamFrame.create overflows nowhere at d=8, n=32 (8*5 bits), so it is usable here
+    frame = rsolvers.make_solver_frame(b, cfg, seed=1)
+    saved = (rsolvers.tt_round, rstreaming.tt_round)
+    rsolvers.tt_round = nozero_round
+    rstreaming.tt_round = nozero_round
+    try:
+        t0 = time.perf_counter()
+        solver_case("cfg1", op, b, cfg, s, out, frame=frame)
+        # the frame is regenerated from its seed (SeedSequence(1).spawn(2)) by the tests
+        for key in [k for k in out if k.startswith("cfg1_left") or k.startswith("cfg1_right")]:
+            del out[key]
+        out["cfg1_wall"] = np.array(time.perf_counter() - t0)
+    finally:
+        rsolvers.tt_round, rstreaming.tt_round = saved
+    np.savez_compressed(os.path.join(HERE, "solver_cfg1.npz"), **out)
+
+
+if __name__ == "__main__":
+    gen_tt_ops()
+    gen_sketch()
+    gen_streaming()
+    gen_solver_small()
+    gen_solver_cfg1()
+    print("golden fixtures written to", HERE)

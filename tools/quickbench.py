@@ -1,0 +1,59 @@
+"""Quick CUDA-event timings of individual kernels at BASELINE sizes (dev tool)."""
+import sys, time, json
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import paper_2409_09471_b200 as T
+
+dev = torch.device("cuda", 0)
+res = {}
+
+def timeit(fn, reps=5, warm=2):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); fn(); e1.record(); e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return min(ts), float(np.median(ts))
+
+which = sys.argv[1:] or ["matvec", "kr", "dots", "concat"]
+if "matvec" in which:
+    d, n, r, rho = 32, 128, 64, 3
+    rng = np.random.default_rng(0)
+    full = [1] + [rho] * (d - 1) + [1]
+    op = T.TTOperator([rng.standard_normal((full[k], n, n, full[k + 1])) for k in range(d)], device=dev)
+    rr = [1] + [r] * (d - 1) + [1]
+    x = T.TTVector([rng.standard_normal((rr[k], n, rr[k + 1])) for k in range(d)], device=dev)
+    flops = sum(2.0 * full[k] * n * n * full[k + 1] * rr[k] * rr[k + 1] for k in range(d))
+    out_bytes = sum(8.0 * full[k] * rr[k] * n * full[k + 1] * rr[k + 1] for k in range(d))
+    best, med = timeit(lambda: T.tt_matvec(op, x))
+    res["matvec_cfg3"] = {"ms": best, "med_ms": med, "gflop": flops / 1e9, "tflops": flops / best / 1e9,
+                          "out_gb": out_bytes / 1e9, "gbs": out_bytes / best / 1e6}
+if "kr" in which:
+    d, n, r, s, B = 20, 64, 100, 512, 64
+    rng = np.random.default_rng(0)
+    sk = T.KhatriRaoSketch([rng.normal(0, 1 / np.sqrt(n), size=(s, n)) for _ in range(d)], device=dev)
+    rng = np.random.default_rng(1)
+    rr = [1] + [r] * (d - 1) + [1]
+    vs = [T.TTVector([rng.standard_normal((rr[k], n, rr[k + 1])) / np.sqrt(n * r) for k in range(d)], device=dev)
+          for _ in range(B)]
+    flops = B * sum(2.0 * s * n * rr[k] * rr[k + 1] for k in range(d))
+    best, med = timeit(lambda: T.kr_apply_batch(sk, vs), reps=3, warm=1)
+    res["kr_cfg4"] = {"ms": best, "med_ms": med, "gflop": flops / 1e9, "tflops": flops / best / 1e9}
+if "dots" in which:
+    d, n = 50, 256
+    x = T.tt_random([n] * d, [40] * (d - 1), seed=1, device=dev)
+    ys = [T.tt_random([n] * d, [20] * (d - 1), seed=2 + i, device=dev) for i in range(3)] + [x]
+    best, med = timeit(lambda: T.tt_dots(x, ys))
+    res["dots_cfg5"] = {"ms": best, "med_ms": med}
+if "concat" in which:
+    d, n = 50, 256
+    vt = T.tt_random([n] * d, [40] * (d - 1), seed=1, device=dev)
+    ws = [T.tt_random([n] * d, [20] * (d - 1), seed=2 + i, device=dev) for i in range(3)]
+    tot = sum(c.numel() for c in T.tt_combine([vt] + ws, [1, -0.1, -0.2, -0.3]).cores) * 8
+    inb = sum(c.numel() for v in [vt] + ws for c in v.cores) * 8
+    best, med = timeit(lambda: T.tt_combine([vt] + ws, [1, -0.1, -0.2, -0.3]))
+    res["concat_cfg5"] = {"ms": best, "med_ms": med, "bytes": tot + inb, "gbs": (tot + inb) / best / 1e6}
+print(json.dumps(res, indent=1))
