@@ -108,6 +108,59 @@ int ttk_kr_sketch_path(int path, int d, const int* n, int s_lo, int s_hi, const 
                        int nvec, const int* ranks, const double* const* cores, double* out,
                        void* ws, size_t ws_bytes, void* stream);
 
+/* ---- dense factorisations (replace np.linalg.qr/svd at tt.py:330,361) ------
+ * Householder TSQR of A (m x l), A(i,j) = A[i*a_rs + j*a_cs]: explicit Q (m x k,
+ * k = min(m,l)) at Q[i*q_rs + j*q_cs] and, if R != NULL, R (k x l, row-major).
+ * Multi-panel inputs (m above one shared-memory panel) need l <= 112. */
+int ttk_qr(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+           long long q_cs, double* R, void* ws, size_t ws_bytes, void* stream);
+size_t ttk_qr_ws_bytes(int m, int l);
+/* one-sided Jacobi SVD of B (k x l, row-major, k,l <= 128): B V = U S with
+ * S[min(k,l)] descending, U (k x min(k,l)), V (l x min(k,l)) if V != NULL. */
+int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream);
+
+/* ---- tt_round, TT-SVD (reference tt.py:337-368) ----------------------------
+ * out[k] holds ranks[k]*dims[k]*ranks[k+1] doubles; out_ranks (host, d+1)
+ * receives the result ranks and core k fills the first
+ * out_ranks[k]*dims[k]*out_ranks[k+1] entries of out[k].  max_rank <= 0: no
+ * cap; zero_rel < 0: no cancellation test (reference tt.py:348-356, quirk Q1).
+ * Synchronises `stream` (rank decisions are read back per core). */
+int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* cores,
+                 double rel_tol, int max_rank, double zero_rel, double* const* out, int* out_ranks,
+                 void* ws, size_t ws_bytes, void* stream);
+size_t ttk_tt_round_ws_bytes(int d, const int* dims, const int* ranks);
+
+/* ---- randomize-then-orthogonalize sweeps (absent from the reference,
+ * SPEC.md:313; restated in oracle/ttoracle.py rto_sweeps) --------------------
+ * X: cores (R[k], n_k, R[k+1]); G: Gaussian TT-DRM cores (L[k], n_k, L[k+1])
+ * (reference tt_drm_new, streaming.py:135-150) with L[c] <= min(R[c],
+ * L[c-1] n_{c-1}); out: cores (L[k], n_k, L[k+1]), cores 0..d-2 left-orthonormal. */
+int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X, const int* L,
+                   const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream);
+size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L);
+
+/* ---- streaming sketches (reference streaming.py:214-302) -------------------
+ * stream_sketch: psi[mu] ((lr[mu] n_mu) x rr[mu+1]) and omega[mu-1]
+ * (lr[mu] x rr[mu]) of a TT with ranks tr against the frame's left (Y, ranks
+ * lr) and right (X, ranks rr) TT-DRMs. */
+int ttk_stream_sketch(int d, const int* dims, const int* tr, const double* const* C, const int* lr,
+                      const double* const* Y, const int* rr, const double* const* X,
+                      double* const* psi, double* const* omega, void* ws, size_t ws_bytes,
+                      void* stream);
+size_t ttk_stream_sketch_ws_bytes(int d, const int* dims, const int* tr, const int* lr, const int* rr);
+/* combine_pairs kernel: out = sum_t coeff[t] in_t, left-to-right (streaming.py:242-260) */
+int ttk_axpy_multi(int nterms, const double* coeff, const double* const* in, long long n, double* out,
+                   void* stream);
+/* stream_recover up to its final tt_round: truncated-SVD pseudo-inverse halves
+ * of every Omega (relative cutoff rcond) applied to the Psi blocks; writes the
+ * recovered cores (capacity max(lr,rr)*n*rr[mu+1]) and their ranks (host).
+ * *is_zero = 1 when every Psi is zero; TTK_DEGENERATE on a zero Omega. */
+int ttk_stream_recover_cores(int d, const int* dims, const int* lr, const int* rr,
+                             const double* const* psi, const double* const* omega, double rcond,
+                             double* const* out, int* out_ranks, int* is_zero, void* ws,
+                             size_t ws_bytes, void* stream);
+size_t ttk_stream_recover_ws_bytes(int d, const int* dims, const int* lr, const int* rr);
+
 #ifdef __cplusplus
 }
 #endif

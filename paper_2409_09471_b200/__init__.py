@@ -8,9 +8,31 @@ arithmetic runs in libttk_b200.so (C ABI: include/ttk_b200.h).
 """
 
 from .errors import DegenerateRecovery, ShapeMismatch, SizeLimit
+from .rto import rto_flops, rto_ranks, rto_sweeps, tt_round_rto
 from .sketch import KhatriRaoSketch, kr_apply, kr_apply_batch, kr_apply_device, kr_apply_rows, kr_sketch_new
+from .solvers import (
+    PHASES,
+    SolveReport,
+    SolverConfig,
+    make_solver_frame,
+    sketched_lsq,
+    solver_rto_drm,
+    true_residual,
+    tt_sgmres,
+)
+from .streaming import (
+    PINV_RCOND,
+    TTDRM,
+    SketchPair,
+    StreamFrame,
+    combine_pairs,
+    stream_recover,
+    stream_sketch,
+    tt_drm_new,
+)
 from .tt import (
     DENSE_CAP,
+    ZERO_REL,
     RoundSpec,
     TTOperator,
     TTVector,
@@ -24,9 +46,11 @@ from .tt import (
     tt_dots,
     tt_matvec,
     tt_norm,
+    tt_norm_left_orthogonal,
     tt_op_to_dense,
     tt_random,
     tt_rank_one,
+    tt_round,
     tt_scale,
     tt_to_dense,
     tt_zero,

@@ -110,3 +110,24 @@ def stream_ptr(device=None) -> int:
 def workspace(nbytes: int, device) -> torch.Tensor:
     """Caller-owned scratch from torch's caching allocator."""
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+SIGNATURES.update({
+    "ttk_qr": (c_int, [c_int, c_int, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_vp, c_vp, c_size, c_vp]),
+    "ttk_qr_ws_bytes": (c_size, [c_int, c_int]),
+    "ttk_svd_small": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "ttk_tt_round": (c_int, [c_int, P_int, P_int, P_vp, c_double, c_int, c_double, P_vp, P_int, c_vp,
+                             c_size, c_vp]),
+    "ttk_tt_round_ws_bytes": (c_size, [c_int, P_int, P_int]),
+    "ttk_rto_sweeps": (c_int, [c_int, P_int, P_int, P_vp, P_int, P_vp, P_vp, c_vp, c_size, c_vp]),
+    "ttk_rto_ws_bytes": (c_size, [c_int, P_int, P_int, P_int]),
+})
+
+SIGNATURES.update({
+    "ttk_stream_sketch": (c_int, [c_int, P_int, P_int, P_vp, P_int, P_vp, P_int, P_vp, P_vp, P_vp, c_vp,
+                                  c_size, c_vp]),
+    "ttk_stream_sketch_ws_bytes": (c_size, [c_int, P_int, P_int, P_int, P_int]),
+    "ttk_axpy_multi": (c_int, [c_int, P_double, P_vp, c_ll, c_vp, c_vp]),
+    "ttk_stream_recover_cores": (c_int, [c_int, P_int, P_int, P_int, P_vp, P_vp, c_double, P_vp, P_int,
+                                         ctypes.POINTER(ctypes.c_int), c_vp, c_size, c_vp]),
+    "ttk_stream_recover_ws_bytes": (c_size, [c_int, P_int, P_int, P_int]),
+})

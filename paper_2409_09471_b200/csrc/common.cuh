@@ -121,4 +121,7 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// sum of squares of x[0..n) into out_dev[0] (fixed-order reduction; part >= 256 doubles)
+int launch_sumsq(const double* x, long long n, double* out_dev, double* part, cudaStream_t st);
+
 }  // namespace ttk

@@ -46,7 +46,7 @@ constexpr int BM = WARPS * 8 * FM;    // 128 rows per CTA
 constexpr int BN = 128;               // max rank handled by the fused path
 constexpr int FNMAX = BN / 8;
 constexpr int BK = 16;
-constexpr int STAGES = 3;
+constexpr int STAGES = 2;
 constexpr int SST = BN + 1;           // odd stride: conflict-free state reads
 constexpr int SF = BM + 4;
 constexpr int SB = BN + 4;

@@ -1,0 +1,420 @@
+// Householder TSQR + one-sided Jacobi SVD (see qr.cuh).
+//
+// TSQR: the m x l input is cut into panels of H rows; one CTA factors a panel
+// with Householder reflectors entirely in shared memory (LAPACK dlarfg sign
+// convention), keeps the reflectors for the explicit-Q pass and emits its
+// l x l R.  The stacked R's form the next level's input until one panel is
+// left.  The explicit Q is then formed top-down: every panel applies its
+// reflectors (in reverse order) to its l x l block of the level-above Q padded
+// with zeros.  Rank-deficient inputs are handled exactly like LAPACK (a zero
+// column gives tau = 0 and an identity reflector), so Q is always orthonormal.
+#include "qr.cuh"
+#include "../../include/ttk_b200.h"
+
+#include <algorithm>
+#include <vector>
+
+namespace ttk {
+
+constexpr int kQrThreads = 1024;
+constexpr int kQrSmemDoubles = 28672;  // 224 KB of shared memory, in doubles
+
+__device__ __forceinline__ int qr_ld(int l) { return l | 1; }  // odd stride: conflict-free columns
+
+// -------------------------------------------------------------------------
+// panel factorisation: one CTA per panel
+__global__ void __launch_bounds__(kQrThreads, 1)
+    qr_panel_factor_kernel(int m, int l, int H, const double* __restrict__ A, long long a_rs,
+                           long long a_cs, double* __restrict__ Vt, double* __restrict__ tau,
+                           double* __restrict__ Rout) {
+  extern __shared__ double sm[];
+  const int ld = qr_ld(l);
+  double* S = sm;                 // H x ld
+  double* vsh = S + (size_t)H * ld;  // 2 x H
+  double* tsh = vsh + 2 * H;      // l
+  const int p = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const long long row0 = (long long)p * H;
+
+  for (int e = threadIdx.x; e < H * l; e += blockDim.x) {
+    int r, c;
+    if (a_cs == 1) { r = e / l; c = e - r * l; } else { c = e / H; r = e - c * H; }
+    long long gr = row0 + r;
+    S[r * ld + c] = (gr < m) ? A[gr * a_rs + (long long)c * a_cs] : 0.0;
+  }
+  const int kmax = min(l, H);  // reflectors; the rest are identities
+  for (int j = kmax + threadIdx.x; j < l; j += blockDim.x) tsh[j] = 0.0;
+  __syncthreads();
+
+  for (int j = 0; j < kmax; ++j) {
+    double* v = vsh + (j & 1) * H;
+    if (warp == 0) {
+      // reflector for column j (rows j..H-1); warp 0 also updated this column
+      double s2 = 0.0;
+      for (int r = j + 1 + lane; r < H; r += 32) {
+        double x = S[r * ld + j];
+        s2 += x * x;
+      }
+      s2 = warp_sum(s2);
+      const double alpha = S[j * ld + j];
+      double t = 0.0, beta = alpha, scal = 0.0;
+      if (s2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+        t = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int r = j + 1 + lane; r < H; r += 32) {
+        double x = S[r * ld + j] * scal;
+        S[r * ld + j] = x;
+        v[r] = x;
+      }
+      if (lane == 0) {
+        S[j * ld + j] = beta;
+        v[j] = 1.0;
+        tsh[j] = t;
+      }
+    }
+    __syncthreads();
+    const double t = tsh[j];
+    if (t != 0.0) {
+      // columns c > j round-robin over warps; warp 0 always takes column j+1
+      for (int c = j + 1 + warp; c < l; c += nwarps) {
+        double s = 0.0;
+        for (int r = j + lane; r < H; r += 32) s += v[r] * S[r * ld + c];
+        s = warp_sum(s) * t;
+        for (int r = j + lane; r < H; r += 32) S[r * ld + c] -= v[r] * s;
+      }
+    }
+    // no second barrier: the next reflector is computed by warp 0 from the
+    // column it just updated, and the v buffers are double-buffered.
+  }
+  __syncthreads();
+  // R block (rows 0..l-1), reflectors (column-major per panel), tau
+  double* Rp = Rout + (long long)p * l * l;
+  for (int e = threadIdx.x; e < l * l; e += blockDim.x) {
+    int r = e / l, c = e - r * l;
+    Rp[e] = (c >= r && r < H) ? S[r * ld + c] : 0.0;
+  }
+  double* Vp = Vt + (long long)p * l * H;
+  for (int e = threadIdx.x; e < l * H; e += blockDim.x) {
+    int j = e / H, r = e - j * H;
+    Vp[e] = (r > j) ? S[r * ld + j] : (r == j ? 1.0 : 0.0);
+  }
+  for (int j = threadIdx.x; j < l; j += blockDim.x) tau[(long long)p * l + j] = tsh[j];
+}
+
+// -------------------------------------------------------------------------
+// explicit Q of one panel: E (H x l) = [Qup block (l x l); 0], E <- H_0 ... H_{l-1} E
+__global__ void __launch_bounds__(kQrThreads, 1)
+    qr_panel_apply_kernel(int l, int H, int kcols, const double* __restrict__ Vt,
+                          const double* __restrict__ tau, const double* __restrict__ Qup,
+                          long long m_out, double* __restrict__ Q, long long q_rs, long long q_cs) {
+  extern __shared__ double sm[];
+  const int ld = qr_ld(l);
+  double* E = sm;  // H x ld
+  const int p = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < H * l; e += blockDim.x) {
+    int r = e / l, c = e - r * l;
+    double x = 0.0;
+    if (r < l) x = Qup ? Qup[((long long)p * l + r) * l + c] : (r == c ? 1.0 : 0.0);
+    // (single-panel wide case H < l: rows >= H do not exist)
+    E[r * ld + c] = x;
+  }
+  __syncthreads();
+  const double* Vp = Vt + (long long)p * l * H;
+  const double* tp = tau + (long long)p * l;
+  for (int j = min(l, H) - 1; j >= 0; --j) {
+    const double t = tp[j];
+    if (t == 0.0) continue;
+    const double* v = Vp + (long long)j * H;
+    for (int c = warp; c < l; c += nwarps) {
+      double s = 0.0;
+      for (int r = j + lane; r < H; r += 32) s += __ldg(v + r) * E[r * ld + c];
+      s = warp_sum(s) * t;
+      for (int r = j + lane; r < H; r += 32) E[r * ld + c] -= __ldg(v + r) * s;
+    }
+  }
+  __syncthreads();
+  const long long row0 = (long long)p * H;
+  for (int e = threadIdx.x; e < H * kcols; e += blockDim.x) {
+    int r, c;
+    if (q_cs == 1) { r = e / kcols; c = e - r * kcols; } else { c = e / H; r = e - c * H; }
+    long long gr = row0 + r;
+    if (gr < m_out) Q[gr * q_rs + (long long)c * q_cs] = E[r * ld + c];
+  }
+}
+
+// -------------------------------------------------------------------------
+int qr_plan(int m, int l, QrPlan* P) {
+  P->m = m; P->l = l; P->k = std::min(m, l);
+  P->cpw = P->rpl = 0;
+  TTK_REQUIRE(l >= 1, kInvalidValue, "tsqr: l=%d must be positive", l);
+  const int ld = l | 1;
+  // shared memory holds the panel (H x ld), two reflector buffers (2 x H) and tau (l)
+  int H = (kQrSmemDoubles - 128 - l) / (ld + 2);
+  H = std::min(H, 2048);
+  if (m <= H) {
+    H = m;  // single panel, exactly m rows (wide inputs: min(m, l) reflectors)
+  } else {
+    TTK_REQUIRE(H >= 2 * l, kInvalidValue,
+                "tsqr: %d x %d needs a multi-panel tree; columns limited to %d", m, l, H / 2);
+  }
+  P->h = H;
+  int rows = m, lev = 0;
+  size_t ws = 0;
+  while (true) {
+    TTK_REQUIRE(lev < 16, kInvalidValue, "tsqr: too many levels");
+    int panels = (rows + H - 1) / H;
+    P->rows[lev] = rows;
+    P->panels[lev] = panels;
+    ws += align_up((size_t)panels * l * H * 8, 256);          // reflectors
+    ws += align_up((size_t)panels * l * 8, 256);              // tau
+    ws += align_up((size_t)panels * l * l * 8, 256);          // stacked R (next input)
+    ws += align_up((size_t)rows * l * 8, 256);                // Q of this level (levels > 0)
+    ++lev;
+    if (panels == 1) break;
+    rows = panels * l;
+  }
+  P->levels = lev;
+  P->ws_bytes = ws + 4096;
+  return kOk;
+}
+
+size_t tsqr_ws_bytes(int m, int l) {
+  QrPlan P;
+  if (m <= 0 || l <= 0) return 0;
+  if (qr_plan(m, l, &P) != kOk) return 0;
+  return P.ws_bytes;
+}
+
+static int qr_set_smem(const void* fn, size_t bytes) {
+  TTK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return kOk;
+}
+
+int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+         long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (m <= 0 || l <= 0) return kOk;
+  QrPlan P;
+  TTK_TRY(qr_plan(m, l, &P));
+  TTK_REQUIRE(ws != nullptr && ws_bytes >= P.ws_bytes, kWorkspace,
+              "tsqr: workspace %zu < %zu bytes", ws_bytes, P.ws_bytes);
+  const int H = P.h, ld = l | 1;
+  static bool attr = false;
+  if (!attr) {
+    TTK_TRY(qr_set_smem((const void*)qr_panel_factor_kernel, 227 * 1024));
+    TTK_TRY(qr_set_smem((const void*)qr_panel_apply_kernel, 227 * 1024));
+    attr = true;
+  }
+  const size_t smem_f = sizeof(double) * ((size_t)H * ld + 2 * H + l);
+  const size_t smem_a = sizeof(double) * ((size_t)H * ld);
+  Arena ar(ws, ws_bytes);
+  std::vector<double*> V(P.levels), T(P.levels), RS(P.levels), QL(P.levels);
+  for (int i = 0; i < P.levels; ++i) {
+    V[i] = ar.take<double>((size_t)P.panels[i] * l * H);
+    T[i] = ar.take<double>((size_t)P.panels[i] * l);
+    RS[i] = ar.take<double>((size_t)P.panels[i] * l * l);
+    QL[i] = ar.take<double>((size_t)P.rows[i] * l);
+  }
+  // factor, bottom-up
+  for (int i = 0; i < P.levels; ++i) {
+    const double* in = (i == 0) ? A : RS[i - 1];
+    long long rs = (i == 0) ? a_rs : l, cs = (i == 0) ? a_cs : 1;
+    qr_panel_factor_kernel<<<P.panels[i], kQrThreads, smem_f, st>>>(P.rows[i], l, H, in, rs, cs, V[i],
+                                                                    T[i], RS[i]);
+    TTK_CHECK_LAUNCH();
+  }
+  const int top = P.levels - 1;
+  if (R) {
+    // top-level R (l x l) -> k x l
+    TTK_CHECK_CUDA(cudaMemcpyAsync(R, RS[top], sizeof(double) * (size_t)P.k * l,
+                                   cudaMemcpyDeviceToDevice, st));
+  }
+  // explicit Q, top-down
+  for (int i = top; i >= 0; --i) {
+    const double* qup = (i == top) ? nullptr : QL[i + 1];
+    if (i == 0) {
+      qr_panel_apply_kernel<<<P.panels[0], kQrThreads, smem_a, st>>>(l, H, P.k, V[0], T[0], qup, m, Q,
+                                                                     q_rs, q_cs);
+    } else {
+      qr_panel_apply_kernel<<<P.panels[i], kQrThreads, smem_a, st>>>(l, H, l, V[i], T[i], qup,
+                                                                     P.rows[i], QL[i], l, 1);
+    }
+    TTK_CHECK_LAUNCH();
+  }
+  return kOk;
+}
+
+// -------------------------------------------------------------------------
+// One-sided Jacobi SVD of B (k x l, row-major).  Columns of B are stored
+// column-major in shared memory; l/2 disjoint column pairs rotate per round
+// (round-robin tournament), one 16-lane group per pair.
+constexpr int kSvdThreads = 1024;
+
+__global__ void __launch_bounds__(kSvdThreads, 1)
+    jacobi_svd_kernel(int k, int l, const double* __restrict__ B, double* __restrict__ U,
+                      double* __restrict__ S, double* __restrict__ V, int want_v) {
+  extern __shared__ double sm[];
+  const int le = l + (l & 1);           // even number of columns (dummy zero column)
+  const int kk = k;                     // column length
+  const int ldc = kk | 1;
+  double* C = sm;                       // le columns x ldc
+  double* Vs = C + (size_t)le * ldc;    // le x le (col-major) when want_v
+  __shared__ int changed;
+  __shared__ double nrm[kQrMaxCols + 2];
+  __shared__ int order[kQrMaxCols + 2];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < le * kk; e += blockDim.x) {
+    int c = e / kk, r = e - c * kk;
+    C[c * ldc + r] = (c < l) ? B[(long long)r * l + c] : 0.0;
+  }
+  if (want_v)
+    for (int e = tid; e < le * le; e += blockDim.x) {
+      int c = e / le, r = e - c * le;
+      Vs[c * le + r] = (r == c) ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  const double tol = (double)max(kk, 1) * 1.1102230246251565e-16;
+  const int group = tid >> 4, gl = tid & 15;
+  const int npairs = le / 2;
+  const unsigned gmask = 0xffffu << (threadIdx.x & 16);
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) changed = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < le - 1; ++rnd) {
+      for (int pi = group; pi < npairs; pi += blockDim.x >> 4) {
+        int ia = pi, ib = le - 1 - pi;
+        int p = (ia == 0) ? 0 : 1 + (ia - 1 + rnd) % (le - 1);
+        int q = (ib == 0) ? 0 : 1 + (ib - 1 + rnd) % (le - 1);
+        double* cp = C + p * ldc;
+        double* cq = C + q * ldc;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int r = gl; r < kk; r += 16) {
+          double x = cp[r], y = cq[r];
+          a += x * x; b += y * y; g += x * y;
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(gmask, a, o);
+          b += __shfl_xor_sync(gmask, b, o);
+          g += __shfl_xor_sync(gmask, g, o);
+        }
+        if (a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
+          double zeta = (b - a) / (2.0 * g);
+          double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int r = gl; r < kk; r += 16) {
+            double x = cp[r], y = cq[r];
+            cp[r] = c * x - s * y;
+            cq[r] = s * x + c * y;
+          }
+          if (want_v) {
+            double* vp = Vs + p * le;
+            double* vq = Vs + q * le;
+            for (int r = gl; r < le; r += 16) {
+              double x = vp[r], y = vq[r];
+              vp[r] = c * x - s * y;
+              vq[r] = s * x + c * y;
+            }
+          }
+          if (gl == 0) changed = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!changed) break;
+  }
+  // norms, ranking (descending, ties by index), outputs
+  for (int c = tid >> 5; c < l; c += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int r = tid & 31; r < kk; r += 32) s += C[c * ldc + r] * C[c * ldc + r];
+    s = warp_sum(s);
+    if ((tid & 31) == 0) nrm[c] = sqrt(s);
+  }
+  __syncthreads();
+  for (int c = tid; c < l; c += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < l; ++j) rank += (nrm[j] > nrm[c]) || (nrm[j] == nrm[c] && j < c);
+    order[rank] = c;
+  }
+  __syncthreads();
+  const int kout = min(kk, l);
+  for (int i = tid; i < kout; i += blockDim.x) S[i] = nrm[order[i]];
+  for (int e = tid; e < kk * kout; e += blockDim.x) {
+    int r = e / kout, i = e - r * kout;
+    int c = order[i];
+    double sv = nrm[c];
+    U[e] = (sv > 0.0) ? C[c * ldc + r] / sv : 0.0;
+  }
+  if (want_v && V)
+    for (int e = tid; e < l * kout; e += blockDim.x) {
+      int r = e / kout, i = e - r * kout;
+      V[e] = Vs[order[i] * le + r];
+    }
+}
+
+int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, cudaStream_t st) {
+  if (k <= 0 || l <= 0) return kOk;
+  TTK_REQUIRE(l <= kQrMaxCols && k <= kQrMaxCols, kInvalidValue,
+              "jacobi_svd: %d x %d exceeds %d", k, l, kQrMaxCols);
+  const int le = l + (l & 1);
+  size_t smem = sizeof(double) * ((size_t)le * (k | 1) + (V ? (size_t)le * le : 0));
+  TTK_REQUIRE(smem <= 200 * 1024, kInvalidValue, "jacobi_svd: %d x %d (V=%d) exceeds shared memory", k,
+              l, V != nullptr);
+  static bool attr = false;
+  if (!attr) {
+    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel, 200 * 1024));
+    attr = true;
+  }
+  jacobi_svd_kernel<<<1, kSvdThreads, smem, st>>>(k, l, B, U, S, V, V != nullptr);
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
+__global__ void truncation_rank_kernel(const double* S, int n, double budget, int max_rank, int* r_out) {
+  if (threadIdx.x != 0) return;
+  // tail[r] = sqrt(sum_{i>=r} S_i^2), accumulated from the smallest value as
+  // np.cumsum(sv[::-1]**2)[::-1] does (tt.py:207)
+  int r = n;
+  double acc = 0.0;
+  // find the smallest r with tail[r] <= budget: scan from the end
+  int best = n;
+  for (int i = n - 1; i >= 0; --i) {
+    acc += S[i] * S[i];
+    if (sqrt(fmax(acc, 0.0)) <= budget) best = i;
+  }
+  r = best;
+  if (n == 0) r = 1;
+  if (r < 1) r = 1;
+  if (max_rank > 0 && r > max_rank) r = max_rank;
+  *r_out = r;
+}
+
+int truncation_rank_dev(const double* S, int n, double budget, int max_rank, int* r_dev,
+                        cudaStream_t st) {
+  truncation_rank_kernel<<<1, 32, 0, st>>>(S, n, budget, max_rank, r_dev);
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
+}  // namespace ttk
+
+using namespace ttk;
+
+extern "C" {
+
+size_t ttk_qr_ws_bytes(int m, int l) { return tsqr_ws_bytes(m, l); }
+
+int ttk_qr(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+           long long q_cs, double* R, void* ws, size_t ws_bytes, void* stream) {
+  return tsqr(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream) {
+  return jacobi_svd(k, l, B, U, S, V, (cudaStream_t)stream);
+}
+
+}  // extern "C"

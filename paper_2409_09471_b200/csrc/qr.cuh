@@ -1,0 +1,44 @@
+// Tall-skinny Householder QR (TSQR) and one-sided Jacobi SVD for the
+// rounding sweeps.  Replaces np.linalg.qr / np.linalg.svd (LAPACK) at the
+// reference call sites tt.py:330, tt.py:361, streaming.py:284.
+#pragma once
+#include "common.cuh"
+
+namespace ttk {
+
+// Largest column count handled by the register-resident panel kernels.
+constexpr int kQrMaxCols = 128;
+
+struct QrPlan {
+  int m, l, k;       // k = min(m, l) columns of Q / rows of R
+  int cpw, rpl, h;   // panel config (h = 32 * rpl rows per panel)
+  int levels;
+  int rows[16];      // rows of the level-i input
+  int panels[16];
+  size_t ws_bytes;
+};
+
+int qr_plan(int m, int l, QrPlan* plan);
+
+// Householder TSQR of A (m x l), A(i,j) = A[i*a_rs + j*a_cs].  Writes the
+// explicit Q (m x k) to Q(i,j) = Q[i*q_rs + j*q_cs] and, when R != nullptr,
+// the upper-trapezoidal R (k x l, row-major, ldr = l).  Q may alias nothing
+// of A.  Sign convention: Householder reflectors as LAPACK dgeqrf (R is
+// unique up to the signs of its rows, Q up to the signs of its columns).
+int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+         long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t tsqr_ws_bytes(int m, int l);
+
+// One-sided (Hestenes) Jacobi SVD of B (k x l, row-major, ldb = l), k, l <= 128:
+// B V = U S.  Outputs, columns sorted by decreasing singular value:
+//   S[min(k,l)], U (k x min(k,l), row-major, ld = min(k,l)), and optionally
+//   V (l x min(k,l), row-major) when V != nullptr (needs l*l + k*l <= 26624 doubles).
+// Columns with zero norm give zero singular vectors.
+int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, cudaStream_t st);
+
+// r = max(1, first index with sqrt(sum_{i>=r} S_i^2) <= budget) capped by
+// max_rank (<= 0: no cap) and by n; reference _truncation_rank (tt.py:203-211).
+int truncation_rank_dev(const double* S, int n, double budget, int max_rank, int* r_dev,
+                        cudaStream_t st);
+
+}  // namespace ttk

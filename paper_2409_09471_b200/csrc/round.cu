@@ -1,0 +1,323 @@
+// TT rounding drivers (host-orchestrated sequences of device kernels):
+//  * ttk_tt_round   -- TT-SVD (reference tt_round, tt.py:337-368): right-to-left
+//                      Householder-QR orthogonalisation sweep, then left-to-right
+//                      truncated SVDs (QR + Jacobi SVD of the small R factor).
+//  * ttk_rto_sweeps -- randomize-then-orthogonalize (absent from the reference,
+//                      SPEC.md:313; restated in oracle/ttoracle.py:rto_sweeps):
+//                      right partial contractions with a Gaussian TT-DRM, then
+//                      the left-to-right sketch / TSQR / project sweep.
+#include "gemm.cuh"
+#include "qr.cuh"
+#include "../../include/ttk_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+namespace ttk {
+
+namespace {
+
+constexpr size_t kSplitKBytes = 32u << 20;
+
+int gemm1(int M, int N, int K, const double* A, long long a_ms, long long a_ks, const double* B,
+          long long b_ks, long long b_ns, double* C, long long c_ms, long long c_ns, void* split_ws,
+          cudaStream_t st, double alpha = 1.0, double beta = 0.0) {
+  GemmProblem p = make_gemm(M, N, K, A, a_ms, a_ks, B, b_ks, b_ns, C, c_ms, c_ns, alpha, beta);
+  return gemm_group_launch(&p, 1, split_ws, split_ws ? kSplitKBytes : 0, st);
+}
+
+__global__ void sumsq_multi_kernel(const double* const* ptrs, const long long* sizes, double* out) {
+  __shared__ double red[32];
+  const double* x = ptrs[blockIdx.x];
+  const long long n = sizes[blockIdx.x];
+  double s = 0.0;
+  for (long long e = threadIdx.x; e < n; e += blockDim.x) s += x[e] * x[e];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) out[blockIdx.x] = v;
+  }
+}
+
+struct PinnedScratch {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      if (cudaMallocHost(&p, bytes) != cudaSuccess) { p = nullptr; cap = 0; return nullptr; }
+      cap = bytes;
+    }
+    return p;
+  }
+};
+thread_local PinnedScratch g_pinned;
+
+size_t core_elems(const int* dims, const int* ranks, int k) {
+  return (size_t)ranks[k] * dims[k] * ranks[k + 1];
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+// TT-SVD workspace plan
+static size_t round_ws_bytes(int d, const int* dims, const int* ranks) {
+  size_t sum = 0, mx = 0, qrws = 0;
+  int rmax = 1;
+  for (int k = 0; k < d; ++k) {
+    size_t e = core_elems(dims, ranks, k);
+    sum += align_up(e * 8, 256);
+    mx = std::max(mx, e);
+    rmax = std::max(rmax, std::max(ranks[k], ranks[k + 1]));
+  }
+  for (int k = 0; k < d; ++k) {
+    int r0 = ranks[k], r1 = ranks[k + 1], n = dims[k];
+    if (k > 0) qrws = std::max(qrws, tsqr_ws_bytes(n * r1, r0));
+    qrws = std::max(qrws, tsqr_ws_bytes(r0 * n, r1));
+  }
+  size_t small = (size_t)rmax * rmax;
+  return sum + 3 * align_up(mx * 8, 256) + 4 * align_up(small * 8, 256) + align_up(qrws, 256) +
+         kSplitKBytes + (size_t)(d + 8) * 256 + 65536 + 4096;
+}
+
+}  // namespace ttk
+
+using namespace ttk;
+
+extern "C" {
+
+size_t ttk_tt_round_ws_bytes(int d, const int* dims, const int* ranks) {
+  return round_ws_bytes(d, dims, ranks);
+}
+
+// TT-SVD rounding.  out[k] must hold ranks[k]*dims[k]*ranks[k+1] doubles (the
+// result never exceeds the input ranks); out_ranks (host, d+1) receives the
+// result ranks; result core k occupies the first out_ranks[k]*dims[k]*out_ranks[k+1]
+// entries of out[k], C-order.  max_rank <= 0: no cap.  zero_rel < 0 disables
+// the reference's cancellation test (tt.py:348-356).  Synchronises `stream`.
+int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* cores,
+                 double rel_tol, int max_rank, double zero_rel, double* const* out, int* out_ranks,
+                 void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TTK_REQUIRE(d >= 1, kInvalidValue, "tt_round: d must be >= 1");
+  TTK_REQUIRE(rel_tol >= 0.0, kInvalidValue, "rel_tol must be nonnegative");
+  for (int k = 0; k <= d; ++k) out_ranks[k] = ranks[k];
+  if (d == 1) {
+    TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cores[0], sizeof(double) * core_elems(dims, ranks, 0),
+                                   cudaMemcpyDeviceToDevice, st));
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    return kOk;
+  }
+  const size_t need = round_ws_bytes(d, dims, ranks);
+  TTK_REQUIRE(ws != nullptr && ws_bytes >= need, kWorkspace, "tt_round: workspace %zu < %zu", ws_bytes,
+              need);
+  Arena ar(ws, ws_bytes);
+  size_t mx = 0;
+  int rmax = 1;
+  for (int k = 0; k < d; ++k) {
+    mx = std::max(mx, core_elems(dims, ranks, k));
+    rmax = std::max(rmax, std::max(ranks[k], ranks[k + 1]));
+  }
+  std::vector<double*> wk(d);
+  for (int k = 0; k < d; ++k) wk[k] = ar.take<double>(core_elems(dims, ranks, k));
+  double* alt[2] = {ar.take<double>(mx), ar.take<double>(mx)};
+  double* tq = ar.take<double>(mx);
+  double* tR = ar.take<double>((size_t)rmax * rmax);
+  double* tU = ar.take<double>((size_t)rmax * rmax);
+  double* tS = ar.take<double>((size_t)rmax + 8);
+  double* tC = ar.take<double>((size_t)rmax * rmax);
+  double* red = ar.take<double>((size_t)d + 8);
+  double* part = ar.take<double>(256);
+  int* rdev = ar.take<int>(8);
+  const double** pdev = ar.take<const double*>((size_t)d);
+  long long* sdev = ar.take<long long>((size_t)d);
+  size_t qr_off = align_up(ar.used, 256);
+  size_t qr_bytes = 0;
+  for (int k = 0; k < d; ++k) {
+    int r0 = ranks[k], r1 = ranks[k + 1], n = dims[k];
+    if (k > 0) qr_bytes = std::max(qr_bytes, tsqr_ws_bytes(n * r1, r0));
+    qr_bytes = std::max(qr_bytes, tsqr_ws_bytes(r0 * n, r1));
+  }
+  void* qws = (char*)ws + qr_off;
+  ar.used = qr_off + qr_bytes;
+  void* split_ws = ar.take<char>(kSplitKBytes);
+  TTK_REQUIRE(split_ws != nullptr, kWorkspace, "tt_round: workspace too small");
+
+  double* pin = (double*)g_pinned.get(sizeof(double) * (d + 8));
+  TTK_REQUIRE(pin != nullptr, kCudaError, "tt_round: cannot allocate pinned scratch");
+
+  // optional zero test: prod_k ||C_k||_F of the INPUT cores
+  std::vector<int> r(ranks, ranks + d + 1);
+  double prod_norm = 1.0;
+  if (zero_rel >= 0.0) {
+    std::vector<const double*> hp(cores, cores + d);
+    std::vector<long long> hs(d);
+    for (int k = 0; k < d; ++k) hs[k] = (long long)core_elems(dims, ranks, k);
+    TTK_CHECK_CUDA(cudaMemcpyAsync(pdev, hp.data(), sizeof(double*) * d, cudaMemcpyHostToDevice, st));
+    TTK_CHECK_CUDA(cudaMemcpyAsync(sdev, hs.data(), sizeof(long long) * d, cudaMemcpyHostToDevice, st));
+    sumsq_multi_kernel<<<d, 256, 0, st>>>(pdev, sdev, red);
+    TTK_CHECK_LAUNCH();
+    TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double) * d, cudaMemcpyDeviceToHost, st));
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    for (int k = 0; k < d; ++k) prod_norm *= std::sqrt(pin[k]);
+  }
+
+  // ---- right-to-left orthogonalisation (tt.py:321-334) ----
+  for (int k = d - 1; k >= 1; --k) {
+    const double* ck = (k == d - 1) ? cores[k] : wk[k];
+    const int r0 = r[k], n = dims[k], r1 = r[k + 1];
+    const int m = n * r1, kk = std::min(m, r0);
+    // QR of C_k^T (m x r0): element (row=(i,b), col=a) at a*m + row
+    TTK_TRY(tsqr(m, r0, ck, 1, m, wk[k], 1, m, tR, qws, qr_bytes, st));
+    // new core k = Q^T reshaped (kk, n, r1): element (c, row) at c*m + row  -> written above
+    // C_{k-1} <- C_{k-1} x_3 R^T : new[a,i,c] = sum_b C_{k-1}[a,i,b] R[c,b]
+    // core k-1 is still the untouched input core at this point of the sweep
+    const double* cprev = cores[k - 1];
+    const int p0 = r[k - 1], pn = dims[k - 1];
+    TTK_TRY(gemm1(p0 * pn, kk, r0, cprev, r0, 1, tR, 1, r0, wk[k - 1], kk, 1, split_ws, st));
+    r[k] = kk;
+  }
+  // ---- norm / zero test ----
+  TTK_TRY(launch_sumsq(wk[0], (long long)r[0] * dims[0] * r[1], red, part, st));
+  TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  const double nrm = std::sqrt(pin[0]);
+  if (nrm == 0.0 || (zero_rel >= 0.0 && nrm <= zero_rel * prod_norm)) {
+    for (int k = 0; k < d; ++k) TTK_CHECK_CUDA(cudaMemsetAsync(out[k], 0, sizeof(double) * dims[k], st));
+    for (int k = 0; k <= d; ++k) out_ranks[k] = 1;
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    return kOk;
+  }
+  const double budget = rel_tol * nrm / std::sqrt((double)(d - 1));
+
+  // ---- left-to-right truncated SVD sweep (tt.py:358-367) ----
+  const double* cur = wk[0];
+  for (int k = 0; k < d - 1; ++k) {
+    const int r0 = r[k], n = dims[k], r1 = r[k + 1];
+    const int m = r0 * n, kk = std::min(m, r1);
+    // A = Q R (Q: m x kk in tq, R: kk x r1 in tR)
+    TTK_TRY(tsqr(m, r1, cur, r1, 1, tq, kk, 1, tR, qws, qr_bytes, st));
+    // R = U S V^T (U: kk x kk', S), kk' = min(kk, r1) = kk
+    TTK_TRY(jacobi_svd(kk, r1, tR, tU, tS, nullptr, st));
+    TTK_TRY(truncation_rank_dev(tS, kk, budget, max_rank, rdev, st));
+    TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    const int rk = *(int*)pin;
+    // out_k = Q U[:, :rk]  (m x rk)
+    TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], rk, 1, split_ws, st));
+    // carry = U[:, :rk]^T R  (rk x r1)
+    TTK_TRY(gemm1(rk, r1, kk, tU, 1, kk, tR, r1, 1, tC, r1, 1, split_ws, st));
+    // next core <- carry x_1 C_{k+1}: (rk x r1) (r1 x n' r2)
+    const int n1 = dims[k + 1], r2 = r[k + 2];
+    double* dst = alt[k & 1];
+    TTK_TRY(gemm1(rk, n1 * r2, r1, tC, r1, 1, wk[k + 1], (long long)n1 * r2, 1, dst,
+                  (long long)n1 * r2, 1, split_ws, st));
+    cur = dst;
+    r[k + 1] = rk;
+  }
+  TTK_CHECK_CUDA(cudaMemcpyAsync(out[d - 1], cur, sizeof(double) * (size_t)r[d - 1] * dims[d - 1],
+                                 cudaMemcpyDeviceToDevice, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
+  return kOk;
+}
+
+// --------------------------------------------------------------------------
+size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L) {
+  size_t wsum = 0, tmax = 0, ymax = 0, zmax = 0, qr = 0;
+  for (int c = 1; c < d; ++c) wsum += align_up((size_t)R[c] * L[c] * 8, 256);
+  for (int c = 1; c < d; ++c) {
+    tmax = std::max(tmax, (size_t)R[c] * dims[c] * L[c + 1]);
+    size_t m = (size_t)L[c - 1] * dims[c - 1];
+    ymax = std::max(ymax, m * L[c]);
+    zmax = std::max(zmax, (size_t)L[c] * dims[c] * R[c + 1]);
+    qr = std::max(qr, tsqr_ws_bytes((int)m, L[c]));
+  }
+  return wsum + align_up(tmax * 8, 256) + align_up(ymax * 8, 256) + 2 * align_up(zmax * 8, 256) +
+         align_up(qr, 256) + kSplitKBytes + 65536;
+}
+
+// Randomize-then-orthogonalize sweeps.  X: d cores (R[k], n_k, R[k+1]); G: DRM
+// cores (L[k], n_k, L[k+1]) with L[0] = L[d] = 1 and, for every cut c,
+// L[c] <= min(R[c], L[c-1] * n_{c-1}); out: d cores (L[k], n_k, L[k+1]).
+// Cores 0..d-2 of the result are left-orthonormal.
+int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X, const int* L,
+                   const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TTK_REQUIRE(d >= 1, kInvalidValue, "rto: d must be >= 1");
+  TTK_REQUIRE(R[0] == 1 && R[d] == 1 && L[0] == 1 && L[d] == 1, kShapeMismatch,
+              "rto: boundary ranks must equal 1");
+  if (d == 1) {
+    TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], X[0], sizeof(double) * dims[0], cudaMemcpyDeviceToDevice, st));
+    return kOk;
+  }
+  for (int c = 1; c < d; ++c) {
+    TTK_REQUIRE(L[c] >= 1 && L[c] <= R[c] && L[c] <= L[c - 1] * dims[c - 1], kInvalidValue,
+                "rto: sketch rank L[%d]=%d must lie in [1, min(R=%d, L[c-1]*n=%d)]", c, L[c], R[c],
+                L[c - 1] * dims[c - 1]);
+  }
+  const size_t need = ttk_rto_ws_bytes(d, dims, R, L);
+  TTK_REQUIRE(ws != nullptr && ws_bytes >= need, kWorkspace, "rto: workspace %zu < %zu", ws_bytes, need);
+  Arena ar(ws, ws_bytes);
+  std::vector<double*> W(d + 1, nullptr);
+  for (int c = 1; c < d; ++c) W[c] = ar.take<double>((size_t)R[c] * L[c]);
+  size_t tmax = 0, ymax = 0, zmax = 0, qrb = 0;
+  for (int c = 1; c < d; ++c) {
+    tmax = std::max(tmax, (size_t)R[c] * dims[c] * L[c + 1]);
+    size_t m = (size_t)L[c - 1] * dims[c - 1];
+    ymax = std::max(ymax, m * L[c]);
+    zmax = std::max(zmax, (size_t)L[c] * dims[c] * R[c + 1]);
+    qrb = std::max(qrb, tsqr_ws_bytes((int)m, L[c]));
+  }
+  double* T = ar.take<double>(tmax);
+  double* Y = ar.take<double>(ymax);
+  double* Z0 = ar.take<double>(zmax);
+  double* Z1 = ar.take<double>(zmax);
+  size_t qoff = align_up(ar.used, 256);
+  void* qws = (char*)ws + qoff;
+  ar.used = qoff + qrb;
+  void* split_ws = ar.take<char>(kSplitKBytes);
+  TTK_REQUIRE(split_ws != nullptr, kWorkspace, "rto: workspace too small");
+
+  // ---- right sweep: W_c = sum_i X_c[:, i, :] W_{c+1} G_c[:, i, :]^T ----
+  for (int c = d - 1; c >= 1; --c) {
+    const int n = dims[c], rc = R[c], lc = L[c], l1 = L[c + 1], r1 = R[c + 1];
+    const double* Tin;
+    if (c == d - 1) {
+      Tin = X[c];  // (R_c, n, 1): W_d = [[1]]
+    } else {
+      // T (R_c n x L_{c+1}) = X_c (R_c n x R_{c+1}) W_{c+1} (R_{c+1} x L_{c+1})
+      TTK_TRY(gemm1(rc * n, l1, r1, X[c], r1, 1, W[c + 1], l1, 1, T, l1, 1, split_ws, st));
+      Tin = T;
+    }
+    // W_c (R_c x L_c) = T (R_c x n L_{c+1}) G_c^T ; G_c viewed (L_c x n L_{c+1})
+    const long long K = (long long)n * l1;
+    TTK_TRY(gemm1(rc, lc, (int)K, Tin, K, 1, G[c], 1, K, W[c], lc, 1, split_ws, st));
+  }
+  // ---- left sweep ----
+  const double* Z = X[0];  // (L_0 n_0 x R_1) = (n_0 x R_1)
+  double* Zbuf[2] = {Z0, Z1};
+  for (int c = 1; c < d; ++c) {
+    const int np = dims[c - 1];
+    const int m = L[c - 1] * np, l = L[c], rc = R[c];
+    // Y (m x l) = Z (m x R_c) W_c (R_c x l)
+    TTK_TRY(gemm1(m, l, rc, Z, rc, 1, W[c], l, 1, Y, l, 1, split_ws, st));
+    // Q (m x l) -> out core c-1, (L_{c-1}, n_{c-1}, L_c)
+    TTK_TRY(tsqr(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st));
+    // M (l x R_c) = Q^T Z   (K = m, split over the long dimension)
+    TTK_TRY(gemm1(l, rc, m, out[c - 1], 1, l, Z, rc, 1, Y, rc, 1, split_ws, st));
+    // Z' (l x n_c R_{c+1}) = M X_c
+    const int n = dims[c], r1 = R[c + 1];
+    double* dst = (c == d - 1) ? out[d - 1] : Zbuf[c & 1];
+    TTK_TRY(gemm1(l, n * r1, rc, Y, rc, 1, X[c], (long long)n * r1, 1, dst, (long long)n * r1, 1,
+                  split_ws, st));
+    Z = dst;
+  }
+  return kOk;
+}
+
+}  // extern "C"

@@ -47,8 +47,10 @@ __global__ void concat_kernel(const __grid_constant__ ConcatParams P) {
     if (C.kind == 3) {  // d == 1: elementwise sum, reference order ((t0 + c1 t1) + c2 t2)...
       for (int col = lane; col < C.R1; col += 32) {
         double acc = P.coeff[0] == 1.0 ? C.in[0][(long long)i * C.R1 + col]
-                                       : P.coeff[0] * C.in[0][(long long)i * C.R1 + col];
-        for (int t = 1; t < P.nterms; ++t) acc += P.coeff[t] * C.in[t][(long long)i * C.R1 + col];
+                                       : __dmul_rn(P.coeff[0], C.in[0][(long long)i * C.R1 + col]);
+        // separate multiply and add (no FMA contraction): bit-exact with numpy
+        for (int t = 1; t < P.nterms; ++t)
+          acc = __dadd_rn(acc, __dmul_rn(P.coeff[t], C.in[t][(long long)i * C.R1 + col]));
         dst[col] = acc;
       }
       continue;

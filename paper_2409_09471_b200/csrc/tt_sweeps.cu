@@ -94,3 +94,109 @@ int ttk_tt_dots(int d, const int* dims, const int* xr, const double* const* x, i
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// stream_sketch (reference streaming.py:214-239).  Left partial contractions
+// L_{k+1} = Y_k^T (L_k x_1 C_k) and right partial contractions
+// R_k = (C_k x_3 R_{k+1}) X_k^T run as two independent chains; step j of the
+// left chain and step j of the right chain share one grouped GEMM launch.
+// Then every Psi_mu = (L_mu C_mu) R_{mu+1} and Omega_mu = L_mu R_mu is formed
+// with grouped launches.
+extern "C" {
+
+size_t ttk_stream_sketch_ws_bytes(int d, const int* dims, const int* tr, const int* lr, const int* rr) {
+  size_t tot = 0;
+  for (int k = 0; k <= d; ++k) {
+    tot += align_up((size_t)lr[k] * tr[k] * 8, 256);  // L_k (l_k x t_k)
+    tot += align_up((size_t)tr[k] * rr[k] * 8, 256);  // R_k (t_k x r_k)
+  }
+  size_t tmax = 0;
+  for (int k = 0; k < d; ++k) {
+    tmax = std::max(tmax, (size_t)lr[k] * dims[k] * tr[k + 1]);
+    tmax = std::max(tmax, (size_t)tr[k] * dims[k] * rr[k + 1]);
+  }
+  // two chain temporaries + d psi temporaries
+  size_t tsum = 0;
+  for (int k = 0; k < d; ++k) tsum += align_up((size_t)lr[k] * dims[k] * tr[k + 1] * 8, 256);
+  return tot + 2 * align_up(tmax * 8, 256) + tsum + (16u << 20) + 65536;
+}
+
+// psi[mu]: (lr[mu]*dims[mu]) x rr[mu+1]; omega[mu-1]: lr[mu] x rr[mu] for mu=1..d-1.
+// tr: ranks of the sketched TT (d+1); lr / rr: ranks of the left (Y) and right (X) DRMs.
+int ttk_stream_sketch(int d, const int* dims, const int* tr, const double* const* C, const int* lr,
+                      const double* const* Y, const int* rr, const double* const* X,
+                      double* const* psi, double* const* omega, void* ws, size_t ws_bytes,
+                      void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TTK_REQUIRE(d >= 1, kInvalidValue, "stream_sketch: d must be >= 1");
+  const size_t need = ttk_stream_sketch_ws_bytes(d, dims, tr, lr, rr);
+  TTK_REQUIRE(ws != nullptr && ws_bytes >= need, kWorkspace, "stream_sketch: workspace %zu < %zu",
+              ws_bytes, need);
+  Arena ar(ws, ws_bytes);
+  std::vector<double*> L(d + 1), R(d + 1);
+  for (int k = 0; k <= d; ++k) {
+    L[k] = ar.take<double>((size_t)lr[k] * tr[k]);
+    R[k] = ar.take<double>((size_t)tr[k] * rr[k]);
+  }
+  size_t tmax = 0;
+  for (int k = 0; k < d; ++k) {
+    tmax = std::max(tmax, (size_t)lr[k] * dims[k] * tr[k + 1]);
+    tmax = std::max(tmax, (size_t)tr[k] * dims[k] * rr[k + 1]);
+  }
+  double* TL = ar.take<double>(tmax);
+  double* TR = ar.take<double>(tmax);
+  std::vector<double*> TP(d);
+  for (int k = 0; k < d; ++k) TP[k] = ar.take<double>((size_t)lr[k] * dims[k] * tr[k + 1]);
+  void* split_ws = ar.take<char>(16u << 20);
+  TTK_REQUIRE(split_ws != nullptr, kWorkspace, "stream_sketch: workspace too small");
+  const double one = 1.0;
+  TTK_CHECK_CUDA(cudaMemcpyAsync(L[0], &one, sizeof(double), cudaMemcpyHostToDevice, st));
+  TTK_CHECK_CUDA(cudaMemcpyAsync(R[d], &one, sizeof(double), cudaMemcpyHostToDevice, st));
+  // chains: step s of the left chain computes L_{s+1}; of the right chain R_{d-1-s}
+  for (int s = 0; s < d - 1; ++s) {
+    GemmProblem pr[2];
+    int np = 0;
+    {  // left: T = L_k (l x t) C_k (t x n t')  -> (l, n, t')
+      const int k = s, l = lr[k], t = tr[k], n = dims[k], t1 = tr[k + 1];
+      pr[np++] = make_gemm(l, n * t1, t, L[k], t, 1, C[k], (long long)n * t1, 1, TL, (long long)n * t1, 1);
+    }
+    {  // right: T = C_k (t n x t') R_{k+1} (t' x r')  -> (t, n, r')
+      const int k = d - 1 - s, t = tr[k], n = dims[k], t1 = tr[k + 1], r1 = rr[k + 1];
+      pr[np++] = make_gemm(t * n, r1, t1, C[k], t1, 1, R[k + 1], r1, 1, TR, r1, 1);
+    }
+    TTK_TRY(gemm_group_launch(pr, np, split_ws, 16u << 20, st));
+    np = 0;
+    {  // L_{k+1} (l' x t') = Y_k^T (l' x l n) T (l n x t')
+      const int k = s, l = lr[k], n = dims[k], t1 = tr[k + 1], l1 = lr[k + 1];
+      pr[np++] = make_gemm(l1, t1, l * n, Y[k], 1, l1, TL, t1, 1, L[k + 1], t1, 1);
+    }
+    {  // R_k (t x r) = T (t x n r') X_k^T (n r' x r)
+      const int k = d - 1 - s, t = tr[k], n = dims[k], r1 = rr[k + 1], r = rr[k];
+      const long long K = (long long)n * r1;
+      pr[np++] = make_gemm(t, r, (int)K, TR, K, 1, X[k], 1, K, R[k], r, 1);
+    }
+    TTK_TRY(gemm_group_launch(pr, np, split_ws, 16u << 20, st));
+  }
+  // Psi_mu = (L_mu C_mu) R_{mu+1}: two grouped launches over mu
+  std::vector<GemmProblem> pp(d);
+  for (int mu = 0; mu < d; ++mu) {
+    const int l = lr[mu], t = tr[mu], n = dims[mu], t1 = tr[mu + 1];
+    pp[mu] = make_gemm(l, n * t1, t, L[mu], t, 1, C[mu], (long long)n * t1, 1, TP[mu], (long long)n * t1, 1);
+  }
+  TTK_TRY(gemm_group_launch(pp.data(), d, split_ws, 16u << 20, st));
+  for (int mu = 0; mu < d; ++mu) {
+    const int l = lr[mu], n = dims[mu], t1 = tr[mu + 1], r1 = rr[mu + 1];
+    pp[mu] = make_gemm(l * n, r1, t1, TP[mu], t1, 1, R[mu + 1], r1, 1, psi[mu], r1, 1);
+  }
+  TTK_TRY(gemm_group_launch(pp.data(), d, split_ws, 16u << 20, st));
+  if (d > 1) {
+    std::vector<GemmProblem> po(d - 1);
+    for (int mu = 1; mu < d; ++mu)
+      po[mu - 1] = make_gemm(lr[mu], rr[mu], tr[mu], L[mu], tr[mu], 1, R[mu], rr[mu], 1, omega[mu - 1],
+                             rr[mu], 1);
+    TTK_TRY(gemm_group_launch(po.data(), d - 1, split_ws, 16u << 20, st));
+  }
+  return kOk;
+}
+
+}  // extern "C"

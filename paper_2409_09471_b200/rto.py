@@ -1,0 +1,107 @@
+"""Randomize-then-orthogonalize TT rounding on the B200.
+
+Absent from the reference (SPEC.md:313 lists it as a non-goal); restated from
+PAPER.md:435-445 and SURVEY.md Appendix B, with the CPU restatement in
+oracle/ttoracle.py (rto_sweeps / rto_round) as the checker:
+
+  1. right partial contractions W_c = X_{>=c}^T G_{>=c} with a Gaussian TT-DRM
+     G (streaming.py:133-136 recurrence), two chained DMMA GEMMs per core;
+  2. left-to-right: Y_c = Z_c W_c, Q_c = TSQR(Y_c) (explicit Householder Q),
+     M_c = Q_c^T Z_c, Z_{c+1} = M_c x_1 X_c;
+  3. TT-SVD truncation (tt_round) of the left-orthogonal result.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .errors import ShapeMismatch
+from .streaming import TTDRM, tt_drm_new
+from .tt import RoundSpec, TTVector, attainable_ranks, tt_round
+
+
+def rto_ranks(dims, in_ranks, ell):
+    """Sketch ranks l_c (c = 1..d-1): min(ell_c, R_c, attainable), then
+    l_c <= l_{c-1} n_{c-1} so every QR is tall (oracle.rto_ranks)."""
+    d = len(dims)
+    if isinstance(ell, int):
+        ell = [ell] * (d - 1)
+    ls = [int(min(e, r)) for e, r in zip(ell, in_ranks[1:-1])]
+    ls = attainable_ranks(list(dims), ls)
+    prev = 1
+    for c in range(d - 1):
+        ls[c] = max(1, min(ls[c], prev * dims[c]))
+        prev = ls[c]
+    return ls
+
+
+def rto_flops(dims, in_ranks, ls) -> float:
+    """Algorithmic FLOPs of the two sweeps (QR counted as 4ml^2 - 4l^3/3)."""
+    d = len(dims)
+    L = [1] + list(ls) + [1]
+    R = list(in_ranks)
+    f = 0.0
+    for c in range(d - 1, 0, -1):
+        f += 2.0 * R[c] * dims[c] * R[c + 1] * L[c + 1] + 2.0 * R[c] * dims[c] * L[c + 1] * L[c]
+    for c in range(1, d):
+        m, l = L[c - 1] * dims[c - 1], L[c]
+        f += 2.0 * m * R[c] * l + (4.0 * m * l * l - 4.0 * l ** 3 / 3.0) + 2.0 * l * m * R[c]
+        f += 2.0 * l * R[c] * dims[c] * R[c + 1]
+    return f
+
+
+def _drm_slices(drm_cores, ls, device):
+    full = [1] + list(ls) + [1]
+    out = []
+    for k, g in enumerate(drm_cores):
+        if g.shape[0] < full[k] or g.shape[2] < full[k + 1]:
+            raise ShapeMismatch(f"DRM core {k} of shape {tuple(g.shape)} is smaller than the sketch ranks")
+        s = g[: full[k], :, : full[k + 1]]
+        out.append(s if s.is_contiguous() else s.contiguous())
+    return out
+
+
+def rto_sweeps(v: TTVector, drm) -> TTVector:
+    """Left-orthogonal TT with the DRM's ranks (clamped by rto_ranks)."""
+    if isinstance(drm, TTDRM):
+        drm = drm.cores
+    if tuple(int(g.shape[1]) for g in drm) != v.dims:
+        raise ShapeMismatch("DRM dims do not match the vector")
+    d = v.d
+    _lib.require_cuda(v.cores[0], "TT vector")
+    if d == 1:
+        return v.copy()
+    ls = rto_ranks(v.dims, v.ranks, [int(g.shape[2]) for g in drm[:-1]])
+    G = _drm_slices(drm, ls, v.device)
+    lib = _lib.load()
+    dev = v.device
+    L = [1] + ls + [1]
+    out = [torch.empty((L[k], v.dims[k], L[k + 1]), dtype=torch.float64, device=dev) for k in range(d)]
+    dims = _lib.int_array(v.dims)
+    R = _lib.int_array(v.ranks)
+    Lc = _lib.int_array(L)
+    ws = _lib.workspace(lib.ttk_rto_ws_bytes(d, dims, R, Lc), dev)
+    _lib.check(lib.ttk_rto_sweeps(d, dims, R, _lib.ptr_array(v.cores), Lc, _lib.ptr_array(G),
+                                  _lib.ptr_array(out), ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)))
+    return TTVector(out)
+
+
+def tt_round_rto(v: TTVector, spec: RoundSpec, ell=None, drm=None, seed=0,
+                 zero_rel: float | None = None) -> TTVector:
+    """Randomized rounding: RTO sweeps at sketch rank ``ell`` (or with the
+    given DRM), then TT-SVD truncation to ``spec``.
+
+    ell defaults to max_rank + 20 (oversampling as in the reference's
+    StreamFrame, streaming.py:175).  The DRM is drawn on the host with
+    tt_drm_new(dims, l, seed) so CPU and GPU see identical sketches."""
+    if drm is None:
+        if ell is None:
+            if spec.max_rank is None:
+                raise ValueError("tt_round_rto needs ell, drm or spec.max_rank")
+            ell = spec.max_rank + 20
+        ls = rto_ranks(v.dims, v.ranks, ell)
+        drm = tt_drm_new(v.dims, ls, seed=seed, device=v.device)
+    return tt_round(rto_sweeps(v, drm), spec, zero_rel=zero_rel)

@@ -369,3 +369,49 @@ def tt_dot(a: TTVector, b: TTVector) -> float:
 def tt_norm(a: TTVector) -> float:
     """Frobenius norm of the denoted tensor (tt.py:297-299)."""
     return float(math.sqrt(max(tt_dot(a, a), 0.0)))
+
+
+# ---------------------------------------------------------------------------
+# rounding (tt.py:203-211, 321-368)
+
+
+def tt_round(v: TTVector, spec: RoundSpec, zero_rel: float | None = ZERO_REL) -> TTVector:
+    """TT-SVD recompression on the device (tt.py:337-368).
+
+    Right-to-left Householder-QR sweep, then left-to-right truncated SVDs with
+    the per-mode budget rel_tol*||v||/sqrt(d-1) and the max_rank cap.
+    ``zero_rel`` keeps the reference's cancellation test (tt.py:348-356);
+    pass None to disable it (reference quirk Q1: the test fires on every
+    BASELINE-size input)."""
+    d = v.d
+    if d == 1:
+        return v.copy()
+    _check_cuda_vec(v)
+    lib = _lib.load()
+    dev = v.device
+    dims = _lib.int_array(v.dims)
+    ranks = _lib.int_array(v.ranks)
+    outs = [torch.empty(max(c.numel(), c.shape[1]), dtype=torch.float64, device=dev) for c in v.cores]
+    out_ranks = (_lib.ctypes.c_int * (d + 1))()
+    ws = _lib.workspace(lib.ttk_tt_round_ws_bytes(d, dims, ranks), dev)
+    _lib.check(lib.ttk_tt_round(d, dims, ranks, _lib.ptr_array(v.cores), float(spec.rel_tol),
+                                int(spec.max_rank or 0), -1.0 if zero_rel is None else float(zero_rel),
+                                _lib.ptr_array(outs), out_ranks, ws.data_ptr(), ws.numel(),
+                                _lib.stream_ptr(dev)))
+    r = list(out_ranks)
+    cores = [outs[k][: r[k] * v.dims[k] * r[k + 1]].view(r[k], v.dims[k], r[k + 1]) for k in range(d)]
+    return TTVector(cores)
+
+
+def tt_norm_left_orthogonal(v: TTVector) -> float:
+    """||v|| of a TT whose cores 0..d-2 are left-orthonormal (the output of
+    tt_round / rto_sweeps): the Frobenius norm of the last core, one fixed-order
+    device reduction instead of a full dot sweep."""
+    _check_cuda_vec(v)
+    lib = _lib.load()
+    c = v.cores[-1]
+    out = torch.empty(1, dtype=torch.float64, device=v.device)
+    ws = _lib.workspace(4096, v.device)
+    _lib.check(lib.ttk_sumsq(c.data_ptr(), c.numel(), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                             _lib.stream_ptr(v.device)))
+    return float(math.sqrt(max(out.item(), 0.0)))

@@ -1,0 +1,193 @@
+"""GPU parity of the factorisations (TSQR, Jacobi SVD), TT-SVD rounding,
+randomize-then-orthogonalize rounding and the streaming sketches."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2409_09471_b200 as T
+from paper_2409_09471_b200 import _lib
+from golden_io import cores, load
+
+pytestmark = pytest.mark.gpu
+
+
+def tt_np(v):
+    return [c.cpu().numpy() for c in v.cores]
+
+
+def run_qr(A, cuda, transposed=False):
+    lib = _lib.load()
+    m, l = A.shape
+    k = min(m, l)
+    if transposed:
+        At = torch.as_tensor(np.ascontiguousarray(A.T), device=cuda)
+        a_rs, a_cs = 1, m
+    else:
+        At = torch.as_tensor(A, device=cuda)
+        a_rs, a_cs = l, 1
+    Q = torch.empty((m, k), dtype=torch.float64, device=cuda)
+    R = torch.empty((k, l), dtype=torch.float64, device=cuda)
+    ws = _lib.workspace(lib.ttk_qr_ws_bytes(m, l), cuda)
+    _lib.check(lib.ttk_qr(m, l, At.data_ptr(), a_rs, a_cs, Q.data_ptr(), k, 1, R.data_ptr(), ws.data_ptr(),
+                          ws.numel(), _lib.stream_ptr(cuda)))
+    return Q.cpu().numpy(), R.cpu().numpy()
+
+
+@pytest.mark.parametrize("m,l", [(10240, 80), (3200, 50), (100000, 16), (500, 112), (7, 3), (3, 7),
+                                 (64, 64), (25600, 100), (1, 1), (300, 1)])
+def test_tsqr_orthonormal_and_exact(cuda, m, l):
+    rng = np.random.default_rng(m + l)
+    A = rng.standard_normal((m, l))
+    Q, R = run_qr(A, cuda)
+    k = min(m, l)
+    assert np.abs(Q.T @ Q - np.eye(k)).max() <= 1e-13 * max(l, 1) ** 0.5 * 10
+    assert np.linalg.norm(Q @ R - A) <= 1e-13 * np.linalg.norm(A) * max(1, np.log2(m))
+    assert np.allclose(np.tril(R, -1), 0.0)
+
+
+def test_tsqr_rank_deficient_and_zero(cuda):
+    rng = np.random.default_rng(1)
+    B = rng.standard_normal((5000, 5))
+    A = np.concatenate([B, B @ rng.standard_normal((5, 35)), np.zeros((5000, 10))], axis=1)  # rank 5 of 50
+    Q, R = run_qr(A, cuda)
+    assert np.abs(Q.T @ Q - np.eye(50)).max() <= 1e-12
+    assert np.linalg.norm(Q @ R - A) <= 1e-13 * np.linalg.norm(A) * 10
+    Z = np.zeros((900, 20))
+    Q, R = run_qr(Z, cuda)
+    assert np.abs(Q.T @ Q - np.eye(20)).max() <= 1e-14
+    assert np.all(R == 0)
+
+
+def test_tsqr_transposed_input(cuda):
+    rng = np.random.default_rng(2)
+    A = rng.standard_normal((4096, 37))
+    Q, R = run_qr(A, cuda, transposed=True)
+    assert np.linalg.norm(Q @ R - A) <= 1e-13 * np.linalg.norm(A) * 12
+
+
+@pytest.mark.parametrize("k,l", [(80, 80), (50, 50), (128, 128), (10, 30), (60, 40), (1, 5), (7, 1)])
+def test_jacobi_svd(cuda, k, l):
+    lib = _lib.load()
+    rng = np.random.default_rng(k * 7 + l)
+    # graded singular values down to 1e-13: one-sided Jacobi keeps relative accuracy
+    U0, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    V0, _ = np.linalg.qr(rng.standard_normal((l, l)))
+    kn = min(k, l)
+    s0 = np.logspace(0, -13, kn)
+    B = (U0[:, :kn] * s0) @ V0[:, :kn].T
+    Bt = torch.as_tensor(B, device=cuda)
+    U = torch.empty((k, kn), dtype=torch.float64, device=cuda)
+    S = torch.empty(kn, dtype=torch.float64, device=cuda)
+    want_v = k * l + l * l <= 26000
+    V = torch.empty((l, kn), dtype=torch.float64, device=cuda) if want_v else None
+    _lib.check(lib.ttk_svd_small(k, l, Bt.data_ptr(), U.data_ptr(), S.data_ptr(),
+                                 V.data_ptr() if V is not None else None, _lib.stream_ptr(cuda)))
+    S, U = S.cpu().numpy(), U.cpu().numpy()
+    np.testing.assert_allclose(S, np.linalg.svd(B, compute_uv=False)[:kn], rtol=1e-9, atol=1e-15)
+    assert np.all(np.diff(S) <= 0)
+    if V is not None:
+        V = V.cpu().numpy()
+        assert np.linalg.norm((U * S) @ V.T - B) <= 1e-13 * np.linalg.norm(B) * 10
+
+
+def test_tt_round_golden(cuda):
+    z = load("tt_ops.npz")
+    for name in z["rd_names"]:
+        tol, cap = z[f"{name}_spec"]
+        cap = None if cap < 0 else int(cap)
+        v = T.TTVector(cores(z, f"{name}_x"), device=cuda)
+        r = T.tt_round(v, T.RoundSpec(float(tol), cap))
+        assert r.ranks == tuple(z[f"{name}_ranks"]), name
+        want = z[f"{name}_dense"]
+        got = T.tt_to_dense(r).cpu().numpy()
+        assert np.linalg.norm(got - want) <= 1e-12 * max(np.linalg.norm(want), 1.0), name
+
+
+@pytest.mark.parametrize("tol,cap", [(1e-8, None), (1e-3, None), (0.0, 12), (1e-10, 25)])
+def test_tt_round_vs_oracle(cuda, tol, cap):
+    dims = [12, 9, 16, 7, 11, 10]
+    a = O.tt_random(dims, [8, 14, 10, 9, 6], seed=3)
+    b = O.tt_random(dims, [5, 6, 12, 7, 4], seed=4)
+    x = O.add(a, O.scale(O.add(a, b), 0.5))  # redundant ranks
+    want = O.tt_round(x, tol, cap, zero_rel=None)
+    got = T.tt_round(T.TTVector(x, device=cuda), T.RoundSpec(tol, cap), zero_rel=None)
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.rel_diff(tt_np(got), want) <= 1e-10
+
+
+def test_rto_exactness_kat(cuda):
+    """l >= true rank => RTO is exact (the RTO known-answer test)."""
+    dims = [6, 6, 6, 6, 6]
+    x = O.tt_random(dims, [3, 5, 4, 2], seed=11)
+    big = O.add(x, O.scale(x, 0.25))  # rank doubled, true rank unchanged
+    drm = O.drm_new(dims, [7, 7, 7, 7], seed=5)
+    ls = O.rto_ranks(dims, [1] + [c.shape[2] for c in big], [7, 7, 7, 7])
+    got = T.rto_sweeps(T.TTVector(big, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm])
+    assert got.ranks == tuple([1] + ls + [1])
+    assert O.rel_diff(tt_np(got), O.scale(x, 1.25)) <= 1e-12
+    # left-orthonormal cores
+    for c in tt_np(got)[:-1]:
+        q = c.reshape(-1, c.shape[2])
+        assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-13
+
+
+def test_rto_vs_oracle(cuda):
+    dims = [16, 12, 20, 16, 10, 14]
+    x = O.tt_random(dims, [30, 40, 40, 30, 14], seed=21)
+    drm = O.drm_new(dims, [18, 25, 25, 18, 10], seed=9)
+    ls = O.rto_ranks(dims, [1] + [c.shape[2] for c in x], [18, 25, 25, 18, 10])
+    want = O.rto_sweeps(x, O.slice_drm(drm, ls))
+    got = T.rto_sweeps(T.TTVector(x, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm])
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.rel_diff(tt_np(got), want) <= 1e-10
+    # full randomized rounding (sweeps + truncation)
+    want_r = O.rto_round(x, O.slice_drm(drm, ls), 1e-6, 15)
+    got_r = T.tt_round(got, T.RoundSpec(1e-6, 15), zero_rel=None)
+    assert got_r.ranks == tuple([1] + [c.shape[2] for c in want_r])
+    assert O.rel_diff(tt_np(got_r), want_r) <= 1e-10
+
+
+def test_rto_config2_shape(cuda):
+    """BASELINE config 2 structure at d=6 (rank-200 sum of 10 rank-20 TTs, l=50, cap 40)."""
+    d, n = 6, 64
+    rng = np.random.default_rng(0)
+    terms = [O.gaussian_tt([n] * d, [20] * (d - 1), rng, 1 / np.sqrt(n * 20)) for _ in range(10)]
+    x = terms[0]
+    for t in terms[1:]:
+        x = O.add(x, t)
+    drm = O.drm_new([n] * d, [50] * (d - 1), seed=1)
+    want = O.rto_round(x, drm, 0.0, 40)
+    got = T.tt_round_rto(T.TTVector(x, device=cuda), T.RoundSpec(0.0, 40),
+                         drm=[torch.as_tensor(g, device=cuda) for g in drm])
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.rel_diff(tt_np(got), want) <= 1e-10
+
+
+def test_stream_sketch_and_recover_golden(cuda):
+    z = load("streaming.npz")
+    to = lambda cs: [torch.as_tensor(c, device=cuda) for c in cs]  # noqa: E731
+    left = T.TTDRM([3, 4, 3], [1, 5, 5, 1], to(cores(z, "ss_left")))
+    right = T.TTDRM([3, 4, 3], [1, 2, 2, 1], to(cores(z, "ss_right")))
+    frame = T.StreamFrame(right, left)
+    pair = T.stream_sketch(T.TTVector(cores(z, "ss_x"), device=cuda), frame)
+    for k, p in enumerate(pair.psi):
+        np.testing.assert_allclose(p.cpu().numpy(), z[f"ss_psi__{k}"], rtol=0, atol=1e-13)
+    for k, o in enumerate(pair.omega):
+        np.testing.assert_allclose(o.cpu().numpy(), z[f"ss_omega__{k}"], rtol=0, atol=1e-13)
+    lc, rc = cores(z, "rc_left"), cores(z, "rc_right")
+    frame = T.StreamFrame(T.TTDRM([4] * 4, [1] + [c.shape[2] for c in rc], to(rc)),
+                          T.TTDRM([4] * 4, [1] + [c.shape[2] for c in lc], to(lc)))
+    pairs = [T.stream_sketch(T.TTVector(cores(z, f"rc_v{i}"), device=cuda), frame) for i in range(5)]
+    got = T.stream_recover(T.combine_pairs(pairs, list(z["rc_y"])), T.RoundSpec(1e-12))
+    assert got.ranks == tuple(z["rc_ranks"])
+    want = z["rc_dense"]
+    assert np.linalg.norm(T.tt_to_dense(got).cpu().numpy() - want) <= 1e-10 * np.linalg.norm(want)
+
+
+def test_frame_create_matches_reference_draws(cuda):
+    z = load("streaming.npz")
+    f = T.StreamFrame.create([3, 4, 3], [2, 2], oversampling=3, seed=6, device=cuda)
+    for a, b in zip(f.left.cores + f.right.cores, cores(z, "ss_left") + cores(z, "ss_right")):
+        assert np.array_equal(a.cpu().numpy(), b)

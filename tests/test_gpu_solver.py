@@ -1,0 +1,103 @@
+"""GPU TT-sGMRES against the reference's own solver histories (golden) and the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2409_09471_b200 as T
+from golden_io import cores, factors, load
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg_from(z, name, **extra):
+    c = z[f"{name}_cfg"]
+    return T.SolverConfig(maxit=int(c[0]), tol=float(c[1]), ell=int(c[2]), eta=float(c[3]),
+                          max_rank=None if c[4] < 0 else int(c[4]), sketch_rows=int(c[5]),
+                          oversampling=int(c[6]), solution_rank=None if c[7] < 0 else int(c[7]),
+                          seed=int(c[8]), combine_mode="stta" if c[9] else "explicit", **extra)
+
+
+def probe(x):
+    f = O.kr_factors_new(list(x.dims), 24, seed=777)
+    return O.kr_apply(f, [c.cpu().numpy() for c in x.cores])
+
+
+@pytest.mark.parametrize("name", ["sv_pde", "sv_ell2", "sv_stta"])
+def test_solver_small_golden(cuda, name):
+    z = load("solver_small.npz")
+    cfg = cfg_from(z, name)
+    a = T.TTOperator(cores(z, f"{name}_op"), device=cuda)
+    b = T.TTVector(cores(z, f"{name}_b"), device=cuda)
+    s = T.KhatriRaoSketch(factors(z, name), device=cuda)
+    x, rep = T.tt_sgmres(a, b, None, cfg, s)
+    assert rep.iterations == int(z[f"{name}_iters"])
+    assert rep.converged == bool(z[f"{name}_conv"])
+    assert rep.basis_rank == list(z[f"{name}_ranks"])
+    np.testing.assert_allclose(rep.res_sketched, z[f"{name}_res"], rtol=1e-6)
+    want = z[f"{name}_xprobe"]
+    assert np.linalg.norm(probe(x) - want) <= 1e-7 * np.linalg.norm(want)
+    assert len(rep.times["round"]) == rep.iterations
+
+
+def test_solver_config1_golden(cuda):
+    """BASELINE config 1 (d=8, n=32, maxit 40) vs the reference run with the Q1 test bypassed."""
+    z = load("solver_cfg1.npz")
+    cfg = cfg_from(z, "cfg1", zero_rel=None)
+    a = T.TTOperator(cores(z, "cfg1_op"), device=cuda)
+    b = T.TTVector(cores(z, "cfg1_b"), device=cuda)
+    s = T.KhatriRaoSketch(factors(z, "cfg1"), device=cuda)
+    frame = T.make_solver_frame(b, cfg, seed=1)
+    x, rep = T.tt_sgmres(a, b, None, cfg, s, frame)
+    assert rep.iterations == int(z["cfg1_iters"])
+    assert rep.basis_rank == list(z["cfg1_ranks"])
+    np.testing.assert_allclose(rep.res_sketched, z["cfg1_res"], rtol=1e-8)
+    want = z["cfg1_xprobe"]
+    assert np.linalg.norm(probe(x) - want) <= 1e-8 * np.linalg.norm(want)
+
+
+def test_solver_config1_rto_vs_oracle(cuda):
+    """Randomized-rounding mode: identical iteration count and rank history,
+    residual history within 1e-8 relative of the CPU oracle."""
+    z = load("solver_cfg1.npz")
+    cfg = cfg_from(z, "cfg1", zero_rel=None, rounding="rto")
+    a_np, b_np, f_np = cores(z, "cfg1_op"), cores(z, "cfg1_b"), factors(z, "cfg1")
+    a = T.TTOperator(a_np, device=cuda)
+    b = T.TTVector(b_np, device=cuda)
+    s = T.KhatriRaoSketch(f_np, device=cuda)
+    x, rep = T.tt_sgmres(a, b, None, cfg, s, T.make_solver_frame(b, cfg, seed=1))
+    ocfg = {"maxit": cfg.maxit, "tol": cfg.tol, "ell": cfg.ell, "eta": cfg.eta, "max_rank": cfg.max_rank,
+            "oversampling": cfg.oversampling, "seed": cfg.seed, "zero_rel": None}
+    drm = T.solver_rto_drm(b.dims, cfg, device="cpu").cores
+    ox, orep = O.sgmres(a_np, b_np, ocfg, f_np, frame=O.solver_frame(b_np, ocfg, seed=1), rounding="rto",
+                        rto_drm=[g.numpy() for g in drm])
+    assert rep.iterations == orep["iterations"]
+    assert rep.basis_rank == orep["basis_rank"]
+    np.testing.assert_allclose(rep.res_sketched, orep["res_sketched"], rtol=1e-8)
+    assert O.rel_diff([c.cpu().numpy() for c in x.cores], ox) <= 1e-8
+
+
+def test_identity_converges_immediately(cuda):
+    dims = [3, 3, 3]
+    b = T.tt_random(dims, [1, 1], seed=8, device=cuda)
+    cfg = T.SolverConfig(maxit=6, tol=1e-9, seed=4)
+    s = T.kr_sketch_new(dims, cfg.sketch_rows, seed=5, device=cuda)
+    x, rep = T.tt_sgmres(T.identity_operator(dims, device=cuda), b, None, cfg, s)
+    assert rep.converged and rep.iterations == 1
+    gap = T.tt_norm(T.tt_combine([x, b], [1.0, -1.0])) / T.tt_norm(b)
+    assert gap <= 1e-8
+
+
+def test_determinism(cuda):
+    z = load("solver_small.npz")
+    a = T.TTOperator(cores(z, "sv_pde_op"), device=cuda)
+    b = T.TTVector(cores(z, "sv_pde_b"), device=cuda)
+    outs = []
+    for _ in range(2):
+        cfg = T.SolverConfig(maxit=40, tol=1e-6, ell=1, seed=19)
+        s = T.kr_sketch_new(b.dims, cfg.sketch_rows, seed=20, device=cuda)
+        frame = T.StreamFrame.create(b.dims, [8, 8], seed=21, device=cuda)
+        _, rep = T.tt_sgmres(a, b, None, cfg, s, frame)
+        outs.append(rep.res_sketched)
+    assert outs[0] == outs[1]

@@ -116,3 +116,32 @@ def test_solver_cfg1_golden():
     probe = O.kr_apply(O.kr_factors_new([c.shape[1] for c in x], 24, seed=777), x)
     want = z["cfg1_xprobe"]
     assert np.linalg.norm(probe - want) <= 1e-8 * np.linalg.norm(want)
+
+
+def test_oracle_rto_exactness_kat():
+    """Pins the RTO restatement (no reference implementation exists): with
+    sketch rank >= true rank the randomized rounding is exact."""
+    dims = [6, 6, 6, 6, 6]
+    x = O.tt_random(dims, [3, 5, 4, 2], seed=11)
+    big = O.add(x, O.scale(x, 0.25))
+    drm = O.drm_new(dims, [7, 7, 7, 7], seed=5)
+    ls = O.rto_ranks(dims, [1] + [c.shape[2] for c in big], [7, 7, 7, 7])
+    out = O.rto_sweeps(big, O.slice_drm(drm, ls))
+    assert O.rel_diff(out, O.scale(x, 1.25)) <= 1e-12
+    r = O.rto_round(big, O.slice_drm(drm, ls), 1e-12)
+    assert [c.shape[2] for c in r][:-1] == [c.shape[2] for c in x][:-1]
+
+
+def test_oracle_rto_dense_randomized_svd():
+    """At the first cut RTO's core spans range(X_(1) G_(1)^T): the randomized
+    range finder on the dense unfolding with the DRM's right interface."""
+    dims = [5, 6, 4]
+    x = O.tt_random(dims, [5, 4], seed=3)
+    drm = O.slice_drm(O.drm_new(dims, [3, 2], seed=4), O.rto_ranks(dims, [1, 5, 4, 1], [3, 2]))
+    out = O.rto_sweeps(x, drm)
+    full = O.to_dense(x).reshape(5, -1)
+    gr = np.tensordot(drm[1], drm[2], axes=([2], [0]))[:, :, :, 0]  # (l1, n1, n2)
+    y = full @ gr.reshape(gr.shape[0], -1).T
+    q = out[0].reshape(5, -1)
+    assert np.abs(q.T @ q - np.eye(q.shape[1])).max() <= 1e-14
+    assert np.linalg.norm(y - q @ (q.T @ y)) <= 1e-13 * np.linalg.norm(y)

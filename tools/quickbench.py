@@ -19,6 +19,7 @@ def timeit(fn, reps=5, warm=2):
     return min(ts), float(np.median(ts))
 
 which = sys.argv[1:] or ["matvec", "kr", "dots", "concat"]
+import traceback
 if "matvec" in which:
     d, n, r, rho = 32, 128, 64, 3
     rng = np.random.default_rng(0)
