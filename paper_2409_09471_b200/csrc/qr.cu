@@ -148,6 +148,137 @@ __global__ void __launch_bounds__(kQrThreads, 1)
 }
 
 // -------------------------------------------------------------------------
+// Tree mode: QR of two stacked upper-triangular l x l factors [R1; R2].
+// Reflector j touches row j of R1 and rows 0..j of R2 only, so both stay
+// upper triangular; they live packed column-major in shared memory
+// (entry (r, c), r <= c, at c(c+1)/2 + r).  The reflector vectors overwrite
+// R2 (unit entry at row j of R1 implicit).
+__device__ __forceinline__ int pk_idx(int r, int c) { return c * (c + 1) / 2 + r; }
+
+__global__ void __launch_bounds__(kQrThreads, 1)
+    qr_pair_factor_kernel(int l, int nchild, const double* __restrict__ Rin, double* __restrict__ Rout,
+                          double* __restrict__ Vp, double* __restrict__ tau) {
+  extern __shared__ double sm[];
+  const size_t pk = (size_t)l * (l + 1) / 2;
+  double* T1 = sm;
+  double* T2 = sm + pk;
+  double* tsh = T2 + pk;
+  const int node = blockIdx.x;
+  const int a = 2 * node, b = 2 * node + 1;
+  const bool pair = b < nchild;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const double* R1 = Rin + (size_t)a * l * l;
+  const double* R2 = Rin + (size_t)b * l * l;
+  for (int e = threadIdx.x; e < l * l; e += blockDim.x) {
+    int r = e / l, c = e - r * l;
+    if (r <= c) {
+      T1[pk_idx(r, c)] = R1[e];
+      T2[pk_idx(r, c)] = pair ? R2[e] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    if (warp == 0) {
+      double s2 = 0.0;
+      for (int i = lane; i <= j; i += 32) {
+        double x = T2[pk_idx(i, j)];
+        s2 += x * x;
+      }
+      s2 = warp_sum(s2);
+      const double alpha = T1[pk_idx(j, j)];
+      double t = 0.0, beta = alpha, scal = 0.0;
+      if (s2 > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+        t = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      for (int i = lane; i <= j; i += 32) T2[pk_idx(i, j)] *= scal;
+      if (lane == 0) {
+        T1[pk_idx(j, j)] = beta;
+        tsh[j] = t;
+      }
+    }
+    __syncthreads();
+    const double t = tsh[j];
+    if (t != 0.0) {
+      const double* v = T2 + pk_idx(0, j);
+      for (int c = j + 1 + warp; c < l; c += nwarps) {
+        double* col = T2 + pk_idx(0, c);
+        double s = 0.0;
+        for (int i = lane; i <= j; i += 32) s += v[i] * col[i];
+        s = (warp_sum(s) + T1[pk_idx(j, c)]) * t;
+        for (int i = lane; i <= j; i += 32) col[i] -= v[i] * s;
+        if (lane == 0) T1[pk_idx(j, c)] -= s;
+      }
+    }
+  }
+  __syncthreads();
+  double* Ro = Rout + (size_t)node * l * l;
+  for (int e = threadIdx.x; e < l * l; e += blockDim.x) {
+    int r = e / l, c = e - r * l;
+    Ro[e] = (r <= c) ? T1[pk_idx(r, c)] : 0.0;
+  }
+  double* vo = Vp + (size_t)node * pk;
+  for (size_t e = threadIdx.x; e < pk; e += blockDim.x) vo[e] = T2[e];
+  for (int j = threadIdx.x; j < l; j += blockDim.x) tau[(size_t)node * l + j] = tsh[j];
+}
+
+// E_node (l x l) -> [E_top; E_bot] = H_0..H_{l-1} [E_node; 0]; column chunks of 32.
+__global__ void __launch_bounds__(256)
+    qr_pair_apply_kernel(int l, int nchild, const double* __restrict__ Vp, const double* __restrict__ tau,
+                         const double* __restrict__ Ein, double* __restrict__ Eout) {
+  constexpr int CB = 32;
+  extern __shared__ double sm[];
+  double* Et = sm;            // l x CB
+  double* Eb = sm + l * CB;   // l x CB
+  const int node = blockIdx.x, c0 = blockIdx.y * CB;
+  const int cb = min(CB, l - c0);
+  const int a = 2 * node, b = 2 * node + 1;
+  const bool pair = b < nchild;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const double* E = Ein + (size_t)node * l * l;
+  for (int e = threadIdx.x; e < l * CB; e += blockDim.x) {
+    int r = e / CB, c = e - r * CB;
+    Et[e] = (c < cb) ? E[(size_t)r * l + c0 + c] : 0.0;
+    Eb[e] = 0.0;
+  }
+  __syncthreads();
+  const size_t pk = (size_t)l * (l + 1) / 2;
+  const double* V = Vp + (size_t)node * pk;
+  const double* tp = tau + (size_t)node * l;
+  if (pair) {
+    for (int j = l - 1; j >= 0; --j) {
+      const double t = tp[j];
+      if (t == 0.0) continue;
+      const double* v = V + pk_idx(0, j);
+      for (int c = warp; c < cb; c += nwarps) {
+        double s = 0.0;
+        for (int i = lane; i <= j; i += 32) s += __ldg(v + i) * Eb[i * CB + c];
+        s = (warp_sum(s) + Et[j * CB + c]) * t;
+        for (int i = lane; i <= j; i += 32) Eb[i * CB + c] -= __ldg(v + i) * s;
+        if (lane == 0) Et[j * CB + c] -= s;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  double* Oa = Eout + (size_t)a * l * l;
+  double* Ob = Eout + (size_t)b * l * l;
+  for (int e = threadIdx.x; e < l * cb; e += blockDim.x) {
+    int r = e / cb, c = e - r * cb;
+    Oa[(size_t)r * l + c0 + c] = Et[r * CB + c];
+    if (pair) Ob[(size_t)r * l + c0 + c] = Eb[r * CB + c];
+  }
+}
+
+__global__ void identity_kernel(double* E, int l) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < l * l; e += gridDim.x * blockDim.x)
+    E[e] = (e / l == e % l) ? 1.0 : 0.0;
+}
+
+// -------------------------------------------------------------------------
 int qr_plan(int m, int l, QrPlan* P) {
   P->m = m; P->l = l; P->k = std::min(m, l);
   P->cpw = P->rpl = 0;
@@ -156,8 +287,35 @@ int qr_plan(int m, int l, QrPlan* P) {
   // shared memory holds the panel (H x ld), two reflector buffers (2 x H) and tau (l)
   int H = (kQrSmemDoubles - 128 - l) / (ld + 2);
   H = std::min(H, 2048);
+  P->tree = 0;
+  P->depth = 0;
   if (m <= H) {
     H = m;  // single panel, exactly m rows (wide inputs: min(m, l) reflectors)
+  } else if (H < 2 * l) {
+    // stacked-R levels would not shrink: leaf panels + binary tree of R pairs
+    TTK_REQUIRE(l <= kQrMaxCols && H >= l, kInvalidValue, "tsqr: %d x %d: at most %d columns", m, l,
+                kQrMaxCols);
+    P->h = H;
+    P->tree = 1;
+    P->levels = 1;
+    P->rows[0] = m;
+    P->panels[0] = (m + H - 1) / H;
+    int nodes = P->panels[0], t = 0;
+    P->nodes[0] = nodes;
+    size_t ws = align_up((size_t)nodes * l * H * 8, 256) + align_up((size_t)nodes * l * 8, 256);
+    const size_t pk = (size_t)l * (l + 1) / 2;
+    while (true) {
+      ws += align_up((size_t)nodes * l * l * 8, 256) * 2;  // R and E of this tree level
+      if (t > 0) ws += align_up((size_t)nodes * pk * 8, 256) + align_up((size_t)nodes * l * 8, 256);
+      if (nodes == 1) break;
+      nodes = (nodes + 1) / 2;
+      ++t;
+      TTK_REQUIRE(t < 24, kInvalidValue, "tsqr: tree too deep");
+      P->nodes[t] = nodes;
+    }
+    P->depth = t;
+    P->ws_bytes = ws + 4096;
+    return kOk;
   } else {
     TTK_REQUIRE(H >= 2 * l, kInvalidValue,
                 "tsqr: %d x %d needs a multi-panel tree; columns limited to %d", m, l, H / 2);
@@ -195,6 +353,55 @@ static int qr_set_smem(const void* fn, size_t bytes) {
   return kOk;
 }
 
+static int tsqr_tree(const QrPlan& P, const double* A, long long a_rs, long long a_cs, double* Q,
+                     long long q_rs, long long q_cs, double* R, void* ws, size_t ws_bytes, size_t smem_f,
+                     size_t smem_a, cudaStream_t st) {
+  const int l = P.l, H = P.h, D = P.depth;
+  static bool attr = false;
+  if (!attr) {
+    TTK_TRY(qr_set_smem((const void*)qr_pair_factor_kernel, 227 * 1024));
+    TTK_TRY(qr_set_smem((const void*)qr_pair_apply_kernel, 128 * 1024));
+    attr = true;
+  }
+  const size_t pk = (size_t)l * (l + 1) / 2;
+  Arena ar(ws, ws_bytes);
+  double* V0 = ar.take<double>((size_t)P.nodes[0] * l * H);
+  double* T0 = ar.take<double>((size_t)P.nodes[0] * l);
+  std::vector<double*> Rl(D + 1), El(D + 1), Vl(D + 1, nullptr), Tl(D + 1, nullptr);
+  for (int t = 0; t <= D; ++t) {
+    Rl[t] = ar.take<double>((size_t)P.nodes[t] * l * l);
+    El[t] = ar.take<double>((size_t)P.nodes[t] * l * l);
+    if (t > 0) {
+      Vl[t] = ar.take<double>((size_t)P.nodes[t] * pk);
+      Tl[t] = ar.take<double>((size_t)P.nodes[t] * l);
+    }
+  }
+  TTK_REQUIRE(ar.used <= ws_bytes, kWorkspace, "tsqr(tree): workspace too small");
+  qr_panel_factor_kernel<<<P.nodes[0], kQrThreads, smem_f, st>>>(P.rows[0], l, H, A, a_rs, a_cs, V0, T0,
+                                                                 Rl[0]);
+  TTK_CHECK_LAUNCH();
+  const size_t smem_p = sizeof(double) * (2 * pk + l);
+  for (int t = 1; t <= D; ++t) {
+    qr_pair_factor_kernel<<<P.nodes[t], kQrThreads, smem_p, st>>>(l, P.nodes[t - 1], Rl[t - 1], Rl[t],
+                                                                  Vl[t], Tl[t]);
+    TTK_CHECK_LAUNCH();
+  }
+  if (R) TTK_CHECK_CUDA(cudaMemcpyAsync(R, Rl[D], sizeof(double) * (size_t)P.k * l,
+                                        cudaMemcpyDeviceToDevice, st));
+  identity_kernel<<<8, 256, 0, st>>>(El[D], l);
+  TTK_CHECK_LAUNCH();
+  for (int t = D; t >= 1; --t) {
+    dim3 grid(P.nodes[t], (l + 31) / 32);
+    qr_pair_apply_kernel<<<grid, 256, sizeof(double) * 2 * l * 32, st>>>(l, P.nodes[t - 1], Vl[t], Tl[t],
+                                                                         El[t], El[t - 1]);
+    TTK_CHECK_LAUNCH();
+  }
+  qr_panel_apply_kernel<<<P.nodes[0], kQrThreads, smem_a, st>>>(l, H, P.k, V0, T0, El[0], P.rows[0], Q,
+                                                                q_rs, q_cs);
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
 int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
          long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (m <= 0 || l <= 0) return kOk;
@@ -211,6 +418,7 @@ int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* 
   }
   const size_t smem_f = sizeof(double) * ((size_t)H * ld + 2 * H + l);
   const size_t smem_a = sizeof(double) * ((size_t)H * ld);
+  if (P.tree) return tsqr_tree(P, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, smem_f, smem_a, st);
   Arena ar(ws, ws_bytes);
   std::vector<double*> V(P.levels), T(P.levels), RS(P.levels), QL(P.levels);
   for (int i = 0; i < P.levels; ++i) {
@@ -362,11 +570,11 @@ int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, c
               "jacobi_svd: %d x %d exceeds %d", k, l, kQrMaxCols);
   const int le = l + (l & 1);
   size_t smem = sizeof(double) * ((size_t)le * (k | 1) + (V ? (size_t)le * le : 0));
-  TTK_REQUIRE(smem <= 200 * 1024, kInvalidValue, "jacobi_svd: %d x %d (V=%d) exceeds shared memory", k,
+  TTK_REQUIRE(smem <= 215 * 1024, kInvalidValue, "jacobi_svd: %d x %d (V=%d) exceeds shared memory", k,
               l, V != nullptr);
   static bool attr = false;
   if (!attr) {
-    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel, 200 * 1024));
+    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel, 215 * 1024));
     attr = true;
   }
   jacobi_svd_kernel<<<1, kSvdThreads, smem, st>>>(k, l, B, U, S, V, V != nullptr);

@@ -7,7 +7,7 @@
 namespace ttk {
 
 // Largest column count handled by the register-resident panel kernels.
-constexpr int kQrMaxCols = 128;
+constexpr int kQrMaxCols = 160;
 
 struct QrPlan {
   int m, l, k;       // k = min(m, l) columns of Q / rows of R
@@ -15,6 +15,10 @@ struct QrPlan {
   int levels;
   int rows[16];      // rows of the level-i input
   int panels[16];
+  // tree mode (H < 2l): one leaf level, then a binary tree of triangle pairs
+  int tree;
+  int depth;
+  int nodes[24];     // nodes per tree level (nodes[0] = leaf panels)
   size_t ws_bytes;
 };
 

@@ -36,7 +36,8 @@ def run_qr(A, cuda, transposed=False):
 
 
 @pytest.mark.parametrize("m,l", [(10240, 80), (3200, 50), (100000, 16), (500, 112), (7, 3), (3, 7),
-                                 (64, 64), (25600, 100), (1, 1), (300, 1)])
+                                 (64, 64), (25600, 100), (1, 1), (300, 1), (3584, 119), (30720, 120),
+                                 (5000, 128), (2000, 160), (150, 160)])
 def test_tsqr_orthonormal_and_exact(cuda, m, l):
     rng = np.random.default_rng(m + l)
     A = rng.standard_normal((m, l))
@@ -60,6 +61,15 @@ def test_tsqr_rank_deficient_and_zero(cuda):
     assert np.all(R == 0)
 
 
+def test_tsqr_tree_rank_deficient(cuda):
+    rng = np.random.default_rng(3)
+    B = rng.standard_normal((6000, 30))
+    A = np.concatenate([B, B, np.zeros((6000, 40)), B @ rng.standard_normal((30, 20))], axis=1)  # 120 cols
+    Q, R = run_qr(A, cuda)
+    assert np.abs(Q.T @ Q - np.eye(120)).max() <= 1e-12
+    assert np.linalg.norm(Q @ R - A) <= 1e-13 * np.linalg.norm(A) * 10
+
+
 def test_tsqr_transposed_input(cuda):
     rng = np.random.default_rng(2)
     A = rng.standard_normal((4096, 37))
@@ -67,7 +77,8 @@ def test_tsqr_transposed_input(cuda):
     assert np.linalg.norm(Q @ R - A) <= 1e-13 * np.linalg.norm(A) * 12
 
 
-@pytest.mark.parametrize("k,l", [(80, 80), (50, 50), (128, 128), (10, 30), (60, 40), (1, 5), (7, 1)])
+@pytest.mark.parametrize("k,l", [(80, 80), (50, 50), (128, 128), (10, 30), (60, 40), (1, 5), (7, 1),
+                                 (150, 150), (120, 160)])
 def test_jacobi_svd(cuda, k, l):
     lib = _lib.load()
     rng = np.random.default_rng(k * 7 + l)
