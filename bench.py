@@ -1,0 +1,408 @@
+"""Benchmark of the B200 TT-sGMRES hot path (BASELINE.json metric).
+
+Headline workload (BASELINE.json configs[2], "TT matvec + rounding"): one step
+applies the d=32, n=128, op-rank-3 anisotropic convection-diffusion TT
+operator to a rank-64 Gaussian TT (tt_matvec, output rank 192) and rounds the
+result with randomize-then-orthogonalize at sketch rank l=80 followed by TT-SVD
+truncation to rank 64.  value = (matvec + RTO-sweep FLOPs) / step time in
+GFLOP/s (the truncation is timed but not counted).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--extras]
+
+N > 1 runs under torchrun: every rank runs an independent replica (the
+matvec/rounding chain does not shard -- "replicas only"), value is
+the FLOPs of all ranks / the max-over-ranks device time.  --impl reference
+times the CPU oracle (numpy restatement of the reference path, oracle/) on
+the host cores for the same workload.
+"""
+
+from __future__ import annotations
+
+import os
+
+if "OPENBLAS_NUM_THREADS" not in os.environ:  # CPU legs use every host core
+    os.environ["OPENBLAS_NUM_THREADS"] = str(os.cpu_count() or 1)
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+
+import argparse
+import json
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "randomized TT-round+matvec GFLOP/s (fp64)"
+UNIT = "GFLOP/s"
+WORKLOAD = ("config3: tt_matvec of the d=32 n=128 op-rank-3 convection-diffusion TT operator on a "
+            "rank-64 Gaussian TT (-> rank 192), then randomize-then-orthogonalize rounding l=80 + "
+            "TT-SVD truncation to rank 64")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--extras", action="store_true", help="also time configs 1, 2, 4 and 5")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region (B200_PROFILING.md recipe)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+def fp64_peak(torch, dev):
+    """cuBLAS DGEMM 4096^3, best of 5 (the FP64 tensor-pipe roofline denominator;
+    MEASURED_PEAKS.json carries no fp64 entry)."""
+    n = 4096
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); a @ b; e1.record(); e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e9
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def cfg3_flops(C):
+    from paper_2409_09471_b200.configs import matvec_flops
+    from paper_2409_09471_b200.rto import rto_flops, rto_ranks
+    xr = [1] + [c.shape[2] for c in C["x"]]
+    mv = matvec_flops(C["op"], xr)
+    yr = [1] + [c.shape[2] * g.shape[3] for c, g in zip(C["x"], C["op"])]
+    ls = rto_ranks(C["dims"], yr, C["ell"])
+    return mv, rto_flops(C["dims"], yr, ls)
+
+
+def cpu_oracle_step(C):
+    import oracle as O
+    y = O.matvec(C["op"], C["x"])
+    return O.rto_round(y, C["drm"], C["rel_tol"], C["max_rank"], zero_rel=None)
+
+
+def cpu_baseline(C, flops, budget_s=20.0):
+    """The oracle port on the host cores; bounded sample = whole steps until
+    ~budget_s of CPU work (at least one)."""
+    t0 = time.perf_counter()
+    cpu_oracle_step(C)  # warm-up (BLAS thread pool, page faults)
+    t_warm = time.perf_counter() - t0
+    reps = max(1, min(3, int(budget_s / max(t_warm, 1e-3))))
+    ts, out = [], None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = cpu_oracle_step(C)
+        ts.append(time.perf_counter() - t0)
+    t = float(np.median(ts))
+    return {"value": flops / t / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{reps} full config-3 steps after 1 warm-up (median {t:.2f} s/step); numpy "
+                      f"restatement oracle/ttoracle.py (matvec + rto_round), OpenBLAS threads = "
+                      f"{os.environ.get('OPENBLAS_NUM_THREADS')}",
+            "s_per_step": t}, out
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2409_09471_b200 import configs
+    C = configs.config3()
+    mv, rto = cfg3_flops(C)
+    flops = mv + rto
+    for _ in range(args.warmup):
+        cpu_oracle_step(C)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_oracle_step(C)
+        ts.append(time.perf_counter() - t0)
+    tot = sum(ts)
+    value = flops * args.steps / tot / 1e9
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "flops_per_step": flops},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{args.steps} full config-3 steps (numpy restatement of the "
+                                       f"reference path, oracle/ttoracle.py; the Python reference "
+                                       f"itself is not on the GPU box)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2409_09471_b200 as T
+    from paper_2409_09471_b200 import _lib, configs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _lib.load()
+
+    C = configs.config3()
+    mv_flops, rto_fl = cfg3_flops(C)
+    flops = mv_flops + rto_fl
+    spec = T.RoundSpec(C["rel_tol"], C["max_rank"])
+    op = T.TTOperator(C["op"], device=dev)
+    x = T.TTVector(C["x"], device=dev)
+    drm = [torch.as_tensor(g, device=dev) for g in C["drm"]]
+
+    def step(op, x):
+        y = T.tt_matvec(op, x)
+        return T.tt_round(T.rto_sweeps(y, drm), spec, zero_rel=None)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-resident timing (value) ----
+    for _ in range(max(args.warmup, 3)):
+        out = step(op, x)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    n0 = lib.ttk_launch_count()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            out = step(op, x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = (lib.ttk_launch_count() - n0) // args.steps
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    barrier()
+
+    # ---- phase breakdown of one step (device events) ----
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(stream)
+    y = T.tt_matvec(op, x)
+    ev[1].record(stream)
+    z = T.rto_sweeps(y, drm)
+    ev[2].record(stream)
+    T.tt_round(z, spec, zero_rel=None)
+    ev[3].record(stream)
+    torch.cuda.synchronize()
+    phases = {"matvec_ms": ev[0].elapsed_time(ev[1]), "rto_sweeps_ms": ev[1].elapsed_time(ev[2]),
+              "truncation_ms": ev[2].elapsed_time(ev[3])}
+
+    # ---- dominant kernel roofline: the matvec grouped DMMA GEMM (one launch) ----
+    reps = 5
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for _ in range(reps):
+        T.tt_matvec(op, x)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    mv_ms = k0.elapsed_time(k1) / reps
+    peak = fp64_peak(torch, dev)
+    achieved = mv_flops / (mv_ms * 1e-3) / 1e12
+    roofline = {"bound": "tensor", "kernel": "gemm_group_kernel<128,128> (tt_matvec, 1 launch/step)",
+                "achieved": achieved, "peak": peak / 1e3, "unit": "TFLOP/s", "frac": achieved / (peak / 1e3),
+                "peak_source": "live cuBLAS DGEMM 4096^3 (fp64 tensor pipe; MEASURED_PEAKS.json has no "
+                               "fp64 entry; DMMA issue peak measured 37.1 TF/s, profiles/fp64_peak_r01.log)",
+                "traffic": None, "algorithmic_flops": mv_flops,
+                "algorithmic_bytes": 8.0 * sum(c.numel() for c in y.cores)}
+
+    # ---- end-to-end through the public API with host buffers ----
+    host_op = [torch.as_tensor(g).pin_memory() for g in C["op"]]
+    host_x = [torch.as_tensor(c).pin_memory() for c in C["x"]]
+    h2d = sum(t.numel() * 8 for t in host_op + host_x)
+    res_host = None
+
+    def e2e_step():
+        a = T.TTOperator([t.to(dev, non_blocking=True) for t in host_op], device=dev)
+        v = T.TTVector([t.to(dev, non_blocking=True) for t in host_x], device=dev)
+        r = step(a, v)
+        return [c.to("cpu", non_blocking=True) for c in r.cores]
+
+    for _ in range(2):
+        res_host = e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        res_host = e2e_step()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    d2h = sum(c.numel() * 8 for c in res_host)
+
+    line = {"metric": METRIC, "value": flops * world / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                       "flops_per_step": flops, "matvec_flops": mv_flops, "rto_sweep_flops": rto_fl,
+                       "l2": "inputs larger than L2 (matvec output 1.13 GB per step)",
+                       "out_ranks_max": max(out.ranks)},
+            "roofline": roofline,
+            "e2e": {"value": flops * world / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "breakdown": phases}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb, cpu_out = cpu_baseline(C, flops)
+        line["cpu_baseline"] = cb
+        import oracle as O
+        line["parity"] = {"rel_diff_vs_oracle": O.rel_diff([c.cpu().numpy() for c in out.cores], cpu_out),
+                          "ranks_equal": list(out.ranks) == [1] + [c.shape[2] for c in cpu_out]}
+    if args.extras and rank == 0:
+        line["extras"] = run_extras(T, torch, dev)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_extras(T, torch, dev):
+    """Configs 2 and 4 (kernel GFLOP/s) and the solver configs 1 and 5 (it/s)."""
+    from paper_2409_09471_b200 import configs
+    from paper_2409_09471_b200.rto import rto_flops, rto_ranks
+    out = {}
+    st = torch.cuda.current_stream(dev)
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(reps):
+            fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+    # config 2
+    C2 = configs.config2()
+    x2 = T.TTVector(C2["x"], device=dev)
+    drm2 = [torch.as_tensor(g, device=dev) for g in C2["drm"]]
+    ls = rto_ranks(C2["dims"], list(x2.ranks), C2["ell"])
+    f2 = rto_flops(C2["dims"], list(x2.ranks), ls)
+    ms_sw = timed(lambda: T.rto_sweeps(x2, drm2))
+    ms_all = timed(lambda: T.tt_round(T.rto_sweeps(x2, drm2), T.RoundSpec(0.0, 40), zero_rel=None))
+    out["config2_rto"] = {"gflop": f2 / 1e9, "sweeps_ms": ms_sw, "sweeps_gflops": f2 / ms_sw / 1e6,
+                          "with_truncation_ms": ms_all}
+    # config 4
+    C4 = configs.config4()
+    sk = T.KhatriRaoSketch(C4["factors"], device=dev)
+    vs = [T.TTVector(v, device=dev) for v in C4["vecs"]]
+    f4 = sum(configs.kr_flops(C4["rows"], C4["dims"], list(v.ranks)) for v in vs)
+    ms4 = timed(lambda: T.kr_apply_batch(sk, vs), reps=2)
+    out["config4_kr"] = {"gflop": f4 / 1e9, "ms": ms4, "gflops": f4 / ms4 / 1e6}
+    del vs, sk
+    # solvers
+    for name, builder in (("config1_sgmres_rto", configs.config1), ("config5_sgmres_rto", configs.config5)):
+        C = builder()
+        cfg = T.SolverConfig(**C["cfg"], zero_rel=None, rounding="rto")
+        a = T.TTOperator(C["op"], device=dev)
+        b = T.TTVector(C["b"], device=dev)
+        s = T.kr_sketch_new(C["dims"], cfg.sketch_rows, seed=C["sketch_seed"], device=dev)
+        frame = T.make_solver_frame(b, cfg, seed=C["frame_seed"])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, rep = T.tt_sgmres(a, b, None, cfg, s, frame)
+        wall = time.perf_counter() - t0
+        out[name] = {"iterations": rep.iterations, "converged": rep.converged, "wall_s": wall,
+                     "it_per_s": rep.iterations / wall, "final_res_sketched": rep.res_sketched[-1],
+                     "peak_rank": rep.peak_rank, "time_to_1e-6_s": rep.time_to_tol.get(1e-6),
+                     "phase_s": rep.phase_totals()}
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

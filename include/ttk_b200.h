@@ -48,6 +48,7 @@ extern "C" {
 const char* ttk_last_error(void);
 int ttk_version(void);
 int ttk_device_arch(void); /* compute capability of the current device, e.g. 100 */
+long long ttk_launch_count(void); /* kernels launched by this library so far (all threads) */
 
 /* ---- dense building block ------------------------------------------------
  * Strided batched fp64 GEMM on the DMMA tensor pipe:

@@ -30,6 +30,7 @@ SIGNATURES = {
     "ttk_last_error": (ctypes.c_char_p, []),
     "ttk_version": (c_int, []),
     "ttk_device_arch": (c_int, []),
+    "ttk_launch_count": (c_ll, []),
     "ttk_gemm_strided": (c_int, [c_int, c_int, c_int, c_int, c_double, c_vp, c_ll, c_ll, c_ll,
                                  c_vp, c_ll, c_ll, c_ll, c_double, c_vp, c_ll, c_ll, c_ll,
                                  c_vp, c_size, c_vp]),

@@ -8,6 +8,7 @@
 namespace ttk {
 
 static thread_local char g_err[1024] = {0};
+std::atomic<long long> g_launches{0};
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -27,6 +28,8 @@ extern "C" {
 const char* ttk_last_error(void) { return ttk::last_error(); }
 
 int ttk_version(void) { return TTK_ABI_VERSION; }
+
+long long ttk_launch_count(void) { return ttk::g_launches.load(); }
 
 int ttk_device_arch(void) {
   int dev = 0, major = 0, minor = 0;

@@ -5,8 +5,13 @@
 #include <cstdio>
 #include <cstdarg>
 #include <cmath>
+#include <atomic>
 
 namespace ttk {
+
+// number of kernels this library has launched (ttk_launch_count); bumped by
+// TTK_CHECK_LAUNCH, which follows every <<<...>>> launch site
+extern std::atomic<long long> g_launches;
 
 // ---------------------------------------------------------------------------
 // error reporting: every extern "C" entry point returns 0 on success and a
@@ -35,6 +40,7 @@ const char* last_error();
 
 #define TTK_CHECK_LAUNCH()                                                       \
   do {                                                                           \
+    ::ttk::g_launches.fetch_add(1, std::memory_order_relaxed);                   \
     cudaError_t _e = cudaGetLastError();                                         \
     if (_e != cudaSuccess) {                                                     \
       ::ttk::set_error("%s:%d: launch failed -> %s", __FILE__, __LINE__,        \
