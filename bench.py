@@ -144,7 +144,7 @@ def cfg3_flops(C):
 def cpu_oracle_step(C):
     import oracle as O
     y = O.matvec(C["op"], C["x"])
-    return O.rto_round(y, C["drm"], C["rel_tol"], C["max_rank"], zero_rel=None)
+    return O.rto_round(y, C["drm"], C["rel_tol"], C["max_rank"])
 
 
 def cpu_baseline(C, flops, budget_s=20.0):
@@ -225,7 +225,7 @@ def run_b200(args):
 
     def step(op, x):
         y = T.tt_matvec(op, x)
-        return T.tt_round(T.rto_sweeps(y, drm), spec, zero_rel=None)
+        return T.tt_truncate_left_orth(T.rto_sweeps(y, drm), spec)
 
     def barrier():
         if world > 1:
@@ -261,7 +261,7 @@ def run_b200(args):
     ev[1].record(stream)
     z = T.rto_sweeps(y, drm)
     ev[2].record(stream)
-    T.tt_round(z, spec, zero_rel=None)
+    T.tt_truncate_left_orth(z, spec)
     ev[3].record(stream)
     torch.cuda.synchronize()
     phases = {"matvec_ms": ev[0].elapsed_time(ev[1]), "rto_sweeps_ms": ev[1].elapsed_time(ev[2]),
@@ -367,7 +367,7 @@ def run_extras(T, torch, dev):
     ls = rto_ranks(C2["dims"], list(x2.ranks), C2["ell"])
     f2 = rto_flops(C2["dims"], list(x2.ranks), ls)
     ms_sw = timed(lambda: T.rto_sweeps(x2, drm2))
-    ms_all = timed(lambda: T.tt_round(T.rto_sweeps(x2, drm2), T.RoundSpec(0.0, 40), zero_rel=None))
+    ms_all = timed(lambda: T.tt_truncate_left_orth(T.rto_sweeps(x2, drm2), T.RoundSpec(0.0, 40)))
     out["config2_rto"] = {"gflop": f2 / 1e9, "sweeps_ms": ms_sw, "sweeps_gflops": f2 / ms_sw / 1e6,
                           "with_truncation_ms": ms_all}
     # config 4

@@ -119,6 +119,8 @@ size_t ttk_qr_ws_bytes(int m, int l);
 /* one-sided Jacobi SVD of B (k x l, row-major, k,l <= 128): B V = U S with
  * S[min(k,l)] descending, U (k x min(k,l)), V (l x min(k,l)) if V != NULL. */
 int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream);
+/* diagnostics: subsequent Jacobi SVDs store their sweep count in *dev_counter (NULL: off) */
+int ttk_debug_svd_sweeps(int* dev_counter);
 
 /* ---- tt_round, TT-SVD (reference tt.py:337-368) ----------------------------
  * out[k] holds ranks[k]*dims[k]*ranks[k+1] doubles; out_ranks (host, d+1)
@@ -161,6 +163,15 @@ int ttk_stream_recover_cores(int d, const int* dims, const int* lr, const int* r
                              double* const* out, int* out_ranks, int* is_zero, void* ws,
                              size_t ws_bytes, void* stream);
 size_t ttk_stream_recover_ws_bytes(int d, const int* dims, const int* lr, const int* rr);
+
+/* ---- truncation of a LEFT-orthogonal TT (the RTO output), right to left ------
+ * TT-SVD without an orthogonalisation sweep; same budget rule
+ * rel_tol*||v||/sqrt(d-1) and cap as tt_round (tt.py:357-364); output layout as
+ * ttk_tt_round.  Oracle: oracle/ttoracle.py truncate_left_orth.  Synchronises. */
+int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
+                    int max_rank, double* const* out, int* out_ranks, void* ws, size_t ws_bytes,
+                    void* stream);
+size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks);
 
 #ifdef __cplusplus
 }

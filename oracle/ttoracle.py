@@ -321,9 +321,39 @@ def rto_sweeps(cores, drm):
     return out
 
 
-def rto_round(cores, drm, rel_tol=0.0, max_rank=None, zero_rel=None):
-    """RTO sweeps followed by TT-SVD truncation."""
-    return tt_round(rto_sweeps(cores, drm), rel_tol, max_rank, zero_rel=zero_rel)
+def truncate_left_orth(cores, rel_tol=0.0, max_rank=None):
+    """TT-SVD truncation of a LEFT-orthogonal TT, right to left.
+
+    For a TT whose cores 0..d-2 are left-orthonormal (the RTO output) the
+    norm sits in the last core and the right unfoldings of the cores carry the
+    singular values of the tensor's unfoldings, so the TT-SVD needs no
+    orthogonalisation sweep: for k = d-1..1 take the SVD of C_k as
+    (r_{k-1} x n_k r_k), keep the _truncation_rank (tt.py:203-211) with the
+    budget rel_tol ||v|| / sqrt(d-1) (tt.py:357) and the cap, keep V^T in C_k and
+    absorb U S into C_{k-1}."""
+    d = len(cores)
+    work = [c.copy() for c in cores]
+    if d == 1:
+        return work
+    nrm = np.linalg.norm(work[-1])
+    if nrm == 0:
+        return zero_tt([c.shape[1] for c in cores])
+    budget = rel_tol * nrm / np.sqrt(d - 1)
+    for k in range(d - 1, 0, -1):
+        r0, n, r1 = work[k].shape
+        u, sv, vt = np.linalg.svd(work[k].reshape(r0, n * r1), full_matrices=False)
+        r = truncation_rank(sv, budget)
+        if max_rank is not None:
+            r = min(r, max_rank)
+        work[k] = vt[:r].reshape(r, n, r1)
+        work[k - 1] = np.tensordot(work[k - 1], u[:, :r] * sv[None, :r], axes=([2], [0]))
+    return work
+
+
+def rto_round(cores, drm, rel_tol=0.0, max_rank=None):
+    """Randomized rounding: RTO sweeps, then the right-to-left TT-SVD
+    truncation of the left-orthogonal result."""
+    return truncate_left_orth(rto_sweeps(cores, drm), rel_tol, max_rank)
 
 
 def rto_flops(dims, in_ranks, ls):
@@ -482,7 +512,7 @@ def sgmres(op, b, cfg, factors, frame=None, rounding="svd", rto_drm=None):
             return tt_round(v, rel, cap, zero_rel=zero_rel)
         rk = [1] + [c.shape[2] for c in v]
         ls = rto_ranks(dims, rk, [g.shape[2] for g in rto_drm[:-1]])
-        return rto_round(v, slice_drm(rto_drm, ls), rel, cap, zero_rel=zero_rel)
+        return rto_round(v, slice_drm(rto_drm, ls), rel, cap)
 
     rep = {"res_sketched": [], "basis_rank": [], "iterations": 0, "converged": False,
            "max_resident_basis": 0, "warnings": [], "h": []}

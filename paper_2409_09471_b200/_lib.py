@@ -132,3 +132,10 @@ SIGNATURES.update({
                                          ctypes.POINTER(ctypes.c_int), c_vp, c_size, c_vp]),
     "ttk_stream_recover_ws_bytes": (c_size, [c_int, P_int, P_int, P_int]),
 })
+
+SIGNATURES.update({
+    "ttk_tt_truncate": (c_int, [c_int, P_int, P_int, P_vp, c_double, c_int, P_vp, P_int, c_vp, c_size, c_vp]),
+    "ttk_tt_truncate_ws_bytes": (c_size, [c_int, P_int, P_int]),
+})
+
+SIGNATURES.update({"ttk_debug_svd_sweeps": (c_int, [c_vp])})

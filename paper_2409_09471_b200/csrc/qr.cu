@@ -461,10 +461,13 @@ int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* 
 // column-major in shared memory; l/2 disjoint column pairs rotate per round
 // (round-robin tournament), one 16-lane group per pair.
 constexpr int kSvdThreads = 1024;
+__device__ int* g_svd_sweeps = nullptr;  // optional diagnostic sink (tests)
+constexpr int kSvdGroup = 16;  // lanes per column pair
 
 __global__ void __launch_bounds__(kSvdThreads, 1)
-    jacobi_svd_kernel(int k, int l, const double* __restrict__ B, double* __restrict__ U,
-                      double* __restrict__ S, double* __restrict__ V, int want_v) {
+    jacobi_svd_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
+                      double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
+                      int scaled_u) {
   extern __shared__ double sm[];
   const int le = l + (l & 1);           // even number of columns (dummy zero column)
   const int kk = k;                     // column length
@@ -474,47 +477,73 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
   __shared__ int changed;
   __shared__ double nrm[kQrMaxCols + 2];
   __shared__ int order[kQrMaxCols + 2];
+  __shared__ int slot[kQrMaxCols + 2];  // round-robin position -> column
   const int tid = threadIdx.x;
+  // initial column order: decreasing norm (speeds up convergence)
+  for (int c = tid >> 5; c < l; c += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int r = tid & 31; r < kk; r += 32) {
+      double x = B[(long long)r * b_rs + (long long)c * b_cs];
+      s += x * x;
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) nrm[c] = s;
+  }
+  __syncthreads();
+  for (int c = tid; c < l; c += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < l; ++j) rank += (nrm[j] > nrm[c]) || (nrm[j] == nrm[c] && j < c);
+    order[rank] = c;
+  }
+  __syncthreads();
   for (int e = tid; e < le * kk; e += blockDim.x) {
     int c = e / kk, r = e - c * kk;
-    C[c * ldc + r] = (c < l) ? B[(long long)r * l + c] : 0.0;
+    C[c * ldc + r] = (c < l) ? B[(long long)r * b_rs + (long long)order[c] * b_cs] : 0.0;
   }
   if (want_v)
     for (int e = tid; e < le * le; e += blockDim.x) {
       int c = e / le, r = e - c * le;
-      Vs[c * le + r] = (r == c) ? 1.0 : 0.0;
+      Vs[c * le + r] = (c < l && r == order[c]) ? 1.0 : 0.0;
     }
   __syncthreads();
   const double tol = (double)max(kk, 1) * 1.1102230246251565e-16;
-  const int group = tid >> 4, gl = tid & 15;
+  const double tol2 = tol * tol;
+  const int group = tid / kSvdGroup, gl = tid % kSvdGroup;
+  const int ngroups = blockDim.x / kSvdGroup;
   const int npairs = le / 2;
-  const unsigned gmask = 0xffffu << (threadIdx.x & 16);
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0) changed = 0;
+  const unsigned gmask = (kSvdGroup == 32) ? 0xffffffffu
+                         : (((1u << kSvdGroup) - 1u) << (threadIdx.x & (32 - kSvdGroup)));
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
     __syncthreads();
+    if (tid == 0) changed = 0;
     for (int rnd = 0; rnd < le - 1; ++rnd) {
-      for (int pi = group; pi < npairs; pi += blockDim.x >> 4) {
-        int ia = pi, ib = le - 1 - pi;
-        int p = (ia == 0) ? 0 : 1 + (ia - 1 + rnd) % (le - 1);
-        int q = (ib == 0) ? 0 : 1 + (ib - 1 + rnd) % (le - 1);
+      __syncthreads();
+      for (int pi = group; pi < npairs; pi += ngroups) {
+        // round-robin tournament: position 0 fixed, positions 1..le-1 rotate
+        const int qi = le - 1 - pi;
+        int p = 0, q;
+        if (pi > 0) { p = pi - 1 + rnd; if (p >= le - 1) p -= le - 1; p += 1; }
+        q = qi - 1 + rnd; if (q >= le - 1) q -= le - 1; q += 1;
         double* cp = C + p * ldc;
         double* cq = C + q * ldc;
         double a = 0.0, b = 0.0, g = 0.0;
-        for (int r = gl; r < kk; r += 16) {
-          double x = cp[r], y = cq[r];
+        for (int r = gl; r < kk; r += kSvdGroup) {
+          const double x = cp[r], y = cq[r];
           a += x * x; b += y * y; g += x * y;
         }
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
+        for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
           a += __shfl_xor_sync(gmask, a, o);
           b += __shfl_xor_sync(gmask, b, o);
           g += __shfl_xor_sync(gmask, g, o);
         }
-        if (a > 0.0 && b > 0.0 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
-          double zeta = (b - a) / (2.0 * g);
-          double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int r = gl; r < kk; r += 16) {
+        if (a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
+          // t = tan(theta) = sign(d) w / (|d| + sqrt(d^2 + w^2)), d = b - a, w = 2g
+          const double dd = b - a, w = 2.0 * g;
+          const double t = (dd >= 0.0 ? w : -w) / (fabs(dd) + sqrt(dd * dd + w * w));
+          const double c = rsqrt(1.0 + t * t), s = c * t;
+          for (int r = gl; r < kk; r += kSvdGroup) {
             double x = cp[r], y = cq[r];
             cp[r] = c * x - s * y;
             cq[r] = s * x + c * y;
@@ -522,7 +551,7 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
           if (want_v) {
             double* vp = Vs + p * le;
             double* vq = Vs + q * le;
-            for (int r = gl; r < le; r += 16) {
+            for (int r = gl; r < le; r += kSvdGroup) {
               double x = vp[r], y = vq[r];
               vp[r] = c * x - s * y;
               vq[r] = s * x + c * y;
@@ -531,11 +560,16 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
           if (gl == 0) changed = 1;
         }
       }
-      __syncthreads();
     }
-    if (!changed) break;
+    __syncthreads();
+    const int ch = changed;
+    __syncthreads();  // everyone has read the flag before thread 0 resets it
+    if (!ch) break;
   }
-  // norms, ranking (descending, ties by index), outputs
+  if (tid == 0 && g_svd_sweeps) *g_svd_sweeps = sweep + 1;
+  __syncthreads();
+  // norms, ranking (descending, ties by index), outputs; C column c holds
+  // original column order[c]
   for (int c = tid >> 5; c < l; c += blockDim.x >> 5) {
     double s = 0.0;
     for (int r = tid & 31; r < kk; r += 32) s += C[c * ldc + r] * C[c * ldc + r];
@@ -546,25 +580,26 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
   for (int c = tid; c < l; c += blockDim.x) {
     int rank = 0;
     for (int j = 0; j < l; ++j) rank += (nrm[j] > nrm[c]) || (nrm[j] == nrm[c] && j < c);
-    order[rank] = c;
+    slot[rank] = c;
   }
   __syncthreads();
   const int kout = min(kk, l);
-  for (int i = tid; i < kout; i += blockDim.x) S[i] = nrm[order[i]];
+  for (int i = tid; i < kout; i += blockDim.x) S[i] = nrm[slot[i]];
   for (int e = tid; e < kk * kout; e += blockDim.x) {
     int r = e / kout, i = e - r * kout;
-    int c = order[i];
+    int c = slot[i];
     double sv = nrm[c];
-    U[e] = (sv > 0.0) ? C[c * ldc + r] / sv : 0.0;
+    U[e] = scaled_u ? C[c * ldc + r] : ((sv > 0.0) ? C[c * ldc + r] / sv : 0.0);
   }
   if (want_v && V)
     for (int e = tid; e < l * kout; e += blockDim.x) {
       int r = e / kout, i = e - r * kout;
-      V[e] = Vs[order[i] * le + r];
+      V[e] = Vs[slot[i] * le + r];
     }
 }
 
-int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, cudaStream_t st) {
+int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs, double* U, double* S,
+                  double* V, bool scaled_u, cudaStream_t st) {
   if (k <= 0 || l <= 0) return kOk;
   TTK_REQUIRE(l <= kQrMaxCols && k <= kQrMaxCols, kInvalidValue,
               "jacobi_svd: %d x %d exceeds %d", k, l, kQrMaxCols);
@@ -577,9 +612,20 @@ int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, c
     TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel, 215 * 1024));
     attr = true;
   }
-  jacobi_svd_kernel<<<1, kSvdThreads, smem, st>>>(k, l, B, U, S, V, V != nullptr);
+  const int threads = std::min(kSvdThreads, std::max(64, ((le / 2) * kSvdGroup + 31) / 32 * 32));
+  jacobi_svd_kernel<<<1, threads, smem, st>>>(k, l, B, b_rs, b_cs, U, S, V, V != nullptr, scaled_u);
   TTK_CHECK_LAUNCH();
   return kOk;
+}
+
+bool jacobi_fits_v(int k, int l) {
+  const int le = l + (l & 1);
+  return l <= kQrMaxCols && k <= kQrMaxCols &&
+         sizeof(double) * ((size_t)le * (k | 1) + (size_t)le * le) <= 215 * 1024;
+}
+
+int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, cudaStream_t st) {
+  return jacobi_svd_ex(k, l, B, l, 1, U, S, V, false, st);
 }
 
 __global__ void truncation_rank_kernel(const double* S, int n, double budget, int max_rank, int* r_out) {
@@ -625,4 +671,225 @@ int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V
   return jacobi_svd(k, l, B, U, S, V, (cudaStream_t)stream);
 }
 
+// diagnostics: route the sweep count of subsequent Jacobi SVDs to a device int (NULL: off)
+int ttk_debug_svd_sweeps(int* dev_counter) {
+  TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_svd_sweeps, &dev_counter, sizeof(int*)));
+  return kOk;
+}
+
 }  // extern "C"
+
+// ===========================================================================
+// CholeskyQR2 fast path (all heavy work on the DMMA GEMM):
+//   G1 = Y^T Y, R1 = chol(G1), Q1 = Y R1^{-1}; G2 = Q1^T Q1, R2 = chol(G2),
+//   Q = Q1 R2^{-1}, R = R2 R1.
+// Accepted only when both factorisations succeed and ||G2 - I||_max <= 1e-3
+// (then Q is orthonormal to working precision, Yamamoto et al. 2015);
+// otherwise the caller falls back to Householder TSQR.
+#include "gemm.cuh"
+
+namespace ttk {
+
+constexpr int kCholMaxCols = 112;
+
+// one CTA: upper Cholesky G = R^T R of an l x l SPD matrix and R^{-1};
+// status |= 1 on a non-positive / tiny pivot, |= 2 if check_identity and
+// max|G - I| > 1e-3.
+__global__ void __launch_bounds__(1024, 1)
+    chol_inv_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                    double* __restrict__ Rinv, int* status, int check_identity) {
+  extern __shared__ double sm[];
+  const int ld = l + 1;
+  double* A = sm;               // l x ld, becomes R (upper)
+  double* X = sm + l * ld;      // l x ld, R^{-1}
+  __shared__ int bad;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int ty = tid >> 5, tx = tid & 31, nty = nt >> 5;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int e = tid; e < l * l; e += nt) {
+    int r = e / l, c = e - r * l;
+    double g = G[e];
+    A[r * ld + c] = g;
+    if (check_identity && fabs(g - (r == c ? 1.0 : 0.0)) > 1e-3) atomicOr(&bad, 2);
+  }
+  __syncthreads();
+  __shared__ double gmax_s;
+  if (ty == 0) {
+    double g = 0.0;
+    for (int i = tx; i < l; i += 32) g = fmax(g, A[i * ld + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if (tx == 0) gmax_s = g;
+  }
+  __syncthreads();
+  const double tiny = gmax_s * 1e-28 + 1e-300;  // pivot floor (kappa(Y) up to ~1e14)
+  // right-looking Cholesky on the upper triangle; row j is scaled afterwards
+  // (A[i][c] -= A[j][i] A[j][c] / A[j][j]), one barrier per step
+  for (int j = 0; j < l; ++j) {
+    double piv = A[j * ld + j];
+    if (!(piv > tiny)) {
+      if (tid == 0) atomicOr(&bad, 1);
+      piv = 1.0;
+    }
+    const double inv = 1.0 / piv;
+    for (int i = j + 1 + ty; i < l; i += nty) {
+      const double aji = A[j * ld + i] * inv;
+      for (int c = i + tx; c < l; c += 32) A[i * ld + c] -= aji * A[j * ld + c];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < l * l; e += nt) {
+    int r = e / l, c = e - r * l;
+    if (c > r) {
+      double p = A[r * ld + r];
+      A[r * ld + c] = A[r * ld + c] / sqrt(p > tiny ? p : 1.0);
+    }
+  }
+  __syncthreads();
+  for (int r = tid; r < l; r += nt) {
+    double p = A[r * ld + r];
+    A[r * ld + r] = sqrt(p > tiny ? p : 1.0);
+  }
+  __syncthreads();
+  // R^{-1} by blocks of 16: (1) every warp inverts one 16x16 diagonal block
+  // (forward over columns, 16 dependent steps), (2) off-diagonal blocks by
+  // block back-substitution X_IJ = -inv(R_II) sum_{I<K<=J} R_IK X_KJ, one
+  // block-diagonal distance at a time (all blocks of a distance in parallel).
+  {
+    const int nb = (l + 15) / 16;
+    for (int e = tid; e < l * l; e += nt) {
+      int r = e / l, c = e - r * l;
+      X[r * ld + c] = 0.0;
+    }
+    __syncthreads();
+    for (int bI = ty; bI < nb; bI += nty) {
+      const int o = bI * 16, bs = min(16, l - o);
+      // lane tx owns column tx of the block; solve R_II x = e_tx by back substitution
+      if (tx < bs) {
+        double xr[16];
+#pragma unroll
+        for (int i = 15; i >= 0; --i) {
+          if (i < bs) {
+            double acc = (i == tx) ? 1.0 : 0.0;
+#pragma unroll
+            for (int k = i + 1; k < 16; ++k)
+              if (k < bs) acc -= A[(o + i) * ld + o + k] * xr[k];
+            xr[i] = (i <= tx) ? acc / A[(o + i) * ld + o + i] : 0.0;
+          } else {
+            xr[i] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < bs) X[(o + i) * ld + o + tx] = xr[i];
+      }
+    }
+    __syncthreads();
+    double* Tb = X + l * ld;  // (nb-1) x 16 x 16 scratch
+    for (int dist = 1; dist < nb; ++dist) {
+      const int nblk = nb - dist;
+      for (int e = tid; e < nblk * 256; e += nt) {
+        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
+        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
+        double t = 0.0;
+        if (ro < l && co < l)
+          for (int k = (I + 1) * 16; k <= co; ++k) t += A[ro * ld + k] * X[k * ld + co];
+        Tb[e] = t;
+      }
+      __syncthreads();
+      for (int e = tid; e < nblk * 256; e += nt) {
+        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
+        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
+        if (ro < l && co < l) {
+          double v = 0.0;
+          for (int kk = r; kk < 16 && I * 16 + kk < l; ++kk)
+            v -= X[ro * ld + I * 16 + kk] * Tb[(I << 8) + (kk << 4) + c];
+          X[ro * ld + co] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = tid; e < l * l; e += nt) {
+    int r = e / l, c = e - r * l;
+    Rout[e] = (c >= r) ? A[r * ld + c] : 0.0;
+    Rinv[e] = (c >= r) ? X[r * ld + c] : 0.0;
+  }
+  if (tid == 0 && bad) atomicOr(status, bad);
+}
+
+size_t cholqr2_ws_bytes(int m, int l) {
+  return align_up((size_t)m * l * 8, 256) + 6 * align_up((size_t)l * l * 8, 256) + 256 + (32u << 20);
+}
+
+// returns kOk and *ok = 1 when the CholeskyQR2 result was accepted
+int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, double* Q, long long q_rs,
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* ok) {
+  *ok = 0;
+  if (l > kCholMaxCols || m < l) return kOk;
+  TTK_REQUIRE(ws_bytes >= cholqr2_ws_bytes(m, l), kWorkspace, "cholqr2: workspace too small");
+  Arena ar(ws, ws_bytes);
+  double* Q1 = ar.take<double>((size_t)m * l);
+  double* G = ar.take<double>((size_t)l * l);
+  double* R1 = ar.take<double>((size_t)l * l);
+  double* I1 = ar.take<double>((size_t)l * l);
+  double* R2 = ar.take<double>((size_t)l * l);
+  double* I2 = ar.take<double>((size_t)l * l);
+  int* status = ar.take<int>(16);
+  void* split = ar.take<char>(32u << 20);
+  const size_t split_bytes = 32u << 20;
+  static bool attr = false;
+  if (!attr) {
+    TTK_TRY(qr_set_smem((const void*)chol_inv_kernel, 220 * 1024));
+    attr = true;
+  }
+  const size_t smem = sizeof(double) * (2 * (size_t)l * (l + 1) + 256 * (size_t)((l + 15) / 16));
+  TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
+  // G1 = Y^T Y
+  GemmProblem p = make_gemm(l, l, m, Y, y_cs, y_rs, Y, y_rs, y_cs, G, l, 1);
+  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, R1, I1, status, 0);
+  TTK_CHECK_LAUNCH();
+  // Q1 = Y R1^{-1}
+  p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
+  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  // G2 = Q1^T Q1
+  p = make_gemm(l, l, m, Q1, 1, l, Q1, l, 1, G, l, 1);
+  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, R2, I2, status, 1);
+  TTK_CHECK_LAUNCH();
+  int hstatus = 0;
+  TTK_CHECK_CUDA(cudaMemcpyAsync(&hstatus, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (hstatus != 0) return kOk;  // not accepted: caller falls back
+  // Q = Q1 R2^{-1}
+  p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
+  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  if (R) {
+    p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, R, l, 1);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  }
+  *ok = 1;
+  return kOk;
+}
+
+size_t qr_auto_ws_bytes(int m, int l) {
+  size_t a = tsqr_ws_bytes(m, l);
+  size_t b = (l <= kCholMaxCols && m >= l) ? cholqr2_ws_bytes(m, l) : 0;
+  return std::max(a, b);
+}
+
+int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (m <= 0 || l <= 0) return kOk;
+  // CholeskyQR2 pays off only for tall inputs that need a multi-panel tree
+  if (l <= kCholMaxCols && m >= 4 * l && m > 512) {
+    int ok = 0;
+    TTK_TRY(cholqr2(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, st, &ok));
+    if (ok) return kOk;
+  }
+  return tsqr(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, st);
+}
+
+}  // namespace ttk

@@ -33,12 +33,23 @@ int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* 
          long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st);
 size_t tsqr_ws_bytes(int m, int l);
 
+// QR front door: CholeskyQR2 (GEMM-based) when it is accepted, else Householder TSQR
+int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t qr_auto_ws_bytes(int m, int l);
+
 // One-sided (Hestenes) Jacobi SVD of B (k x l, row-major, ldb = l), k, l <= 128:
 // B V = U S.  Outputs, columns sorted by decreasing singular value:
 //   S[min(k,l)], U (k x min(k,l), row-major, ld = min(k,l)), and optionally
 //   V (l x min(k,l), row-major) when V != nullptr (needs l*l + k*l <= 26624 doubles).
 // Columns with zero norm give zero singular vectors.
 int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, cudaStream_t st);
+// general form: B(i,j) = B[i*b_rs + j*b_cs]; scaled_u returns U*S (the rotated
+// columns) instead of U
+int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs, double* U, double* S,
+                  double* V, bool scaled_u, cudaStream_t st);
+// whether the V-accumulating variant fits in shared memory
+bool jacobi_fits_v(int k, int l);
 
 // r = max(1, first index with sqrt(sum_{i>=r} S_i^2) <= budget) capped by
 // max_rank (<= 0: no cap) and by n; reference _truncation_rank (tt.py:203-211).

@@ -76,8 +76,8 @@ static size_t round_ws_bytes(int d, const int* dims, const int* ranks) {
   }
   for (int k = 0; k < d; ++k) {
     int r0 = ranks[k], r1 = ranks[k + 1], n = dims[k];
-    if (k > 0) qrws = std::max(qrws, tsqr_ws_bytes(n * r1, r0));
-    qrws = std::max(qrws, tsqr_ws_bytes(r0 * n, r1));
+    if (k > 0) qrws = std::max(qrws, qr_auto_ws_bytes(n * r1, r0));
+    qrws = std::max(qrws, qr_auto_ws_bytes(r0 * n, r1));
   }
   size_t small = (size_t)rmax * rmax;
   return sum + 3 * align_up(mx * 8, 256) + 4 * align_up(small * 8, 256) + align_up(qrws, 256) +
@@ -139,8 +139,8 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
   size_t qr_bytes = 0;
   for (int k = 0; k < d; ++k) {
     int r0 = ranks[k], r1 = ranks[k + 1], n = dims[k];
-    if (k > 0) qr_bytes = std::max(qr_bytes, tsqr_ws_bytes(n * r1, r0));
-    qr_bytes = std::max(qr_bytes, tsqr_ws_bytes(r0 * n, r1));
+    if (k > 0) qr_bytes = std::max(qr_bytes, qr_auto_ws_bytes(n * r1, r0));
+    qr_bytes = std::max(qr_bytes, qr_auto_ws_bytes(r0 * n, r1));
   }
   void* qws = (char*)ws + qr_off;
   ar.used = qr_off + qr_bytes;
@@ -172,7 +172,7 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = n * r1, kk = std::min(m, r0);
     // QR of C_k^T (m x r0): element (row=(i,b), col=a) at a*m + row
-    TTK_TRY(tsqr(m, r0, ck, 1, m, wk[k], 1, m, tR, qws, qr_bytes, st));
+    TTK_TRY(qr_auto(m, r0, ck, 1, m, wk[k], 1, m, tR, qws, qr_bytes, st));
     // new core k = Q^T reshaped (kk, n, r1): element (c, row) at c*m + row  -> written above
     // C_{k-1} <- C_{k-1} x_3 R^T : new[a,i,c] = sum_b C_{k-1}[a,i,b] R[c,b]
     // core k-1 is still the untouched input core at this point of the sweep
@@ -200,26 +200,154 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = r0 * n, kk = std::min(m, r1);
     // A = Q R (Q: m x kk in tq, R: kk x r1 in tR)
-    TTK_TRY(tsqr(m, r1, cur, r1, 1, tq, kk, 1, tR, qws, qr_bytes, st));
-    // R = U S V^T (U: kk x kk', S), kk' = min(kk, r1) = kk
-    TTK_TRY(jacobi_svd(kk, r1, tR, tU, tS, nullptr, st));
+    TTK_TRY(qr_auto(m, r1, cur, r1, 1, tq, kk, 1, tR, qws, qr_bytes, st));
+    const bool vt = jacobi_fits_v(r1, kk);
+    if (vt) {
+      // Jacobi on R^T (converges in far fewer sweeps for graded spectra):
+      // R^T V' = W (= U' S), so R = V' S U'^T: left vectors V' in tU, W in tC
+      TTK_TRY(jacobi_svd_ex(r1, kk, tR, 1, r1, tC, tS, tU, true, st));
+    } else {
+      // R = U S V^T (U: kk x kk, S)
+      TTK_TRY(jacobi_svd(kk, r1, tR, tU, tS, nullptr, st));
+    }
     TTK_TRY(truncation_rank_dev(tS, kk, budget, max_rank, rdev, st));
     TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, sizeof(int), cudaMemcpyDeviceToHost, st));
     TTK_CHECK_CUDA(cudaStreamSynchronize(st));
     const int rk = *(int*)pin;
     // out_k = Q U[:, :rk]  (m x rk)
     TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], rk, 1, split_ws, st));
-    // carry = U[:, :rk]^T R  (rk x r1)
-    TTK_TRY(gemm1(rk, r1, kk, tU, 1, kk, tR, r1, 1, tC, r1, 1, split_ws, st));
+    if (vt) {
+      // carry = S_r U'_r^T = W[:, :rk]^T  (rk x r1); copy-transpose via GEMM with I is
+      // avoided by reading W transposed in the next product
+    } else {
+      // carry = U[:, :rk]^T R  (rk x r1)
+      TTK_TRY(gemm1(rk, r1, kk, tU, 1, kk, tR, r1, 1, tC, r1, 1, split_ws, st));
+    }
     // next core <- carry x_1 C_{k+1}: (rk x r1) (r1 x n' r2)
     const int n1 = dims[k + 1], r2 = r[k + 2];
     double* dst = alt[k & 1];
-    TTK_TRY(gemm1(rk, n1 * r2, r1, tC, r1, 1, wk[k + 1], (long long)n1 * r2, 1, dst,
+    // carry (rk x r1): vt -> W^T with W (r1 x kk) row-major, else tC (rk x r1)
+    const long long c_ms = vt ? 1 : r1, c_ks = vt ? kk : 1;
+    TTK_TRY(gemm1(rk, n1 * r2, r1, tC, c_ms, c_ks, wk[k + 1], (long long)n1 * r2, 1, dst,
                   (long long)n1 * r2, 1, split_ws, st));
     cur = dst;
     r[k + 1] = rk;
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(out[d - 1], cur, sizeof(double) * (size_t)r[d - 1] * dims[d - 1],
+                                 cudaMemcpyDeviceToDevice, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
+  return kOk;
+}
+
+
+// --------------------------------------------------------------------------
+// Right-to-left truncation of a LEFT-ORTHOGONAL TT (cores 0..d-2 left-
+// orthonormal, e.g. the RTO output): the TT-SVD in its right-to-left form,
+// which needs no orthogonalisation sweep.  For k = d-1 .. 1:
+//   C_k (r_{k-1} x n r_k) = V S (Q U)^T  via  C_k^T = Q R,  R = U S V^T,
+//   keep r = truncation rank of S (budget rel_tol ||v|| / sqrt(d-1), cap),
+//   C_k <- (Q U_r)^T,  C_{k-1} <- C_{k-1} x_3 (R^T U_r)   [= V_r S_r].
+// Oracle: oracle/ttoracle.py truncate_left_orth.
+size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks) {
+  size_t sum = 0, mx = 0, qrws = 0;
+  int rmax = 1;
+  for (int k = 0; k < d; ++k) {
+    size_t e = core_elems(dims, ranks, k);
+    sum += align_up(e * 8, 256);
+    mx = std::max(mx, e);
+    rmax = std::max(rmax, std::max(ranks[k], ranks[k + 1]));
+    if (k > 0) qrws = std::max(qrws, qr_auto_ws_bytes(dims[k] * ranks[k + 1], ranks[k]));
+  }
+  return sum + 3 * align_up(mx * 8, 256) + 5 * align_up((size_t)rmax * rmax * 8, 256) +
+         align_up(qrws, 256) + kSplitKBytes + 131072;
+}
+
+int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
+                    int max_rank, double* const* out, int* out_ranks, void* ws, size_t ws_bytes,
+                    void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  TTK_REQUIRE(d >= 1 && rel_tol >= 0.0, kInvalidValue, "tt_truncate: bad arguments");
+  for (int k = 0; k <= d; ++k) out_ranks[k] = ranks[k];
+  if (d == 1) {
+    TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cores[0], sizeof(double) * dims[0], cudaMemcpyDeviceToDevice, st));
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    return kOk;
+  }
+  const size_t need = ttk_tt_truncate_ws_bytes(d, dims, ranks);
+  TTK_REQUIRE(ws != nullptr && ws_bytes >= need, kWorkspace, "tt_truncate: workspace %zu < %zu", ws_bytes,
+              need);
+  Arena ar(ws, ws_bytes);
+  size_t mx = 0, qrb = 0;
+  int rmax = 1;
+  for (int k = 0; k < d; ++k) {
+    mx = std::max(mx, core_elems(dims, ranks, k));
+    rmax = std::max(rmax, std::max(ranks[k], ranks[k + 1]));
+    if (k > 0) qrb = std::max(qrb, qr_auto_ws_bytes(dims[k] * ranks[k + 1], ranks[k]));
+  }
+  double* alt[2] = {ar.take<double>(mx), ar.take<double>(mx)};
+  double* tq = ar.take<double>(mx);
+  double* tR = ar.take<double>((size_t)rmax * rmax);
+  double* tU = ar.take<double>((size_t)rmax * rmax);
+  double* tS = ar.take<double>((size_t)rmax + 8);
+  double* tL = ar.take<double>((size_t)rmax * rmax);
+  double* red = ar.take<double>(16);
+  double* part = ar.take<double>(256);
+  int* rdev = ar.take<int>(8);
+  size_t qoff = align_up(ar.used, 256);
+  void* qws = (char*)ws + qoff;
+  ar.used = qoff + qrb;
+  void* split_ws = ar.take<char>(kSplitKBytes);
+  TTK_REQUIRE(split_ws != nullptr, kWorkspace, "tt_truncate: workspace too small");
+  double* pin = (double*)g_pinned.get(64);
+  TTK_REQUIRE(pin != nullptr, kCudaError, "tt_truncate: cannot allocate pinned scratch");
+  std::vector<int> r(ranks, ranks + d + 1);
+  // ||v|| = ||C_{d-1}||_F for a left-orthogonal TT
+  TTK_TRY(launch_sumsq(cores[d - 1], (long long)r[d - 1] * dims[d - 1], red, part, st));
+  TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double), cudaMemcpyDeviceToHost, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  const double nrm = std::sqrt(pin[0]);
+  if (nrm == 0.0) {
+    for (int k = 0; k < d; ++k) TTK_CHECK_CUDA(cudaMemsetAsync(out[k], 0, sizeof(double) * dims[k], st));
+    for (int k = 0; k <= d; ++k) out_ranks[k] = 1;
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    return kOk;
+  }
+  const double budget = rel_tol * nrm / std::sqrt((double)(d - 1));
+  const double* cur = cores[d - 1];
+  for (int k = d - 1; k >= 1; --k) {
+    const int r0 = r[k], n = dims[k], r1 = r[k + 1];
+    const int m = n * r1, kk = std::min(m, r0);
+    // C_k^T (m x r0) = Q R ; element (row=(i,b), col=a) of C_k^T at a*m + row
+    TTK_TRY(qr_auto(m, r0, cur, 1, m, tq, kk, 1, tR, qws, qrb, st));
+    const bool vt = jacobi_fits_v(r0, kk);
+    if (vt) {
+      // Jacobi on R^T (r0 x kk): R^T V' = W = U' S; left vectors of R = V' (tU),
+      // and L = R^T V'_r = W[:, :r] (tL, r0 x kk, leading rk columns used)
+      TTK_TRY(jacobi_svd_ex(r0, kk, tR, 1, r0, tL, tS, tU, true, st));
+    } else {
+      TTK_TRY(jacobi_svd(kk, r0, tR, tU, tS, nullptr, st));
+    }
+    TTK_TRY(truncation_rank_dev(tS, kk, budget, max_rank, rdev, st));
+    TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    const int rk = *(int*)pin;
+    // C_k <- (Q U_r)^T : out[k][c][row] = sum_j Q[row][j] U[j][c]
+    TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_ws, st));
+    long long l_ld = kk;
+    if (!vt) {
+      // L = R^T U_r (r0 x rk)
+      TTK_TRY(gemm1(r0, rk, kk, tR, 1, r0, tU, kk, 1, tL, rk, 1, split_ws, st));
+      l_ld = rk;
+    }
+    // C_{k-1} <- C_{k-1} x_3 L
+    const int p0 = r[k - 1], pn = dims[k - 1];
+    double* dst = alt[k & 1];
+    TTK_TRY(gemm1(p0 * pn, rk, r0, cores[k - 1], r0, 1, tL, l_ld, 1, dst, rk, 1, split_ws, st));
+    cur = dst;
+    r[k] = rk;
+  }
+  TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cur, sizeof(double) * (size_t)dims[0] * r[1],
                                  cudaMemcpyDeviceToDevice, st));
   TTK_CHECK_CUDA(cudaStreamSynchronize(st));
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
@@ -235,7 +363,7 @@ size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L) {
     size_t m = (size_t)L[c - 1] * dims[c - 1];
     ymax = std::max(ymax, m * L[c]);
     zmax = std::max(zmax, (size_t)L[c] * dims[c] * R[c + 1]);
-    qr = std::max(qr, tsqr_ws_bytes((int)m, L[c]));
+    qr = std::max(qr, qr_auto_ws_bytes((int)m, L[c]));
   }
   return wsum + align_up(tmax * 8, 256) + align_up(ymax * 8, 256) + 2 * align_up(zmax * 8, 256) +
          align_up(qr, 256) + kSplitKBytes + 65536;
@@ -271,7 +399,7 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
     size_t m = (size_t)L[c - 1] * dims[c - 1];
     ymax = std::max(ymax, m * L[c]);
     zmax = std::max(zmax, (size_t)L[c] * dims[c] * R[c + 1]);
-    qrb = std::max(qrb, tsqr_ws_bytes((int)m, L[c]));
+    qrb = std::max(qrb, qr_auto_ws_bytes((int)m, L[c]));
   }
   double* T = ar.take<double>(tmax);
   double* Y = ar.take<double>(ymax);
@@ -307,7 +435,7 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
     // Y (m x l) = Z (m x R_c) W_c (R_c x l)
     TTK_TRY(gemm1(m, l, rc, Z, rc, 1, W[c], l, 1, Y, l, 1, split_ws, st));
     // Q (m x l) -> out core c-1, (L_{c-1}, n_{c-1}, L_c)
-    TTK_TRY(tsqr(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st));
+    TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st));
     // M (l x R_c) = Q^T Z   (K = m, split over the long dimension)
     TTK_TRY(gemm1(l, rc, m, out[c - 1], 1, l, Z, rc, 1, Y, rc, 1, split_ws, st));
     // Z' (l x n_c R_{c+1}) = M X_c

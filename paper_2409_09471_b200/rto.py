@@ -8,7 +8,8 @@ oracle/ttoracle.py (rto_sweeps / rto_round) as the checker:
      G (streaming.py:133-136 recurrence), two chained DMMA GEMMs per core;
   2. left-to-right: Y_c = Z_c W_c, Q_c = TSQR(Y_c) (explicit Householder Q),
      M_c = Q_c^T Z_c, Z_{c+1} = M_c x_1 X_c;
-  3. TT-SVD truncation (tt_round) of the left-orthogonal result.
+  3. right-to-left TT-SVD truncation of the left-orthogonal result
+     (tt_truncate_left_orth; no orthogonalisation sweep needed).
 """
 
 from __future__ import annotations
@@ -20,7 +21,7 @@ import torch
 from . import _lib
 from .errors import ShapeMismatch
 from .streaming import TTDRM, tt_drm_new
-from .tt import RoundSpec, TTVector, attainable_ranks, tt_round
+from .tt import RoundSpec, TTVector, attainable_ranks
 
 
 def rto_ranks(dims, in_ranks, ell):
@@ -89,10 +90,33 @@ def rto_sweeps(v: TTVector, drm) -> TTVector:
     return TTVector(out)
 
 
-def tt_round_rto(v: TTVector, spec: RoundSpec, ell=None, drm=None, seed=0,
-                 zero_rel: float | None = None) -> TTVector:
+def tt_truncate_left_orth(v: TTVector, spec: RoundSpec) -> TTVector:
+    """TT-SVD truncation of a LEFT-orthogonal TT, right to left (cores 0..d-2
+    left-orthonormal, e.g. rto_sweeps output): per core one TSQR of the
+    transposed right unfolding, a Jacobi SVD of its R factor and two GEMMs;
+    budget rel_tol ||v|| / sqrt(d-1) and the max_rank cap as tt_round
+    (tt.py:357-364).  Oracle: oracle.truncate_left_orth."""
+    d = v.d
+    if d == 1:
+        return v.copy()
+    _lib.require_cuda(v.cores[0], "TT vector")
+    lib = _lib.load()
+    dev = v.device
+    dims = _lib.int_array(v.dims)
+    ranks = _lib.int_array(v.ranks)
+    outs = [torch.empty(max(c.numel(), c.shape[1]), dtype=torch.float64, device=dev) for c in v.cores]
+    out_ranks = (_lib.ctypes.c_int * (d + 1))()
+    ws = _lib.workspace(lib.ttk_tt_truncate_ws_bytes(d, dims, ranks), dev)
+    _lib.check(lib.ttk_tt_truncate(d, dims, ranks, _lib.ptr_array(v.cores), float(spec.rel_tol),
+                                   int(spec.max_rank or 0), _lib.ptr_array(outs), out_ranks, ws.data_ptr(),
+                                   ws.numel(), _lib.stream_ptr(dev)))
+    r = list(out_ranks)
+    return TTVector([outs[k][: r[k] * v.dims[k] * r[k + 1]].view(r[k], v.dims[k], r[k + 1]) for k in range(d)])
+
+
+def tt_round_rto(v: TTVector, spec: RoundSpec, ell=None, drm=None, seed=0) -> TTVector:
     """Randomized rounding: RTO sweeps at sketch rank ``ell`` (or with the
-    given DRM), then TT-SVD truncation to ``spec``.
+    given DRM), then the right-to-left TT-SVD truncation to ``spec``.
 
     ell defaults to max_rank + 20 (oversampling as in the reference's
     StreamFrame, streaming.py:175).  The DRM is drawn on the host with
@@ -104,4 +128,4 @@ def tt_round_rto(v: TTVector, spec: RoundSpec, ell=None, drm=None, seed=0,
             ell = spec.max_rank + 20
         ls = rto_ranks(v.dims, v.ranks, ell)
         drm = tt_drm_new(v.dims, ls, seed=seed, device=v.device)
-    return tt_round(rto_sweeps(v, drm), spec, zero_rel=zero_rel)
+    return tt_truncate_left_orth(rto_sweeps(v, drm), spec)

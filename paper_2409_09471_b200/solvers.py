@@ -20,11 +20,11 @@ import torch
 
 from . import _lib
 from .errors import ShapeMismatch
-from .rto import rto_ranks, rto_sweeps
+from .rto import rto_ranks, rto_sweeps, tt_truncate_left_orth
 from .sketch import KhatriRaoSketch, kr_apply
 from .streaming import StreamFrame, combine_pairs, stream_recover, stream_sketch, tt_drm_new
 from .tt import (ZERO_REL, RoundSpec, TTOperator, TTVector, tt_combine, tt_dots, tt_matvec, tt_norm,
-                 tt_norm_left_orthogonal, tt_round, tt_scale)
+                 tt_norm_orthogonal, tt_round, tt_scale)
 
 PHASES = ("matvec", "sketch", "orth", "round", "lsq", "recovery")
 
@@ -39,7 +39,8 @@ class SolverConfig:
 
     rounding      "svd" (reference TT-SVD tt_round) or "rto" (randomize-then-
                   orthogonalize sweeps at sketch rank max_rank + rto_oversampling,
-                  one TT-DRM per solve drawn with seed+2, then TT-SVD truncation)
+                  one TT-DRM per solve drawn with seed+2, then the right-to-left
+                  TT-SVD truncation of the left-orthogonal result)
     zero_rel      the reference's rounding zero test (tt.py:348-356); None
                   disables it (reference quirk Q1 -- needed at BASELINE sizes)
     """
@@ -208,12 +209,14 @@ class _SketchedRun:
     def _round(self, v, spec):
         if self.cfg.rounding == "svd":
             return tt_round(v, spec, zero_rel=self.cfg.zero_rel)
-        return tt_round(rto_sweeps(v, self.rto_drm.cores), spec, zero_rel=self.cfg.zero_rel)
+        return tt_truncate_left_orth(rto_sweeps(v, self.rto_drm.cores), spec)
 
-    @staticmethod
-    def _last_core_norm(v):
-        """Rounded vectors are left-orthogonal: ||v|| = ||last core||_F."""
-        return tt_norm_left_orthogonal(v)
+    def _rounded_norm(self, v):
+        """||v|| of a rounded vector from the core carrying the norm: the last
+        core after tt_round (left-orthogonal), core 0 after the right-to-left
+        truncation of the rto mode (right-orthogonal)."""
+        core = 0 if (self.cfg.rounding == "rto" and self.cfg.combine_mode == "explicit") else -1
+        return tt_norm_orthogonal(v, core)
 
     def run(self):
         cfg = self.cfg
@@ -267,7 +270,7 @@ class _SketchedRun:
                 comb = combine_pairs([pv] + [self.pairs[gi] for gi, _ in self.window],
                                      [1.0] + [-h for h in hs])
                 vt = stream_recover(comb, spec_basis, zero_rel=cfg.zero_rel)
-            hnew = self._last_core_norm(vt)
+            hnew = self._rounded_norm(vt)
             lucky = hnew <= _BREAKDOWN_FACTOR * norm_av
             if not lucky:
                 vnew = tt_scale(vt, 1.0 / hnew)

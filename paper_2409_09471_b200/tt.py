@@ -403,15 +403,22 @@ def tt_round(v: TTVector, spec: RoundSpec, zero_rel: float | None = ZERO_REL) ->
     return TTVector(cores)
 
 
-def tt_norm_left_orthogonal(v: TTVector) -> float:
-    """||v|| of a TT whose cores 0..d-2 are left-orthonormal (the output of
-    tt_round / rto_sweeps): the Frobenius norm of the last core, one fixed-order
-    device reduction instead of a full dot sweep."""
+def tt_norm_orthogonal(v: TTVector, core: int = -1) -> float:
+    """||v|| of an orthogonalised TT: the Frobenius norm of the core that
+    carries it (last core after tt_round / rto_sweeps, which leave cores
+    0..d-2 left-orthonormal; core 0 after tt_truncate_left_orth, which leaves
+    cores 1..d-1 right-orthonormal).  One fixed-order device reduction
+    instead of a full dot sweep."""
     _check_cuda_vec(v)
     lib = _lib.load()
-    c = v.cores[-1]
+    c = v.cores[core]
     out = torch.empty(1, dtype=torch.float64, device=v.device)
     ws = _lib.workspace(4096, v.device)
     _lib.check(lib.ttk_sumsq(c.data_ptr(), c.numel(), out.data_ptr(), ws.data_ptr(), ws.numel(),
                              _lib.stream_ptr(v.device)))
     return float(math.sqrt(max(out.item(), 0.0)))
+
+
+def tt_norm_left_orthogonal(v: TTVector) -> float:
+    """||v|| when cores 0..d-2 are left-orthonormal (norm in the last core)."""
+    return tt_norm_orthogonal(v, -1)

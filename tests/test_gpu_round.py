@@ -155,9 +155,20 @@ def test_rto_vs_oracle(cuda):
     assert O.rel_diff(tt_np(got), want) <= 1e-10
     # full randomized rounding (sweeps + truncation)
     want_r = O.rto_round(x, O.slice_drm(drm, ls), 1e-6, 15)
-    got_r = T.tt_round(got, T.RoundSpec(1e-6, 15), zero_rel=None)
+    got_r = T.tt_truncate_left_orth(got, T.RoundSpec(1e-6, 15))
     assert got_r.ranks == tuple([1] + [c.shape[2] for c in want_r])
     assert O.rel_diff(tt_np(got_r), want_r) <= 1e-10
+
+
+@pytest.mark.parametrize("tol,cap", [(1e-8, None), (1e-3, None), (0.0, 12), (1e-10, 25)])
+def test_truncate_left_orth_vs_oracle(cuda, tol, cap):
+    dims = [12, 9, 16, 7, 11, 10]
+    x = O.tt_random(dims, [8, 14, 10, 9, 6], seed=3)
+    lo = O.rto_sweeps(O.add(x, O.scale(x, 0.5)), O.drm_new(dims, [12, 20, 20, 12, 10], seed=4))
+    want = O.truncate_left_orth(lo, tol, cap)
+    got = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(tol, cap))
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.rel_diff(tt_np(got), want) <= 1e-10
 
 
 def test_rto_config2_shape(cuda):

@@ -130,6 +130,24 @@ def test_oracle_rto_exactness_kat():
     assert O.rel_diff(out, O.scale(x, 1.25)) <= 1e-12
     r = O.rto_round(big, O.slice_drm(drm, ls), 1e-12)
     assert [c.shape[2] for c in r][:-1] == [c.shape[2] for c in x][:-1]
+    assert O.rel_diff(r, O.scale(x, 1.25)) <= 1e-12
+
+
+def test_oracle_truncate_left_orth_matches_tt_round_when_exact():
+    """On a left-orthogonal input the right-to-left truncation and the
+    reference-order TT-SVD agree whenever the discarded mass is ~0, and both
+    honour the rel_tol contract otherwise."""
+    dims = [5, 6, 4, 5]
+    a = O.tt_random(dims, [4, 6, 4], seed=1)
+    x = O.add(a, O.scale(a, 2.0))
+    lo = O.rto_sweeps(x, O.drm_new(dims, [5, 12, 5], seed=2))  # left-orthogonal, exact (rank 4,6,4 <= 5,12,5)
+    t1 = O.truncate_left_orth(lo, 1e-12)
+    t2 = O.tt_round(lo, 1e-12, zero_rel=None)
+    assert [c.shape for c in t1] == [c.shape for c in t2]
+    assert O.rel_diff(t1, t2) <= 1e-12
+    for tol in (1e-1, 1e-2):
+        t = O.truncate_left_orth(lo, tol)
+        assert O.rel_diff(t, lo) <= tol
 
 
 def test_oracle_rto_dense_randomized_svd():
