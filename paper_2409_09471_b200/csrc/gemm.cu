@@ -1,6 +1,8 @@
 // Host launch logic for the grouped fp64 DMMA GEMM (see gemm.cuh).
 #include "gemm.cuh"
 
+#include <algorithm>
+
 namespace ttk {
 
 __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G) {
@@ -24,10 +26,24 @@ __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G) {
 
 namespace {
 
-enum TileCfg { kT128x128 = 0, kT128x64 = 1, kT64x64 = 2, kT64x32 = 3 };
+enum TileCfg { kT128x128 = 0, kT128x64 = 1, kT64x64 = 2, kT64x32 = 3, kT128x80 = 4 };
 
 struct CfgDims { int bm, bn; };
-constexpr CfgDims kDims[] = {{128, 128}, {128, 64}, {64, 64}, {64, 32}};
+constexpr CfgDims kDims[] = {{128, 128}, {128, 64}, {64, 64}, {64, 32}, {128, 80}};
+
+// C = A B  <=>  C^T = B^T A^T: make the output's contiguous direction the
+// column (n) index so the epilogue stores are coalesced (1-level maps only)
+void normalize_output(GemmProblem& p) {
+  const int big = 1 << 30;
+  if (!(p.c_ns0 != 1 && p.c_ms0 == 1)) return;
+  if (p.a_mdiv != big || p.b_ndiv != big || p.c_mdiv != big || p.c_ndiv != big) return;
+  GemmProblem q = p;
+  q.M = p.N; q.N = p.M;
+  q.A = p.B; q.a_ms0 = p.b_ns0; q.a_ks = p.b_ks;
+  q.B = p.A; q.b_ns0 = p.a_ms0; q.b_ks = p.a_ks;
+  q.c_ms0 = p.c_ns0; q.c_ns0 = p.c_ms0;
+  p = q;
+}
 
 TileCfg pick_cfg(const GemmProblem* probs, int count) {
   // pick by the largest problem; small-N problems use narrower tiles
@@ -39,6 +55,7 @@ TileCfg pick_cfg(const GemmProblem* probs, int count) {
   long tiles128 = 0;
   for (int i = 0; i < count; ++i) tiles128 += (long)ceil_div(probs[i].M, 128) * ceil_div(probs[i].N, 128);
   if (bn <= 32 && bm >= 64) return kT64x32;
+  if (bm >= 512 && bn > 64 && bn <= 80) return kT128x80;
   if (bm >= 128 && bn >= 128 && tiles128 >= kNumSMs) return kT128x128;
   if (bm >= 128 && bn > 32 && bn <= 64) return kT128x64;
   if (bm >= 128 && bn >= 96) return tiles128 >= kNumSMs / 2 ? kT128x128 : kT64x64;
@@ -103,7 +120,7 @@ size_t gemm_group_ws_bytes(const GemmProblem* probs_in, int count, bool allow_sp
   for (int base = 0; base < count; base += kMaxGroup) {
     int c = std::min(kMaxGroup, count - base);
     GemmProblem tmp[kMaxGroup];
-    for (int i = 0; i < c; ++i) tmp[i] = probs_in[base + i];
+    for (int i = 0; i < c; ++i) { tmp[i] = probs_in[base + i]; normalize_output(tmp[i]); }
     TileCfg cfg = pick_cfg(tmp, c);
     size_t pe; int tt;
     plan(tmp, c, cfg, allow_split, &pe, &tt);
@@ -121,7 +138,9 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
     for (int i = 0; i < c; ++i) {
       const GemmProblem& p = probs[base + i];
       if (p.M <= 0 || p.N <= 0) continue;
-      g.p[nonempty++] = p;
+      g.p[nonempty] = p;
+      normalize_output(g.p[nonempty]);
+      ++nonempty;
     }
     if (nonempty == 0) continue;
     g.count = nonempty;
@@ -147,6 +166,7 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
       case kT128x128: rc = launch_cfg<128, 128, 2, 4>(g, st); break;
       case kT128x64: rc = launch_cfg<128, 64, 2, 2>(g, st); break;
       case kT64x64: rc = launch_cfg<64, 64, 2, 2>(g, st); break;
+      case kT128x80: rc = launch_cfg<128, 80, 4, 2>(g, st); break;
       default: rc = launch_cfg<64, 32, 2, 1>(g, st); break;
     }
     if (rc != kOk) return rc;

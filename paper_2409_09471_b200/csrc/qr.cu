@@ -527,11 +527,19 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
         q = qi - 1 + rnd; if (q >= le - 1) q -= le - 1; q += 1;
         double* cp = C + p * ldc;
         double* cq = C + q * ldc;
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (int r = gl; r < kk; r += kSvdGroup) {
+        double a = 0.0, b = 0.0, g = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
+        int r = gl;
+        for (; r + kSvdGroup < kk; r += 2 * kSvdGroup) {  // two independent chains
+          const double x = cp[r], y = cq[r];
+          const double x2 = cp[r + kSvdGroup], y2 = cq[r + kSvdGroup];
+          a += x * x; b += y * y; g += x * y;
+          a2 += x2 * x2; b2 += y2 * y2; g2 += x2 * y2;
+        }
+        if (r < kk) {
           const double x = cp[r], y = cq[r];
           a += x * x; b += y * y; g += x * y;
         }
+        a += a2; b += b2; g += g2;
 #pragma unroll
         for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
           a += __shfl_xor_sync(gmask, a, o);

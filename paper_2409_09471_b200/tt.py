@@ -258,8 +258,10 @@ def _check_cuda_vec(v: TTVector, what="TT vector"):
     _lib.require_cuda(v.cores[0], what)
 
 
-def tt_matvec(a: TTOperator, v: TTVector) -> TTVector:
-    """Apply the operator core by core; output ranks multiply, no rounding (tt.py:302-314)."""
+def tt_matvec(a: TTOperator, v: TTVector, out=None) -> TTVector:
+    """Apply the operator core by core; output ranks multiply, no rounding (tt.py:302-314).
+
+    ``out``: optional preallocated output cores (reused across calls)."""
     if a.col_dims != v.dims:
         raise ShapeMismatch(f"operator col_dims {a.col_dims} do not match {v.dims}")
     _check_cuda_vec(v)
@@ -268,8 +270,11 @@ def tt_matvec(a: TTOperator, v: TTVector) -> TTVector:
     rho, r = list(a.ranks), list(v.ranks)
     m, n = list(a.row_dims), list(a.col_dims)
     dev = v.device
-    out = [torch.empty((r[k] * rho[k], m[k], r[k + 1] * rho[k + 1]), dtype=torch.float64, device=dev)
-           for k in range(d)]
+    shapes = [(r[k] * rho[k], m[k], r[k + 1] * rho[k + 1]) for k in range(d)]
+    if out is None:
+        out = [torch.empty(sh, dtype=torch.float64, device=dev) for sh in shapes]
+    elif [tuple(c.shape) for c in out] != shapes:
+        raise ShapeMismatch("preallocated matvec output has the wrong shapes")
     _lib.check(lib.ttk_matvec(d, _lib.int_array(rho), _lib.int_array(m), _lib.int_array(n),
                               _lib.int_array(r), _lib.ptr_array(a.op_cores), _lib.ptr_array(v.cores),
                               _lib.ptr_array(out), _lib.stream_ptr(dev)))
