@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--extras", action="store_true", help="also time configs 1, 2, 4 and 5")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--workload", default="cfg3", choices=["cfg3", "kr", "solver"],
+                   help="cfg3 (headline, replicas), kr (config 4, rows sharded over ranks + all-gather), "
+                        "solver (config 5, 8 right-hand sides sharded over ranks)")
     return p.parse_args()
 
 
@@ -400,10 +403,125 @@ def run_extras(T, torch, dev):
     return out
 
 
+def _dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    return world, rank, local, dev
+
+
+def _max_over_ranks(torch, dev, world, v):
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_kr(args):
+    """Config 4: 64 TTs (d=20, n=64, r=100) sketched with s=512 Khatri-Rao rows,
+    rows sharded over the ranks, NCCL all-gather of the row blocks."""
+    import torch
+    import torch.distributed as dist
+    import paper_2409_09471_b200 as T
+    from paper_2409_09471_b200 import _lib, configs
+    from paper_2409_09471_b200.parallel import kr_apply_sharded, row_partition
+    world, rank, local, dev = _dist_setup()
+    lib = _lib.load()
+    C = configs.config4()
+    sk = T.KhatriRaoSketch(C["factors"], device=dev)
+    vs = [T.TTVector(v, device=dev) for v in C["vecs"]]
+    flops_total = sum(configs.kr_flops(C["rows"], C["dims"], list(v.ranks)) for v in vs)
+    lo, hi = row_partition(C["rows"], world)[rank]
+    for _ in range(max(args.warmup, 3)):
+        out = kr_apply_sharded(sk, vs, rank, world)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = lib.ttk_launch_count()
+    with ClockSampler(local) as clocks:
+        e0.record(st)
+        for _ in range(args.steps):
+            out = kr_apply_sharded(sk, vs, rank, world)
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = _max_over_ranks(torch, dev, world, e0.elapsed_time(e1) / args.steps)
+    launches = (lib.ttk_launch_count() - n0) // args.steps
+    line = {"metric": "Khatri-Rao sketch GFLOP/s (fp64), config 4", "value": flops_total / (ms * 1e-3) / 1e9,
+            "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "config4: s=512 rows, 64 TTs d=20 n=64 r=100; rows sharded, NCCL all-gather",
+                       "rows_per_rank": hi - lo, "flops_per_step": flops_total},
+            "gpu_launches": int(launches), "clocks": clocks.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_solver(args):
+    """Config 5: 8 right-hand sides of the d=50, n=256 anisotropic Laplacian,
+    RHS j on rank j mod G (no device collective), randomized rounding."""
+    import torch
+    import torch.distributed as dist
+    import paper_2409_09471_b200 as T
+    from paper_2409_09471_b200 import configs
+    from paper_2409_09471_b200.parallel import solve_rhs_sharded
+    world, rank, local, dev = _dist_setup()
+
+    def solve_one(j):
+        C = configs.config5(j)
+        cfg = T.SolverConfig(**C["cfg"], zero_rel=None, rounding="rto")
+        a = T.TTOperator(C["op"], device=dev)
+        b = T.TTVector(C["b"], device=dev)
+        sk = T.kr_sketch_new(C["dims"], cfg.sketch_rows, seed=C["sketch_seed"], device=dev)
+        frame = T.make_solver_frame(b, cfg, seed=C["frame_seed"])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, rep = T.tt_sgmres(a, b, None, cfg, sk, frame)
+        wall = time.perf_counter() - t0
+        return {"iterations": rep.iterations, "converged": rep.converged, "wall_s": wall,
+                "res_sketched": rep.res_sketched[-1], "peak_rank": rep.peak_rank,
+                "time_to_1e-6_s": rep.time_to_tol.get(1e-6)}
+    n_rhs = 8
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clocks:
+        reports, agg = solve_rhs_sharded(n_rhs, rank, world, solve_one)
+    line = {"metric": "TT-sGMRES iterations/s (fp64), config 5, 8 RHS", "value": agg["it_per_s"],
+            "unit": "it/s", "n_gpus": world, "steps": n_rhs, "warmup": 0,
+            "ms_per_step": agg["max_wall_s"] * 1e3 / max(1, n_rhs), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config5: d=50 n=256, ell=3, s=120, maxit=60, tol=1e-8, cap 100, RTO rounding; "
+                                   "RHS j on rank j mod G", "parallelism": f"rhs x{world}"},
+            "reports": reports, "clocks": clocks.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "kr":
+        return run_kr(args)
+    if args.workload == "solver":
+        return run_solver(args)
     return run_b200(args)
 
 
