@@ -13,8 +13,18 @@ __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G) {
     const size_t mn = (size_t)P.M * P.N;
     for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < mn;
          e += (size_t)gridDim.x * blockDim.x) {
+      // fixed summation order; loads issued 8 at a time so the L2 latency of the
+      // partials overlaps instead of chaining
       double s = 0.0;
-      for (int k = 0; k < P.splits; ++k) s += P.partial[k * mn + e];  // fixed order
+      int k = 0;
+      for (; k + 8 <= P.splits; k += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(P.partial + (size_t)(k + u) * mn + e);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; k < P.splits; ++k) s += __ldcg(P.partial + (size_t)k * mn + e);
       int m = (int)(e / P.N), n = (int)(e % P.N);
       double* dst = P.C + cmap_m(P, m) + cmap_n(P, n);
       double v = P.alpha * s;
@@ -171,7 +181,11 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
     }
     if (rc != kOk) return rc;
     if (pe > 0) {
-      gemm_splitk_reduce_kernel<<<2 * kNumSMs, 256, 0, st>>>(g);
+      size_t maxmn = 0;
+      for (int i = 0; i < g.count; ++i)
+        if (g.p[i].splits > 1) maxmn = std::max(maxmn, (size_t)g.p[i].M * g.p[i].N);
+      const int rblocks = (int)std::min<size_t>((maxmn + 127) / 128, 4 * kNumSMs);
+      gemm_splitk_reduce_kernel<<<std::max(rblocks, 1), 128, 0, st>>>(g);
       TTK_CHECK_LAUNCH();
     }
   }
