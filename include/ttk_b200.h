@@ -116,6 +116,12 @@ int ttk_kr_sketch_path(int path, int d, const int* n, int s_lo, int s_hi, const 
 int ttk_qr(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
            long long q_cs, double* R, void* ws, size_t ws_bytes, void* stream);
 size_t ttk_qr_ws_bytes(int m, int l);
+/* the rounding drivers' QR: shifted CholeskyQR2/3 (GEMM-based, accepted only if the
+ * Gram of the computed Q is within 1e-3 of I before the last pass), Householder
+ * TSQR otherwise (exactly rank-deficient inputs).  Same contract as ttk_qr;
+ * synchronises `stream` for the acceptance test. */
+int ttk_qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+                long long q_cs, double* R, void* ws, size_t ws_bytes, void* stream);
 /* one-sided Jacobi SVD of B (k x l, row-major, k,l <= 128): B V = U S with
  * S[min(k,l)] descending, U (k x min(k,l)), V (l x min(k,l)) if V != NULL. */
 int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream);

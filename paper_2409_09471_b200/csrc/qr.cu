@@ -668,7 +668,14 @@ using namespace ttk;
 
 extern "C" {
 
-size_t ttk_qr_ws_bytes(int m, int l) { return tsqr_ws_bytes(m, l); }
+size_t ttk_qr_ws_bytes(int m, int l) { return qr_auto_ws_bytes(m, l); }
+
+// QR front door used by the rounding drivers: shifted CholeskyQR2/3 when
+// accepted, Householder TSQR otherwise (same contract as ttk_qr)
+int ttk_qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+                long long q_cs, double* R, void* ws, size_t ws_bytes, void* stream) {
+  return qr_auto(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, (cudaStream_t)stream);
+}
 
 int ttk_qr(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
            long long q_cs, double* R, void* ws, size_t ws_bytes, void* stream) {
@@ -705,7 +712,8 @@ constexpr int kCholMaxCols = 112;
 // max|G - I| > 1e-3.
 __global__ void __launch_bounds__(1024, 1)
     chol_inv_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
-                    double* __restrict__ Rinv, int* status, int check_identity) {
+                    double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
+                    double tiny_rel) {
   extern __shared__ double sm[];
   const int ld = l + 1;
   double* A = sm;               // l x ld, becomes R (upper)
@@ -731,7 +739,21 @@ __global__ void __launch_bounds__(1024, 1)
     if (tx == 0) gmax_s = g;
   }
   __syncthreads();
-  const double tiny = gmax_s * 1e-28 + 1e-300;  // pivot floor (kappa(Y) up to ~1e14)
+  if (shift_rel > 0.0) {
+    // shifted CholeskyQR (Fukaya et al.): G + s I with s = shift_rel * trace(G)
+    __shared__ double tr_s;
+    if (ty == 0) {
+      double t = 0.0;
+      for (int i = tx; i < l; i += 32) t += A[i * ld + i];
+      t = warp_sum(t);
+      if (tx == 0) tr_s = t;
+    }
+    __syncthreads();
+    const double sh = shift_rel * tr_s;
+    for (int i = tid; i < l; i += nt) A[i * ld + i] += sh;
+    __syncthreads();
+  }
+  const double tiny = gmax_s * tiny_rel + 1e-300;  // pivot^2 floor relative to max diag(G)
   // right-looking Cholesky on the upper triangle; row j is scaled afterwards
   // (A[i][c] -= A[j][i] A[j][c] / A[j][j]), one barrier per step
   for (int j = 0; j < l; ++j) {
@@ -827,16 +849,45 @@ __global__ void __launch_bounds__(1024, 1)
   if (tid == 0 && bad) atomicOr(status, bad);
 }
 
+__global__ void copy_strided_kernel(int m, int l, const double* __restrict__ X, long long x_rs,
+                                    long long x_cs, double* __restrict__ Y, long long y_rs, long long y_cs) {
+  const long long n = (long long)m * l;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    int r, c;
+    if (y_cs == 1) { r = (int)(e / l); c = (int)(e - (long long)r * l); }
+    else { c = (int)(e / m); r = (int)(e - (long long)c * m); }
+    Y[r * y_rs + c * y_cs] = X[r * x_rs + c * x_cs];
+  }
+}
+
+int copy_strided(int m, int l, const double* X, long long x_rs, long long x_cs, double* Y, long long y_rs,
+                 long long y_cs, cudaStream_t st) {
+  const long long n = (long long)m * l;
+  if (n <= 0) return kOk;
+  copy_strided_kernel<<<(int)std::min<long long>((n + 255) / 256, 4 * kNumSMs), 256, 0, st>>>(
+      m, l, X, x_rs, x_cs, Y, y_rs, y_cs);
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
 size_t cholqr2_ws_bytes(int m, int l) {
   return align_up((size_t)m * l * 8, 256) + 6 * align_up((size_t)l * l * 8, 256) + 256 + (32u << 20);
 }
 
-// returns kOk and *ok = 1 when the CholeskyQR2 result was accepted
+// Shifted CholeskyQR2/3.  Pass 1 factors G + s I with s = 11 (m l + l(l+1)) u
+// trace(G) (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020), so it
+// succeeds for kappa(Y) up to ~1e16 and leaves kappa(Q1) <~ 1e4; pass 2 is
+// plain CholeskyQR.  If Q1 was already orthonormal to 1e-3 (||G2 - I||_max),
+// Q2 is orthonormal to working precision and we stop; otherwise a third pass
+// (checked the same way) finishes.  Exactly rank-deficient inputs fail the
+// checks and the caller falls back to Householder TSQR.
+// returns kOk and *ok = 1 when the result was accepted
 int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, double* Q, long long q_rs,
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* ok) {
   *ok = 0;
   if (l > kCholMaxCols || m < l) return kOk;
-  TTK_REQUIRE(ws_bytes >= cholqr2_ws_bytes(m, l), kWorkspace, "cholqr2: workspace too small");
+  TTK_REQUIRE(ws_bytes >= cholqr2_ws_bytes(m, l), kWorkspace, "cholqr: workspace too small");
   Arena ar(ws, ws_bytes);
   double* Q1 = ar.take<double>((size_t)m * l);
   double* G = ar.take<double>((size_t)l * l);
@@ -853,32 +904,65 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     attr = true;
   }
   const size_t smem = sizeof(double) * (2 * (size_t)l * (l + 1) + 256 * (size_t)((l + 15) / 16));
-  TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, sizeof(int), st));
-  // G1 = Y^T Y
-  GemmProblem p = make_gemm(l, l, m, Y, y_cs, y_rs, Y, y_rs, y_cs, G, l, 1);
-  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-  chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, R1, I1, status, 0);
-  TTK_CHECK_LAUNCH();
-  // Q1 = Y R1^{-1}
-  p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
-  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-  // G2 = Q1^T Q1
-  p = make_gemm(l, l, m, Q1, 1, l, Q1, l, 1, G, l, 1);
-  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-  chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, R2, I2, status, 1);
-  TTK_CHECK_LAUNCH();
-  int hstatus = 0;
-  TTK_CHECK_CUDA(cudaMemcpyAsync(&hstatus, status, sizeof(int), cudaMemcpyDeviceToHost, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (hstatus != 0) return kOk;  // not accepted: caller falls back
-  // Q = Q1 R2^{-1}
-  p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
-  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-  if (R) {
-    p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, R, l, 1);
+  const double shift_rel = 11.0 * ((double)m * l + (double)l * (l + 1)) * 1.1102230246251565e-16;
+  GemmProblem p;
+  // one "pass": Gram of X (m x l, strides), chol (+shift) into (Rk, Ik), status bits into st_slot
+  auto gram_chol = [&](const double* X, long long x_rs, long long x_cs, double* Rk, double* Ik, int* st_slot,
+                       int check, double shift, double tiny) -> int {
+    GemmProblem g = make_gemm(l, l, m, X, x_cs, x_rs, X, x_rs, x_cs, G, l, 1);
+    TTK_TRY(gemm_group_launch(&g, 1, split, split_bytes, st));
+    chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, Rk, Ik, st_slot, check, shift, tiny);
+    TTK_CHECK_LAUNCH();
+    return kOk;
+  };
+  int hs[4] = {0, 0, 0, 0};
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool shifted = attempt == 1;
+    TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
+    // pass 1: unshifted CholeskyQR accepted only for kappa(Y) <~ 3e7 (pivot floor 1e-15);
+    // the retry shifts G by 11 (m l + l(l+1)) u trace(G) (sCholQR3, Fukaya et al. 2020)
+    TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, shifted ? shift_rel : 0.0, shifted ? 1e-28 : 1e-15));
+    p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    // pass 2 on Q1; its Gram's distance to I decides whether a third pass is needed
+    TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
+    TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    if ((hs[0] & 1) || (hs[1] & 1)) {
+      if (shifted) return kOk;  // exactly deficient: Householder fallback
+      continue;                 // retry with the shift
+    }
+    // Q2 = Q1 R2^{-1} -> Q, R12 = R2 R1
+    p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    if ((hs[1] & 2) == 0) {
+      if (R) {
+        p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, R, l, 1);
+        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      }
+      *ok = 1;
+      return kOk;
+    }
+    // pass 3 on Q2 (in Q): Q = Q2 R3^{-1}
+    p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, I1, l, 1);  // R12 into I1's slot
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    TTK_TRY(gram_chol(Q, q_rs, q_cs, R2, I2, status + 2, 1, 0.0, 1e-28));
+    TTK_CHECK_CUDA(cudaMemcpyAsync(hs + 2, status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    if (hs[2] != 0) {
+      if (shifted) return kOk;
+      continue;
+    }
+    p = make_gemm(m, l, l, Q, q_rs, q_cs, I2, l, 1, Q1, l, 1);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    TTK_TRY(copy_strided(m, l, Q1, l, 1, Q, q_rs, q_cs, st));
+    if (R) {
+      p = make_gemm(l, l, l, R2, l, 1, I1, l, 1, R, l, 1);
+      TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    }
+    *ok = 1;
+    return kOk;
   }
-  *ok = 1;
   return kOk;
 }
 

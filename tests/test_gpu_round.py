@@ -17,7 +17,7 @@ def tt_np(v):
     return [c.cpu().numpy() for c in v.cores]
 
 
-def run_qr(A, cuda, transposed=False):
+def run_qr(A, cuda, transposed=False, auto=False):
     lib = _lib.load()
     m, l = A.shape
     k = min(m, l)
@@ -30,8 +30,9 @@ def run_qr(A, cuda, transposed=False):
     Q = torch.empty((m, k), dtype=torch.float64, device=cuda)
     R = torch.empty((k, l), dtype=torch.float64, device=cuda)
     ws = _lib.workspace(lib.ttk_qr_ws_bytes(m, l), cuda)
-    _lib.check(lib.ttk_qr(m, l, At.data_ptr(), a_rs, a_cs, Q.data_ptr(), k, 1, R.data_ptr(), ws.data_ptr(),
-                          ws.numel(), _lib.stream_ptr(cuda)))
+    fn = lib.ttk_qr_auto if auto else lib.ttk_qr
+    _lib.check(fn(m, l, At.data_ptr(), a_rs, a_cs, Q.data_ptr(), k, 1, R.data_ptr(), ws.data_ptr(),
+                  ws.numel(), _lib.stream_ptr(cuda)))
     return Q.cpu().numpy(), R.cpu().numpy()
 
 
@@ -68,6 +69,30 @@ def test_tsqr_tree_rank_deficient(cuda):
     Q, R = run_qr(A, cuda)
     assert np.abs(Q.T @ Q - np.eye(120)).max() <= 1e-12
     assert np.linalg.norm(Q @ R - A) <= 1e-13 * np.linalg.norm(A) * 10
+
+
+@pytest.mark.parametrize("kind", ["gauss", "graded1e6", "graded1e12", "graded1e15", "dup", "zero"])
+@pytest.mark.parametrize("trans", [False, True])
+def test_qr_auto_cholqr_paths(cuda, kind, trans):
+    """Shifted CholeskyQR2/3 fast path and its Householder fallback: Q orthonormal,
+    A = QR to working precision, for well-, ill- and exactly-deficient inputs."""
+    rng = np.random.default_rng(11)
+    m, l = 12800, 80
+    if kind == "gauss":
+        A = rng.standard_normal((m, l))
+    elif kind.startswith("graded"):
+        kap = float(kind[len("graded"):])
+        U, _ = np.linalg.qr(rng.standard_normal((m, l)))
+        V, _ = np.linalg.qr(rng.standard_normal((l, l)))
+        A = (U * np.logspace(0, -np.log10(kap), l)) @ V.T
+    elif kind == "dup":
+        B = rng.standard_normal((m, 40))
+        A = np.concatenate([B, B], axis=1)
+    else:
+        A = np.zeros((m, l))
+    Q, R = run_qr(A, cuda, transposed=trans, auto=True)
+    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-12
+    assert np.linalg.norm(Q @ R - A) <= 1e-13 * max(np.linalg.norm(A), 1e-300) * 10 + (0 if kind != "zero" else 1e-300)
 
 
 def test_tsqr_transposed_input(cuda):

@@ -23,6 +23,15 @@ elif which == "cfg2":
     drm = [torch.as_tensor(g, device=dev) for g in C["drm"]]
     def step():
         return T.tt_truncate_left_orth(T.rto_sweeps(x, drm), T.RoundSpec(0.0, 40))
+if which == "cfg5":
+    C = configs.config5(0)
+    cfg = T.SolverConfig(**{**C["cfg"], "maxit": 6}, zero_rel=None, rounding="rto")
+    a = T.TTOperator(C["op"], device=dev); b = T.TTVector(C["b"], device=dev)
+    sk = T.kr_sketch_new(C["dims"], cfg.sketch_rows, seed=C["sketch_seed"], device=dev)
+    frame = T.make_solver_frame(b, cfg, seed=C["frame_seed"])
+    def step():
+        _, rep = T.tt_sgmres(a, b, None, cfg, sk, frame)
+        print({k: round(v, 4) for k, v in rep.phase_totals().items()}, rep.basis_rank)
 step()
 torch.cuda.synchronize()
 from paper_2409_09471_b200 import _lib
