@@ -710,6 +710,71 @@ constexpr int kCholMaxCols = 112;
 // one CTA: upper Cholesky G = R^T R of an l x l SPD matrix and R^{-1};
 // status |= 1 on a non-positive / tiny pivot, |= 2 if check_identity and
 // max|G - I| > 1e-3.
+// X = inv(A) for the upper-triangular l x l A (row stride ld) held in shared
+// memory; Tb: 256 * ceil(l/16) doubles of scratch.  All threads of the CTA.
+__device__ void tri_inv_blocked(const double* A, double* X, double* Tb, int ld, int l) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int ty = tid >> 5, tx = tid & 31, nty = nt >> 5;
+  // R^{-1} by blocks of 16: (1) every warp inverts one 16x16 diagonal block
+  // (forward over columns, 16 dependent steps), (2) off-diagonal blocks by
+  // block back-substitution X_IJ = -inv(R_II) sum_{I<K<=J} R_IK X_KJ, one
+  // block-diagonal distance at a time (all blocks of a distance in parallel).
+  {
+    const int nb = (l + 15) / 16;
+    for (int e = tid; e < l * l; e += nt) {
+      int r = e / l, c = e - r * l;
+      X[r * ld + c] = 0.0;
+    }
+    __syncthreads();
+    for (int bI = ty; bI < nb; bI += nty) {
+      const int o = bI * 16, bs = min(16, l - o);
+      // lane tx owns column tx of the block; solve R_II x = e_tx by back substitution
+      if (tx < bs) {
+        double xr[16];
+#pragma unroll
+        for (int i = 15; i >= 0; --i) {
+          if (i < bs) {
+            double acc = (i == tx) ? 1.0 : 0.0;
+#pragma unroll
+            for (int k = i + 1; k < 16; ++k)
+              if (k < bs) acc -= A[(o + i) * ld + o + k] * xr[k];
+            xr[i] = (i <= tx) ? acc / A[(o + i) * ld + o + i] : 0.0;
+          } else {
+            xr[i] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < bs) X[(o + i) * ld + o + tx] = xr[i];
+      }
+    }
+    __syncthreads();
+    for (int dist = 1; dist < nb; ++dist) {
+      const int nblk = nb - dist;
+      for (int e = tid; e < nblk * 256; e += nt) {
+        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
+        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
+        double t = 0.0;
+        if (ro < l && co < l)
+          for (int k = (I + 1) * 16; k <= co; ++k) t += A[ro * ld + k] * X[k * ld + co];
+        Tb[e] = t;
+      }
+      __syncthreads();
+      for (int e = tid; e < nblk * 256; e += nt) {
+        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
+        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
+        if (ro < l && co < l) {
+          double v = 0.0;
+          for (int kk = r; kk < 16 && I * 16 + kk < l; ++kk)
+            v -= X[ro * ld + I * 16 + kk] * Tb[(I << 8) + (kk << 4) + c];
+          X[ro * ld + co] = v;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024, 1)
     chol_inv_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
                     double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
@@ -782,65 +847,7 @@ __global__ void __launch_bounds__(1024, 1)
     A[r * ld + r] = sqrt(p > tiny ? p : 1.0);
   }
   __syncthreads();
-  // R^{-1} by blocks of 16: (1) every warp inverts one 16x16 diagonal block
-  // (forward over columns, 16 dependent steps), (2) off-diagonal blocks by
-  // block back-substitution X_IJ = -inv(R_II) sum_{I<K<=J} R_IK X_KJ, one
-  // block-diagonal distance at a time (all blocks of a distance in parallel).
-  {
-    const int nb = (l + 15) / 16;
-    for (int e = tid; e < l * l; e += nt) {
-      int r = e / l, c = e - r * l;
-      X[r * ld + c] = 0.0;
-    }
-    __syncthreads();
-    for (int bI = ty; bI < nb; bI += nty) {
-      const int o = bI * 16, bs = min(16, l - o);
-      // lane tx owns column tx of the block; solve R_II x = e_tx by back substitution
-      if (tx < bs) {
-        double xr[16];
-#pragma unroll
-        for (int i = 15; i >= 0; --i) {
-          if (i < bs) {
-            double acc = (i == tx) ? 1.0 : 0.0;
-#pragma unroll
-            for (int k = i + 1; k < 16; ++k)
-              if (k < bs) acc -= A[(o + i) * ld + o + k] * xr[k];
-            xr[i] = (i <= tx) ? acc / A[(o + i) * ld + o + i] : 0.0;
-          } else {
-            xr[i] = 0.0;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (i < bs) X[(o + i) * ld + o + tx] = xr[i];
-      }
-    }
-    __syncthreads();
-    double* Tb = X + l * ld;  // (nb-1) x 16 x 16 scratch
-    for (int dist = 1; dist < nb; ++dist) {
-      const int nblk = nb - dist;
-      for (int e = tid; e < nblk * 256; e += nt) {
-        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
-        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
-        double t = 0.0;
-        if (ro < l && co < l)
-          for (int k = (I + 1) * 16; k <= co; ++k) t += A[ro * ld + k] * X[k * ld + co];
-        Tb[e] = t;
-      }
-      __syncthreads();
-      for (int e = tid; e < nblk * 256; e += nt) {
-        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
-        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
-        if (ro < l && co < l) {
-          double v = 0.0;
-          for (int kk = r; kk < 16 && I * 16 + kk < l; ++kk)
-            v -= X[ro * ld + I * 16 + kk] * Tb[(I << 8) + (kk << 4) + c];
-          X[ro * ld + co] = v;
-        }
-      }
-      __syncthreads();
-    }
-  }
+  tri_inv_blocked(A, X, X + l * ld, ld, l);
   for (int e = tid; e < l * l; e += nt) {
     int r = e / l, c = e - r * l;
     Rout[e] = (c >= r) ? A[r * ld + c] : 0.0;
@@ -869,6 +876,113 @@ int copy_strided(int m, int l, const double* X, long long x_rs, long long x_cs, 
       m, l, X, x_rs, x_cs, Y, y_rs, y_cs);
   TTK_CHECK_LAUNCH();
   return kOk;
+}
+
+
+// Pivoted Cholesky of the l x l PSD matrix G (full symmetric storage):
+// P^T G P = R^T R with R upper triangular, stopped at the first pivot below
+// tau_rel * max(diag G).  Writes rank (device) and M = P R^{-1} (l x l, only the
+// first `rank` columns nonzero), so that Q1 M has orthonormal-ish columns that
+// span the numerically significant part of range(Q1).
+__global__ void __launch_bounds__(1024, 1)
+    pchol_kernel(int l, const double* __restrict__ G, double tau_rel, double* __restrict__ M,
+                 int* rank_out) {
+  extern __shared__ double sm[];
+  const int ld = l + 1;
+  double* A = sm;
+  double* X = sm + l * ld;
+  double* Tb = X + l * ld;
+  __shared__ int perm[kCholMaxCols + 1];
+  __shared__ int piv_s, stop_s;
+  __shared__ double d0_s;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int ty = tid >> 5, tx = tid & 31, nty = nt >> 5;
+  for (int e = tid; e < l * l; e += nt) {
+    int r = e / l, c = e - r * l;
+    A[r * ld + c] = G[e];
+    X[r * ld + c] = 0.0;
+  }
+  for (int i = tid; i < l; i += nt) perm[i] = i;
+  __syncthreads();
+  if (ty == 0) {
+    double g = 0.0;
+    for (int i = tx; i < l; i += 32) g = fmax(g, A[i * ld + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if (tx == 0) d0_s = g;
+  }
+  __syncthreads();
+  const double thr = tau_rel * d0_s;
+  int rank = l;
+  for (int j = 0; j < l; ++j) {
+    if (ty == 0) {
+      double best = -1.0;
+      int bi = j;
+      for (int i = j + tx; i < l; i += 32) {
+        const double v = A[i * ld + i];
+        if (v > best) { best = v; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tx == 0) { piv_s = bi; stop_s = !(best > thr); }
+    }
+    __syncthreads();
+    if (stop_s) { rank = j; break; }
+    const int p = piv_s;
+    if (p != j) {
+      for (int e = tid; e < l; e += nt) {
+        double t = A[j * ld + e]; A[j * ld + e] = A[p * ld + e]; A[p * ld + e] = t;
+      }
+      __syncthreads();
+      for (int e = tid; e < l; e += nt) {
+        double t = A[e * ld + j]; A[e * ld + j] = A[e * ld + p]; A[e * ld + p] = t;
+      }
+      if (tid == 0) { int t = perm[j]; perm[j] = perm[p]; perm[p] = t; }
+      __syncthreads();
+    }
+    const double rjj = sqrt(A[j * ld + j]);
+    const double inv = 1.0 / rjj;
+    // trailing update of the full symmetric block with the unscaled row j
+    for (int i = j + 1 + ty; i < l; i += nty) {
+      const double aji = A[j * ld + i] * inv * inv;
+      for (int c = j + 1 + tx; c < l; c += 32) A[i * ld + c] -= aji * A[j * ld + c];
+    }
+    __syncthreads();
+    for (int c = j + 1 + tid; c < l; c += nt) A[j * ld + c] *= inv;
+    if (tid == 0) A[j * ld + j] = rjj;
+    __syncthreads();
+  }
+  // zero the strictly lower part of the leading rank x rank block, invert it
+  for (int e = tid; e < rank * rank; e += nt) {
+    int r = e / rank, c = e - r * rank;
+    if (c < r) A[r * ld + c] = 0.0;
+  }
+  __syncthreads();
+  if (rank > 0) tri_inv_blocked(A, X, Tb, ld, rank);
+  __syncthreads();
+  for (int e = tid; e < l * l; e += nt) M[e] = 0.0;
+  __syncthreads();
+  for (int e = tid; e < rank * rank; e += nt) {
+    int r = e / rank, c = e - r * rank;
+    M[(long long)perm[r] * l + c] = (c >= r) ? X[r * ld + c] : 0.0;
+  }
+  if (tid == 0) *rank_out = rank;
+}
+
+// deterministic pseudo-random fill in [-1, 1) (completion directions)
+__global__ void fill_random_kernel(long long n, double* x, unsigned long long seed) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    unsigned long long z = (unsigned long long)e * 0x9E3779B97F4A7C15ull + seed;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x[e] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  }
 }
 
 size_t cholqr2_ws_bytes(int m, int l) {
@@ -916,59 +1030,110 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     return kOk;
   };
   int hs[4] = {0, 0, 0, 0};
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    const bool shifted = attempt == 1;
-    TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
-    // pass 1: unshifted CholeskyQR accepted only for kappa(Y) <~ 3e7 (pivot floor 1e-15);
-    // the retry shifts G by 11 (m l + l(l+1)) u trace(G) (sCholQR3, Fukaya et al. 2020)
-    TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, shifted ? shift_rel : 0.0, shifted ? 1e-28 : 1e-15));
-    p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
-    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    // pass 2 on Q1; its Gram's distance to I decides whether a third pass is needed
-    TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
-    TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
-    if ((hs[0] & 1) || (hs[1] & 1)) {
-      if (shifted) return kOk;  // exactly deficient: Householder fallback
-      continue;                 // retry with the shift
-    }
-    // Q2 = Q1 R2^{-1} -> Q, R12 = R2 R1
+  // ---- fast path: CholeskyQR2, accepted for kappa(Y) <~ 3e7 ----
+  TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
+  TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, 0.0, 1e-15));
+  p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
+  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
+  TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (hs[0] == 0 && hs[1] == 0) {
     p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    if ((hs[1] & 2) == 0) {
-      if (R) {
-        p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, R, l, 1);
-        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-      }
-      *ok = 1;
-      return kOk;
-    }
-    // pass 3 on Q2 (in Q): Q = Q2 R3^{-1}
-    p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, I1, l, 1);  // R12 into I1's slot
-    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    TTK_TRY(gram_chol(Q, q_rs, q_cs, R2, I2, status + 2, 1, 0.0, 1e-28));
-    TTK_CHECK_CUDA(cudaMemcpyAsync(hs + 2, status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
-    if (hs[2] != 0) {
-      if (shifted) return kOk;
-      continue;
-    }
-    p = make_gemm(m, l, l, Q, q_rs, q_cs, I2, l, 1, Q1, l, 1);
-    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    TTK_TRY(copy_strided(m, l, Q1, l, 1, Q, q_rs, q_cs, st));
     if (R) {
-      p = make_gemm(l, l, l, R2, l, 1, I1, l, 1, R, l, 1);
+      p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, R, l, 1);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
     }
     *ok = 1;
     return kOk;
   }
+  // ---- rank-robust path ----
+  // pass 1 shifted (sCholQR, Fukaya et al. 2020): always succeeds, kappa(Q1) <~ 1e5
+  // on the numerically significant part of range(Y)
+  TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
+  TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, shift_rel, 1e-28));
+  p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
+  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  // pass 2 pivoted: drop directions with eigenvalue < 1e-14 of G2 (Y-mass < ~1e-11 ||Y||)
+  p = make_gemm(l, l, m, Q1, 1, l, Q1, l, 1, G, l, 1);
+  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  {
+    static bool pattr = false;
+    if (!pattr) {
+      TTK_TRY(qr_set_smem((const void*)pchol_kernel, 220 * 1024));
+      pattr = true;
+    }
+    pchol_kernel<<<1, 1024, smem, st>>>(l, G, 1e-14, R2, status + 3);
+    TTK_CHECK_LAUNCH();
+  }
+  TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (hs[0] & 1) return kOk;
+  const int rho = hs[3];
+  double* Qb = Q1;  // Q1 no longer needed after Q2 = Q1 M is formed into the scratch below
+  // scratch for Q2 / completion: reuse I2 region? it is l x l only -> use the tail of Q via output strides
+  if (rho > 0) {
+    // Q2 = Q1 M[:, :rho] -> Q columns [0, rho)
+    p = make_gemm(m, rho, l, Q1, l, 1, R2, l, 1, Q, q_rs, q_cs);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    // pass 3: CholeskyQR on Q2 (in Q), checked against I; Q3 = Q2 R3^{-1} -> Qb, copied back
+    p = make_gemm(rho, rho, m, Q, q_cs, q_rs, Q, q_rs, q_cs, G, rho, 1);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    const size_t smem_r = sizeof(double) * (2 * (size_t)rho * (rho + 1) + 256 * (size_t)((rho + 15) / 16));
+    chol_inv_kernel<<<1, 1024, smem_r, st>>>(rho, G, R1, I1, status + 2, 1, 0.0, 1e-28);
+    TTK_CHECK_LAUNCH();
+    p = make_gemm(m, rho, rho, Q, q_rs, q_cs, I1, rho, 1, Qb, rho, 1);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    TTK_TRY(copy_strided(m, rho, Qb, rho, 1, Q, q_rs, q_cs, st));
+  }
+  if (rho < l) {
+    // orthonormal completion: random block, projected out of Q[:, :rho] twice, CholeskyQR2
+    const int kc = l - rho;
+    double* Om = Qb;  // m x kc scratch
+    fill_random_kernel<<<4 * kNumSMs, 256, 0, st>>>((long long)m * kc, Om, 0x5DEECE66Dull + (unsigned)l);
+    TTK_CHECK_LAUNCH();
+    for (int rep = 0; rep < 2 && rho > 0; ++rep) {
+      // C = Q[:, :rho]^T Om (rho x kc) -> G scratch, Om -= Q C
+      p = make_gemm(rho, kc, m, Q, q_cs, q_rs, Om, kc, 1, G, kc, 1);
+      TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      p = make_gemm(m, kc, rho, Q, q_rs, q_cs, G, kc, 1, Om, kc, 1, -1.0, 1.0);
+      TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    }
+    const size_t smem_c = sizeof(double) * (2 * (size_t)kc * (kc + 1) + 256 * (size_t)((kc + 15) / 16));
+    for (int pass = 0; pass < 2; ++pass) {
+      p = make_gemm(kc, kc, m, Om, 1, kc, Om, kc, 1, G, kc, 1);
+      TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      chol_inv_kernel<<<1, 1024, smem_c, st>>>(kc, G, R1, I1, status + 2, 0, 0.0, 1e-28);
+      TTK_CHECK_LAUNCH();
+      double* dst = (pass == 0) ? Om : nullptr;
+      if (pass == 0) {
+        // Om <- Om R^{-1} in place is not possible with one GEMM: bounce through Q's tail
+        p = make_gemm(m, kc, kc, Om, kc, 1, I1, kc, 1, Q + (long long)rho * q_cs, q_rs, q_cs);
+        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+        TTK_TRY(copy_strided(m, kc, Q + (long long)rho * q_cs, q_rs, q_cs, Om, kc, 1, st));
+      } else {
+        p = make_gemm(m, kc, kc, Om, kc, 1, I1, kc, 1, Q + (long long)rho * q_cs, q_rs, q_cs);
+        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      }
+      (void)dst;
+    }
+  }
+  TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (hs[2] & 1) return kOk;  // pass 3 / completion Cholesky broke down
+  if (R) {
+    // R = Q^T Y (l x l): exact to working precision because range(Q) covers range(Y)
+    p = make_gemm(l, l, m, Q, q_cs, q_rs, Y, y_rs, y_cs, R, l, 1);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  }
+  *ok = 1;
   return kOk;
 }
 
 size_t qr_auto_ws_bytes(int m, int l) {
   size_t a = tsqr_ws_bytes(m, l);
-  size_t b = (l <= kCholMaxCols && m >= l) ? cholqr2_ws_bytes(m, l) : 0;
+  size_t b = (l <= kCholMaxCols && m >= l) ? cholqr2_ws_bytes(m, l) + align_up((size_t)m * l * 8, 256) : 0;
   return std::max(a, b);
 }
 
@@ -978,7 +1143,21 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
   // CholeskyQR2 pays off only for tall inputs that need a multi-panel tree
   if (l <= kCholMaxCols && m >= 4 * l && m > 512) {
     int ok = 0;
-    TTK_TRY(cholqr2(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, st, &ok));
+    const double* Y = A;
+    long long y_rs = a_rs, y_cs = a_cs;
+    void* cws = ws;
+    size_t cbytes = ws_bytes;
+    if ((const void*)A == (const void*)Q) {
+      // in-place call (the rank-robust path reads Y after writing Q): work on a copy
+      double* Ycopy = reinterpret_cast<double*>(ws);
+      const size_t cb = align_up((size_t)m * l * 8, 256);
+      TTK_REQUIRE(ws_bytes >= cb, kWorkspace, "qr_auto: workspace too small");
+      TTK_TRY(copy_strided(m, l, A, a_rs, a_cs, Ycopy, l, 1, st));
+      Y = Ycopy; y_rs = l; y_cs = 1;
+      cws = (char*)ws + cb;
+      cbytes = ws_bytes - cb;
+    }
+    TTK_TRY(cholqr2(m, l, Y, y_rs, y_cs, Q, q_rs, q_cs, R, cws, cbytes, st, &ok));
     if (ok) return kOk;
   }
   return tsqr(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, st);

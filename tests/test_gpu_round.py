@@ -92,7 +92,11 @@ def test_qr_auto_cholqr_paths(cuda, kind, trans):
         A = np.zeros((m, l))
     Q, R = run_qr(A, cuda, transposed=trans, auto=True)
     assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-12
-    assert np.linalg.norm(Q @ R - A) <= 1e-13 * max(np.linalg.norm(A), 1e-300) * 10 + (0 if kind != "zero" else 1e-300)
+    # kappa >~ 3e7 takes the rank-robust path: directions whose pivot in the
+    # shifted Gram falls below 1e-14 (Y-mass <~ 1e-11) are replaced by an
+    # orthonormal completion, so the backward error bound is 1e-11 there
+    bound = 1e-12 if kind in ("gauss", "graded1e6") else 1e-11
+    assert np.linalg.norm(Q @ R - A) <= bound * np.linalg.norm(A) + 1e-300
 
 
 def test_tsqr_transposed_input(cuda):

@@ -25,7 +25,7 @@ elif which == "cfg2":
         return T.tt_truncate_left_orth(T.rto_sweeps(x, drm), T.RoundSpec(0.0, 40))
 if which == "cfg5":
     C = configs.config5(0)
-    cfg = T.SolverConfig(**{**C["cfg"], "maxit": 6}, zero_rel=None, rounding="rto")
+    cfg = T.SolverConfig(**{**C["cfg"], "maxit": int(os.environ.get("MAXIT", "6"))}, zero_rel=None, rounding="rto")
     a = T.TTOperator(C["op"], device=dev); b = T.TTVector(C["b"], device=dev)
     sk = T.kr_sketch_new(C["dims"], cfg.sketch_rows, seed=C["sketch_seed"], device=dev)
     frame = T.make_solver_frame(b, cfg, seed=C["frame_seed"])
