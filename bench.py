@@ -134,6 +134,45 @@ def load_peaks():
         return {}
 
 
+def jacobi_roofline(T, torch, dev, stream, l=80):
+    """The step's dominant kernel by time is the single-CTA one-sided Jacobi SVD
+    of the truncation (one per core).  Time one l x l instance live and report
+    its algorithmic FLOPs against ONE SM's fp64 peak (the kernel is a single
+    CTA by construction: the TT-SVD chain is sequential)."""
+    from paper_2409_09471_b200 import _lib
+    lib = _lib.load()
+    g = torch.Generator().manual_seed(0)
+    A = torch.randn(10 * l, l, dtype=torch.float64, generator=g)
+    R = torch.linalg.qr(A)[1].to(dev).contiguous()
+    U = torch.empty((l, l), dtype=torch.float64, device=dev)
+    S = torch.empty(l, dtype=torch.float64, device=dev)
+    V = torch.empty((l, l), dtype=torch.float64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib.ttk_debug_svd_sweeps(cnt.data_ptr())
+    # the truncation runs Jacobi on R^T with V accumulated (qr.cu jacobi_svd_ex)
+    call = lambda: lib.ttk_svd_small(l, l, R.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(),
+                                     _lib.stream_ptr(dev))
+    call()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(5):
+        call()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / 5
+    sweeps = int(cnt.item())
+    lib.ttk_debug_svd_sweeps(None)
+    # per sweep l(l-1)/2 pairs x (3 dot FMAs + 2x2 rotation FMAs on C and on V) per row
+    flops = sweeps * (l * (l - 1) / 2) * (6.0 * l + 12.0 * l)
+    sm_peak = 33.9e3 / 148  # GFLOP/s, measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
+    ach = flops / (ms * 1e-3) / 1e9
+    return {"kernel": "jacobi_svd_kernel (1 CTA, %dx%d, V accumulated)" % (l, l), "ms": ms, "sweeps": sweeps,
+            "bound": "latency (single-SM sequential sweeps)", "achieved_gflops": ach,
+            "peak_gflops_one_sm": sm_peak, "frac_of_one_sm": ach / sm_peak,
+            "share_of_step": "~55% (profiles/r01_launches_cfg3_summary.txt)"}
+
+
 def cfg3_flops(C):
     from paper_2409_09471_b200.configs import matvec_flops
     from paper_2409_09471_b200.rto import rto_flops, rto_ranks
@@ -288,8 +327,12 @@ def run_b200(args):
                 "achieved": achieved, "peak": peak / 1e3, "unit": "TFLOP/s", "frac": achieved / (peak / 1e3),
                 "peak_source": "live cuBLAS DGEMM 4096^3 (fp64 tensor pipe; MEASURED_PEAKS.json has no "
                                "fp64 entry; DMMA issue peak measured 37.1 TF/s, profiles/fp64_peak_r01.log)",
-                "traffic": None, "algorithmic_flops": mv_flops,
+                # dram__bytes_read.sum + dram__bytes_write.sum of this launch from the committed
+                # ncu --set full capture (profiles/r01_matvec_r01_metrics.txt): 0.162 + 1.077 GB
+                "traffic": 1.239e9, "traffic_source": "ncu --set full, profiles/r01_matvec_r01_metrics.txt",
+                "algorithmic_flops": mv_flops,
                 "algorithmic_bytes": 8.0 * sum(c.numel() for c in y.cores)}
+    roofline["dominant_kernel"] = jacobi_roofline(T, torch, dev, stream)
 
     # ---- end-to-end through the public API with host buffers ----
     host_op = [torch.as_tensor(g).pin_memory() for g in C["op"]]
@@ -496,6 +539,14 @@ def run_solver(args):
                 "res_sketched": rep.res_sketched[-1], "peak_rank": rep.peak_rank,
                 "time_to_1e-6_s": rep.time_to_tol.get(1e-6)}
     n_rhs = 8
+    # untimed warm-up solve (kernel attributes, allocator pools, pinned scratch)
+    C0 = configs.config5(rank)
+    cfg0 = T.SolverConfig(**{**C0["cfg"], "maxit": 3}, zero_rel=None, rounding="rto")
+    b0 = T.TTVector(C0["b"], device=dev)
+    T.tt_sgmres(T.TTOperator(C0["op"], device=dev), b0, None, cfg0,
+                T.kr_sketch_new(C0["dims"], cfg0.sketch_rows, seed=C0["sketch_seed"], device=dev),
+                T.make_solver_frame(b0, cfg0, seed=C0["frame_seed"]))
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clocks:

@@ -1088,11 +1088,18 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     TTK_TRY(copy_strided(m, rho, Qb, rho, 1, Q, q_rs, q_cs, st));
   }
   if (rho < l) {
-    // orthonormal completion: random block, projected out of Q[:, :rho] twice, CholeskyQR2
+    // orthonormal completion aligned with what the pivoted pass dropped: a
+    // randomized range finder on the residual, Om = (I - Q3 Q3^T) Y Omega_s
+    // (Omega_s random l x kc), projected twice, then CholeskyQR2.  The dropped
+    // directions of range(Y) (mass <~ 1e-11) are captured, so Y = Q Q^T Y holds
+    // to working precision; exactly deficient directions get noise directions
+    // that carry no mass.
     const int kc = l - rho;
     double* Om = Qb;  // m x kc scratch
-    fill_random_kernel<<<4 * kNumSMs, 256, 0, st>>>((long long)m * kc, Om, 0x5DEECE66Dull + (unsigned)l);
+    fill_random_kernel<<<8, 256, 0, st>>>((long long)l * kc, I2, 0x5DEECE66Dull + (unsigned)l);
     TTK_CHECK_LAUNCH();
+    p = make_gemm(m, kc, l, Y, y_rs, y_cs, I2, kc, 1, Om, kc, 1);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
     for (int rep = 0; rep < 2 && rho > 0; ++rep) {
       // C = Q[:, :rho]^T Om (rho x kc) -> G scratch, Om -= Q C
       p = make_gemm(rho, kc, m, Q, q_cs, q_rs, Om, kc, 1, G, kc, 1);
