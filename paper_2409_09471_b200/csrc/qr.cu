@@ -511,19 +511,23 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
   const int group = tid / kSvdGroup, gl = tid % kSvdGroup;
   const int ngroups = blockDim.x / kSvdGroup;
   const int npairs = le / 2;
-  const unsigned gmask = (kSvdGroup == 32) ? 0xffffffffu
-                         : (((1u << kSvdGroup) - 1u) << (threadIdx.x & (32 - kSvdGroup)));
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
     __syncthreads();
     if (tid == 0) changed = 0;
     for (int rnd = 0; rnd < le - 1; ++rnd) {
       __syncthreads();
-      for (int pi = group; pi < npairs; pi += ngroups) {
+      // warp-uniform loop over pair slots (two 16-lane halves per warp) so the
+      // butterfly reductions use full-warp shuffles (no collective fix-ups)
+      constexpr int kGroupsPerWarp = 32 / kSvdGroup;
+      for (int base = (tid >> 5) * kGroupsPerWarp; base < npairs; base += (blockDim.x >> 5) * kGroupsPerWarp) {
+        const int pi = base + ((tid & 31) / kSvdGroup);
+        const bool active = pi < npairs;
         // round-robin tournament: position 0 fixed, positions 1..le-1 rotate
-        const int qi = le - 1 - pi;
+        const int pic = active ? pi : 0;
+        const int qi = le - 1 - pic;
         int p = 0, q;
-        if (pi > 0) { p = pi - 1 + rnd; if (p >= le - 1) p -= le - 1; p += 1; }
+        if (pic > 0) { p = pic - 1 + rnd; if (p >= le - 1) p -= le - 1; p += 1; }
         q = qi - 1 + rnd; if (q >= le - 1) q -= le - 1; q += 1;
         double* cp = C + p * ldc;
         double* cq = C + q * ldc;
@@ -542,27 +546,27 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
         a += a2; b += b2; g += g2;
 #pragma unroll
         for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
-          a += __shfl_xor_sync(gmask, a, o);
-          b += __shfl_xor_sync(gmask, b, o);
-          g += __shfl_xor_sync(gmask, g, o);
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
         }
-        if (a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
+        if (active && a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
           // t = tan(theta) = sign(d) w / (|d| + sqrt(d^2 + w^2)), d = b - a, w = 2g
           const double dd = b - a, w = 2.0 * g;
           const double t = (dd >= 0.0 ? w : -w) / (fabs(dd) + sqrt(dd * dd + w * w));
           const double c = rsqrt(1.0 + t * t), s = c * t;
-          for (int r = gl; r < kk; r += kSvdGroup) {
-            double x = cp[r], y = cq[r];
-            cp[r] = c * x - s * y;
-            cq[r] = s * x + c * y;
+          for (int rr = gl; rr < kk; rr += kSvdGroup) {
+            double x = cp[rr], y = cq[rr];
+            cp[rr] = c * x - s * y;
+            cq[rr] = s * x + c * y;
           }
           if (want_v) {
             double* vp = Vs + p * le;
             double* vq = Vs + q * le;
-            for (int r = gl; r < le; r += kSvdGroup) {
-              double x = vp[r], y = vq[r];
-              vp[r] = c * x - s * y;
-              vq[r] = s * x + c * y;
+            for (int rr = gl; rr < le; rr += kSvdGroup) {
+              double x = vp[rr], y = vq[rr];
+              vp[rr] = c * x - s * y;
+              vq[rr] = s * x + c * y;
             }
           }
           if (gl == 0) changed = 1;
