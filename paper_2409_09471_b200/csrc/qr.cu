@@ -464,6 +464,7 @@ constexpr int kSvdThreads = 1024;
 __device__ int* g_svd_sweeps = nullptr;  // optional diagnostic sink (tests)
 constexpr int kSvdGroup = 16;  // lanes per column pair
 
+template <int RPL>
 __global__ void __launch_bounds__(kSvdThreads, 1)
     jacobi_svd_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
                       double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
@@ -531,17 +532,21 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
         q = qi - 1 + rnd; if (q >= le - 1) q -= le - 1; q += 1;
         double* cp = C + p * ldc;
         double* cq = C + q * ldc;
-        double a = 0.0, b = 0.0, g = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
-        int r = gl;
-        for (; r + kSvdGroup < kk; r += 2 * kSvdGroup) {  // two independent chains
-          const double x = cp[r], y = cq[r];
-          const double x2 = cp[r + kSvdGroup], y2 = cq[r + kSvdGroup];
-          a += x * x; b += y * y; g += x * y;
-          a2 += x2 * x2; b2 += y2 * y2; g2 += x2 * y2;
+        // this lane's rows of the pair, loaded once (independent loads, one
+        // shared-memory latency) and kept in registers for the rotation
+        double x[RPL], y[RPL];
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = gl + i * kSvdGroup;
+          const bool ok = r < kk;
+          x[i] = ok ? cp[r] : 0.0;
+          y[i] = ok ? cq[r] : 0.0;
         }
-        if (r < kk) {
-          const double x = cp[r], y = cq[r];
-          a += x * x; b += y * y; g += x * y;
+        double a = 0.0, b = 0.0, g = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; i += 2) {
+          a += x[i] * x[i]; b += y[i] * y[i]; g += x[i] * y[i];
+          if (i + 1 < RPL) { a2 += x[i + 1] * x[i + 1]; b2 += y[i + 1] * y[i + 1]; g2 += x[i + 1] * y[i + 1]; }
         }
         a += a2; b += b2; g += g2;
 #pragma unroll
@@ -555,18 +560,31 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
           const double dd = b - a, w = 2.0 * g;
           const double t = (dd >= 0.0 ? w : -w) / (fabs(dd) + sqrt(dd * dd + w * w));
           const double c = rsqrt(1.0 + t * t), s = c * t;
-          for (int rr = gl; rr < kk; rr += kSvdGroup) {
-            double x = cp[rr], y = cq[rr];
-            cp[rr] = c * x - s * y;
-            cq[rr] = s * x + c * y;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const int r = gl + i * kSvdGroup;
+            if (r < kk) {
+              cp[r] = c * x[i] - s * y[i];
+              cq[r] = s * x[i] + c * y[i];
+            }
           }
           if (want_v) {
             double* vp = Vs + p * le;
             double* vq = Vs + q * le;
-            for (int rr = gl; rr < le; rr += kSvdGroup) {
-              double x = vp[rr], y = vq[rr];
-              vp[rr] = c * x - s * y;
-              vq[rr] = s * x + c * y;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              const int r = gl + i * kSvdGroup;
+              const bool ok = r < le;
+              x[i] = ok ? vp[r] : 0.0;
+              y[i] = ok ? vq[r] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              const int r = gl + i * kSvdGroup;
+              if (r < le) {
+                vp[r] = c * x[i] - s * y[i];
+                vq[r] = s * x[i] + c * y[i];
+              }
             }
           }
           if (gl == 0) changed = 1;
@@ -621,11 +639,22 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
               l, V != nullptr);
   static bool attr = false;
   if (!attr) {
-    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel, 215 * 1024));
+    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<4>, 215 * 1024));
+    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<6>, 215 * 1024));
+    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<8>, 215 * 1024));
+    TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<10>, 215 * 1024));
     attr = true;
   }
   const int threads = std::min(kSvdThreads, std::max(64, ((le / 2) * kSvdGroup + 31) / 32 * 32));
-  jacobi_svd_kernel<<<1, threads, smem, st>>>(k, l, B, b_rs, b_cs, U, S, V, V != nullptr, scaled_u);
+  const int rows = std::max(k, le);
+  if (rows <= 4 * kSvdGroup)
+    jacobi_svd_kernel<4><<<1, threads, smem, st>>>(k, l, B, b_rs, b_cs, U, S, V, V != nullptr, scaled_u);
+  else if (rows <= 6 * kSvdGroup)
+    jacobi_svd_kernel<6><<<1, threads, smem, st>>>(k, l, B, b_rs, b_cs, U, S, V, V != nullptr, scaled_u);
+  else if (rows <= 8 * kSvdGroup)
+    jacobi_svd_kernel<8><<<1, threads, smem, st>>>(k, l, B, b_rs, b_cs, U, S, V, V != nullptr, scaled_u);
+  else
+    jacobi_svd_kernel<10><<<1, threads, smem, st>>>(k, l, B, b_rs, b_cs, U, S, V, V != nullptr, scaled_u);
   TTK_CHECK_LAUNCH();
   return kOk;
 }
