@@ -127,6 +127,9 @@ int ttk_qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, d
 int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream);
 /* diagnostics: subsequent Jacobi SVDs store their sweep count in *dev_counter (NULL: off) */
 int ttk_debug_svd_sweeps(int* dev_counter);
+/* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,
+ * pull, rounds; 5 int64 per CTA, 8 CTAs) into dev_acc (NULL: off) */
+int ttk_debug_jacobi_profile(long long* dev_acc);
 
 /* ---- tt_round, TT-SVD (reference tt.py:337-368) ----------------------------
  * out[k] holds ranks[k]*dims[k]*ranks[k+1] doubles; out_ranks (host, d+1)

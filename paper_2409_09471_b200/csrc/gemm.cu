@@ -2,44 +2,71 @@
 #include "gemm.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace ttk {
 
+// Deterministic split-K reduction.  A block owns 32 consecutive output
+// elements of one problem; its kRedGroups thread groups each sum a fixed,
+// interleaved subset of the splits (group g: splits g, g+G, ...), then group 0
+// adds the group sums in order.  The summation order depends only on `splits`.
+constexpr int kRedGroups = 8;
+
 __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G) {
-  // one CTA-strided pass over every problem that was split
-  for (int pi = 0; pi < G.count; ++pi) {
+  __shared__ double part[kRedGroups][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  long long total = 0;
+  for (int pi = 0; pi < G.count; ++pi)
+    if (G.p[pi].splits > 1) total += ((long long)G.p[pi].M * G.p[pi].N + 31) / 32;
+  for (long long gc = blockIdx.x; gc < total; gc += gridDim.x) {
+    // locate the problem and chunk (block-uniform)
+    long long c = gc;
+    int pi = 0;
+    for (; pi < G.count; ++pi) {
+      if (G.p[pi].splits <= 1) continue;
+      const long long n = ((long long)G.p[pi].M * G.p[pi].N + 31) / 32;
+      if (c < n) break;
+      c -= n;
+    }
     const GemmProblem& P = G.p[pi];
-    if (P.splits <= 1) continue;
     const size_t mn = (size_t)P.M * P.N;
-    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < mn;
-         e += (size_t)gridDim.x * blockDim.x) {
-      // fixed summation order; loads issued 8 at a time so the L2 latency of the
-      // partials overlaps instead of chaining
-      double s = 0.0;
-      int k = 0;
-      for (; k + 8 <= P.splits; k += 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcg(P.partial + (size_t)(k + u) * mn + e);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
+    const size_t e = (size_t)c * 32 + lane;
+    double s = 0.0;
+    if (e < mn) {
+      int k = grp;
+      for (; k + 3 * kRedGroups < P.splits; k += 4 * kRedGroups) {
+        const double v0 = __ldcg(P.partial + (size_t)k * mn + e);
+        const double v1 = __ldcg(P.partial + (size_t)(k + kRedGroups) * mn + e);
+        const double v2 = __ldcg(P.partial + (size_t)(k + 2 * kRedGroups) * mn + e);
+        const double v3 = __ldcg(P.partial + (size_t)(k + 3 * kRedGroups) * mn + e);
+        s += v0; s += v1; s += v2; s += v3;
       }
-      for (; k < P.splits; ++k) s += __ldcg(P.partial + (size_t)k * mn + e);
-      int m = (int)(e / P.N), n = (int)(e % P.N);
+      for (; k < P.splits; k += kRedGroups) s += __ldcg(P.partial + (size_t)k * mn + e);
+    }
+    part[grp][lane] = s;
+    __syncthreads();
+    if (grp == 0 && e < mn) {
+      double t = part[0][lane];
+#pragma unroll
+      for (int g = 1; g < kRedGroups; ++g) t += part[g][lane];
+      const int m = (int)(e / P.N), n = (int)(e % P.N);
       double* dst = P.C + cmap_m(P, m) + cmap_n(P, n);
-      double v = P.alpha * s;
+      double v = P.alpha * t;
       if (P.beta != 0.0) v += P.beta * *dst;
       *dst = v;
     }
+    __syncthreads();
   }
 }
 
 namespace {
 
-enum TileCfg { kT128x128 = 0, kT128x64 = 1, kT64x64 = 2, kT64x32 = 3, kT128x80 = 4 };
+enum TileCfg { kT128x128 = 0, kT128x64 = 1, kT64x64 = 2, kT64x32 = 3, kT128x80 = 4, kT64x80 = 5,
+               kT80x64 = 6, kT80x80 = 7 };
 
 struct CfgDims { int bm, bn; };
-constexpr CfgDims kDims[] = {{128, 128}, {128, 64}, {64, 64}, {64, 32}, {128, 80}};
+constexpr CfgDims kDims[] = {{128, 128}, {128, 64}, {64, 64}, {64, 32}, {128, 80}, {64, 80}, {80, 64}, {80, 80}};
 
 // C = A B  <=>  C^T = B^T A^T: make the output's contiguous direction the
 // column (n) index so the epilogue stores are coalesced (1-level maps only)
@@ -62,10 +89,20 @@ TileCfg pick_cfg(const GemmProblem* probs, int count) {
     long mn = (long)probs[i].M * probs[i].N;
     if (mn > best) { best = mn; bm = probs[i].M; bn = probs[i].N; }
   }
-  long tiles128 = 0;
-  for (int i = 0; i < count; ++i) tiles128 += (long)ceil_div(probs[i].M, 128) * ceil_div(probs[i].N, 128);
+  long tiles128 = 0, tiles128x80 = 0;
+  for (int i = 0; i < count; ++i) {
+    tiles128 += (long)ceil_div(probs[i].M, 128) * ceil_div(probs[i].N, 128);
+    tiles128x80 += (long)ceil_div(probs[i].M, 128) * ceil_div(probs[i].N, 80);
+  }
   if (bn <= 32 && bm >= 64) return kT64x32;
-  if (bm >= 512 && bn > 64 && bn <= 80) return kT128x80;
+  // N in (64, 80]: the TT-rank-80 tall-skinny products and Gram matrices
+  if (bn > 64 && bn <= 80) {
+    if (bm <= 80) return kT80x80;
+    // prefer more, smaller tiles over a split-K reduction when M alone fills the GPU
+    return tiles128x80 >= 2L * kNumSMs ? kT128x80 : kT64x80;
+  }
+  // M in (64, 80] with wide N (rank-80 carries times cores)
+  if (bm > 64 && bm <= 80) return kT80x64;
   if (bm >= 128 && bn >= 128 && tiles128 >= kNumSMs) return kT128x128;
   if (bm >= 128 && bn > 32 && bn <= 64) return kT128x64;
   if (bm >= 128 && bn >= 96) return tiles128 >= kNumSMs / 2 ? kT128x128 : kT64x64;
@@ -93,7 +130,7 @@ void plan(GemmProblem* probs, int count, TileCfg c, bool allow_split, size_t* pa
       // spread the K reduction so the whole group covers ~2 waves
       long want = (2L * kNumSMs + tiles - 1) / tiles;
       long maxs = p.K / (4 * kBK);
-      s = (int)std::max(1L, std::min(want, std::min(maxs, 64L)));
+      s = (int)std::max(1L, std::min(want, std::min(maxs, 192L)));
     }
     p.splits = s;
     p.k_per_split = ceil_div(ceil_div(p.K, s), kBK) * kBK;
@@ -171,21 +208,30 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
       if (p.splits > 1) { p.partial = part + off; off += (size_t)p.splits * p.M * p.N; }
     }
     g.total_tiles = total;
+    static const bool trace = getenv("TTK_GEMM_TRACE") != nullptr;  // shape log (diagnostics)
+    if (trace)
+      for (int i = 0; i < g.count; ++i)
+        fprintf(stderr, "gemm cfg=%d M=%d N=%d K=%d splits=%d tiles=%d a_ks=%lld b_ks=%lld\n", (int)cfg,
+                g.p[i].M, g.p[i].N, g.p[i].K, g.p[i].splits, g.p[i].tiles_m * g.p[i].tiles_n,
+                g.p[i].a_ks, g.p[i].b_ks);
     int rc;
     switch (cfg) {
       case kT128x128: rc = launch_cfg<128, 128, 2, 4>(g, st); break;
       case kT128x64: rc = launch_cfg<128, 64, 2, 2>(g, st); break;
       case kT64x64: rc = launch_cfg<64, 64, 2, 2>(g, st); break;
       case kT128x80: rc = launch_cfg<128, 80, 4, 2>(g, st); break;
+      case kT64x80: rc = launch_cfg<64, 80, 2, 2>(g, st); break;
+      case kT80x64: rc = launch_cfg<80, 64, 2, 2>(g, st); break;
+      case kT80x80: rc = launch_cfg<80, 80, 2, 2>(g, st); break;
       default: rc = launch_cfg<64, 32, 2, 1>(g, st); break;
     }
     if (rc != kOk) return rc;
     if (pe > 0) {
-      size_t maxmn = 0;
+      size_t chunks = 0;
       for (int i = 0; i < g.count; ++i)
-        if (g.p[i].splits > 1) maxmn = std::max(maxmn, (size_t)g.p[i].M * g.p[i].N);
-      const int rblocks = (int)std::min<size_t>((maxmn + 127) / 128, 4 * kNumSMs);
-      gemm_splitk_reduce_kernel<<<std::max(rblocks, 1), 128, 0, st>>>(g);
+        if (g.p[i].splits > 1) chunks += ((size_t)g.p[i].M * g.p[i].N + 31) / 32;
+      const int rblocks = (int)std::min<size_t>(chunks, 8 * kNumSMs);
+      gemm_splitk_reduce_kernel<<<std::max(rblocks, 1), 32 * kRedGroups, 0, st>>>(g);
       TTK_CHECK_LAUNCH();
     }
   }

@@ -11,7 +11,10 @@
 #include "qr.cuh"
 #include "../../include/ttk_b200.h"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace ttk {
@@ -628,12 +631,380 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster-parallel one-sided Jacobi (same tournament, same rotation formula).
+//
+// The single-CTA kernel above runs on one SM and is bound by its shared-memory
+// pipe: every round re-reads and re-writes both columns of every pair (and of
+// V).  Here the le/2 pair slots are spread over a cluster of kJcCluster CTAs
+// (one SM each); every 16-lane group keeps its two columns of C and of V in
+// registers for the whole factorisation.  The round-robin schedule only moves
+// columns between neighbouring slots, so after each round a slot pushes its
+// outgoing columns straight into the destination slot's inbox (local or
+// remote shared memory, DSMEM) and one cluster barrier publishes them:
+//   position v -> v-1 (v >= 1, position 1 -> le-1, position 0 fixed), i.e.
+//   left(s)  -> left(s-1)   (s >= 2),  left(1) -> right(0),  left(0) stays
+//   right(s) -> right(s+1)  (s <= np-2),  right(np-1) -> left(np-1)
+// which is exactly the p/q index rotation of jacobi_svd_kernel.
+
+constexpr int kJcCluster = 8;
+constexpr int kJcMaxSlots = 8;   // pair slots per CTA (le <= 128)
+constexpr int kJcThreads = kJcMaxSlots * kSvdGroup;
+
+__device__ __forceinline__ uint32_t jc_map(const void* p, int rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// asynchronous store into (possibly remote) shared memory; completion is
+// counted in bytes on the destination CTA's mbarrier
+__device__ __forceinline__ void jc_st_v2(uint32_t addr, double a, double b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "d"(a), "d"(b), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void jc_st_u32(uint32_t addr, uint32_t v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
+               "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void jc_arm(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void jc_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+__device__ long long* g_jc_prof = nullptr;  // optional per-phase clock sink (diagnostics)
+
+template <int RPL>
+__global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads, 1)
+    jacobi_cluster_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
+                          double* __restrict__ U, double* __restrict__ S, double* __restrict__ V,
+                          int want_v, int scaled_u) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  // inboxes [2 bufs][spc][2 sides][2 (C,V)][RPL/2][16 lanes] of double2 (conflict-free)
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double nrm[kQrMaxCols + 2];
+  __shared__ double fin[kQrMaxCols + 2];  // final column norms, every column (all CTAs)
+  __shared__ int order[kQrMaxCols + 2];
+  __shared__ int flags[64];               // per-sweep "rotated" flag (never reset)
+  __shared__ int inid[2][kJcMaxSlots][2];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int le = l + (l & 1), kk = k, np = le / 2;
+  const int spc = (np + kJcCluster - 1) / kJcCluster;
+  const int tid = threadIdx.x, li = tid / kSvdGroup, gl = tid % kSvdGroup;
+  const int si = crank * spc + li;
+  const bool active = li < spc && si < np;
+  constexpr int box = RPL * kSvdGroup;  // doubles per column part
+  const int nv = want_v ? 2 : 1;
+  const uint32_t msg_bytes = (uint32_t)(box * 8 * nv + 4);
+  // bytes this CTA receives per round: a right column for every slot, a left
+  // column for slots 1..np-2 (slot 0 keeps its left, slot np-1 takes its own right)
+  // (only columns arriving from another CTA are counted)
+  uint32_t rx_bytes = 0;
+  if (np > 1)
+    for (int j = 0; j < spc; ++j) {
+      const int s = crank * spc + j;
+      if (s >= np) break;
+      const int from_r = (s == 0) ? 1 : s - 1;  // source of the new right column
+      if (from_r / spc != crank) rx_bytes += msg_bytes;
+      if (s >= 1 && s <= np - 2 && (s + 1) / spc != crank) rx_bytes += msg_bytes;
+    }
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (rx_bytes) { jc_arm(bar0, rx_bytes); jc_arm(bar0 + 8, rx_bytes); }
+  }
+  // initial order: decreasing norm, ties by index (identical in every CTA)
+  for (int c = tid >> 5; c < l; c += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int r = tid & 31; r < kk; r += 32) {
+      double x = B[(long long)r * b_rs + (long long)c * b_cs];
+      s += x * x;
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) nrm[c] = s;
+  }
+  for (int i = tid; i < 64; i += blockDim.x) flags[i] = 0;
+  __syncthreads();
+  for (int c = tid; c < l; c += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < l; ++j) rank += (nrm[j] > nrm[c]) || (nrm[j] == nrm[c] && j < c);
+    order[rank] = c;
+  }
+  __syncthreads();
+  int idl = active ? si : 0, idr = active ? le - 1 - si : 0;
+  double x[RPL], y[RPL], vx[RPL], vy[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = gl + i * kSvdGroup;
+    const bool okl = active && r < kk && idl < l, okr = active && r < kk && idr < l;
+    x[i] = okl ? B[(long long)r * b_rs + (long long)order[idl] * b_cs] : 0.0;
+    y[i] = okr ? B[(long long)r * b_rs + (long long)order[idr] * b_cs] : 0.0;
+    vx[i] = (want_v && active && idl < l && r == order[idl]) ? 1.0 : 0.0;
+    vy[i] = (want_v && active && idr < l && r == order[idr]) ? 1.0 : 0.0;
+  }
+  const double tol = (double)max(kk, 1) * 1.1102230246251565e-16;
+  const double tol2 = tol * tol;
+  auto inbox = [&](int buf, int slot_local, int side, int cv) {
+    return sm + ((((size_t)buf * spc + slot_local) * 2 + side) * 2 + cv) * box + gl * 2;
+  };
+  const uint32_t buf_bytes = (uint32_t)(spc * 4 * box * 8);
+  const uint32_t id_bytes = (uint32_t)(kJcMaxSlots * 2 * sizeof(int));
+  // destinations (shared::cluster addresses of buffer 0), fixed for the whole run:
+  //   left(s) -> left(s-1) (s >= 2), left(1) -> right(0); right(s) -> right(s+1) (s <= np-2)
+  const bool send_l = active && si >= 1 && si <= np - 1 && np > 1 && !(si == np - 1 && si == 0);
+  const bool send_r = active && si <= np - 2;
+  // same-CTA moves are plain shared-memory stores (ordered by __syncthreads);
+  // only moves across a CTA boundary travel as st.async (completion counted on
+  // the destination's mbarrier)
+  uint32_t l_c = 0, l_id = 0, l_bar = 0, r_c = 0, r_id = 0, r_bar = 0;
+  double *l_loc = nullptr, *r_loc = nullptr;
+  int* l_idloc = nullptr;
+  int* r_idloc = nullptr;
+  bool l_remote = false, r_remote = false;
+  if (send_l) {
+    const int ds = si - 1, side = (si == 1) ? 1 : 0;
+    const int dc = ds / spc, dl = ds - dc * spc;
+    l_remote = dc != crank;
+    l_loc = sm + ((((size_t)dl) * 2 + side) * 2) * box + gl * 2;
+    l_idloc = &inid[0][dl][side];
+    l_c = jc_map(l_loc, dc);
+    l_id = jc_map(l_idloc, dc);
+    l_bar = jc_map(&mbar[0], dc);
+  }
+  if (send_r) {
+    const int ds = si + 1;
+    const int dc = ds / spc, dl = ds - dc * spc;
+    r_remote = dc != crank;
+    r_loc = sm + ((((size_t)dl) * 2 + 1) * 2) * box + gl * 2;
+    r_idloc = &inid[0][dl][1];
+    r_c = jc_map(r_loc, dc);
+    r_id = jc_map(r_idloc, dc);
+    r_bar = jc_map(&mbar[0], dc);
+  }
+  // a warp waits for this CTA's incoming columns only if it holds a slot
+  const bool warp_active = __any_sync(0xffffffffu, active);
+  cl.sync();  // barriers initialised and armed in every CTA before the first remote store
+  long long* const prof = (tid == 0) ? g_jc_prof : nullptr;
+  long long pt[4] = {0, 0, 0, 0}, tc = 0;
+  int sweep = 0, round = 0;
+  for (; sweep < 60; ++sweep) {
+    for (int rnd = 0; rnd < le - 1; ++rnd, ++round) {
+      if (prof) tc = clock64();
+      double a = 0.0, b = 0.0, g = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; i += 2) {
+        a += x[i] * x[i]; b += y[i] * y[i]; g += x[i] * y[i];
+        if (i + 1 < RPL) { a2 += x[i + 1] * x[i + 1]; b2 += y[i + 1] * y[i + 1]; g2 += x[i + 1] * y[i + 1]; }
+      }
+      a += a2; b += b2; g += g2;
+#pragma unroll
+      for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        g += __shfl_xor_sync(0xffffffffu, g, o);
+      }
+      if (active && a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
+        // same angle as tan = sign(d) w / (|d| + rho), division-free:
+        //   c = (|d| + rho) / sqrt(q), s = sign(d) w / sqrt(q), q = 2 rho (|d| + rho)
+        const double dd = b - a, w = 2.0 * g;
+        const double rho = sqrt(dd * dd + w * w);
+        const double sum = fabs(dd) + rho;
+        const double rq = rsqrt(2.0 * rho * sum);
+        const double c = sum * rq, s = (dd >= 0.0 ? w : -w) * rq;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const double xi = x[i], yi = y[i];
+          x[i] = c * xi - s * yi;
+          y[i] = s * xi + c * yi;
+        }
+        if (want_v) {
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const double xi = vx[i], yi = vy[i];
+            vx[i] = c * xi - s * yi;
+            vy[i] = s * xi + c * yi;
+          }
+        }
+        if (gl == 0) flags[sweep] = 1;
+      }
+      if (prof) { long long t = clock64(); pt[0] += t - tc; tc = t; }
+      if (np > 1) {
+        const int buf = round & 1;
+        const uint32_t bo = buf * buf_bytes, io = buf * id_bytes, mo = buf * 8;
+        if (send_l) {
+          if (l_remote) {
+#pragma unroll
+            for (int j = 0; j < RPL; j += 2) jc_st_v2(l_c + bo + 128 * j, x[j], x[j + 1], l_bar + mo);
+            if (want_v) {
+#pragma unroll
+              for (int j = 0; j < RPL; j += 2) jc_st_v2(l_c + bo + box * 8 + 128 * j, vx[j], vx[j + 1], l_bar + mo);
+            }
+            if (gl == 0) jc_st_u32(l_id + io, (uint32_t)idl, l_bar + mo);
+          } else {
+            double2* pc = reinterpret_cast<double2*>(l_loc + buf * (buf_bytes / 8));
+#pragma unroll
+            for (int j = 0; j < RPL / 2; ++j) pc[j * kSvdGroup] = make_double2(x[2 * j], x[2 * j + 1]);
+            if (want_v) {
+#pragma unroll
+              for (int j = 0; j < RPL / 2; ++j) pc[box / 2 + j * kSvdGroup] = make_double2(vx[2 * j], vx[2 * j + 1]);
+            }
+            if (gl == 0) l_idloc[buf * kJcMaxSlots * 2] = idl;
+          }
+        }
+        if (send_r) {
+          if (r_remote) {
+#pragma unroll
+            for (int j = 0; j < RPL; j += 2) jc_st_v2(r_c + bo + 128 * j, y[j], y[j + 1], r_bar + mo);
+            if (want_v) {
+#pragma unroll
+              for (int j = 0; j < RPL; j += 2) jc_st_v2(r_c + bo + box * 8 + 128 * j, vy[j], vy[j + 1], r_bar + mo);
+            }
+            if (gl == 0) jc_st_u32(r_id + io, (uint32_t)idr, r_bar + mo);
+          } else {
+            double2* pc = reinterpret_cast<double2*>(r_loc + buf * (buf_bytes / 8));
+#pragma unroll
+            for (int j = 0; j < RPL / 2; ++j) pc[j * kSvdGroup] = make_double2(y[2 * j], y[2 * j + 1]);
+            if (want_v) {
+#pragma unroll
+              for (int j = 0; j < RPL / 2; ++j) pc[box / 2 + j * kSvdGroup] = make_double2(vy[2 * j], vy[2 * j + 1]);
+            }
+            if (gl == 0) r_idloc[buf * kJcMaxSlots * 2] = idr;
+          }
+        }
+        __syncthreads();  // same-CTA moves visible
+        if (prof) { long long t = clock64(); pt[1] += t - tc; tc = t; }
+        if (warp_active && rx_bytes) {
+          jc_wait(bar0 + mo, (round >> 1) & 1);
+          if (tid == 0) jc_arm(bar0 + mo, rx_bytes);  // for round + 2
+        }
+        if (prof) { long long t = clock64(); pt[2] += t - tc; tc = t; }
+        if (active) {
+          if (si >= 1) {
+            if (si == np - 1) {
+#pragma unroll
+              for (int i = 0; i < RPL; ++i) { x[i] = y[i]; vx[i] = vy[i]; }
+              idl = idr;
+            } else {
+              const double2* pc = reinterpret_cast<const double2*>(inbox(buf, li, 0, 0));
+#pragma unroll
+              for (int j = 0; j < RPL / 2; ++j) { double2 v2 = pc[j * kSvdGroup]; x[2 * j] = v2.x; x[2 * j + 1] = v2.y; }
+              if (want_v) {
+                const double2* pv = reinterpret_cast<const double2*>(inbox(buf, li, 0, 1));
+#pragma unroll
+                for (int j = 0; j < RPL / 2; ++j) { double2 v2 = pv[j * kSvdGroup]; vx[2 * j] = v2.x; vx[2 * j + 1] = v2.y; }
+              }
+              idl = inid[buf][li][0];
+            }
+          }
+          const double2* pc = reinterpret_cast<const double2*>(inbox(buf, li, 1, 0));
+#pragma unroll
+          for (int j = 0; j < RPL / 2; ++j) { double2 v2 = pc[j * kSvdGroup]; y[2 * j] = v2.x; y[2 * j + 1] = v2.y; }
+          if (want_v) {
+            const double2* pv = reinterpret_cast<const double2*>(inbox(buf, li, 1, 1));
+#pragma unroll
+            for (int j = 0; j < RPL / 2; ++j) { double2 v2 = pv[j * kSvdGroup]; vy[2 * j] = v2.x; vy[2 * j + 1] = v2.y; }
+          }
+          idr = inid[buf][li][1];
+        }
+        if (prof) { long long t = clock64(); pt[3] += t - tc; tc = t; }
+      }
+    }
+    // every rotation of this sweep is ordered before this cluster barrier
+    cl.sync();
+    int ch = 0;
+#pragma unroll 1
+    for (int r = 0; r < kJcCluster; ++r) ch |= *cl.map_shared_rank(&flags[sweep], r);
+    if (!ch) break;
+  }
+  if (crank == 0 && tid == 0 && g_svd_sweeps) *g_svd_sweeps = sweep + 1;
+  if (prof) {
+    for (int i = 0; i < 4; ++i) atomicAdd((unsigned long long*)&prof[crank * 5 + i], (unsigned long long)pt[i]);
+    atomicAdd((unsigned long long*)&prof[crank * 5 + 4], (unsigned long long)round);
+  }
+  // final norms of every column, broadcast to every CTA
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) { a += x[i] * x[i]; b += y[i] * y[i]; }
+#pragma unroll
+  for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  a = sqrt(a); b = sqrt(b);
+  if (active && gl == 0)
+    for (int r = 0; r < kJcCluster; ++r) {
+      *cl.map_shared_rank(&fin[idl], r) = a;
+      *cl.map_shared_rank(&fin[idr], r) = b;
+    }
+  cl.sync();
+  if (!active) return;
+  const int kout = min(kk, l);
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const int id = side ? idr : idl;
+    const double nv2 = side ? b : a;
+    int rank = 0;
+    for (int j = 0; j < le; ++j) rank += (fin[j] > nv2) || (fin[j] == nv2 && j < id);
+    if (id >= l || rank >= kout) continue;
+    if (gl == 0) S[rank] = nv2;
+    const double inv = (scaled_u || nv2 <= 0.0) ? 1.0 : 1.0 / nv2;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = gl + i * kSvdGroup;
+      const double cv = side ? y[i] : x[i];
+      if (r < kk) U[(size_t)r * kout + rank] = scaled_u ? cv : (nv2 > 0.0 ? cv * inv : 0.0);
+      if (want_v && V && r < l) V[(size_t)r * kout + rank] = side ? vy[i] : vx[i];
+    }
+  }
+}
+
 int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs, double* U, double* S,
                   double* V, bool scaled_u, cudaStream_t st) {
   if (k <= 0 || l <= 0) return kOk;
   TTK_REQUIRE(l <= kQrMaxCols && k <= kQrMaxCols, kInvalidValue,
               "jacobi_svd: %d x %d exceeds %d", k, l, kQrMaxCols);
   const int le = l + (l & 1);
+  static const bool single_cta = getenv("TTK_JACOBI_SINGLE") != nullptr;  // A/B switch
+  if (!single_cta && le <= 2 * kJcCluster * kJcMaxSlots && k <= 8 * kSvdGroup) {
+    static bool cattr = false;
+    if (!cattr) {
+      TTK_TRY(qr_set_smem((const void*)jacobi_cluster_kernel<4>, 96 * 1024));
+      TTK_TRY(qr_set_smem((const void*)jacobi_cluster_kernel<6>, 96 * 1024));
+      TTK_TRY(qr_set_smem((const void*)jacobi_cluster_kernel<8>, 96 * 1024));
+      cattr = true;
+    }
+    const int spc = (le / 2 + kJcCluster - 1) / kJcCluster;
+    const int rows = std::max(k, le);
+    const int threads = std::max(32, (spc * kSvdGroup + 31) / 32 * 32);
+    const int want = V != nullptr;
+    if (rows <= 4 * kSvdGroup) {
+      const size_t jsm = sizeof(double) * 8 * spc * 4 * kSvdGroup;
+      jacobi_cluster_kernel<4><<<kJcCluster, threads, jsm, st>>>(k, l, B, b_rs, b_cs, U, S, V, want, scaled_u);
+    } else if (rows <= 6 * kSvdGroup) {
+      const size_t jsm = sizeof(double) * 8 * spc * 6 * kSvdGroup;
+      jacobi_cluster_kernel<6><<<kJcCluster, threads, jsm, st>>>(k, l, B, b_rs, b_cs, U, S, V, want, scaled_u);
+    } else {
+      const size_t jsm = sizeof(double) * 8 * spc * 8 * kSvdGroup;
+      jacobi_cluster_kernel<8><<<kJcCluster, threads, jsm, st>>>(k, l, B, b_rs, b_cs, U, S, V, want, scaled_u);
+    }
+    TTK_CHECK_LAUNCH();
+    return kOk;
+  }
   size_t smem = sizeof(double) * ((size_t)le * (k | 1) + (V ? (size_t)le * le : 0));
   TTK_REQUIRE(smem <= 215 * 1024, kInvalidValue, "jacobi_svd: %d x %d (V=%d) exceeds shared memory", k,
               l, V != nullptr);
@@ -717,6 +1088,13 @@ int ttk_qr(int m, int l, const double* A, long long a_rs, long long a_cs, double
 
 int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream) {
   return jacobi_svd(k, l, B, U, S, V, (cudaStream_t)stream);
+}
+
+// diagnostics: accumulate per-CTA phase clocks of the cluster Jacobi (5 int64 per CTA:
+// rotate, send, wait, pull, rounds) into dev_acc (NULL: off)
+int ttk_debug_jacobi_profile(long long* dev_acc) {
+  TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_jc_prof, &dev_acc, sizeof(long long*)));
+  return kOk;
 }
 
 // diagnostics: route the sweep count of subsequent Jacobi SVDs to a device int (NULL: off)
@@ -852,39 +1230,47 @@ __global__ void __launch_bounds__(1024, 1)
     __syncthreads();
   }
   const double tiny = gmax_s * tiny_rel + 1e-300;  // pivot^2 floor relative to max diag(G)
-  // right-looking Cholesky on the upper triangle; row j is scaled afterwards
-  // (A[i][c] -= A[j][i] A[j][c] / A[j][j]), one barrier per step
+  // Gaussian elimination of [G | I] without pivoting (SPD): E G = U with E unit
+  // lower, U = D L1^T upper, and E = L1^{-1}.  Hence R = D^{-1/2} U and
+  // R^{-1} = E^T D^{-1/2}: one pass gives both (no separate triangular inverse).
+  // Only the upper triangle of A and the lower triangle of X (= E) are touched;
+  // one barrier per step, the next pivot's reciprocal is formed by the lane that
+  // finishes it while the other rows are still being updated.
+  __shared__ double pinv[kQrMaxCols + 1];
+  for (int e = tid; e < l * ld; e += nt) {
+    int r = e / ld, c = e - r * ld;
+    X[e] = (r == c) ? 1.0 : 0.0;
+  }
+  if (tid == 0) {
+    const double p0 = A[0];
+    if (!(p0 > tiny)) { atomicOr(&bad, 1); pinv[0] = 1.0; } else { pinv[0] = 1.0 / p0; }
+  }
+  __syncthreads();
   for (int j = 0; j < l; ++j) {
-    double piv = A[j * ld + j];
-    if (!(piv > tiny)) {
-      if (tid == 0) atomicOr(&bad, 1);
-      piv = 1.0;
-    }
-    const double inv = 1.0 / piv;
+    const double inv = pinv[j];
     for (int i = j + 1 + ty; i < l; i += nty) {
       const double aji = A[j * ld + i] * inv;
       for (int c = i + tx; c < l; c += 32) A[i * ld + c] -= aji * A[j * ld + c];
+      if (i == j + 1 && tx == 0) {
+        const double pn = A[i * ld + i];
+        if (!(pn > tiny)) { atomicOr(&bad, 1); pinv[i] = 1.0; } else { pinv[i] = 1.0 / pn; }
+      }
+      for (int c = tx; c <= j; c += 32) X[i * ld + c] -= aji * X[j * ld + c];
     }
     __syncthreads();
   }
-  for (int e = tid; e < l * l; e += nt) {
-    int r = e / l, c = e - r * l;
-    if (c > r) {
-      double p = A[r * ld + r];
-      A[r * ld + c] = A[r * ld + c] / sqrt(p > tiny ? p : 1.0);
-    }
-  }
-  __syncthreads();
+  __shared__ double dsq[kQrMaxCols + 1], rsq[kQrMaxCols + 1];
   for (int r = tid; r < l; r += nt) {
-    double p = A[r * ld + r];
-    A[r * ld + r] = sqrt(p > tiny ? p : 1.0);
+    const double p = A[r * ld + r];
+    const double d = sqrt(p > tiny ? p : 1.0);
+    dsq[r] = d;
+    rsq[r] = 1.0 / d;
   }
   __syncthreads();
-  tri_inv_blocked(A, X, X + l * ld, ld, l);
   for (int e = tid; e < l * l; e += nt) {
     int r = e / l, c = e - r * l;
-    Rout[e] = (c >= r) ? A[r * ld + c] : 0.0;
-    Rinv[e] = (c >= r) ? X[r * ld + c] : 0.0;
+    Rout[e] = (c > r) ? A[r * ld + c] * rsq[r] : (c == r ? dsq[r] : 0.0);
+    Rinv[e] = (c >= r) ? X[c * ld + r] * rsq[c] : 0.0;
   }
   if (tid == 0 && bad) atomicOr(status, bad);
 }
@@ -914,12 +1300,14 @@ int copy_strided(int m, int l, const double* X, long long x_rs, long long x_cs, 
 
 // Pivoted Cholesky of the l x l PSD matrix G (full symmetric storage):
 // P^T G P = R^T R with R upper triangular, stopped at the first pivot below
-// tau_rel * max(diag G).  Writes rank (device) and M = P R^{-1} (l x l, only the
-// first `rank` columns nonzero), so that Q1 M has orthonormal-ish columns that
-// span the numerically significant part of range(Q1).
+// tau_rel * max(diag G).  Writes rank (device), the leading rank x rank block
+// of R compactly (row-major, ld = rank) into Rk and the pivot order into
+// perm_out, so that Q2 = Q1[:, perm[:rank]] / Rk (a triangular solve, no
+// explicit inverse) has orthonormal-ish columns spanning the numerically
+// significant part of range(Q1).
 __global__ void __launch_bounds__(1024, 1)
-    pchol_kernel(int l, const double* __restrict__ G, double tau_rel, double* __restrict__ M,
-                 int* rank_out) {
+    pchol_kernel(int l, const double* __restrict__ G, double tau_rel, double* __restrict__ Rk,
+                 int* perm_out, int* rank_out) {
   extern __shared__ double sm[];
   const int ld = l + 1;
   double* A = sm;
@@ -989,21 +1377,26 @@ __global__ void __launch_bounds__(1024, 1)
     if (tid == 0) A[j * ld + j] = rjj;
     __syncthreads();
   }
-  // zero the strictly lower part of the leading rank x rank block, invert it
+  (void)X; (void)Tb;
   for (int e = tid; e < rank * rank; e += nt) {
     int r = e / rank, c = e - r * rank;
-    if (c < r) A[r * ld + c] = 0.0;
+    Rk[e] = (c >= r) ? A[r * ld + c] : 0.0;
   }
-  __syncthreads();
-  if (rank > 0) tri_inv_blocked(A, X, Tb, ld, rank);
-  __syncthreads();
-  for (int e = tid; e < l * l; e += nt) M[e] = 0.0;
-  __syncthreads();
-  for (int e = tid; e < rank * rank; e += nt) {
-    int r = e / rank, c = e - r * rank;
-    M[(long long)perm[r] * l + c] = (c >= r) ? X[r * ld + c] : 0.0;
-  }
+  for (int i = tid; i < l; i += nt) perm_out[i] = perm[i];
   if (tid == 0) *rank_out = rank;
+}
+
+// Y[:, c] = X[:, idx[c]] for c < n (column gather, strided output)
+__global__ void gather_cols_kernel(int m, int n, const double* __restrict__ X, long long x_rs,
+                                   const int* __restrict__ idx, double* __restrict__ Y, long long y_rs,
+                                   long long y_cs) {
+  const long long tot = (long long)m * n;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / n;
+    const int c = (int)(e - r * n);
+    Y[r * y_rs + (long long)c * y_cs] = X[r * x_rs + idx[c]];
+  }
 }
 
 // deterministic pseudo-random fill in [-1, 1) (completion directions)
@@ -1019,7 +1412,8 @@ __global__ void fill_random_kernel(long long n, double* x, unsigned long long se
 }
 
 size_t cholqr2_ws_bytes(int m, int l) {
-  return align_up((size_t)m * l * 8, 256) + 6 * align_up((size_t)l * l * 8, 256) + 256 + (32u << 20);
+  return align_up((size_t)m * l * 8, 256) + 6 * align_up((size_t)l * l * 8, 256) +
+         align_up(sizeof(int) * (16 + kCholMaxCols), 256) + (32u << 20);
 }
 
 // Shifted CholeskyQR2/3.  Pass 1 factors G + s I with s = 11 (m l + l(l+1)) u
@@ -1030,6 +1424,96 @@ size_t cholqr2_ws_bytes(int m, int l) {
 // (checked the same way) finishes.  Exactly rank-deficient inputs fail the
 // checks and the caller falls back to Householder TSQR.
 // returns kOk and *ok = 1 when the result was accepted
+// ---------------------------------------------------------------------------
+// Q = Y R^{-1} for an upper-triangular R (l x l, row-major) by forward
+// substitution, row by row.  Backward stable (Q R = Y + O(eps |Y|)), unlike a
+// GEMM with an explicit inverse whose error grows like eps kappa(R) ||Y||: the
+// first CholeskyQR pass of a rank-deficient / shifted Gram has kappa(R) up to
+// ~1e8 and the explicit inverse then loses 8 digits of the factorisation.
+// One warp solves two rows at once (independent chains interleaved); lane
+// owns columns lane + 32 q.  Rows are independent, so Q may alias Y.
+constexpr int kTrsmWarps = 16;
+
+template <int CPL>
+__global__ void __launch_bounds__(kTrsmWarps * 32)
+    trsm_rows_kernel(int m, int l, const double* Y, long long y_rs, long long y_cs,
+                     const double* __restrict__ R, double* Q, long long q_rs, long long q_cs) {
+  extern __shared__ double sR[];  // l x l (row-major) then rinv[l]
+  double* rinv = sR + (size_t)l * l;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < l * l; e += blockDim.x) sR[e] = R[e];
+  for (int j = tid; j < l; j += blockDim.x) rinv[j] = 1.0 / R[(size_t)j * l + j];
+  __syncthreads();
+  for (long long r0 = ((long long)blockIdx.x * kTrsmWarps + warp) * 2; r0 < m;
+       r0 += (long long)gridDim.x * kTrsmWarps * 2) {
+    const bool two = r0 + 1 < m;
+    double t0[CPL], t1[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = lane + 32 * q;
+      t0[q] = (c < l) ? Y[r0 * y_rs + (long long)c * y_cs] : 0.0;
+      t1[q] = (c < l && two) ? Y[(r0 + 1) * y_rs + (long long)c * y_cs] : 0.0;
+    }
+#pragma unroll
+    for (int qb = 0; qb < CPL; ++qb) {
+      const int jend = min(32, l - 32 * qb);
+      for (int jj = 0; jj < jend; ++jj) {
+        const int j = 32 * qb + jj;
+        const double ri = rinv[j];
+        const double v0 = __shfl_sync(0xffffffffu, t0[qb], jj) * ri;
+        const double v1 = __shfl_sync(0xffffffffu, t1[qb], jj) * ri;
+        if (lane == jj) { t0[qb] = v0; t1[qb] = v1; }
+        const double* rj = sR + (size_t)j * l;
+#pragma unroll
+        for (int q = qb; q < CPL; ++q) {
+          const int c = lane + 32 * q;
+          if (c > j && c < l) {
+            const double rjc = rj[c];
+            t0[q] -= v0 * rjc;
+            t1[q] -= v1 * rjc;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = lane + 32 * q;
+      if (c < l) {
+        Q[r0 * q_rs + (long long)c * q_cs] = t0[q];
+        if (two) Q[(r0 + 1) * q_rs + (long long)c * q_cs] = t1[q];
+      }
+    }
+  }
+}
+
+int trsm_right_upper(int m, int l, const double* Y, long long y_rs, long long y_cs, const double* R, double* Q,
+                     long long q_rs, long long q_cs, cudaStream_t st) {
+  if (m <= 0 || l <= 0) return kOk;
+  TTK_REQUIRE(l <= 128, kInvalidValue, "trsm: %d columns exceed 128", l);
+  static bool attr = false;
+  if (!attr) {
+    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<1>, 140 * 1024));
+    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<2>, 140 * 1024));
+    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<3>, 140 * 1024));
+    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<4>, 140 * 1024));
+    attr = true;
+  }
+  const size_t smem = sizeof(double) * ((size_t)l * l + l);
+  const long long rows_per_block = kTrsmWarps * 2;
+  const int grid = (int)std::min<long long>((m + rows_per_block - 1) / rows_per_block, 4LL * kNumSMs);
+  const int cpl = (l + 31) / 32;
+  switch (cpl) {
+    case 1: trsm_rows_kernel<1><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
+    case 2: trsm_rows_kernel<2><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
+    case 3: trsm_rows_kernel<3><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
+    default: trsm_rows_kernel<4><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
+  }
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
+static int g_qr_path_tmp = 0;
+static void g_qr_last_path_set(int v) { g_qr_path_tmp = v; }
 int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, double* Q, long long q_rs,
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* ok) {
   *ok = 0;
@@ -1042,7 +1526,7 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
   double* I1 = ar.take<double>((size_t)l * l);
   double* R2 = ar.take<double>((size_t)l * l);
   double* I2 = ar.take<double>((size_t)l * l);
-  int* status = ar.take<int>(16);
+  int* status = ar.take<int>(16 + kCholMaxCols);  // [0,8) flags/rank, [8, 8+l) pivot order
   void* split = ar.take<char>(32u << 20);
   const size_t split_bytes = 32u << 20;
   static bool attr = false;
@@ -1066,8 +1550,7 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
   // ---- fast path: CholeskyQR2, accepted for kappa(Y) <~ 3e7 ----
   TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
   TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, 0.0, 1e-15));
-  p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
-  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  TTK_TRY(trsm_right_upper(m, l, Y, y_rs, y_cs, R1, Q1, l, 1, st));  // Q1 = Y / R1 (backward stable)
   TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
   TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   TTK_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -1079,15 +1562,17 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
     }
     *ok = 1;
+    g_qr_last_path_set(1);
     return kOk;
   }
   // ---- rank-robust path ----
+  static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;
+  if (qr_mode == 2) return kOk;  // diagnostics: fast path or Householder only
   // pass 1 shifted (sCholQR, Fukaya et al. 2020): always succeeds, kappa(Q1) <~ 1e5
   // on the numerically significant part of range(Y)
   TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
   TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, shift_rel, 1e-28));
-  p = make_gemm(m, l, l, Y, y_rs, y_cs, I1, l, 1, Q1, l, 1);
-  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  TTK_TRY(trsm_right_upper(m, l, Y, y_rs, y_cs, R1, Q1, l, 1, st));
   // pass 2 pivoted: drop directions with eigenvalue < 1e-14 of G2 (Y-mass < ~1e-11 ||Y||)
   p = make_gemm(l, l, m, Q1, 1, l, Q1, l, 1, G, l, 1);
   TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
@@ -1097,7 +1582,7 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
       TTK_TRY(qr_set_smem((const void*)pchol_kernel, 220 * 1024));
       pattr = true;
     }
-    pchol_kernel<<<1, 1024, smem, st>>>(l, G, 1e-14, R2, status + 3);
+    pchol_kernel<<<1, 1024, smem, st>>>(l, G, 1e-14, R2, status + 8, status + 3);
     TTK_CHECK_LAUNCH();
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1107,9 +1592,13 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
   double* Qb = Q1;  // Q1 no longer needed after Q2 = Q1 M is formed into the scratch below
   // scratch for Q2 / completion: reuse I2 region? it is l x l only -> use the tail of Q via output strides
   if (rho > 0) {
-    // Q2 = Q1 M[:, :rho] -> Q columns [0, rho)
-    p = make_gemm(m, rho, l, Q1, l, 1, R2, l, 1, Q, q_rs, q_cs);
-    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    // Q2 = Q1[:, perm[:rho]] / R_rho -> Q columns [0, rho): gather, then an
+    // in-place triangular solve (backward stable: range(Q2) = range of the
+    // gathered columns of Q1 to working precision)
+    gather_cols_kernel<<<(int)std::min<long long>(((long long)m * rho + 255) / 256, 4 * kNumSMs), 256, 0, st>>>(
+        m, rho, Q1, l, status + 8, Q, q_rs, q_cs);
+    TTK_CHECK_LAUNCH();
+    TTK_TRY(trsm_right_upper(m, rho, Q, q_rs, q_cs, R2, Q, q_rs, q_cs, st));
     // pass 3: CholeskyQR on Q2 (in Q), checked against I; Q3 = Q2 R3^{-1} -> Qb, copied back
     p = make_gemm(rho, rho, m, Q, q_cs, q_rs, Q, q_rs, q_cs, G, rho, 1);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
@@ -1133,35 +1622,44 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     TTK_CHECK_LAUNCH();
     p = make_gemm(m, kc, l, Y, y_rs, y_cs, I2, kc, 1, Om, kc, 1);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    for (int rep = 0; rep < 2 && rho > 0; ++rep) {
-      // C = Q[:, :rho]^T Om (rho x kc) -> G scratch, Om -= Q C
-      p = make_gemm(rho, kc, m, Q, q_cs, q_rs, Om, kc, 1, G, kc, 1);
-      TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-      p = make_gemm(m, kc, rho, Q, q_rs, q_cs, G, kc, 1, Om, kc, 1, -1.0, 1.0);
-      TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    }
+    // Om -= Q3 (Q3^T Om), twice (the second pass removes the first one's rounding)
+    auto project_out = [&]() -> int {
+      for (int rep = 0; rep < 2 && rho > 0; ++rep) {
+        p = make_gemm(rho, kc, m, Q, q_cs, q_rs, Om, kc, 1, G, kc, 1);
+        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+        p = make_gemm(m, kc, rho, Q, q_rs, q_cs, G, kc, 1, Om, kc, 1, -1.0, 1.0);
+        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      }
+      return kOk;
+    };
     const size_t smem_c = sizeof(double) * (2 * (size_t)kc * (kc + 1) + 256 * (size_t)((kc + 15) / 16));
-    for (int pass = 0; pass < 2; ++pass) {
+    // one CholeskyQR pass on Om; the result goes to Q's tail columns and, unless
+    // it is the final pass, back into Om
+    auto chol_pass = [&](bool last) -> int {
       p = make_gemm(kc, kc, m, Om, 1, kc, Om, kc, 1, G, kc, 1);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
       chol_inv_kernel<<<1, 1024, smem_c, st>>>(kc, G, R1, I1, status + 2, 0, 0.0, 1e-28);
       TTK_CHECK_LAUNCH();
-      double* dst = (pass == 0) ? Om : nullptr;
-      if (pass == 0) {
-        // Om <- Om R^{-1} in place is not possible with one GEMM: bounce through Q's tail
-        p = make_gemm(m, kc, kc, Om, kc, 1, I1, kc, 1, Q + (long long)rho * q_cs, q_rs, q_cs);
-        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-        TTK_TRY(copy_strided(m, kc, Q + (long long)rho * q_cs, q_rs, q_cs, Om, kc, 1, st));
-      } else {
-        p = make_gemm(m, kc, kc, Om, kc, 1, I1, kc, 1, Q + (long long)rho * q_cs, q_rs, q_cs);
-        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-      }
-      (void)dst;
-    }
+      p = make_gemm(m, kc, kc, Om, kc, 1, I1, kc, 1, Q + (long long)rho * q_cs, q_rs, q_cs);
+      TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      if (!last) TTK_TRY(copy_strided(m, kc, Q + (long long)rho * q_cs, q_rs, q_cs, Om, kc, 1, st));
+      return kOk;
+    };
+    // Om mixes residual directions of size ~1e-13 |Y| with rounding noise, so its
+    // first orthonormalisation amplifies the eps-sized leftovers along Q3 by
+    // kappa(Om): orthonormalise, project out again, and finish with a pass on
+    // the now well-conditioned block.
+    TTK_TRY(project_out());
+    TTK_TRY(chol_pass(false));
+    TTK_TRY(chol_pass(false));
+    TTK_TRY(project_out());
+    TTK_TRY(chol_pass(false));
+    TTK_TRY(chol_pass(true));
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
   TTK_CHECK_CUDA(cudaStreamSynchronize(st));
   if (hs[2] & 1) return kOk;  // pass 3 / completion Cholesky broke down
+  g_qr_last_path_set(2 + 100 * rho);
   if (R) {
     // R = Q^T Y (l x l): exact to working precision because range(Q) covers range(Y)
     p = make_gemm(l, l, m, Q, q_cs, q_rs, Y, y_rs, y_cs, R, l, 1);
@@ -1177,11 +1675,43 @@ size_t qr_auto_ws_bytes(int m, int l) {
   return std::max(a, b);
 }
 
+// diagnostics (TTK_QR_CHECK=1): host-side check of every CholeskyQR factorisation
+static const bool g_qr_check = getenv("TTK_QR_CHECK") != nullptr;
+#define g_qr_last_path g_qr_path_tmp  // 1 fast, 2 + 100 rho robust
+static void qr_check_report(int m, int l, const std::vector<double>& hy, const double* Q, long long q_rs,
+                            long long q_cs, const double* R, cudaStream_t st) {
+  cudaStreamSynchronize(st);
+  std::vector<double> hq((size_t)m * l), hr((size_t)l * l);
+  double* tmp = nullptr;
+  cudaMalloc(&tmp, 8 * (size_t)m * l);
+  copy_strided(m, l, Q, q_rs, q_cs, tmp, l, 1, st);
+  cudaStreamSynchronize(st);
+  cudaMemcpy(hq.data(), tmp, 8 * (size_t)m * l, cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  cudaMemcpy(hr.data(), R, 8 * (size_t)l * l, cudaMemcpyDeviceToHost);
+  double orth = 0, rec = 0, ymax = 0;
+  for (int i = 0; i < l; ++i)
+    for (int j = 0; j < l; ++j) {
+      double s = 0;
+      for (int r = 0; r < m; ++r) s += hq[(size_t)r * l + i] * hq[(size_t)r * l + j];
+      orth = std::max(orth, std::fabs(s - (i == j)));
+    }
+  for (int r = 0; r < m; ++r)
+    for (int c = 0; c < l; ++c) {
+      double s = 0;
+      for (int k = 0; k < l; ++k) s += hq[(size_t)r * l + k] * hr[(size_t)k * l + c];
+      rec = std::max(rec, std::fabs(s - hy[(size_t)r * l + c]));
+      ymax = std::max(ymax, std::fabs(hy[(size_t)r * l + c]));
+    }
+  fprintf(stderr, "qrcheck path=%d m=%d l=%d orth=%.2e rec=%.2e\n", g_qr_last_path, m, l, orth, rec / ymax);
+}
+
 int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (m <= 0 || l <= 0) return kOk;
   // CholeskyQR2 pays off only for tall inputs that need a multi-panel tree
-  if (l <= kCholMaxCols && m >= 4 * l && m > 512) {
+  static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;  // 1: Householder only
+  if (qr_mode != 1 && l <= kCholMaxCols && m >= 4 * l && m > 512) {
     int ok = 0;
     const double* Y = A;
     long long y_rs = a_rs, y_cs = a_cs;
@@ -1197,7 +1727,18 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
       cws = (char*)ws + cb;
       cbytes = ws_bytes - cb;
     }
+    std::vector<double> hy;
+    if (g_qr_check) {  // diagnostics: keep the input for the factorisation check
+      hy.resize((size_t)m * l);
+      double* tmp = nullptr;
+      TTK_CHECK_CUDA(cudaMalloc(&tmp, 8 * (size_t)m * l));
+      TTK_TRY(copy_strided(m, l, Y, y_rs, y_cs, tmp, l, 1, st));
+      TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+      TTK_CHECK_CUDA(cudaMemcpy(hy.data(), tmp, 8 * (size_t)m * l, cudaMemcpyDeviceToHost));
+      cudaFree(tmp);
+    }
     TTK_TRY(cholqr2(m, l, Y, y_rs, y_cs, Q, q_rs, q_cs, R, cws, cbytes, st, &ok));
+    if (ok && g_qr_check && R) qr_check_report(m, l, hy, Q, q_rs, q_cs, R, st);
     if (ok) return kOk;
   }
   return tsqr(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, st);

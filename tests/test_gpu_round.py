@@ -91,12 +91,12 @@ def test_qr_auto_cholqr_paths(cuda, kind, trans):
     else:
         A = np.zeros((m, l))
     Q, R = run_qr(A, cuda, transposed=trans, auto=True)
-    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 1e-12
-    # kappa >~ 3e7 takes the rank-robust path: directions whose pivot in the
-    # shifted Gram falls below 1e-14 (Y-mass <~ 1e-11) are replaced by an
-    # orthonormal completion, so the backward error bound is 1e-11 there
-    bound = 1e-12 if kind in ("gauss", "graded1e6") else 1e-11
-    assert np.linalg.norm(Q @ R - A) <= bound * np.linalg.norm(A) + 1e-300
+    # every path (CholeskyQR2, rank-robust shifted CholeskyQR3 with completion,
+    # Householder) must be a backward-stable QR: orthonormal Q and A = QR to a
+    # few ulps -- the solver's Arnoldi combinations cancel ~1e6x, so a 1e-12
+    # factorisation error shows up as 1e-6 in the residual history
+    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 5e-14
+    assert np.linalg.norm(Q @ R - A) <= 1e-14 * np.linalg.norm(A) + 1e-300
 
 
 def test_tsqr_transposed_input(cuda):

@@ -52,11 +52,12 @@ def test_solver_config1_golden(cuda):
     x, rep = T.tt_sgmres(a, b, None, cfg, s, frame)
     assert rep.iterations == int(z["cfg1_iters"])
     assert rep.basis_rank == list(z["cfg1_ranks"])
-    # north star: identical iteration counts, final residual within 1e-8 relative;
-    # the whole 40-step history is held to 5e-8 (entries reach 8e-7, where the
-    # reference's own 1e-15 input sensitivity is ~1e-11 absolute)
+    # north star: identical iteration counts, final residual within 1e-8 relative.
+    # The whole 40-step history is held to 1e-9: the reference answers 1e-16
+    # noise injected into every rounding with ~1e-10 relative changes
+    # (tools/sensitivity_cfg1.py), and a backward-stable GPU rounding lands there too.
     assert abs(rep.res_sketched[-1] - z["cfg1_res"][-1]) <= 1e-8 * z["cfg1_res"][-1]
-    np.testing.assert_allclose(rep.res_sketched, z["cfg1_res"], rtol=5e-8)
+    np.testing.assert_allclose(rep.res_sketched, z["cfg1_res"], rtol=1e-9)
     want = z["cfg1_xprobe"]
     assert np.linalg.norm(probe(x) - want) <= 1e-8 * np.linalg.norm(want)
 
@@ -79,7 +80,7 @@ def test_solver_config1_rto_vs_oracle(cuda):
     assert rep.iterations == orep["iterations"]
     assert rep.basis_rank == orep["basis_rank"]
     assert abs(rep.res_sketched[-1] - orep["res_sketched"][-1]) <= 1e-8 * orep["res_sketched"][-1]
-    np.testing.assert_allclose(rep.res_sketched, orep["res_sketched"], rtol=5e-8)
+    np.testing.assert_allclose(rep.res_sketched, orep["res_sketched"], rtol=1e-9)
     assert O.rel_diff([c.cpu().numpy() for c in x.cores], ox) <= 1e-8
 
 
