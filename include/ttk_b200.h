@@ -130,6 +130,9 @@ int ttk_debug_svd_sweeps(int* dev_counter);
 /* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,
  * pull, rounds; 5 int64 per CTA, 8 CTAs) into dev_acc (NULL: off) */
 int ttk_debug_jacobi_profile(long long* dev_acc);
+/* diagnostics: the register Cholesky adds per-step clocks (step, thread-0 work,
+ * owner publish + reciprocal) into dev_acc[3] (NULL: off) */
+int ttk_debug_chol_profile(long long* dev_acc);
 
 /* ---- tt_round, TT-SVD (reference tt.py:337-368) ----------------------------
  * out[k] holds ranks[k]*dims[k]*ranks[k+1] doubles; out_ranks (host, d+1)

@@ -140,6 +140,7 @@ SIGNATURES.update({
 
 SIGNATURES.update({"ttk_debug_svd_sweeps": (c_int, [c_vp])})
 SIGNATURES.update({"ttk_debug_jacobi_profile": (c_int, [c_vp])})
+SIGNATURES.update({"ttk_debug_chol_profile": (c_int, [c_vp])})
 
 SIGNATURES.update({"ttk_qr_auto": (c_int, [c_int, c_int, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_vp, c_vp, c_size,
                                            c_vp])})

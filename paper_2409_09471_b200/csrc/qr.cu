@@ -465,6 +465,7 @@ int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* 
 // (round-robin tournament), one 16-lane group per pair.
 constexpr int kSvdThreads = 1024;
 __device__ int* g_svd_sweeps = nullptr;  // optional diagnostic sink (tests)
+__device__ long long* g_chol_prof = nullptr;  // diagnostics: per-step clocks of chol_inv_reg
 constexpr int kSvdGroup = 16;  // lanes per column pair
 
 template <int RPL>
@@ -512,8 +513,7 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
   __syncthreads();
   const double tol = (double)max(kk, 1) * 1.1102230246251565e-16;
   const double tol2 = tol * tol;
-  const int group = tid / kSvdGroup, gl = tid % kSvdGroup;
-  const int ngroups = blockDim.x / kSvdGroup;
+  const int gl = tid % kSvdGroup;
   const int npairs = le / 2;
   int sweep = 0;
   for (; sweep < 60; ++sweep) {
@@ -1090,6 +1090,12 @@ int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V
   return jacobi_svd(k, l, B, U, S, V, (cudaStream_t)stream);
 }
 
+// diagnostics: chol_inv_reg per-step clocks (step total, thread-0 work, owner publish+divide)
+int ttk_debug_chol_profile(long long* dev_acc) {
+  TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_chol_prof, &dev_acc, sizeof(long long*)));
+  return kOk;
+}
+
 // diagnostics: accumulate per-CTA phase clocks of the cluster Jacobi (5 int64 per CTA:
 // rotate, send, wait, pull, rounds) into dev_acc (NULL: off)
 int ttk_debug_jacobi_profile(long long* dev_acc) {
@@ -1189,7 +1195,8 @@ __device__ void tri_inv_blocked(const double* A, double* X, double* Tb, int ld, 
 __global__ void __launch_bounds__(1024, 1)
     chol_inv_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
                     double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
-                    double tiny_rel) {
+                    double tiny_rel, const int* __restrict__ skip) {
+  if (skip && *skip) return;  // chol_near_identity_kernel already produced R, R^{-1}
   extern __shared__ double sm[];
   const int ld = l + 1;
   double* A = sm;               // l x ld, becomes R (upper)
@@ -1275,6 +1282,281 @@ __global__ void __launch_bounds__(1024, 1)
   if (tid == 0 && bad) atomicOr(status, bad);
 }
 
+// Register-resident variant of chol_inv_kernel for l <= 96 (same elimination
+// of [G | I], same outputs and status bits).  kChW warps; warp w owns rows
+// w + kChW r (row-cyclic), lane t owns columns t + 32 q.  The finished pivot
+// row is published through a double-buffered shared row, the multiplier of
+// row i is one shuffle away (pivot-row column i lives in lane i & 31, slot
+// i >> 5), and the lane that finishes the next pivot forms its reciprocal.
+// One barrier per step.  Few fat warps: the step is issue-bound, so per-warp
+// overhead is what to minimise; column slots with nothing left to do (A part
+// left of the pivot, X part right of it) are skipped.
+constexpr int kChW = 8;
+
+template <int RW, int CPL>
+__global__ void __launch_bounds__(kChW * 32, 1)
+    chol_inv_reg_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                        double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
+                        double tiny_rel, const int* __restrict__ skip) {
+  if (skip && *skip) return;  // chol_near_identity_kernel already produced R, R^{-1}
+  extern __shared__ double sm[];  // epilogue staging: A (l x ld), X (l x ld)
+  const int ld = l + 1;
+  double* A = sm;
+  double* X = sm + (size_t)l * ld;
+  __shared__ double prow[2][2][32 * CPL];
+  __shared__ double pinv[kChW * RW];
+  __shared__ double dsq[kChW * RW], rsq[kChW * RW];
+  __shared__ double gmax_s, tr_s;
+  __shared__ int bad;
+  const int tid = threadIdx.x, w = tid >> 5, t = tid & 31;
+  if (tid == 0) bad = 0;
+  if (w == 0) {
+    double g = 0.0, tr = 0.0;
+    for (int i = t; i < l; i += 32) { const double v = G[(size_t)i * l + i]; g = fmax(g, v); tr += v; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    tr = warp_sum(tr);
+    if (t == 0) { gmax_s = g; tr_s = tr; }
+  }
+  __syncthreads();
+  const double sh = shift_rel > 0.0 ? shift_rel * tr_s : 0.0;
+  const double tiny = gmax_s * tiny_rel + 1e-300;
+  double a[RW][CPL], x[RW][CPL];
+  int badl = 0;
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int i = w + kChW * r, c = t + 32 * q;
+      double v = (i < l && c < l) ? G[(size_t)i * l + c] : 0.0;
+      if (check_identity && i < l && c < l && fabs(v - (i == c ? 1.0 : 0.0)) > 1e-3) badl |= 2;
+      if (i == c) v += sh;
+      a[r][q] = v;
+      x[r][q] = (i == c && i < l) ? 1.0 : 0.0;
+    }
+  if (badl) atomicOr(&bad, badl);
+  if (w == 0) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) { prow[0][0][t + 32 * q] = a[0][q]; prow[0][1][t + 32 * q] = x[0][q]; }
+    if (t == 0) {
+      const double p0 = a[0][0];
+      if (!(p0 > tiny)) { atomicOr(&bad, 1); pinv[0] = 1.0; } else { pinv[0] = 1.0 / p0; }
+    }
+  }
+  __syncthreads();
+  long long* const prof = (tid == 0) ? g_chol_prof : nullptr;
+  long long tp = prof ? clock64() : 0, acc_step = 0, acc_mid = 0;
+  for (int j = 0; j < l; ++j) {
+    const int buf = j & 1;
+    const int qa = j >> 5;          // first slot with A columns > j
+    const int qx = (j >> 5) + 1;    // slots with X columns <= j
+    double pa[CPL], px[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      pa[q] = (q >= qa) ? prow[buf][0][t + 32 * q] : 0.0;
+      px[q] = (q < qx) ? prow[buf][1][t + 32 * q] : 0.0;
+    }
+    const double inv = pinv[j];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) {
+      const int i = w + kChW * r;
+      if (i > j && i < l) {  // warp-uniform
+        const int src = ((kChW * r) & 31) + w;  // lane holding pivot-row column i
+        const double mlt = __shfl_sync(0xffffffffu, pa[(kChW * r) >> 5], src) * inv;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          if (q >= qa) a[r][q] -= mlt * pa[q];
+          if (q < qx) x[r][q] -= mlt * px[q];
+        }
+        if (i == j + 1) {
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            prow[buf ^ 1][0][t + 32 * q] = a[r][q];
+            prow[buf ^ 1][1][t + 32 * q] = x[r][q];
+          }
+          if (t == src) {
+            const double pn = a[r][(kChW * r) >> 5];
+            if (!(pn > tiny)) { atomicOr(&bad, 1); pinv[i] = 1.0; } else { pinv[i] = 1.0 / pn; }
+          }
+        }
+      }
+    }
+    if (prof) acc_mid += clock64() - tp;
+    __syncthreads();
+    if (prof) { const long long tn = clock64(); acc_step += tn - tp; tp = tn; }
+  }
+  if (prof) {
+    atomicAdd((unsigned long long*)&prof[0], (unsigned long long)acc_step);
+    atomicAdd((unsigned long long*)&prof[1], (unsigned long long)acc_mid);
+  }
+#pragma unroll
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int i = w + kChW * r, c = t + 32 * q;
+      if (i < l && c < l) { A[(size_t)i * ld + c] = a[r][q]; X[(size_t)i * ld + c] = x[r][q]; }
+    }
+  __syncthreads();
+  for (int r = tid; r < l; r += blockDim.x) {
+    const double p = A[(size_t)r * ld + r];
+    const double d = sqrt(p > tiny ? p : 1.0);
+    dsq[r] = d;
+    rsq[r] = 1.0 / d;
+  }
+  __syncthreads();
+  for (int e = tid; e < l * l; e += blockDim.x) {
+    const int r = e / l, c = e - r * l;
+    Rout[e] = (c > r) ? A[(size_t)r * ld + c] * rsq[r] : (c == r ? dsq[r] : 0.0);
+    Rinv[e] = (c >= r) ? X[(size_t)c * ld + r] * rsq[c] : 0.0;
+  }
+  if (tid == 0 && bad) atomicOr(status, bad);
+}
+
+// C = A B for small matrices in shared memory, on the DMMA pipe: warps take
+// 8x8 output tiles round-robin, two accumulator chains over k (m8n8k4 f64).
+// A(m,k) = A[m a_rs + k a_cs], B(k,n) = B[k b_rs + n b_cs], C row-major (ldc).
+// rinv_out != nullptr: instead of storing C, write the upper triangle of
+// I - F + P - C into rinv_out (row-major, ld = N) with F = rinv_f, P = rinv_p
+// (shared, ld = ldc): the R^{-1} epilogue of chol_near_identity_kernel.
+// Strides that are 4 mod 16 make the fragment loads bank-conflict free.
+__device__ void block_dmma(int M, int N, int K, const double* A, int a_rs, int a_cs, const double* B, int b_rs,
+                           int b_cs, double* C, int ldc, double* rinv_out = nullptr,
+                           const double* rinv_f = nullptr, const double* rinv_p = nullptr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int tn = (N + 7) >> 3, tiles = ((M + 7) >> 3) * tn;
+  for (int tt = warp; tt < tiles; tt += nw) {
+    const int m0 = (tt / tn) * 8, n0 = (tt % tn) * 8;
+    const int m = m0 + fr, n = n0 + fr;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    int k0 = 0;
+    for (; k0 + 8 <= K; k0 += 8) {
+      const int ka = k0 + fk, kb = k0 + 4 + fk;
+      const double a0 = (m < M) ? A[m * a_rs + ka * a_cs] : 0.0;
+      const double b0 = (n < N) ? B[ka * b_rs + n * b_cs] : 0.0;
+      const double a1 = (m < M) ? A[m * a_rs + kb * a_cs] : 0.0;
+      const double b1 = (n < N) ? B[kb * b_rs + n * b_cs] : 0.0;
+      dmma_8x8x4(c0, a0, b0);
+      dmma_8x8x4(c1, a1, b1);
+    }
+    for (; k0 < K; k0 += 4) {
+      const int k = k0 + fk;
+      const double a0 = (m < M && k < K) ? A[m * a_rs + k * a_cs] : 0.0;
+      const double b0 = (n < N && k < K) ? B[k * b_rs + n * b_cs] : 0.0;
+      dmma_8x8x4(c0, a0, b0);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cn = n0 + 2 * fk + h;
+      if (m < M && cn < N) {
+        if (rinv_out) {
+          const double v = (cn > m) ? -rinv_f[m * ldc + cn] + rinv_p[m * ldc + cn] - (c0[h] + c1[h])
+                           : (cn == m ? 1.0 - rinv_f[m * ldc + cn] + rinv_p[m * ldc + cn] - (c0[h] + c1[h]) : 0.0);
+          rinv_out[(size_t)m * N + cn] = v;
+        } else {
+          C[m * ldc + cn] = c0[h] + c1[h];
+        }
+      }
+    }
+  }
+}
+
+// Cholesky factor of a Gram matrix that is already the identity to within
+// tol (the second CholeskyQR pass of a well-conditioned block), by series:
+// with E = G - I, F1 = triu(E) - diag(E)/2 satisfies F1 + F1^T = E, and
+// F2 = F1 - up(F1^T F1) (up: upper triangle, halved diagonal) gives
+// (I + F2)^T (I + F2) = I + E + O(|E|^3); R^{-1} = I - F2 + F2^2 - F2^3 + O(|E|^4).
+// For tol = 1e-7 and l <= 96 both are exact to ~1e-17: three small DMMA
+// products across the block instead of l sequential pivots.
+// Writes *flag = 1 when it produced R and R^{-1}, 0 when G is not close enough
+// (then the elimination kernel launched after it does the work).
+constexpr int kNearIdMax = kCholMaxCols;
+
+__device__ __forceinline__ int near_id_ld(int l) { return ((l + 15) & ~15) + 4; }
+
+__global__ void __launch_bounds__(1024, 1)
+    chol_near_identity_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                              double* __restrict__ Rinv, int* flag, double tol) {
+  extern __shared__ double sm[];
+  const int ld = near_id_ld(l);
+  double* F = sm;
+  double* P = F + (size_t)l * ld;
+  __shared__ double red[32];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double e = 0.0;
+  for (int idx = tid; idx < l * l; idx += nt) {
+    const int r = idx / l, c = idx - r * l;
+    const double g = G[idx];
+    e = fmax(e, fabs(g - (r == c ? 1.0 : 0.0)));
+    F[r * ld + c] = (c > r) ? g : (c == r ? 0.5 * (g - 1.0) : 0.0);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
+  if ((tid & 31) == 0) red[tid >> 5] = e;
+  __syncthreads();
+  double emax = 0.0;
+  for (int i = 0; i < (nt >> 5); ++i) emax = fmax(emax, red[i]);
+  if (!(emax <= tol)) {
+    if (tid == 0) *flag = 0;
+    return;
+  }
+  block_dmma(l, l, l, F, 1, ld, F, ld, 1, P, ld);  // P = F1^T F1
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += nt) {
+    const int i = idx / l, c = idx - i * l;
+    if (c > i) F[i * ld + c] -= P[i * ld + c];
+    else if (c == i) F[i * ld + c] -= 0.5 * P[i * ld + c];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += nt) {
+    const int i = idx / l, c = idx - i * l;
+    Rout[idx] = (c > i) ? F[i * ld + c] : (c == i ? 1.0 + F[i * ld + c] : 0.0);
+  }
+  block_dmma(l, l, l, F, ld, 1, F, ld, 1, P, ld);  // P = F2^2
+  __syncthreads();
+  // R^{-1} = I - F2 + F2^2 - F2^2 F2, the last product folded into the store
+  block_dmma(l, l, l, P, ld, 1, F, ld, 1, nullptr, ld, Rinv, F, P);
+  if (tid == 0) *flag = 1;
+}
+
+// R (upper) and R^{-1} of the Cholesky factor of G (+ shift): register kernel
+// for l <= 96, shared-memory kernel above
+int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status, int check_identity,
+                    double shift_rel, double tiny_rel, cudaStream_t st, int* near_id_flag) {
+  static bool attr = false;
+  if (!attr) {
+    TTK_TRY(qr_set_smem((const void*)chol_inv_kernel, 220 * 1024));
+    TTK_TRY(qr_set_smem((const void*)chol_near_identity_kernel, 220 * 1024));
+    TTK_TRY(qr_set_smem((const void*)chol_inv_reg_kernel<4, 1>, 160 * 1024));
+    TTK_TRY(qr_set_smem((const void*)chol_inv_reg_kernel<8, 2>, 160 * 1024));
+    TTK_TRY(qr_set_smem((const void*)chol_inv_reg_kernel<12, 3>, 160 * 1024));
+    attr = true;
+  }
+  const int* skip = nullptr;
+  if (near_id_flag && shift_rel == 0.0 && l <= kNearIdMax) {
+    const size_t smem_n = sizeof(double) * 2 * (size_t)l * (((l + 15) & ~15) + 4);
+    chol_near_identity_kernel<<<1, 1024, smem_n, st>>>(l, G, R, Rinv, near_id_flag, 1e-7);
+    TTK_CHECK_LAUNCH();
+    skip = near_id_flag;
+  }
+  const size_t smem_reg = sizeof(double) * 2 * (size_t)l * (l + 1);
+  if (l <= 32) {
+    chol_inv_reg_kernel<4, 1><<<1, kChW * 32, smem_reg, st>>>(l, G, R, Rinv, status, check_identity, shift_rel,
+                                                              tiny_rel, skip);
+  } else if (l <= 64) {
+    chol_inv_reg_kernel<8, 2><<<1, kChW * 32, smem_reg, st>>>(l, G, R, Rinv, status, check_identity, shift_rel,
+                                                              tiny_rel, skip);
+  } else if (l <= 96) {
+    chol_inv_reg_kernel<12, 3><<<1, kChW * 32, smem_reg, st>>>(l, G, R, Rinv, status, check_identity, shift_rel,
+                                                               tiny_rel, skip);
+  } else {
+    const size_t smem = sizeof(double) * (2 * (size_t)l * (l + 1) + 256 * (size_t)((l + 15) / 16));
+    chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, R, Rinv, status, check_identity, shift_rel, tiny_rel, skip);
+  }
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
 __global__ void copy_strided_kernel(int m, int l, const double* __restrict__ X, long long x_rs,
                                     long long x_cs, double* __restrict__ Y, long long y_rs, long long y_cs) {
   const long long n = (long long)m * l;
@@ -1312,7 +1594,6 @@ __global__ void __launch_bounds__(1024, 1)
   const int ld = l + 1;
   double* A = sm;
   double* X = sm + l * ld;
-  double* Tb = X + l * ld;
   __shared__ int perm[kCholMaxCols + 1];
   __shared__ int piv_s, stop_s;
   __shared__ double d0_s;
@@ -1377,7 +1658,6 @@ __global__ void __launch_bounds__(1024, 1)
     if (tid == 0) A[j * ld + j] = rjj;
     __syncthreads();
   }
-  (void)X; (void)Tb;
   for (int e = tid; e < rank * rank; e += nt) {
     int r = e / rank, c = e - r * rank;
     Rk[e] = (c >= r) ? A[r * ld + c] : 0.0;
@@ -1542,8 +1822,8 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
                        int check, double shift, double tiny) -> int {
     GemmProblem g = make_gemm(l, l, m, X, x_cs, x_rs, X, x_rs, x_cs, G, l, 1);
     TTK_TRY(gemm_group_launch(&g, 1, split, split_bytes, st));
-    chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, Rk, Ik, st_slot, check, shift, tiny);
-    TTK_CHECK_LAUNCH();
+    // second passes (checked against I) try the near-identity series first
+    TTK_TRY(launch_chol_inv(l, G, Rk, Ik, st_slot, check, shift, tiny, st, check ? status + 4 : nullptr));
     return kOk;
   };
   int hs[4] = {0, 0, 0, 0};
@@ -1602,9 +1882,7 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     // pass 3: CholeskyQR on Q2 (in Q), checked against I; Q3 = Q2 R3^{-1} -> Qb, copied back
     p = make_gemm(rho, rho, m, Q, q_cs, q_rs, Q, q_rs, q_cs, G, rho, 1);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    const size_t smem_r = sizeof(double) * (2 * (size_t)rho * (rho + 1) + 256 * (size_t)((rho + 15) / 16));
-    chol_inv_kernel<<<1, 1024, smem_r, st>>>(rho, G, R1, I1, status + 2, 1, 0.0, 1e-28);
-    TTK_CHECK_LAUNCH();
+    TTK_TRY(launch_chol_inv(rho, G, R1, I1, status + 2, 1, 0.0, 1e-28, st, status + 4));
     p = make_gemm(m, rho, rho, Q, q_rs, q_cs, I1, rho, 1, Qb, rho, 1);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
     TTK_TRY(copy_strided(m, rho, Qb, rho, 1, Q, q_rs, q_cs, st));
@@ -1632,14 +1910,12 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
       }
       return kOk;
     };
-    const size_t smem_c = sizeof(double) * (2 * (size_t)kc * (kc + 1) + 256 * (size_t)((kc + 15) / 16));
     // one CholeskyQR pass on Om; the result goes to Q's tail columns and, unless
     // it is the final pass, back into Om
-    auto chol_pass = [&](bool last) -> int {
+    auto chol_pass = [&](bool last, bool near) -> int {
       p = make_gemm(kc, kc, m, Om, 1, kc, Om, kc, 1, G, kc, 1);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-      chol_inv_kernel<<<1, 1024, smem_c, st>>>(kc, G, R1, I1, status + 2, 0, 0.0, 1e-28);
-      TTK_CHECK_LAUNCH();
+      TTK_TRY(launch_chol_inv(kc, G, R1, I1, status + 2, 0, 0.0, 1e-28, st, near ? status + 4 : nullptr));
       p = make_gemm(m, kc, kc, Om, kc, 1, I1, kc, 1, Q + (long long)rho * q_cs, q_rs, q_cs);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
       if (!last) TTK_TRY(copy_strided(m, kc, Q + (long long)rho * q_cs, q_rs, q_cs, Om, kc, 1, st));
@@ -1650,11 +1926,11 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     // kappa(Om): orthonormalise, project out again, and finish with a pass on
     // the now well-conditioned block.
     TTK_TRY(project_out());
-    TTK_TRY(chol_pass(false));
-    TTK_TRY(chol_pass(false));
+    TTK_TRY(chol_pass(false, false));
+    TTK_TRY(chol_pass(false, true));
     TTK_TRY(project_out());
-    TTK_TRY(chol_pass(false));
-    TTK_TRY(chol_pass(true));
+    TTK_TRY(chol_pass(false, true));
+    TTK_TRY(chol_pass(true, true));
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
   TTK_CHECK_CUDA(cudaStreamSynchronize(st));
