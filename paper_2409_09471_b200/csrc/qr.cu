@@ -1421,7 +1421,7 @@ __global__ void __launch_bounds__(kChW * 32, 1)
 // Strides that are 4 mod 16 make the fragment loads bank-conflict free.
 __device__ void block_dmma(int M, int N, int K, const double* A, int a_rs, int a_cs, const double* B, int b_rs,
                            int b_cs, double* C, int ldc, double* rinv_out = nullptr,
-                           const double* rinv_f = nullptr, const double* rinv_p = nullptr) {
+                           const double* rinv_f = nullptr, const double* rinv_p = nullptr, bool sub = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   const int tn = (N + 7) >> 3, tiles = ((M + 7) >> 3) * tn;
@@ -1453,6 +1453,8 @@ __device__ void block_dmma(int M, int N, int K, const double* A, int a_rs, int a
           const double v = (cn > m) ? -rinv_f[m * ldc + cn] + rinv_p[m * ldc + cn] - (c0[h] + c1[h])
                            : (cn == m ? 1.0 - rinv_f[m * ldc + cn] + rinv_p[m * ldc + cn] - (c0[h] + c1[h]) : 0.0);
           rinv_out[(size_t)m * N + cn] = v;
+        } else if (sub) {
+          C[m * ldc + cn] -= c0[h] + c1[h];
         } else {
           C[m * ldc + cn] = c0[h] + c1[h];
         }
@@ -1519,6 +1521,169 @@ __global__ void __launch_bounds__(1024, 1)
   if (tid == 0) *flag = 1;
 }
 
+// Blocked right-looking Cholesky (blocks of 16) of G + shift*trace(G) I for
+// l <= kCholMaxCols: warp 0 factors each 16 x 16 diagonal block in registers
+// (lane c owns column c; pivots by shuffle, rsqrt, no barrier inside), the
+// panel R_kk^{-T} A_kJ is a thread-per-column forward substitution, and the
+// trailing update A_JJ -= R_kJ^T R_kJ runs on the DMMA pipe.  Three barriers
+// per block instead of one per pivot.  R^{-1} (when Rinv != nullptr) by
+// blocked triangular inversion.  Same status bits as chol_inv_kernel.
+constexpr int kCbThreads = 512;
+
+// 1/sqrt(p) for normal positive p without the library's slow-path CALL (a
+// call inside the unrolled pivot loop forces the register-resident block
+// to local memory): hardware approximation plus two Newton steps (~1 ulp).
+__device__ __forceinline__ double rsqrt_nr(double p) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+  const double h = 0.5 * p;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+// one pivot of the in-register 16 x 16 diagonal-block Cholesky (lane c owns
+// column c); compile-time recursion keeps every index of d[] static
+template <int JJ>
+__device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, int bs, double tiny, int& badd,
+                                              double* invd) {
+  if constexpr (JJ < 16) {
+    double p = __shfl_sync(0xffffffffu, d[JJ], JJ);
+    if (JJ < bs && !(p > tiny)) { badd = 1; p = 1.0; }
+    if (JJ >= bs) p = 1.0;
+    const double inv = rsqrt_nr(p);
+    const double rrow = (c > JJ) ? d[JJ] * inv : (c == JJ ? p * inv : 0.0);
+    d[JJ] = rrow;
+    if (lane == JJ) invd[JJ] = inv;
+#pragma unroll
+    for (int rr = JJ + 1; rr < 16; ++rr) {
+      const double rjr = __shfl_sync(0xffffffffu, rrow, rr);
+      if (c >= rr) d[rr] -= rjr * rrow;
+    }
+    cb_diag_steps<JJ + 1>(d, c, lane, bs, tiny, badd, invd);
+  }
+}
+
+
+__device__ __forceinline__ int cb_ld(int l) { return ((l + 15) & ~15) + 4; }
+
+__global__ void __launch_bounds__(kCbThreads, 1)
+    chol_blocked_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                        double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
+                        double tiny_rel, const int* __restrict__ skip) {
+  if (skip && *skip) return;  // chol_near_identity_kernel already produced R, R^{-1}
+  extern __shared__ double sm[];
+  const int ld = cb_ld(l);
+  double* A = sm;                       // l x ld
+  double* X = A + (size_t)l * ld;       // l x ld (inverse)
+  double* Tb = X + (size_t)l * ld;      // 256 * nb
+  __shared__ double invd[kCholMaxCols + 16];
+  __shared__ double gmax_s, tr_s;
+  __shared__ int bad;
+  const int tid = threadIdx.x, nt = blockDim.x, w = tid >> 5, lane = tid & 31;
+  long long* const prof = (tid == 0) ? g_chol_prof : nullptr;
+  long long t0 = prof ? clock64() : 0, ph[6] = {0, 0, 0, 0, 0, 0};
+  if (tid == 0) bad = 0;
+  if (w == 0) {
+    double g = 0.0, tr = 0.0;
+    for (int i = lane; i < l; i += 32) { const double v = G[(size_t)i * l + i]; g = fmax(g, v); tr += v; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    tr = warp_sum(tr);
+    if (lane == 0) { gmax_s = g; tr_s = tr; }
+  }
+  __syncthreads();
+  const double sh = shift_rel > 0.0 ? shift_rel * tr_s : 0.0;
+  const double tiny = gmax_s * tiny_rel + 1e-300;
+  {
+    int badl = 0;
+    for (int e = tid; e < l * l; e += nt) {
+      const int r = e / l, c = e - r * l;
+      double v = G[e];
+      if (check_identity && fabs(v - (r == c ? 1.0 : 0.0)) > 1e-3) badl |= 2;
+      if (r == c) v += sh;
+      A[r * ld + c] = v;
+    }
+    if (badl) atomicOr(&bad, badl);
+  }
+  __syncthreads();
+  if (prof) { long long t = clock64(); ph[0] += t - t0; t0 = t; }
+  const int nb = (l + 15) >> 4;
+  for (int kb = 0; kb < nb; ++kb) {
+    const int j0 = kb * 16, bs = min(16, l - j0);
+    if (w == 0) {
+      // diagonal block: lane c (< 16) owns column c (rows 0..15 of the block)
+      const int c = lane & 15;
+      double d[16];
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr)
+        d[rr] = (rr < bs && c < bs) ? A[(j0 + rr) * ld + j0 + c] : (rr == c ? 1.0 : 0.0);
+      int badd = 0;
+      cb_diag_steps<0>(d, c, lane, bs, tiny, badd, invd + j0);
+      if (lane < 16) {
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr)
+          if (rr < bs && c < bs) A[(j0 + rr) * ld + j0 + c] = (rr <= c) ? d[rr] : 0.0;
+      }
+      if (badd && lane == 0) atomicOr(&bad, 1);
+    }
+    __syncthreads();
+    if (prof) { long long t = clock64(); ph[1] += t - t0; t0 = t; }
+    // panel: R_kJ = R_kk^{-T} A_kJ, one thread per column
+    for (int c = j0 + bs + tid; c < l; c += nt) {
+      double x[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) x[jj] = (jj < bs) ? A[(j0 + jj) * ld + c] : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        if (jj < bs) {
+          x[jj] *= invd[j0 + jj];
+#pragma unroll
+          for (int kk = jj + 1; kk < 16; ++kk)
+            if (kk < bs) x[kk] -= A[(j0 + jj) * ld + j0 + kk] * x[jj];
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj)
+        if (jj < bs) A[(j0 + jj) * ld + c] = x[jj];
+    }
+    __syncthreads();
+    if (prof) { long long t = clock64(); ph[2] += t - t0; t0 = t; }
+    // trailing update (full square; only the upper triangle is used later)
+    const int rest = l - j0 - bs;
+    if (rest > 0) {
+      const double* P = A + (size_t)j0 * ld + j0 + bs;  // bs x rest panel
+      block_dmma(rest, rest, bs, P, 1, ld, P, ld, 1, A + (size_t)(j0 + bs) * ld + j0 + bs, ld, nullptr,
+                 nullptr, nullptr, true);
+    }
+    __syncthreads();
+    if (prof) { long long t = clock64(); ph[3] += t - t0; t0 = t; }
+  }
+  for (int e = tid; e < l * l; e += nt) {
+    const int r = e / l, c = e - r * l;
+    Rout[e] = (c >= r) ? A[r * ld + c] : 0.0;
+  }
+  if (Rinv) {
+    for (int e = tid; e < l * ld; e += nt) {  // zero the strict lower part for the inverse
+      const int r = e / ld, c = e - r * ld;
+      if (c < r) A[e] = 0.0;
+    }
+    __syncthreads();
+    tri_inv_blocked(A, X, Tb, ld, l);
+    __syncthreads();
+    for (int e = tid; e < l * l; e += nt) {
+      const int r = e / l, c = e - r * l;
+      Rinv[e] = (c >= r) ? X[r * ld + c] : 0.0;
+    }
+  }
+  if (prof) {
+    ph[4] = clock64() - t0;
+    for (int i = 0; i < 5; ++i) atomicAdd((unsigned long long*)&prof[i], (unsigned long long)ph[i]);
+    atomicAdd((unsigned long long*)&prof[5], 1ull);
+  }
+  if (tid == 0 && bad) atomicOr(status, bad);
+}
+
 // R (upper) and R^{-1} of the Cholesky factor of G (+ shift): register kernel
 // for l <= 96, shared-memory kernel above
 int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status, int check_identity,
@@ -1527,9 +1692,7 @@ int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status
   if (!attr) {
     TTK_TRY(qr_set_smem((const void*)chol_inv_kernel, 220 * 1024));
     TTK_TRY(qr_set_smem((const void*)chol_near_identity_kernel, 220 * 1024));
-    TTK_TRY(qr_set_smem((const void*)chol_inv_reg_kernel<4, 1>, 160 * 1024));
-    TTK_TRY(qr_set_smem((const void*)chol_inv_reg_kernel<8, 2>, 160 * 1024));
-    TTK_TRY(qr_set_smem((const void*)chol_inv_reg_kernel<12, 3>, 160 * 1024));
+    TTK_TRY(qr_set_smem((const void*)chol_blocked_kernel, 225 * 1024));
     attr = true;
   }
   const int* skip = nullptr;
@@ -1539,16 +1702,11 @@ int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status
     TTK_CHECK_LAUNCH();
     skip = near_id_flag;
   }
-  const size_t smem_reg = sizeof(double) * 2 * (size_t)l * (l + 1);
-  if (l <= 32) {
-    chol_inv_reg_kernel<4, 1><<<1, kChW * 32, smem_reg, st>>>(l, G, R, Rinv, status, check_identity, shift_rel,
-                                                              tiny_rel, skip);
-  } else if (l <= 64) {
-    chol_inv_reg_kernel<8, 2><<<1, kChW * 32, smem_reg, st>>>(l, G, R, Rinv, status, check_identity, shift_rel,
-                                                              tiny_rel, skip);
-  } else if (l <= 96) {
-    chol_inv_reg_kernel<12, 3><<<1, kChW * 32, smem_reg, st>>>(l, G, R, Rinv, status, check_identity, shift_rel,
-                                                               tiny_rel, skip);
+  if (l <= kCholMaxCols) {
+    const int ldb = ((l + 15) & ~15) + 4;
+    const size_t smem_b = sizeof(double) * (2 * (size_t)l * ldb + 256 * (size_t)((l + 15) / 16));
+    chol_blocked_kernel<<<1, kCbThreads, smem_b, st>>>(l, G, R, Rinv, status, check_identity, shift_rel, tiny_rel,
+                                                       skip);
   } else {
     const size_t smem = sizeof(double) * (2 * (size_t)l * (l + 1) + 256 * (size_t)((l + 15) / 16));
     chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, R, Rinv, status, check_identity, shift_rel, tiny_rel, skip);
@@ -1823,7 +1981,9 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     GemmProblem g = make_gemm(l, l, m, X, x_cs, x_rs, X, x_rs, x_cs, G, l, 1);
     TTK_TRY(gemm_group_launch(&g, 1, split, split_bytes, st));
     // second passes (checked against I) try the near-identity series first
-    TTK_TRY(launch_chol_inv(l, G, Rk, Ik, st_slot, check, shift, tiny, st, check ? status + 4 : nullptr));
+    // first passes feed a triangular solve and need no inverse
+    TTK_TRY(launch_chol_inv(l, G, Rk, check ? Ik : nullptr, st_slot, check, shift, tiny, st,
+                            check ? status + 4 : nullptr));
     return kOk;
   };
   int hs[4] = {0, 0, 0, 0};
