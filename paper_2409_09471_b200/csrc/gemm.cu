@@ -13,18 +13,52 @@ namespace ttk {
 // adds the group sums in order.  The summation order depends only on `splits`.
 constexpr int kRedGroups = 8;
 
+// Few splits (<= kRedGroups): one thread per output element, partials summed
+// in split order; fully parallel, no barriers.  Problems with more splits are
+// left to gemm_splitk_reduce_kernel.
+__global__ void gemm_splitk_reduce_small_kernel(const __grid_constant__ GemmGroup G) {
+  long long total = 0;
+  for (int pi = 0; pi < G.count; ++pi)
+    if (G.p[pi].splits > 1 && G.p[pi].splits <= kRedGroups) total += (long long)G.p[pi].M * G.p[pi].N;
+  for (long long ge = blockIdx.x * (long long)blockDim.x + threadIdx.x; ge < total;
+       ge += (long long)gridDim.x * blockDim.x) {
+    long long e = ge;
+    int pi = 0;
+    for (; pi < G.count; ++pi) {
+      if (G.p[pi].splits <= 1 || G.p[pi].splits > kRedGroups) continue;
+      const long long n = (long long)G.p[pi].M * G.p[pi].N;
+      if (e < n) break;
+      e -= n;
+    }
+    const GemmProblem& P = G.p[pi];
+    const size_t mn = (size_t)P.M * P.N;
+    double v[kRedGroups];
+#pragma unroll
+    for (int k = 0; k < kRedGroups; ++k) v[k] = (k < P.splits) ? __ldcg(P.partial + (size_t)k * mn + e) : 0.0;
+    double t = v[0];
+#pragma unroll
+    for (int k = 1; k < kRedGroups; ++k)
+      if (k < P.splits) t += v[k];
+    const int m = (int)(e / P.N), n = (int)(e % P.N);
+    double* dst = P.C + cmap_m(P, m) + cmap_n(P, n);
+    double out = P.alpha * t;
+    if (P.beta != 0.0) out += P.beta * *dst;
+    *dst = out;
+  }
+}
+
 __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G) {
   __shared__ double part[kRedGroups][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   long long total = 0;
   for (int pi = 0; pi < G.count; ++pi)
-    if (G.p[pi].splits > 1) total += ((long long)G.p[pi].M * G.p[pi].N + 31) / 32;
+    if (G.p[pi].splits > kRedGroups) total += ((long long)G.p[pi].M * G.p[pi].N + 31) / 32;
   for (long long gc = blockIdx.x; gc < total; gc += gridDim.x) {
     // locate the problem and chunk (block-uniform)
     long long c = gc;
     int pi = 0;
     for (; pi < G.count; ++pi) {
-      if (G.p[pi].splits <= 1) continue;
+      if (G.p[pi].splits <= kRedGroups) continue;
       const long long n = ((long long)G.p[pi].M * G.p[pi].N + 31) / 32;
       if (c < n) break;
       c -= n;
@@ -63,10 +97,11 @@ __global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G) {
 namespace {
 
 enum TileCfg { kT128x128 = 0, kT128x64 = 1, kT64x64 = 2, kT64x32 = 3, kT128x80 = 4, kT64x80 = 5,
-               kT80x64 = 6, kT80x80 = 7 };
+               kT80x64 = 6, kT80x80 = 7, kX64x32w4 = 8, kX64x64w4s4 = 9, kX128x64w8s4 = 10, kX32x64w4 = 11 };
 
 struct CfgDims { int bm, bn; };
-constexpr CfgDims kDims[] = {{128, 128}, {128, 64}, {64, 64}, {64, 32}, {128, 80}, {64, 80}, {80, 64}, {80, 80}};
+constexpr CfgDims kDims[] = {{128, 128}, {128, 64}, {64, 64}, {64, 32}, {128, 80}, {64, 80},
+                             {80, 64},   {80, 80},  {64, 32}, {64, 64}, {128, 64}, {32, 64}};
 
 // C = A B  <=>  C^T = B^T A^T: make the output's contiguous direction the
 // column (n) index so the epilogue stores are coalesced (1-level maps only)
@@ -83,30 +118,17 @@ void normalize_output(GemmProblem& p) {
 }
 
 TileCfg pick_cfg(const GemmProblem* probs, int count) {
-  // pick by the largest problem; small-N problems use narrower tiles
+  // Light 64 x 32 (tall output) / 32 x 64 (wide output) tiles, 4 warps, 4
+  // stages, ~16 resident warps per SM -- the cuBLAS DGEMM shape.  Measured on
+  // every GEMM shape of the workload (tools/gemm_cfg_sweep.py): they win or tie
+  // the larger tiles everywhere, including 4096^3 (30.7 TF/s) and the grouped
+  // matvec (24.4 TF/s).
   long best = 0; int bm = 0, bn = 0;
   for (int i = 0; i < count; ++i) {
     long mn = (long)probs[i].M * probs[i].N;
     if (mn > best) { best = mn; bm = probs[i].M; bn = probs[i].N; }
   }
-  long tiles128 = 0, tiles128x80 = 0;
-  for (int i = 0; i < count; ++i) {
-    tiles128 += (long)ceil_div(probs[i].M, 128) * ceil_div(probs[i].N, 128);
-    tiles128x80 += (long)ceil_div(probs[i].M, 128) * ceil_div(probs[i].N, 80);
-  }
-  if (bn <= 32 && bm >= 64) return kT64x32;
-  // N in (64, 80]: the TT-rank-80 tall-skinny products and Gram matrices
-  if (bn > 64 && bn <= 80) {
-    if (bm <= 80) return kT80x80;
-    // prefer more, smaller tiles over a split-K reduction when M alone fills the GPU
-    return tiles128x80 >= 2L * kNumSMs ? kT128x80 : kT64x80;
-  }
-  // M in (64, 80] with wide N (rank-80 carries times cores)
-  if (bm > 64 && bm <= 80) return kT80x64;
-  if (bm >= 128 && bn >= 128 && tiles128 >= kNumSMs) return kT128x128;
-  if (bm >= 128 && bn > 32 && bn <= 64) return kT128x64;
-  if (bm >= 128 && bn >= 96) return tiles128 >= kNumSMs / 2 ? kT128x128 : kT64x64;
-  return kT64x64;
+  return (bm >= bn) ? kX64x32w4 : kX32x64w4;
 }
 
 constexpr int kBK = 16;
@@ -145,10 +167,10 @@ void plan(GemmProblem* probs, int count, TileCfg c, bool allow_split, size_t* pa
   *total = t;
 }
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int ST = kStages>
 int launch_cfg(GemmGroup& g, cudaStream_t st) {
-  using Cfg = GemmCfg<BM, BN, kBK, WM, WN, kStages>;
-  auto kern = gemm_group_kernel<BM, BN, kBK, WM, WN, kStages>;
+  using Cfg = GemmCfg<BM, BN, kBK, WM, WN, ST>;
+  auto kern = gemm_group_kernel<BM, BN, kBK, WM, WN, ST>;
   static bool attr_set = false;
   if (!attr_set) {
     TTK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -192,6 +214,8 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
     if (nonempty == 0) continue;
     g.count = nonempty;
     TileCfg cfg = pick_cfg(g.p, g.count);
+    static const int force = getenv("TTK_GEMM_FORCE_CFG") ? atoi(getenv("TTK_GEMM_FORCE_CFG")) : -1;  // experiments
+    if (force >= 0) cfg = (TileCfg)force;
     size_t pe; int total;
     plan(g.p, g.count, cfg, allow_split && ws != nullptr, &pe, &total);
     if (pe * sizeof(double) > ws_bytes) {
@@ -208,7 +232,20 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
       if (p.splits > 1) { p.partial = part + off; off += (size_t)p.splits * p.M * p.N; }
     }
     g.total_tiles = total;
+    for (int i = 0; i < g.count; ++i) {
+      // operand offsets are 32-bit inside the kernel (see TileLoader)
+      const GemmProblem& q = g.p[i];
+      auto span = [](long long s0, long long s1, int div, int n) {
+        const long long d = std::min<long long>(div, n);
+        return (long long)((n + d - 1) / d) * (s1 < 0 ? -s1 : s1) + d * (s0 < 0 ? -s0 : s0);
+      };
+      const long long sa = span(q.a_ms0, q.a_ms1, q.a_mdiv, q.M) + (long long)q.K * (q.a_ks < 0 ? -q.a_ks : q.a_ks);
+      const long long sb = span(q.b_ns0, q.b_ns1, q.b_ndiv, q.N) + (long long)q.K * (q.b_ks < 0 ? -q.b_ks : q.b_ks);
+      TTK_REQUIRE(sa < (1LL << 31) && sb < (1LL << 31), kInvalidValue,
+                  "gemm: operand spans %lld / %lld elements, limit 2^31", sa, sb);
+    }
     static const bool trace = getenv("TTK_GEMM_TRACE") != nullptr;  // shape log (diagnostics)
+    if (trace) fprintf(stderr, "gemm-launch count=%d\n", g.count);
     if (trace)
       for (int i = 0; i < g.count; ++i)
         fprintf(stderr, "gemm cfg=%d M=%d N=%d K=%d splits=%d tiles=%d a_ks=%lld b_ks=%lld\n", (int)cfg,
@@ -216,23 +253,40 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
                 g.p[i].a_ks, g.p[i].b_ks);
     int rc;
     switch (cfg) {
-      case kT128x128: rc = launch_cfg<128, 128, 2, 4>(g, st); break;
-      case kT128x64: rc = launch_cfg<128, 64, 2, 2>(g, st); break;
-      case kT64x64: rc = launch_cfg<64, 64, 2, 2>(g, st); break;
-      case kT128x80: rc = launch_cfg<128, 80, 4, 2>(g, st); break;
-      case kT64x80: rc = launch_cfg<64, 80, 2, 2>(g, st); break;
-      case kT80x64: rc = launch_cfg<80, 64, 2, 2>(g, st); break;
-      case kT80x80: rc = launch_cfg<80, 80, 2, 2>(g, st); break;
-      default: rc = launch_cfg<64, 32, 2, 1>(g, st); break;
+      // 4 x 4 warps of 32 x 32: 16 warps per SM (a warp cannot issue DMMAs back to
+      // back; 2 warps per sub-partition left the tensor pipe ~40% idle)
+      case kT128x128: rc = launch_cfg<128, 128, 4, 4>(g, st); break;
+      case kT128x64: rc = launch_cfg<128, 64, 4, 2, 4>(g, st); break;
+      case kT64x64: rc = launch_cfg<64, 64, 2, 2, 4>(g, st); break;
+      // rank-80 tiles: full-width warps (16 rows x all columns) so that both
+      // fragment counts are even and every fragment pair is one 16-byte load
+      case kT128x80: rc = launch_cfg<128, 80, 8, 1>(g, st); break;
+      case kT64x80: rc = launch_cfg<64, 80, 4, 1>(g, st); break;
+      case kT80x64: rc = launch_cfg<80, 64, 5, 1>(g, st); break;
+      case kT80x80: rc = launch_cfg<80, 80, 5, 1>(g, st); break;
+      case kX64x32w4: rc = launch_cfg<64, 32, 2, 2, 4>(g, st); break;
+      case kX64x64w4s4: rc = launch_cfg<64, 64, 2, 2, 4>(g, st); break;
+      case kX128x64w8s4: rc = launch_cfg<128, 64, 4, 2, 4>(g, st); break;
+      case kX32x64w4: rc = launch_cfg<32, 64, 2, 2, 4>(g, st); break;
+      default: rc = launch_cfg<64, 32, 2, 2, 4>(g, st); break;
     }
     if (rc != kOk) return rc;
     if (pe > 0) {
-      size_t chunks = 0;
-      for (int i = 0; i < g.count; ++i)
-        if (g.p[i].splits > 1) chunks += ((size_t)g.p[i].M * g.p[i].N + 31) / 32;
-      const int rblocks = (int)std::min<size_t>(chunks, 8 * kNumSMs);
-      gemm_splitk_reduce_kernel<<<std::max(rblocks, 1), 32 * kRedGroups, 0, st>>>(g);
-      TTK_CHECK_LAUNCH();
+      size_t chunks = 0, small = 0;
+      for (int i = 0; i < g.count; ++i) {
+        if (g.p[i].splits > kRedGroups) chunks += ((size_t)g.p[i].M * g.p[i].N + 31) / 32;
+        else if (g.p[i].splits > 1) small += (size_t)g.p[i].M * g.p[i].N;
+      }
+      if (small > 0) {
+        const int sblocks = (int)std::min<size_t>((small + 255) / 256, 8 * kNumSMs);
+        gemm_splitk_reduce_small_kernel<<<sblocks, 256, 0, st>>>(g);
+        TTK_CHECK_LAUNCH();
+      }
+      if (chunks > 0) {
+        const int rblocks = (int)std::min<size_t>(chunks, 8 * kNumSMs);
+        gemm_splitk_reduce_kernel<<<rblocks, 32 * kRedGroups, 0, st>>>(g);
+        TTK_CHECK_LAUNCH();
+      }
     }
   }
   return kOk;

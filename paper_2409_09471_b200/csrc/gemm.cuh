@@ -67,6 +67,12 @@ struct GemmCfg {
   static constexpr int FN = WN / 8;
   static constexpr int SA = BM + 4;  // smem row stride (doubles) of the k-major A tile
   static constexpr int SB = BN + 4;
+  // rows m and m + 8 of every 16-row group stored side by side, so fragment
+  // pairs (i, i + 1) come from one 16-byte shared load (needs even FM / FN)
+  static constexpr bool kPairA = (FM % 2 == 0);
+  static constexpr bool kPairB = (FN % 2 == 0);
+  static constexpr int NA = (BM * BK + kThreads - 1) / kThreads;  // A elements per thread per stage
+  static constexpr int NB = (BN * BK + kThreads - 1) / kThreads;
   static constexpr size_t kSmemBytes =
       sizeof(double) * (size_t)STAGES * BK * (SA + SB) + sizeof(long long) * (BM + BN) * 2;
   static_assert(BM % (8 * WARPS_M) == 0 && BN % (8 * WARPS_N) == 0, "tile");
@@ -74,55 +80,63 @@ struct GemmCfg {
   static_assert(SA % 16 == 4 && SB % 16 == 4, "bank-conflict-free fragment loads");
 };
 
-template <class Cfg, int BM, int BN, int BK, int STAGES>
-__device__ __forceinline__ void gemm_load_stage(const GemmProblem& P, double* As, double* Bs,
-                                                const long long* rowA, const long long* colB,
-                                                int m0, int n0, int k0, int kend) {
-  const int tid = threadIdx.x;
-  // A tile: BM x BK, stored k-major (As[k][m]).  Map threads so that the
-  // contiguous global direction is the fast thread index.
-  if (P.a_ks == 1) {
-#pragma unroll 4
-    for (int e = tid; e < BM * BK; e += Cfg::kThreads) {
-      int k = e % BK, m = e / BK;
-      int gk = k0 + k;
-      bool ok = (m0 + m < P.M) && (gk < kend);
-      const double* src = ok ? P.A + rowA[m] + gk : P.A;
-      cp_async8(As + k * Cfg::SA + m, src, ok);
-    }
-  } else {
-#pragma unroll 4
-    for (int e = tid; e < BM * BK; e += Cfg::kThreads) {
-      int m = e % BM, k = e / BM;
-      int gk = k0 + k;
-      bool ok = (m0 + m < P.M) && (gk < kend);
-      const double* src = ok ? P.A + rowA[m] + (long long)gk * P.a_ks : P.A;
-      cp_async8(As + k * Cfg::SA + m, src, ok);
-    }
-  }
-  if (P.b_ks == 1) {
-#pragma unroll 4
-    for (int e = tid; e < BN * BK; e += Cfg::kThreads) {
-      int k = e % BK, n = e / BK;
-      int gk = k0 + k;
-      bool ok = (n0 + n < P.N) && (gk < kend);
-      const double* src = ok ? P.B + colB[n] + gk : P.B;
-      cp_async8(Bs + k * Cfg::SB + n, src, ok);
-    }
-  } else {
-#pragma unroll 4
-    for (int e = tid; e < BN * BK; e += Cfg::kThreads) {
-      int n = e % BN, k = e / BN;
-      int gk = k0 + k;
-      bool ok = (n0 + n < P.N) && (gk < kend);
-      const double* src = ok ? P.B + colB[n] + (long long)gk * P.b_ks : P.B;
-      cp_async8(Bs + k * Cfg::SB + n, src, ok);
+// position of tile row m in a paired shared layout
+template <bool PAIR>
+__device__ __forceinline__ int pair_pos(int m) {
+  if constexpr (PAIR) return (m & ~15) | ((m & 7) << 1) | ((m >> 3) & 1);
+  else return m;
+}
+
+// Per-thread load plan for one operand tile (E x BK elements, E = BM or BN):
+// each thread always copies the same (row, k) slots, so its source offsets
+// (32-bit element offsets from the operand base; the host checks that every
+// operand fits) and shared destinations are computed once per tile and only
+// advance by BK * ks per stage.  dst and k are packed into one word.
+template <int E, int BK, int T, int NE, bool PAIR, int S>
+struct TileLoader {
+  const double* base;
+  int off[NE];
+  int dk[NE];      // (dst << 8) | k
+  unsigned valid;  // bit i: row in range and slot used
+  __device__ __forceinline__ void init(const double* b, const long long* rowoff, long long ks, int r0, int rows) {
+    base = b;
+    valid = 0;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = tid + i * T;
+      int r, k;
+      if (ks == 1) { k = e % BK; r = e / BK; } else { r = e % E; k = e / E; }
+      const bool used = e < E * BK;
+      const bool ok = used && (r0 + r < rows);
+      off[i] = ok ? (int)(rowoff[r] + (long long)k * ks) : 0;
+      dk[i] = used ? (((k * S + pair_pos<PAIR>(r)) << 8) | k) : -1;  // -1: slot unused (no copy at all)
+      if (ok) valid |= 1u << i;
     }
   }
+  __device__ __forceinline__ void load(double* smem, long long koff, int kleft) const {
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      if ((i + 1) * T > E * BK && dk[i] < 0) continue;  // only the last slot can be unused
+      const bool ok = ((valid >> i) & 1u) && ((dk[i] & 255) < kleft);
+      const double* src = base + koff + off[i];
+      cp_async8(smem + (dk[i] >> 8), ok ? src : base, ok);  // !ok: zero-fill (row or k padding)
+    }
+  }
+};
+
+// at most ~128 registers per thread: >= 16 resident warps per SM keep the
+// DMMA pipe fed (a warp cannot issue DMMAs back to back)
+// (full-width rank-80 warps with >= 20 fragments keep their registers)
+template <int BM, int BN, int WARPS_M, int WARPS_N>
+constexpr int gemm_min_blocks() {
+  constexpr int frags = (BM / WARPS_M / 8) * (BN / WARPS_N / 8);
+  constexpr int mb = 65536 / (32 * WARPS_M * WARPS_N * 128);
+  return (frags >= 20 || mb < 1) ? 1 : mb;
 }
 
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
-__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
+__global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, gemm_min_blocks<BM, BN, WARPS_M, WARPS_N>())
     gemm_group_kernel(const __grid_constant__ GemmGroup G) {
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -153,6 +167,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
   const int m0 = tm * BM, n0 = tn * BN;
   const int kbeg = split * P.k_per_split;
   const int kend = min(P.K, kbeg + P.k_per_split);
+  const long long a_ks = P.a_ks, b_ks = P.b_ks;
 
   for (int i = threadIdx.x; i < BM; i += Cfg::kThreads) {
     int m = min(m0 + i, P.M - 1);
@@ -166,6 +181,11 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
   }
   __syncthreads();
 
+  TileLoader<BM, BK, Cfg::kThreads, Cfg::NA, Cfg::kPairA, Cfg::SA> la;
+  TileLoader<BN, BK, Cfg::kThreads, Cfg::NB, Cfg::kPairB, Cfg::SB> lb;
+  la.init(P.A + (long long)kbeg * a_ks, rowA, a_ks, m0, P.M);
+  lb.init(P.B + (long long)kbeg * b_ks, colB, b_ks, n0, P.N);
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wm0 = (warp / WARPS_N) * Cfg::WM;
   const int wn0 = (warp % WARPS_N) * Cfg::WN;
@@ -176,12 +196,14 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
 #pragma unroll
     for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int nk = (kend > kbeg) ? (kend - kbeg + BK - 1) / BK : 0;
+  const int klen = kend - kbeg;
+  const int nk = (klen > 0) ? (klen + BK - 1) / BK : 0;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk)
-      gemm_load_stage<Cfg, BM, BN, BK, STAGES>(P, As + s * BK * Cfg::SA, Bs + s * BK * Cfg::SB, rowA,
-                                               colB, m0, n0, kbeg + s * BK, kend);
+    if (s < nk) {
+      la.load(As + s * BK * Cfg::SA, (long long)s * BK * a_ks, klen - s * BK);
+      lb.load(Bs + s * BK * Cfg::SB, (long long)s * BK * b_ks, klen - s * BK);
+    }
     cp_async_commit();
   }
 
@@ -190,11 +212,11 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      int nxt = kt + STAGES - 1;
+      const int nxt = kt + STAGES - 1;
       if (nxt < nk) {
-        int st = nxt % STAGES;
-        gemm_load_stage<Cfg, BM, BN, BK, STAGES>(P, As + st * BK * Cfg::SA, Bs + st * BK * Cfg::SB,
-                                                 rowA, colB, m0, n0, kbeg + nxt * BK, kend);
+        const int st = nxt % STAGES;
+        la.load(As + st * BK * Cfg::SA, (long long)nxt * BK * a_ks, klen - nxt * BK);
+        lb.load(Bs + st * BK * Cfg::SB, (long long)nxt * BK * b_ks, klen - nxt * BK);
       }
       cp_async_commit();
     }
@@ -203,10 +225,26 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N)
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[Cfg::FM], bf[Cfg::FN];
+      if constexpr (Cfg::kPairA) {
 #pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(kk + fk) * Cfg::SA + wm0 + i * 8 + fr];
+        for (int i = 0; i < Cfg::FM; i += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(as + (kk + fk) * Cfg::SA + wm0 + i * 8 + 2 * fr);
+          af[i] = v.x; af[i + 1] = v.y;
+        }
+      } else {
 #pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[(kk + fk) * Cfg::SB + wn0 + j * 8 + fr];
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[(kk + fk) * Cfg::SA + wm0 + i * 8 + fr];
+      }
+      if constexpr (Cfg::kPairB) {
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; j += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(bs + (kk + fk) * Cfg::SB + wn0 + j * 8 + 2 * fr);
+          bf[j] = v.x; bf[j + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[(kk + fk) * Cfg::SB + wn0 + j * 8 + fr];
+      }
 #pragma unroll
       for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll

@@ -1924,28 +1924,90 @@ __global__ void __launch_bounds__(kTrsmWarps * 32)
   }
 }
 
+// Blocked variant: a CTA owns 64 rows.  For every 16-column block J the
+// off-diagonal part Y_J -= Q_{<J} R_{<J,J} runs on the DMMA pipe
+// (block_dmma), and only the 16 x 16 diagonal solve is scalar: four threads
+// per row, each owning four columns, pivot value broadcast by shuffle.
+// Same backward-stable forward substitution, ~10x fewer instructions.
+constexpr int kTbRows = 64, kTbThreads = 256;
+
+__global__ void __launch_bounds__(kTbThreads)
+    trsm_blocked_kernel(int m, int l, const double* Y, long long y_rs, long long y_cs,
+                        const double* __restrict__ R, double* Q, long long q_rs, long long q_cs) {
+  extern __shared__ __align__(16) double tsm[];
+  const int ld = ((l + 15) & ~15) + 4;
+  double* sR = tsm;                          // l x ld
+  double* sY = sR + (size_t)l * ld;          // kTbRows x ld
+  double* rinv = sY + (size_t)kTbRows * ld;  // l
+  const int tid = threadIdx.x;
+  for (int e = tid; e < l * l; e += kTbThreads) {
+    const int r = e / l, c = e - r * l;
+    sR[r * ld + c] = R[e];
+  }
+  for (int j = tid; j < l; j += kTbThreads) rinv[j] = 1.0 / R[(size_t)j * l + j];
+  const int row = tid >> 2, g = tid & 3;
+  for (long long r0 = (long long)blockIdx.x * kTbRows; r0 < m; r0 += (long long)gridDim.x * kTbRows) {
+    __syncthreads();
+    for (int e = tid; e < kTbRows * l; e += kTbThreads) {
+      const int r = e / l, c = e - r * l;
+      sY[r * ld + c] = (r0 + r < m) ? Y[(r0 + r) * y_rs + (long long)c * y_cs] : 0.0;
+    }
+    __syncthreads();
+    for (int j0 = 0; j0 < l; j0 += 16) {
+      const int bs = min(16, l - j0);
+      if (j0 > 0) {
+        block_dmma(kTbRows, bs, j0, sY, ld, 1, sR + j0, ld, 1, sY + j0, ld, nullptr, nullptr, nullptr, true);
+        __syncthreads();
+      }
+      // diagonal block: thread (row, g) owns columns j0 + g + 4 k
+      double t[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = g + 4 * k;
+        t[k] = (c < bs) ? sY[row * ld + j0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        if (jj < bs) {
+          const int kj = jj >> 2;
+          double v = t[kj] * rinv[j0 + jj];
+          v = __shfl_sync(0xffffffffu, v, (threadIdx.x & ~3) | (jj & 3), 32);
+          if ((jj & 3) == g) t[kj] = v;
+          const double* rr = sR + (j0 + jj) * ld + j0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int c = g + 4 * k;
+            if (c > jj && c < bs) t[k] -= v * rr[c];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = g + 4 * k;
+        if (c < bs) sY[row * ld + j0 + c] = t[k];
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < kTbRows * l; e += kTbThreads) {
+      const int r = e / l, c = e - r * l;
+      if (r0 + r < m) Q[(r0 + r) * q_rs + (long long)c * q_cs] = sY[r * ld + c];
+    }
+  }
+}
+
 int trsm_right_upper(int m, int l, const double* Y, long long y_rs, long long y_cs, const double* R, double* Q,
                      long long q_rs, long long q_cs, cudaStream_t st) {
   if (m <= 0 || l <= 0) return kOk;
   TTK_REQUIRE(l <= 128, kInvalidValue, "trsm: %d columns exceed 128", l);
   static bool attr = false;
   if (!attr) {
-    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<1>, 140 * 1024));
-    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<2>, 140 * 1024));
-    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<3>, 140 * 1024));
-    TTK_TRY(qr_set_smem((const void*)trsm_rows_kernel<4>, 140 * 1024));
+    TTK_TRY(qr_set_smem((const void*)trsm_blocked_kernel, 220 * 1024));
     attr = true;
   }
-  const size_t smem = sizeof(double) * ((size_t)l * l + l);
-  const long long rows_per_block = kTrsmWarps * 2;
-  const int grid = (int)std::min<long long>((m + rows_per_block - 1) / rows_per_block, 4LL * kNumSMs);
-  const int cpl = (l + 31) / 32;
-  switch (cpl) {
-    case 1: trsm_rows_kernel<1><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
-    case 2: trsm_rows_kernel<2><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
-    case 3: trsm_rows_kernel<3><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
-    default: trsm_rows_kernel<4><<<grid, kTrsmWarps * 32, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs); break;
-  }
+  const int ld = ((l + 15) & ~15) + 4;
+  const size_t smem = sizeof(double) * ((size_t)l * ld + (size_t)kTbRows * ld + l);
+  const int grid = (int)std::min<long long>((m + kTbRows - 1) / kTbRows, 2LL * kNumSMs);
+  trsm_blocked_kernel<<<grid, kTbThreads, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs);
   TTK_CHECK_LAUNCH();
   return kOk;
 }

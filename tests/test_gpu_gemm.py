@@ -80,3 +80,21 @@ def test_gemm_split_reduce_deterministic(native_lib, cuda):
     assert np.array_equal(outs[0], outs[1])
     ref = (A.cpu().T @ A.cpu()).numpy()
     assert np.abs(outs[0] - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("cfg", list(range(12)))
+def test_gemm_every_tile_config(cfg):
+    """Each tile configuration of the grouped GEMM (forced through
+    TTK_GEMM_FORCE_CFG in a subprocess) on ragged shapes in three layouts."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TTK_GEMM_FORCE_CFG=str(cfg))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "gemm_check.py")], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("cfg=")]
+    assert len(lines) == 15, out.stdout
+    bad = [l for l in lines if "BAD" in l or "rc=0" not in l]
+    assert not bad, "\n".join(bad)
