@@ -134,11 +134,13 @@ def load_peaks():
         return {}
 
 
-def jacobi_roofline(T, torch, dev, stream, l=80):
-    """The step's dominant kernel by time is the single-CTA one-sided Jacobi SVD
-    of the truncation (one per core).  Time one l x l instance live and report
-    its algorithmic FLOPs against ONE SM's fp64 peak (the kernel is a single
-    CTA by construction: the TT-SVD chain is sequential)."""
+def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=None):
+    """The step's dominant kernel by time is the one-sided Jacobi SVD of the
+    truncation (one per core, a sequential chain).  It runs on one 8-CTA
+    cluster (qr.cu jacobi_cluster_kernel): pair slots spread over 8 SMs,
+    columns register-resident, neighbour moves over DSMEM.  Time one l x l
+    instance live and report its algorithmic FLOPs against the fp64 peak of
+    the 8 SMs it occupies; the bound is the per-round latency chain."""
     from paper_2409_09471_b200 import _lib
     lib = _lib.load()
     g = torch.Generator().manual_seed(0)
@@ -165,12 +167,18 @@ def jacobi_roofline(T, torch, dev, stream, l=80):
     lib.ttk_debug_svd_sweeps(None)
     # per sweep l(l-1)/2 pairs x (3 dot FMAs + 2x2 rotation FMAs on C and on V) per row
     flops = sweeps * (l * (l - 1) / 2) * (6.0 * l + 12.0 * l)
-    sm_peak = 33.9e3 / 148  # GFLOP/s, measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
+    peak8 = 8 * 33.9e3 / 148  # GFLOP/s of 8 SMs, measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
     ach = flops / (ms * 1e-3) / 1e9
-    return {"kernel": "jacobi_svd_kernel (1 CTA, %dx%d, V accumulated)" % (l, l), "ms": ms, "sweeps": sweeps,
-            "bound": "latency (single-SM sequential sweeps)", "achieved_gflops": ach,
-            "peak_gflops_one_sm": sm_peak, "frac_of_one_sm": ach / sm_peak,
-            "share_of_step": "~55% (profiles/r01_launches_cfg3_summary.txt)"}
+    rounds = sweeps * (l - 1)
+    out = {"kernel": "jacobi_cluster_kernel (8-CTA cluster, %dx%d, V accumulated)" % (l, l), "ms": ms,
+           "sweeps": sweeps, "rounds": rounds, "us_per_round": ms * 1e3 / max(rounds, 1),
+           "bound": "latency (sequential rotation rounds; per round: dot, 16-lane reduction, "
+                    "rotation, DSMEM neighbour exchange)",
+           "achieved_gflops": ach, "peak_gflops_8_sms": peak8, "frac_of_8_sms": ach / peak8}
+    if calls_per_step and step_ms:
+        out["share_of_step_est"] = calls_per_step * ms / step_ms
+        out["share_basis"] = "%d calls/step x this single-call time / ms_per_step" % calls_per_step
+    return out
 
 
 def cfg3_flops(C):
@@ -323,16 +331,23 @@ def run_b200(args):
     mv_ms = k0.elapsed_time(k1) / reps
     peak = fp64_peak(torch, dev)
     achieved = mv_flops / (mv_ms * 1e-3) / 1e12
-    roofline = {"bound": "tensor", "kernel": "gemm_group_kernel<128,128> (tt_matvec, 1 launch/step)",
+    # dram__bytes_read.sum + dram__bytes_write.sum of this launch from the committed
+    # ncu --set full capture (profiles/r01_matvec_traffic.json)
+    traffic, traffic_src = None, "none"
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_matvec_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        traffic, traffic_src = tj.get("traffic_bytes"), "ncu --set full, " + tj.get("source", tpath)
+    roofline = {"bound": "tensor", "kernel": "gemm_group_kernel<64,32> (tt_matvec, 1 grouped launch/step)",
                 "achieved": achieved, "peak": peak / 1e3, "unit": "TFLOP/s", "frac": achieved / (peak / 1e3),
                 "peak_source": "live cuBLAS DGEMM 4096^3 (fp64 tensor pipe; MEASURED_PEAKS.json has no "
                                "fp64 entry; DMMA issue peak measured 37.1 TF/s, profiles/fp64_peak_r01.log)",
-                # dram__bytes_read.sum + dram__bytes_write.sum of this launch from the committed
-                # ncu --set full capture (profiles/r01_matvec_r01_metrics.txt): 0.162 + 1.077 GB
-                "traffic": 1.239e9, "traffic_source": "ncu --set full, profiles/r01_matvec_r01_metrics.txt",
+                "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_flops": mv_flops,
                 "algorithmic_bytes": 8.0 * sum(c.numel() for c in y.cores)}
-    roofline["dominant_kernel"] = jacobi_roofline(T, torch, dev, stream)
+    roofline["dominant_kernel"] = jacobi_roofline(T, torch, dev, stream, calls_per_step=len(C["x"]) - 1,
+                                                  step_ms=ms)
 
     # ---- end-to-end through the public API with host buffers ----
     host_op = [torch.as_tensor(g).pin_memory() for g in C["op"]]

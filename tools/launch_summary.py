@@ -13,7 +13,8 @@ def summary(path, top=25):
         name = name.split("(")[0][:70]
         v = float(r["Metric Value"].replace(",", ""))
         u = r["Metric Unit"]
-        v = v / 1e3 if u == "nsecond" else (v * 1e3 if u == "msecond" else v)
+        # to microseconds
+        v = v / 1e3 if u in ("nsecond", "ns") else (v * 1e3 if u in ("msecond", "ms") else v)
         agg[name][0] += 1
         agg[name][1] += v
     tot = sum(v[1] for v in agg.values())
