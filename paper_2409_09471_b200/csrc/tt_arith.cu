@@ -15,6 +15,7 @@ struct ConcatCore {
   double* out;
   long long rows;     // R0_total * n   (output rows, each of length R1_total)
   long long row_begin;  // prefix over cores (in rows)
+  int blk_begin;        // first CTA of this core
   int R0, R1, n;
   int kind;  // 0 first (concat along axis 2), 1 middle (block diagonal), 2 last (axis 0), 3 d==1 (sum)
   const double* in[kMaxConcatTerms];
@@ -30,58 +31,77 @@ struct ConcatParams {
   ConcatCore c[kMaxConcatCores];
 };
 
-// One warp per output row (r, i) of length R1: zeros outside the diagonal
-// block, a copy (times coeff for the last core) inside it.
-__global__ void concat_kernel(const __grid_constant__ ConcatParams P) {
-  const int lane = threadIdx.x & 31;
-  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-  for (long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       row < P.total_rows; row += warps) {
-    int k = 0;
-    while (k + 1 < P.ncores && P.c[k + 1].row_begin <= row) ++k;
-    const ConcatCore& C = P.c[k];
-    const long long local = row - C.row_begin;
-    const int r = (int)(local / C.n);
-    const int i = (int)(local - (long long)r * C.n);
-    double* dst = C.out + local * C.R1;
-    if (C.kind == 3) {  // d == 1: elementwise sum, reference order ((t0 + c1 t1) + c2 t2)...
-      for (int col = lane; col < C.R1; col += 32) {
-        double acc = P.coeff[0] == 1.0 ? C.in[0][(long long)i * C.R1 + col]
-                                       : __dmul_rn(P.coeff[0], C.in[0][(long long)i * C.R1 + col]);
-        // separate multiply and add (no FMA contraction): bit-exact with numpy
-        for (int t = 1; t < P.nterms; ++t)
-          acc = __dadd_rn(acc, __dmul_rn(P.coeff[t], C.in[t][(long long)i * C.R1 + col]));
-        dst[col] = acc;
+// Block-diagonal concatenation (tt_add generalised to a linear combination,
+// tt.py:254-275 + tt_scale tt.py:278-282).  Each CTA owns kConcatRows output
+// rows of ONE core (found once by binary search over per-core CTA offsets):
+// first/middle cores are written warp-per-row with 16-byte stores (zeros
+// outside the term's column block), last cores and d == 1 thread-per-element.
+// Multiply and add stay separate (no FMA contraction): bit-exact with numpy.
+constexpr int kConcatRows = 64;
+
+__device__ __forceinline__ double concat_elem(const ConcatCore& C, const double* src, int c0, int w, int col) {
+  return (col >= c0 && col < c0 + w) ? src[col - c0] : 0.0;
+}
+
+__global__ void __launch_bounds__(256) concat_kernel(const __grid_constant__ ConcatParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int lo = 0, hi = P.ncores - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.c[mid].blk_begin <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  const ConcatCore& C = P.c[lo];
+  const long long r_begin = (long long)(blockIdx.x - C.blk_begin) * kConcatRows;
+  const long long r_end = min(C.rows, r_begin + kConcatRows);
+  if (C.kind == 2 || C.kind == 3) {
+    // one output element per row: thread per element
+    for (long long row = r_begin + threadIdx.x; row < r_end; row += blockDim.x) {
+      const int r = (int)(row / C.n);
+      const int i = (int)(row - (long long)r * C.n);
+      if (C.kind == 3) {
+        for (int col = 0; col < C.R1; ++col) {  // d == 1: R1 == 1 after normalisation
+          double acc = P.coeff[0] == 1.0 ? C.in[0][(long long)i * C.R1 + col]
+                                         : __dmul_rn(P.coeff[0], C.in[0][(long long)i * C.R1 + col]);
+          for (int t = 1; t < P.nterms; ++t)
+            acc = __dadd_rn(acc, __dmul_rn(P.coeff[t], C.in[t][(long long)i * C.R1 + col]));
+          C.out[row * C.R1 + col] = acc;
+        }
+      } else {
+        int t = 0;
+        while (t + 1 < P.nterms && C.r0_off[t + 1] <= r) ++t;
+        const double v = C.in[t][(long long)(r - C.r0_off[t]) * C.n + i];
+        C.out[row] = (P.coeff[t] == 1.0) ? v : v * P.coeff[t];
       }
-      continue;
     }
-    // which term owns this row?
-    int t = 0;
-    if (C.kind != 0) {
-      while (t + 1 < P.nterms && C.r0_off[t + 1] <= r) ++t;
-    }
-    const int rl = r - C.r0_off[t];
+    return;
+  }
+  const bool vec = (C.R1 % 2 == 0) && ((reinterpret_cast<uintptr_t>(C.out) & 15) == 0);
+  for (long long row = r_begin + warp; row < r_end; row += nwarps) {
+    const int r = (int)(row / C.n);
+    const int i = (int)(row - (long long)r * C.n);
+    double* dst = C.out + row * C.R1;
     if (C.kind == 0) {
-      // first core: R0 == 1, concatenate along the column (axis 2) index
+      // first core: R0 == 1, the terms' columns side by side (axis 2)
       for (int col = lane; col < C.R1; col += 32) {
         int tt = 0;
         while (tt + 1 < P.nterms && C.r1_off[tt + 1] <= col) ++tt;
         const int w = C.r1_off[tt + 1] - C.r1_off[tt];
-        double v = C.in[tt][(long long)i * w + (col - C.r1_off[tt])];
-        dst[col] = v;
+        dst[col] = C.in[tt][(long long)i * w + (col - C.r1_off[tt])];
       }
-    } else if (C.kind == 2) {
-      // last core: R1 == 1, rows of term t scaled by coeff[t] (tt_scale absorbs into last core)
-      const double v = C.in[t][(long long)rl * C.n + i];
-      if (lane == 0) dst[0] = (P.coeff[t] == 1.0) ? v : v * P.coeff[t];
+      continue;
+    }
+    int t = 0;
+    while (t + 1 < P.nterms && C.r0_off[t + 1] <= r) ++t;
+    const int c0 = C.r1_off[t], w = C.r1_off[t + 1] - c0;
+    const double* src = C.in[t] + ((long long)(r - C.r0_off[t]) * C.n + i) * w;
+    if (vec) {
+      double2* d2 = reinterpret_cast<double2*>(dst);
+      for (int cp = lane; cp < (C.R1 >> 1); cp += 32) {
+        const int col = cp << 1;
+        d2[cp] = make_double2(concat_elem(C, src, c0, w, col), concat_elem(C, src, c0, w, col + 1));
+      }
     } else {
-      const int c0 = C.r1_off[t], w = C.r1_off[t + 1] - c0;
-      const double* src = C.in[t] + ((long long)rl * C.n + i) * w;
-      for (int col = lane; col < C.R1; col += 32) {
-        double v = 0.0;
-        if (col >= c0 && col < c0 + w) v = src[col - c0];
-        dst[col] = v;
-      }
+      for (int col = lane; col < C.R1; col += 32) dst[col] = concat_elem(C, src, c0, w, col);
     }
   }
 }
@@ -157,7 +177,7 @@ int ttk_tt_concat(int d, int nterms, const double* coeff, const int* dims, const
     TTK_REQUIRE(ranks[t * (d + 1)] == 1 && ranks[t * (d + 1) + d] == 1, kShapeMismatch,
                 "term %d: boundary ranks must equal 1", t);
   }
-  long long rows = 0;
+  long long rows = 0, blocks_total = 0;
   for (int k = 0; k < d; ++k) {
     ConcatCore& C = P.c[k];
     C.out = out[k];
@@ -174,11 +194,14 @@ int ttk_tt_concat(int d, int nterms, const double* coeff, const int* dims, const
     C.R1 = (C.kind == 2 || C.kind == 3) ? 1 : C.r1_off[nterms];
     C.rows = (long long)C.R0 * C.n;
     C.row_begin = rows;
+    C.blk_begin = (int)blocks_total;
+    blocks_total += (C.rows + kConcatRows - 1) / kConcatRows;
     rows += C.rows;
   }
   P.total_rows = rows;
   if (rows == 0) return kOk;
-  int blocks = (int)std::min<long long>((rows + 7) / 8, 8LL * kNumSMs);
+  TTK_REQUIRE(blocks_total < (1LL << 31), kInvalidValue, "tt_concat: output too large");
+  const int blocks = (int)blocks_total;
   concat_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(P);
   TTK_CHECK_LAUNCH();
   return kOk;

@@ -57,4 +57,13 @@ if "concat" in which:
     inb = sum(c.numel() for v in [vt] + ws for c in v.cores) * 8
     best, med = timeit(lambda: T.tt_combine([vt] + ws, [1, -0.1, -0.2, -0.3]))
     res["concat_cfg5"] = {"ms": best, "med_ms": med, "bytes": tot + inb, "gbs": (tot + inb) / best / 1e6}
+    # SURVEY 8(d) axpy example: ranks [120, 60, 60, 60] -> 300
+    vt = T.tt_random([n] * d, [120] * (d - 1), seed=1, device=dev)
+    ws = [T.tt_random([n] * d, [60] * (d - 1), seed=2 + i, device=dev) for i in range(3)]
+    out = T.tt_combine([vt] + ws, [1, -0.1, -0.2, -0.3])
+    tot = sum(c.numel() for c in out.cores) * 8
+    inb = sum(c.numel() for v in [vt] + ws for c in v.cores) * 8
+    del out
+    best, med = timeit(lambda: T.tt_combine([vt] + ws, [1, -0.1, -0.2, -0.3]))
+    res["concat_r300"] = {"ms": best, "med_ms": med, "bytes": tot + inb, "gbs": (tot + inb) / best / 1e6}
 print(json.dumps(res, indent=1))
