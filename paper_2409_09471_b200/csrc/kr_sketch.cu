@@ -40,46 +40,106 @@ struct KrParams {
 };
 
 namespace kr {
+// 64 rows of one vector per CTA; 8 warps = 4 row groups (16 rows) x 2 column
+// halves (64 state columns each).  The K loop of mode k runs over (a, i-chunk)
+// so the state value s_j[a] is uniform per stage (no index divisions), the
+// F_k tile (64 x n) stays resident in shared memory for the whole mode, and
+// only the core rows C_k[a, i0:i0+16, :] are streamed.
 constexpr int WARPS = 8;
-constexpr int FM = 2;                 // 16 rows per warp
-constexpr int BM = WARPS * 8 * FM;    // 128 rows per CTA
+constexpr int BM = 64;                // rows per CTA
 constexpr int BN = 128;               // max rank handled by the fused path
-constexpr int FNMAX = BN / 8;
-constexpr int BK = 16;
-constexpr int STAGES = 2;
+constexpr int FNH = 10;               // max fragments per warp along n (fn - 2*(fn/4) <= 10 for fn <= 16)
+constexpr int BK = 32;
+constexpr int STAGES = 3;
+constexpr int NMAX = 96;              // mode size handled by the fused path (smem: state + F tile + 3 stages)
 constexpr int SST = BN + 1;           // odd stride: conflict-free state reads
-constexpr int SF = BM + 4;
+constexpr int SFT = BM + 4;           // F tile, i-major: Ft[i][row], 4 mod 16
 constexpr int SB = BN + 4;
-constexpr size_t kSmem = sizeof(double) * ((size_t)BM * SST + (size_t)STAGES * BK * (SF + SB)) +
-                         sizeof(int) * STAGES * BK;
+constexpr int CPT = BK * BN / (WARPS * 32);  // C elements per thread per stage
+// F tile sized by the largest mode of the launch (smem_bytes(nmax))
+constexpr size_t smem_bytes(int nmax) {
+  return sizeof(double) * ((size_t)BM * SST + (size_t)((nmax + BK - 1) / BK * BK) * SFT + (size_t)STAGES * BK * SB);
+}
 }  // namespace kr
 
-__device__ __forceinline__ void kr_load_stage(const KrParams& P, const double* Fk, const double* Ck,
-                                              int n, int r1, int K, int k0, int j0, double* Fs,
-                                              double* Bs, int* r0tab) {
+// One mode of the fused sketch for a warp owning FNW state-column fragments
+// (compile-time: no branches around the warp-synchronous DMMAs).
+template <int FNW>
+__device__ __forceinline__ void kr_mode(double* St, const double* Ft, double* Bs, const double* Ck, int r1,
+                                        int n, int nic, int nst, int wrow, int wcol, const int (&ckk)[kr::CPT],
+                                        const int (&ccol)[kr::CPT]) {
   using namespace kr;
-  const int tid = threadIdx.x;
-  // F chunk: Fs[kk][row] = F[j0+row][i(k0+kk)]
-  for (int e = tid; e < BM * BK; e += WARPS * 32) {
-    int kk = e % BK, row = e / BK;
-    int k = k0 + kk;
-    bool ok = (k < K) && (j0 + row < P.S);
-    int a = ok ? k / n : 0;
-    int i = k - a * n;
-    const double* src = ok ? Fk + (long long)(j0 + row) * n + i : Fk;
-    cp_async8(Fs + kk * SF + row, src, ok);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int fr = lane >> 2, fk = lane & 3;
+  auto load_c = [&](int s, int buf) {
+    const int a = s / nic, ic = s - a * nic;
+    const long long kb = (long long)a * n + ic * BK;
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const bool ok = (ic * BK + ckk[q] < n) && (ccol[q] < r1);
+      const double* src = ok ? Ck + (kb + ckk[q]) * r1 + ccol[q] : Ck;
+      cp_async8(Bs + (size_t)buf * BK * SB + ckk[q] * SB + pair_pos<true>(ccol[q]), src, ok);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nst) load_c(s, s);
+    cp_async_commit();
   }
-  // C chunk: Bs[kk][col] = C[(k0+kk), col]  (C as (r0*n) x r1 row-major)
-  for (int e = tid; e < BN * BK; e += WARPS * 32) {
-    int col = e % BN, kk = e / BN;
-    int k = k0 + kk;
-    bool ok = (k < K) && (col < r1);
-    const double* src = ok ? Ck + (long long)k * r1 + col : Ck;
-    cp_async8(Bs + kk * SB + col, src, ok);
+  double acc[2][FNW > 0 ? FNW : 1][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < FNW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double sa0 = 0.0, sa1 = 0.0;
+  int a_cur = -1;
+  for (int s = 0; s < nst; ++s) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = s + STAGES - 1;
+      if (nxt < nst) load_c(nxt, nxt % STAGES);
+      cp_async_commit();
+    }
+    const int a = s / nic, ic = s - a * nic;
+    if (a != a_cur) {  // state values of this lane's two rows for the new a
+      a_cur = a;
+      sa0 = St[(wrow + fr) * SST + a];
+      sa1 = St[(wrow + 8 + fr) * SST + a];
+    }
+    if constexpr (FNW > 0) {
+      const double* bs = Bs + (size_t)(s % STAGES) * BK * SB + wcol + 2 * fr;
+      const double* ft = Ft + (size_t)(ic * BK) * SFT + wrow + 2 * fr;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        const double2 fv = *reinterpret_cast<const double2*>(ft + (kk + fk) * SFT);
+        const double af0 = fv.x * sa0, af1 = fv.y * sa1;
+#pragma unroll
+        for (int j = 0; j < FNW; j += 2) {
+          const double2 bv = *reinterpret_cast<const double2*>(bs + (kk + fk) * SB + j * 8);
+          dmma_8x8x4(acc[0][j], af0, bv.x);
+          dmma_8x8x4(acc[1][j], af1, bv.x);
+          if constexpr (true) {
+            if (j + 1 < FNW) {
+              dmma_8x8x4(acc[0][j + 1], af0, bv.y);
+              dmma_8x8x4(acc[1][j + 1], af1, bv.y);
+            }
+          }
+        }
+      }
+    }
   }
-  if (tid < BK) {
-    int k = k0 + tid;
-    r0tab[tid] = (k < K) ? k / n : 0;
+  cp_async_wait<0>();
+  __syncthreads();  // every warp is done reading the old state
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = wrow + i * 8 + fr;
+#pragma unroll
+    for (int j = 0; j < FNW; ++j) {
+      const int col = wcol + j * 8 + 2 * fk;
+      if (col < r1) St[row * SST + col] = acc[i][j][0];
+      if (col + 1 < r1) St[row * SST + col + 1] = acc[i][j][1];
+    }
   }
 }
 
@@ -87,96 +147,72 @@ __global__ void __launch_bounds__(kr::WARPS * 32, 1)
     kr_fused_kernel(const __grid_constant__ KrParams P) {
   using namespace kr;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* St = reinterpret_cast<double*>(smem_raw);
-  double* Fs = St + BM * SST;
-  double* Bs = Fs + STAGES * BK * SF;
-  int* r0tab = reinterpret_cast<int*>(Bs + STAGES * BK * SB);
+  int nmax = 0;
+  for (int k = 0; k < P.d; ++k) nmax = max(nmax, P.n[k]);
+  const int nft = (nmax + BK - 1) / BK * BK;
+  double* St = reinterpret_cast<double*>(smem_raw);   // BM x SST
+  double* Ft = St + BM * SST;                          // nft x SFT
+  double* Bs = Ft + (size_t)nft * SFT;                 // STAGES x BK x SB
 
   const int vec = blockIdx.y;
   const int j0 = blockIdx.x * BM;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int fr = lane >> 2, fk = lane & 3;
-  const int wrow = warp * 8 * FM;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int wrow = (warp >> 1) * 16;     // 16 rows = fragment pair (rows r, r + 8)
 
-  for (int e = threadIdx.x; e < BM; e += WARPS * 32) St[e * SST] = 1.0;
-  __syncthreads();
+  for (int e = tid; e < BM; e += WARPS * 32) St[e * SST] = 1.0;
+
+  // per-thread C-chunk slots: (kk, col) fixed for the whole kernel
+  int ckk[CPT], ccol[CPT];
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    const int e = tid + q * WARPS * 32;
+    ckk[q] = e / BN;
+    ccol[q] = e % BN;
+  }
 
   for (int k = 0; k < P.d; ++k) {
     const int r0 = P.rank[vec * (P.d + 1) + k];
     const int r1 = P.rank[vec * (P.d + 1) + k + 1];
     const int n = P.n[k];
-    const int K = r0 * n;
+    const int nic = (n + BK - 1) / BK;   // i-chunks per a
+    const int nst = r0 * nic;            // stages of this mode
     const double* Fk = P.F[k];
     const double* Ck = P.core[vec * P.d + k];
+    // column halves split at an even fragment count (pairs stay 16-aligned) as
+    // evenly as possible: r1 = 100 -> 6 + 7 fragments
     const int fn = (r1 + 7) / 8;
+    const int f0 = 2 * (fn / 4);
+    const int wcol = (warp & 1) ? f0 * 8 : 0;
+    const int fnh = (warp & 1) ? fn - f0 : f0;
 
-    double acc[FM][FNMAX][2];
-#pragma unroll
-    for (int i = 0; i < FM; ++i)
-#pragma unroll
-      for (int j = 0; j < FNMAX; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const int nk = (K + BK - 1) / BK;
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < nk)
-        kr_load_stage(P, Fk, Ck, n, r1, K, s * BK, j0, Fs + s * BK * SF, Bs + s * BK * SB,
-                      r0tab + s * BK);
-      cp_async_commit();
+    __syncthreads();  // previous mode's state written; F tile / stage buffers free
+    // F tile of this row block, i-major, rows paired (r, r + 8) side by side
+    for (int e = tid; e < BM * n; e += WARPS * 32) {
+      const int row = e / n, i = e - row * n;
+      const bool ok = j0 + row < P.S;
+      cp_async8(Ft + i * SFT + pair_pos<true>(row), ok ? Fk + (long long)(j0 + row) * n + i : Fk, ok);
     }
-    for (int kt = 0; kt < nk; ++kt) {
-      cp_async_wait<STAGES - 2>();
-      __syncthreads();
-      {
-        int nxt = kt + STAGES - 1;
-        if (nxt < nk) {
-          int st = nxt % STAGES;
-          kr_load_stage(P, Fk, Ck, n, r1, K, nxt * BK, j0, Fs + st * BK * SF, Bs + st * BK * SB,
-                        r0tab + st * BK);
-        }
-        cp_async_commit();
-      }
-      const int st = kt % STAGES;
-      const double* fs = Fs + st * BK * SF;
-      const double* bs = Bs + st * BK * SB;
-      const int* rt = r0tab + st * BK;
-#pragma unroll
-      for (int kk = 0; kk < BK; kk += 4) {
-        const int a = rt[kk + fk];
-        double af[FM];
-#pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          const int row = wrow + i * 8 + fr;
-          af[i] = fs[(kk + fk) * SF + row] * St[row * SST + a];
-        }
-#pragma unroll
-        for (int j = 0; j < FNMAX; ++j) {
-          if (j < fn) {
-            const double bf = bs[(kk + fk) * SB + j * 8 + fr];
-#pragma unroll
-            for (int i = 0; i < FM; ++i) dmma_8x8x4(acc[i][j], af[i], bf);
-          }
-        }
-      }
+    for (int e = tid; e < (nic * BK - n) * BM; e += WARPS * 32) {
+      // zero rows i >= n of the F tile used by the last, partial i-chunk
+      const int i = n + e / BM, row = e % BM;
+      Ft[i * SFT + row] = 0.0;
     }
-    cp_async_wait<0>();
-    __syncthreads();  // every warp is done with the stage buffers and its old state rows
-    // new state (warp-private rows)
-#pragma unroll
-    for (int i = 0; i < FM; ++i) {
-      const int row = wrow + i * 8 + fr;
-#pragma unroll
-      for (int j = 0; j < FNMAX; ++j) {
-        if (j < fn) {
-          const int col = j * 8 + 2 * fk;
-          if (col < r1) St[row * SST + col] = acc[i][j][0];
-          if (col + 1 < r1) St[row * SST + col + 1] = acc[i][j][1];
-        }
-      }
+    switch (fnh) {  // warp-uniform
+      case 0: kr_mode<0>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 1: kr_mode<1>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 2: kr_mode<2>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 3: kr_mode<3>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 4: kr_mode<4>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 5: kr_mode<5>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 6: kr_mode<6>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 7: kr_mode<7>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 8: kr_mode<8>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 9: kr_mode<9>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      default: kr_mode<10>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
     }
-    __syncthreads();
   }
-  for (int row = threadIdx.x; row < BM; row += WARPS * 32)
+  __syncthreads();
+  for (int row = tid; row < BM; row += WARPS * 32)
     if (j0 + row < P.S) P.out[(long long)vec * P.S + j0 + row] = St[row * SST];
 }
 
@@ -228,7 +264,7 @@ int kr_fused(int d, const int* n, int S, const double* const* F, int nvec, const
   static bool attr = false;
   if (!attr) {
     TTK_CHECK_CUDA(cudaFuncSetAttribute(kr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kr::kSmem));
+                                        (int)kr::smem_bytes(kr::NMAX)));
     attr = true;
   }
   const int per = std::max(1, std::min(kKrMaxSlots / d, 64));
@@ -243,7 +279,9 @@ int kr_fused(int d, const int* n, int S, const double* const* F, int nvec, const
       for (int k = 0; k <= d; ++k) P.rank[v * (d + 1) + k] = (short)ranks[(long long)(v0 + v) * (d + 1) + k];
     }
     dim3 grid(ceil_div(S, kr::BM), nv);
-    kr_fused_kernel<<<grid, kr::WARPS * 32, kr::kSmem, st>>>(P);
+    int nmax = 0;
+    for (int k = 0; k < d; ++k) nmax = std::max(nmax, n[k]);
+    kr_fused_kernel<<<grid, kr::WARPS * 32, kr::smem_bytes(nmax), st>>>(P);
     TTK_CHECK_LAUNCH();
   }
   return kOk;
@@ -311,7 +349,9 @@ int kr_two_phase(int d, const int* n, int S, const double* const* F, int nvec, c
   return kOk;
 }
 
-bool use_fused(int d, int S, int nvec, const int* ranks) {
+bool use_fused(int d, const int* n, int S, int nvec, const int* ranks) {
+  for (int k = 0; k < d; ++k)
+    if (n[k] > kr::NMAX) return false;
   for (int v = 0; v < nvec; ++v)
     for (int k = 0; k <= d; ++k)
       if (ranks[v * (d + 1) + k] > kr::BN) return false;
@@ -330,7 +370,7 @@ extern "C" {
 size_t ttk_kr_sketch_ws_bytes(int d, const int* n, int s_lo, int s_hi, int nvec, const int* ranks) {
   const int S = s_hi - s_lo;
   if (S <= 0 || nvec <= 0) return 0;
-  if (use_fused(d, S, nvec, ranks)) return 0;
+  if (use_fused(d, n, S, nvec, ranks)) return 0;
   return kr_two_phase_elems(d, S, nvec, ranks) * sizeof(double) + 4096;
 }
 
@@ -347,7 +387,7 @@ int ttk_kr_sketch(int d, const int* n, int s_lo, int s_hi, const double* const* 
   std::vector<const double*> Fo(d);
   for (int k = 0; k < d; ++k) Fo[k] = F[k] + (long long)s_lo * n[k];
   cudaStream_t st = (cudaStream_t)stream;
-  if (use_fused(d, S, nvec, ranks)) return kr_fused(d, n, S, Fo.data(), nvec, ranks, cores, out, st);
+  if (use_fused(d, n, S, nvec, ranks)) return kr_fused(d, n, S, Fo.data(), nvec, ranks, cores, out, st);
   return kr_two_phase(d, n, S, Fo.data(), nvec, ranks, cores, out, ws, ws_bytes, st);
 }
 
@@ -361,6 +401,8 @@ int ttk_kr_sketch_path(int path, int d, const int* n, int s_lo, int s_hi, const 
   for (int k = 0; k < d; ++k) Fo[k] = F[k] + (long long)s_lo * n[k];
   cudaStream_t st = (cudaStream_t)stream;
   if (path == 0) {
+    for (int k = 0; k < d; ++k)
+      TTK_REQUIRE(n[k] <= kr::NMAX, kInvalidValue, "fused path needs mode sizes <= %d", kr::NMAX);
     for (int v = 0; v < nvec; ++v)
       for (int k = 0; k <= d; ++k)
         TTK_REQUIRE(ranks[v * (d + 1) + k] <= kr::BN, kInvalidValue, "fused path needs ranks <= %d",
