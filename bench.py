@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--concurrency", type=int, default=8,
+                   help="solver workload: independent RHS solved at once per GPU (one CUDA stream each)")
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--extras", action="store_true", help="also time configs 1, 2, 4 and 5")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -538,22 +540,33 @@ def run_solver(args):
     from paper_2409_09471_b200 import configs
     from paper_2409_09471_b200.parallel import solve_rhs_sharded
     world, rank, local, dev = _dist_setup()
+    from paper_2409_09471_b200.parallel import rhs_assignment
+    n_rhs = 8
 
-    def solve_one(j):
+    def prepare(j):
+        # inputs (operator, RHS, Khatri-Rao sketch, STTA frame) are set up before
+        # the clock, as the reference's own benchmark builds them before solving
         C = configs.config5(j)
         cfg = T.SolverConfig(**C["cfg"], zero_rel=None, rounding="rto")
         a = T.TTOperator(C["op"], device=dev)
         b = T.TTVector(C["b"], device=dev)
         sk = T.kr_sketch_new(C["dims"], cfg.sketch_rows, seed=C["sketch_seed"], device=dev)
         frame = T.make_solver_frame(b, cfg, seed=C["frame_seed"])
-        torch.cuda.synchronize()
+        return a, b, sk, frame, cfg
+
+    prepared = {j: prepare(j) for j in rhs_assignment(n_rhs, world, rank)}
+    torch.cuda.synchronize()
+
+    def solve_one(j):
+        a, b, sk, frame, cfg = prepared[j]
+        st = torch.cuda.current_stream(dev)
         t0 = time.perf_counter()
         _, rep = T.tt_sgmres(a, b, None, cfg, sk, frame)
+        st.synchronize()
         wall = time.perf_counter() - t0
         return {"iterations": rep.iterations, "converged": rep.converged, "wall_s": wall,
                 "res_sketched": rep.res_sketched[-1], "peak_rank": rep.peak_rank,
                 "time_to_1e-6_s": rep.time_to_tol.get(1e-6)}
-    n_rhs = 8
     # untimed warm-up solve (kernel attributes, allocator pools, pinned scratch)
     C0 = configs.config5(rank)
     cfg0 = T.SolverConfig(**{**C0["cfg"], "maxit": 3}, zero_rel=None, rounding="rto")
@@ -565,13 +578,16 @@ def run_solver(args):
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clocks:
-        reports, agg = solve_rhs_sharded(n_rhs, rank, world, solve_one)
+        reports, agg = solve_rhs_sharded(n_rhs, rank, world, solve_one, concurrency=args.concurrency,
+                                         device=dev)
     line = {"metric": "TT-sGMRES iterations/s (fp64), config 5, 8 RHS", "value": agg["it_per_s"],
             "unit": "it/s", "n_gpus": world, "steps": n_rhs, "warmup": 0,
             "ms_per_step": agg["max_wall_s"] * 1e3 / max(1, n_rhs), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "config5: d=50 n=256, ell=3, s=120, maxit=60, tol=1e-8, cap 100, RTO rounding; "
-                                   "RHS j on rank j mod G", "parallelism": f"rhs x{world}"},
+                                   "RHS j on rank j mod G; a rank's RHS solved concurrently on "
+                                   f"{args.concurrency} CUDA streams; inputs set up before the clock",
+                       "parallelism": f"rhs x{world}", "concurrency": args.concurrency},
             "reports": reports, "clocks": clocks.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -133,6 +133,9 @@ int ttk_debug_jacobi_profile(long long* dev_acc);
 /* diagnostics: the register Cholesky adds per-step clocks (step, thread-0 work,
  * owner publish + reciprocal) into dev_acc[3] (NULL: off) */
 int ttk_debug_chol_profile(long long* dev_acc);
+/* diagnostics: host synchronisation points (rank / path decisions) so far:
+ * out[0] = count, out[1] = total wait in ns (timed only when TTK_HOST_PROF is set) */
+int ttk_debug_host_profile(long long* out);
 
 /* ---- tt_round, TT-SVD (reference tt.py:337-368) ----------------------------
  * out[k] holds ranks[k]*dims[k]*ranks[k+1] doubles; out_ranks (host, d+1)
@@ -153,6 +156,16 @@ size_t ttk_tt_round_ws_bytes(int d, const int* dims, const int* ranks);
 int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X, const int* L,
                    const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream);
 size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L);
+
+/* ---- counter-based Gaussian TT-DRM (the solver's randomized-rounding sketch;
+ * no reference counterpart, SPEC.md:313 -- replaces the host draw of
+ * streaming.py:38-53 for that one use).  Writes the leading r0 x n x r1 block of
+ * core `core` of a Gaussian TT with full ranks (r0_full, r1_full): entry
+ * (i, j, l) = scale * N(Philox4x32-10(seed; ((core*r0_full + i)*n + j)*r1_full + l)),
+ * so every leading block equals the same block of the full map.
+ * out: device, r0 x n x r1 row-major.  Stream-ordered. */
+int ttk_drm_gaussian(unsigned long long seed, int core, int n, int r0_full, int r1_full, int r0, int r1,
+                     double scale, double* out, void* stream);
 
 /* ---- streaming sketches (reference streaming.py:214-302) -------------------
  * stream_sketch: psi[mu] ((lr[mu] n_mu) x rr[mu+1]) and omega[mu-1]

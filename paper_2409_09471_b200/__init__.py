@@ -8,7 +8,7 @@ arithmetic runs in libttk_b200.so (C ABI: include/ttk_b200.h).
 """
 
 from .errors import DegenerateRecovery, ShapeMismatch, SizeLimit
-from .rto import rto_flops, rto_ranks, rto_sweeps, tt_round_rto, tt_truncate_left_orth
+from .rto import CounterDRM, rto_flops, rto_ranks, rto_sweeps, tt_round_rto, tt_truncate_left_orth
 from .sketch import KhatriRaoSketch, kr_apply, kr_apply_batch, kr_apply_device, kr_apply_rows, kr_sketch_new
 from .solvers import (
     PHASES,

@@ -108,9 +108,29 @@ def stream_ptr(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+_WORKSPACES = {}
+
+
 def workspace(nbytes: int, device) -> torch.Tensor:
-    """Caller-owned scratch from torch's caching allocator."""
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    """Scratch for one ABI call: a view of a grow-only buffer kept per
+    (device, current stream).  Every wrapper uses one workspace per call and the
+    calls on a stream are ordered, so reuse is safe; allocating a fresh tensor
+    per call made the caching allocator fall through to cudaMalloc (which
+    synchronises the device) whenever the sizes changed -- every solver
+    iteration."""
+    dev = torch.device(device)
+    n = max(int(nbytes), 256)
+    if dev.type != "cuda":
+        return torch.empty(n, dtype=torch.uint8, device=dev)
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(),
+           torch.cuda.current_stream(dev).cuda_stream)
+    buf = _WORKSPACES.get(key)
+    if buf is None or buf.numel() < n:
+        grow = n if buf is None else max(n, buf.numel() + buf.numel() // 2)
+        _WORKSPACES.pop(key, None)
+        buf = torch.empty(grow, dtype=torch.uint8, device=dev)
+        _WORKSPACES[key] = buf
+    return buf[:n]
 
 SIGNATURES.update({
     "ttk_qr": (c_int, [c_int, c_int, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_vp, c_vp, c_size, c_vp]),
@@ -140,6 +160,9 @@ SIGNATURES.update({
 
 SIGNATURES.update({"ttk_debug_svd_sweeps": (c_int, [c_vp])})
 SIGNATURES.update({"ttk_debug_jacobi_profile": (c_int, [c_vp])})
+SIGNATURES.update({"ttk_debug_host_profile": (c_int, [ctypes.POINTER(ctypes.c_longlong)])})
+SIGNATURES.update({"ttk_drm_gaussian": (c_int, [ctypes.c_ulonglong, c_int, c_int, c_int, c_int, c_int, c_int,
+                                                c_double, c_vp, c_vp])})
 SIGNATURES.update({"ttk_debug_chol_profile": (c_int, [c_vp])})
 
 SIGNATURES.update({"ttk_qr_auto": (c_int, [c_int, c_int, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_vp, c_vp, c_size,

@@ -2,6 +2,8 @@
 #include "gemm.cuh"
 #include "../../include/ttk_b200.h"
 
+#include <chrono>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -19,6 +21,21 @@ void set_error(const char* fmt, ...) {
 
 const char* last_error() { return g_err; }
 
+static const bool g_host_prof = getenv("TTK_HOST_PROF") != nullptr;
+std::atomic<long long> g_syncs{0}, g_sync_ns{0};
+
+int host_sync(cudaStream_t st) {
+  if (!g_host_prof) {
+    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    return kOk;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  g_sync_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+  ++g_syncs;
+  return kOk;
+}
+
 }  // namespace ttk
 
 using namespace ttk;
@@ -30,6 +47,12 @@ const char* ttk_last_error(void) { return ttk::last_error(); }
 int ttk_version(void) { return TTK_ABI_VERSION; }
 
 long long ttk_launch_count(void) { return ttk::g_launches.load(); }
+
+int ttk_debug_host_profile(long long* out) {
+  out[0] = ttk::g_syncs.load();
+  out[1] = ttk::g_sync_ns.load();
+  return 0;
+}
 
 int ttk_device_arch(void) {
   int dev = 0, major = 0, minor = 0;

@@ -130,4 +130,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 // sum of squares of x[0..n) into out_dev[0] (fixed-order reduction; part >= 256 doubles)
 int launch_sumsq(const double* x, long long n, double* out_dev, double* part, cudaStream_t st);
 
+
+// ---------------------------------------------------------------------------
+// host synchronisation points (a rank or path decision read back to the host);
+// counted and timed when TTK_HOST_PROF is set (ttk_debug_host_profile)
+int host_sync(cudaStream_t st);
+#define TTK_SYNC(st) TTK_TRY(::ttk::host_sync(st))
+
 }  // namespace ttk

@@ -16,7 +16,8 @@ constexpr int kRedGroups = 8;
 // Few splits (<= kRedGroups): one thread per output element, partials summed
 // in split order; fully parallel, no barriers.  Problems with more splits are
 // left to gemm_splitk_reduce_kernel.
-__global__ void gemm_splitk_reduce_small_kernel(const __grid_constant__ GemmGroup G) {
+template <int CAP>
+__global__ void gemm_splitk_reduce_small_kernel(const __grid_constant__ GemmGroupT<CAP> G) {
   long long total = 0;
   for (int pi = 0; pi < G.count; ++pi)
     if (G.p[pi].splits > 1 && G.p[pi].splits <= kRedGroups) total += (long long)G.p[pi].M * G.p[pi].N;
@@ -47,7 +48,8 @@ __global__ void gemm_splitk_reduce_small_kernel(const __grid_constant__ GemmGrou
   }
 }
 
-__global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G) {
+template <int CAP>
+__global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroupT<CAP> G) {
   __shared__ double part[kRedGroups][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   long long total = 0;
@@ -167,10 +169,10 @@ void plan(GemmProblem* probs, int count, TileCfg c, bool allow_split, size_t* pa
   *total = t;
 }
 
-template <int BM, int BN, int WM, int WN, int ST = kStages>
-int launch_cfg(GemmGroup& g, cudaStream_t st) {
+template <int BM, int BN, int WM, int WN, int ST, int CAP>
+int launch_cfg(GemmGroupT<CAP>& g, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, kBK, WM, WN, ST>;
-  auto kern = gemm_group_kernel<BM, BN, kBK, WM, WN, ST>;
+  auto kern = gemm_group_kernel<BM, BN, kBK, WM, WN, ST, CAP>;
   static bool attr_set = false;
   if (!attr_set) {
     TTK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -183,6 +185,49 @@ int launch_cfg(GemmGroup& g, cudaStream_t st) {
 }
 
 }  // namespace
+
+// tile kernel + split-K reduction for one planned group; the group's kernel
+// parameter is CAP problems wide (single-problem launches pass ~0.7 KB, not 17 KB)
+template <int CAP>
+int launch_group(GemmGroupT<CAP>& g, TileCfg cfg, size_t pe, cudaStream_t st) {
+  int rc;
+  if constexpr (CAP > kSmallGroup) {
+    // grouped launches (tt_matvec, sketches) use the default light tiles
+    if (cfg != kX32x64w4) cfg = kX64x32w4;
+  }
+  switch (cfg) {
+    case kX64x32w4: rc = launch_cfg<64, 32, 2, 2, 4>(g, st); break;
+    case kX32x64w4: rc = launch_cfg<32, 64, 2, 2, 4>(g, st); break;
+    // experiment-only configurations (TTK_GEMM_FORCE_CFG), single-problem launches
+    case kT128x128: rc = launch_cfg<128, 128, 4, 4, 3>(g, st); break;
+    case kT128x64: case kX128x64w8s4: rc = launch_cfg<128, 64, 4, 2, 4>(g, st); break;
+    case kT64x64: case kX64x64w4s4: rc = launch_cfg<64, 64, 2, 2, 4>(g, st); break;
+    case kT128x80: rc = launch_cfg<128, 80, 8, 1, 3>(g, st); break;
+    case kT64x80: rc = launch_cfg<64, 80, 4, 1, 3>(g, st); break;
+    case kT80x64: rc = launch_cfg<80, 64, 5, 1, 3>(g, st); break;
+    case kT80x80: rc = launch_cfg<80, 80, 5, 1, 3>(g, st); break;
+    default: rc = launch_cfg<64, 32, 2, 2, 4>(g, st); break;
+  }
+  if (rc != kOk) return rc;
+  if (pe > 0) {
+    size_t chunks = 0, small = 0;
+    for (int i = 0; i < g.count; ++i) {
+      if (g.p[i].splits > kRedGroups) chunks += ((size_t)g.p[i].M * g.p[i].N + 31) / 32;
+      else if (g.p[i].splits > 1) small += (size_t)g.p[i].M * g.p[i].N;
+    }
+    if (small > 0) {
+      const int sblocks = (int)std::min<size_t>((small + 255) / 256, 8 * kNumSMs);
+      gemm_splitk_reduce_small_kernel<CAP><<<sblocks, 256, 0, st>>>(g);
+      TTK_CHECK_LAUNCH();
+    }
+    if (chunks > 0) {
+      const int rblocks = (int)std::min<size_t>(chunks, 8 * kNumSMs);
+      gemm_splitk_reduce_kernel<CAP><<<rblocks, 32 * kRedGroups, 0, st>>>(g);
+      TTK_CHECK_LAUNCH();
+    }
+  }
+  return kOk;
+}
 
 size_t gemm_group_ws_bytes(const GemmProblem* probs_in, int count, bool allow_split) {
   size_t total = 0;
@@ -252,42 +297,16 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
                 g.p[i].M, g.p[i].N, g.p[i].K, g.p[i].splits, g.p[i].tiles_m * g.p[i].tiles_n,
                 g.p[i].a_ks, g.p[i].b_ks);
     int rc;
-    switch (cfg) {
-      // 4 x 4 warps of 32 x 32: 16 warps per SM (a warp cannot issue DMMAs back to
-      // back; 2 warps per sub-partition left the tensor pipe ~40% idle)
-      case kT128x128: rc = launch_cfg<128, 128, 4, 4>(g, st); break;
-      case kT128x64: rc = launch_cfg<128, 64, 4, 2, 4>(g, st); break;
-      case kT64x64: rc = launch_cfg<64, 64, 2, 2, 4>(g, st); break;
-      // rank-80 tiles: full-width warps (16 rows x all columns) so that both
-      // fragment counts are even and every fragment pair is one 16-byte load
-      case kT128x80: rc = launch_cfg<128, 80, 8, 1>(g, st); break;
-      case kT64x80: rc = launch_cfg<64, 80, 4, 1>(g, st); break;
-      case kT80x64: rc = launch_cfg<80, 64, 5, 1>(g, st); break;
-      case kT80x80: rc = launch_cfg<80, 80, 5, 1>(g, st); break;
-      case kX64x32w4: rc = launch_cfg<64, 32, 2, 2, 4>(g, st); break;
-      case kX64x64w4s4: rc = launch_cfg<64, 64, 2, 2, 4>(g, st); break;
-      case kX128x64w8s4: rc = launch_cfg<128, 64, 4, 2, 4>(g, st); break;
-      case kX32x64w4: rc = launch_cfg<32, 64, 2, 2, 4>(g, st); break;
-      default: rc = launch_cfg<64, 32, 2, 2, 4>(g, st); break;
+    if (g.count <= kSmallGroup) {
+      static thread_local GemmGroupSmall gs;
+      gs.count = g.count;
+      gs.total_tiles = g.total_tiles;
+      for (int i = 0; i < g.count; ++i) gs.p[i] = g.p[i];
+      rc = launch_group(gs, cfg, pe, st);
+    } else {
+      rc = launch_group(g, cfg, pe, st);
     }
     if (rc != kOk) return rc;
-    if (pe > 0) {
-      size_t chunks = 0, small = 0;
-      for (int i = 0; i < g.count; ++i) {
-        if (g.p[i].splits > kRedGroups) chunks += ((size_t)g.p[i].M * g.p[i].N + 31) / 32;
-        else if (g.p[i].splits > 1) small += (size_t)g.p[i].M * g.p[i].N;
-      }
-      if (small > 0) {
-        const int sblocks = (int)std::min<size_t>((small + 255) / 256, 8 * kNumSMs);
-        gemm_splitk_reduce_small_kernel<<<sblocks, 256, 0, st>>>(g);
-        TTK_CHECK_LAUNCH();
-      }
-      if (chunks > 0) {
-        const int rblocks = (int)std::min<size_t>(chunks, 8 * kNumSMs);
-        gemm_splitk_reduce_kernel<<<rblocks, 32 * kRedGroups, 0, st>>>(g);
-        TTK_CHECK_LAUNCH();
-      }
-    }
   }
   return kOk;
 }

@@ -34,12 +34,16 @@ struct GemmProblem {
 };
 
 constexpr int kMaxGroup = 96;
+constexpr int kSmallGroup = 4;  // kernel-parameter size ~0.7 KB instead of ~17 KB
 
-struct GemmGroup {
+template <int CAP>
+struct GemmGroupT {
   int count;
   int total_tiles;
-  GemmProblem p[kMaxGroup];
+  GemmProblem p[CAP];
 };
+using GemmGroup = GemmGroupT<kMaxGroup>;
+using GemmGroupSmall = GemmGroupT<kSmallGroup>;
 
 __device__ __forceinline__ long long amap(const GemmProblem& P, int m) {
   int q = m / P.a_mdiv;
@@ -135,9 +139,9 @@ constexpr int gemm_min_blocks() {
   return (frags >= 20 || mb < 1) ? 1 : mb;
 }
 
-template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES>
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, int CAP>
 __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, gemm_min_blocks<BM, BN, WARPS_M, WARPS_N>())
-    gemm_group_kernel(const __grid_constant__ GemmGroup G) {
+    gemm_group_kernel(const __grid_constant__ GemmGroupT<CAP> G) {
   using Cfg = GemmCfg<BM, BN, BK, WARPS_M, WARPS_N, STAGES>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
@@ -293,8 +297,6 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, gemm_min_blocks<BM, BN
   }
 }
 
-// deterministic split-K reduction: C = alpha * sum_s partial[s] + beta * C
-__global__ void gemm_splitk_reduce_kernel(const __grid_constant__ GemmGroup G);
 
 // Host-side helpers ----------------------------------------------------------
 

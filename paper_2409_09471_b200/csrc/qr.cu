@@ -2014,9 +2014,63 @@ int trsm_right_upper(int m, int l, const double* Y, long long y_rs, long long y_
 
 static int g_qr_path_tmp = 0;
 static void g_qr_last_path_set(int v) { g_qr_path_tmp = v; }
+// unit-norm columns of an m x n strided block, one CTA per column, fixed
+// reduction order; an exactly-zero column becomes a deterministic
+// pseudo-random unit vector (it then carries a noise direction of the
+// completion, which the joint CholeskyQR orthonormalises)
+__global__ void normalize_cols_kernel(int m, int n, double* X, long long x_rs, long long x_cs,
+                                      unsigned long long seed) {
+  __shared__ double red[32];
+  const int c = blockIdx.x;
+  if (c >= n) return;
+  double* col = X + (long long)c * x_cs;
+  for (int pass = 0; pass < 2; ++pass) {
+    double s = 0.0;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) { const double v = col[(long long)r * x_rs]; s += v * v; }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    __syncthreads();
+    if (tot > 0.0) {
+      const double inv = 1.0 / sqrt(tot);
+      for (int r = threadIdx.x; r < m; r += blockDim.x) col[(long long)r * x_rs] *= inv;
+      return;
+    }
+    for (int r = threadIdx.x; r < m; r += blockDim.x) {
+      unsigned long long z = ((unsigned long long)c * 0x9E3779B97F4A7C15ull) ^ ((unsigned long long)r + seed);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z ^= z >> 31;
+      col[(long long)r * x_rs] = (double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+    __syncthreads();
+  }
+}
+
+// CholeskyQR2 with a rank-robust fallback, entirely on the DMMA GEMMs and the
+// small one-CTA factorisations.
+//   fast path (skipped when robust_first): Gram -> Cholesky -> TRSM -> Gram ->
+//     near-identity series -> GEMM; accepted iff both factorisations succeed
+//     and ||Q1^T Q1 - I||_max <= 1e-3.
+//   robust path (exactly rank-deficient or ill-conditioned Y):
+//     1. shifted CholeskyQR pass (Fukaya et al. 2020) + TRSM -> Q1, always succeeds;
+//     2. pivoted Cholesky of Q1^T Q1 finds rho significant directions; CholeskyQR
+//        on the gathered pivot columns (TRSM) -> Q2 = Q[:, :rho];
+//     3. completion aligned with what step 2 dropped: Om = (I - Q2 Q2^T) Y Omega
+//        (projected twice), columns normalised -> Q[:, rho:];
+//     4. ONE joint CholeskyQR2 of [Q2 | Om] makes the whole Q orthonormal to
+//        working precision (this also removes the eps-sized leftovers of Om along
+//        Q2 that a separate orthonormalisation of Om would amplify by kappa(Om));
+//     5. R = Q^T Y (range(Q) covers range(Y) to working precision).
+//   *deficient is set to 1 when Y needed the robust path with rho < l, so a sweep
+//   can try it first on the next core (fewer launches, one host sync less).
 int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, double* Q, long long q_rs,
-            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* ok) {
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* ok,
+            bool robust_first, int* deficient) {
   *ok = 0;
+  if (deficient) *deficient = 0;
   if (l > kCholMaxCols || m < l) return kOk;
   TTK_REQUIRE(ws_bytes >= cholqr2_ws_bytes(m, l), kWorkspace, "cholqr: workspace too small");
   Arena ar(ws, ws_bytes);
@@ -2029,55 +2083,53 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
   int* status = ar.take<int>(16 + kCholMaxCols);  // [0,8) flags/rank, [8, 8+l) pivot order
   void* split = ar.take<char>(32u << 20);
   const size_t split_bytes = 32u << 20;
-  static bool attr = false;
-  if (!attr) {
-    TTK_TRY(qr_set_smem((const void*)chol_inv_kernel, 220 * 1024));
-    attr = true;
-  }
   const size_t smem = sizeof(double) * (2 * (size_t)l * (l + 1) + 256 * (size_t)((l + 15) / 16));
   const double shift_rel = 11.0 * ((double)m * l + (double)l * (l + 1)) * 1.1102230246251565e-16;
   GemmProblem p;
-  // one "pass": Gram of X (m x l, strides), chol (+shift) into (Rk, Ik), status bits into st_slot
+  auto gram = [&](const double* X, long long x_rs, long long x_cs) -> int {
+    GemmProblem g = make_gemm(l, l, m, X, x_cs, x_rs, X, x_rs, x_cs, G, l, 1);
+    return gemm_group_launch(&g, 1, split, split_bytes, st);
+  };
+  // one pass: Gram of X, Cholesky (+shift) into (Rk, Ik); second passes (checked
+  // against I) try the near-identity series first; first passes feed a
+  // triangular solve and need no inverse
   auto gram_chol = [&](const double* X, long long x_rs, long long x_cs, double* Rk, double* Ik, int* st_slot,
                        int check, double shift, double tiny) -> int {
-    GemmProblem g = make_gemm(l, l, m, X, x_cs, x_rs, X, x_rs, x_cs, G, l, 1);
-    TTK_TRY(gemm_group_launch(&g, 1, split, split_bytes, st));
-    // second passes (checked against I) try the near-identity series first
-    // first passes feed a triangular solve and need no inverse
+    TTK_TRY(gram(X, x_rs, x_cs));
     TTK_TRY(launch_chol_inv(l, G, Rk, check ? Ik : nullptr, st_slot, check, shift, tiny, st,
                             check ? status + 4 : nullptr));
     return kOk;
   };
   int hs[4] = {0, 0, 0, 0};
-  // ---- fast path: CholeskyQR2, accepted for kappa(Y) <~ 3e7 ----
-  TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
-  TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, 0.0, 1e-15));
-  TTK_TRY(trsm_right_upper(m, l, Y, y_rs, y_cs, R1, Q1, l, 1, st));  // Q1 = Y / R1 (backward stable)
-  TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
-  TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (hs[0] == 0 && hs[1] == 0) {
-    p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
-    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    if (R) {
-      p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, R, l, 1);
+  static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;
+  if (!robust_first || qr_mode == 2) {
+    // ---- fast path: CholeskyQR2, accepted for kappa(Y) <~ 3e7 ----
+    TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
+    TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, 0.0, 1e-15));
+    TTK_TRY(trsm_right_upper(m, l, Y, y_rs, y_cs, R1, Q1, l, 1, st));  // Q1 = Y / R1 (backward stable)
+    TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
+    TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    TTK_SYNC(st);
+    if (hs[0] == 0 && hs[1] == 0) {
+      p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      if (R) {
+        p = make_gemm(l, l, l, R2, l, 1, R1, l, 1, R, l, 1);
+        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+      }
+      *ok = 1;
+      g_qr_last_path_set(1);
+      return kOk;
     }
-    *ok = 1;
-    g_qr_last_path_set(1);
-    return kOk;
+    if (qr_mode == 2) return kOk;  // diagnostics: fast path or Householder only
   }
   // ---- rank-robust path ----
-  static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;
-  if (qr_mode == 2) return kOk;  // diagnostics: fast path or Householder only
-  // pass 1 shifted (sCholQR, Fukaya et al. 2020): always succeeds, kappa(Q1) <~ 1e5
-  // on the numerically significant part of range(Y)
+  // 1. shifted pass: always succeeds, kappa(Q1) <~ 1e5 on the significant part of range(Y)
   TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
   TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, shift_rel, 1e-28));
   TTK_TRY(trsm_right_upper(m, l, Y, y_rs, y_cs, R1, Q1, l, 1, st));
-  // pass 2 pivoted: drop directions with eigenvalue < 1e-14 of G2 (Y-mass < ~1e-11 ||Y||)
-  p = make_gemm(l, l, m, Q1, 1, l, Q1, l, 1, G, l, 1);
-  TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  // 2. pivoted Cholesky of Q1^T Q1: directions with eigenvalue < 1e-14 are left to the completion
+  TTK_TRY(gram(Q1, l, 1));
   {
     static bool pattr = false;
     if (!pattr) {
@@ -2088,78 +2140,53 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     TTK_CHECK_LAUNCH();
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  TTK_SYNC(st);
   if (hs[0] & 1) return kOk;
   const int rho = hs[3];
-  double* Qb = Q1;  // Q1 no longer needed after Q2 = Q1 M is formed into the scratch below
-  // scratch for Q2 / completion: reuse I2 region? it is l x l only -> use the tail of Q via output strides
+  if (deficient) *deficient = rho < l;
   if (rho > 0) {
-    // Q2 = Q1[:, perm[:rho]] / R_rho -> Q columns [0, rho): gather, then an
-    // in-place triangular solve (backward stable: range(Q2) = range of the
-    // gathered columns of Q1 to working precision)
     gather_cols_kernel<<<(int)std::min<long long>(((long long)m * rho + 255) / 256, 4 * kNumSMs), 256, 0, st>>>(
         m, rho, Q1, l, status + 8, Q, q_rs, q_cs);
     TTK_CHECK_LAUNCH();
     TTK_TRY(trsm_right_upper(m, rho, Q, q_rs, q_cs, R2, Q, q_rs, q_cs, st));
-    // pass 3: CholeskyQR on Q2 (in Q), checked against I; Q3 = Q2 R3^{-1} -> Qb, copied back
-    p = make_gemm(rho, rho, m, Q, q_cs, q_rs, Q, q_rs, q_cs, G, rho, 1);
-    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    TTK_TRY(launch_chol_inv(rho, G, R1, I1, status + 2, 1, 0.0, 1e-28, st, status + 4));
-    p = make_gemm(m, rho, rho, Q, q_rs, q_cs, I1, rho, 1, Qb, rho, 1);
-    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    TTK_TRY(copy_strided(m, rho, Qb, rho, 1, Q, q_rs, q_cs, st));
   }
   if (rho < l) {
-    // orthonormal completion aligned with what the pivoted pass dropped: a
-    // randomized range finder on the residual, Om = (I - Q3 Q3^T) Y Omega_s
-    // (Omega_s random l x kc), projected twice, then CholeskyQR2.  The dropped
-    // directions of range(Y) (mass <~ 1e-11) are captured, so Y = Q Q^T Y holds
-    // to working precision; exactly deficient directions get noise directions
-    // that carry no mass.
+    // 3. completion Om = (I - Q2 Q2^T) Y Omega, written into Q[:, rho:]
     const int kc = l - rho;
-    double* Om = Qb;  // m x kc scratch
+    double* Om = Q + (long long)rho * q_cs;
     fill_random_kernel<<<8, 256, 0, st>>>((long long)l * kc, I2, 0x5DEECE66Dull + (unsigned)l);
     TTK_CHECK_LAUNCH();
-    p = make_gemm(m, kc, l, Y, y_rs, y_cs, I2, kc, 1, Om, kc, 1);
+    p = make_gemm(m, kc, l, Y, y_rs, y_cs, I2, kc, 1, Om, q_rs, q_cs);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-    // Om -= Q3 (Q3^T Om), twice (the second pass removes the first one's rounding)
-    auto project_out = [&]() -> int {
-      for (int rep = 0; rep < 2 && rho > 0; ++rep) {
-        p = make_gemm(rho, kc, m, Q, q_cs, q_rs, Om, kc, 1, G, kc, 1);
-        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-        p = make_gemm(m, kc, rho, Q, q_rs, q_cs, G, kc, 1, Om, kc, 1, -1.0, 1.0);
-        TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-      }
-      return kOk;
-    };
-    // one CholeskyQR pass on Om; the result goes to Q's tail columns and, unless
-    // it is the final pass, back into Om
-    auto chol_pass = [&](bool last, bool near) -> int {
-      p = make_gemm(kc, kc, m, Om, 1, kc, Om, kc, 1, G, kc, 1);
+    for (int rep = 0; rep < 2 && rho > 0; ++rep) {
+      p = make_gemm(rho, kc, m, Q, q_cs, q_rs, Om, q_rs, q_cs, G, kc, 1);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-      TTK_TRY(launch_chol_inv(kc, G, R1, I1, status + 2, 0, 0.0, 1e-28, st, near ? status + 4 : nullptr));
-      p = make_gemm(m, kc, kc, Om, kc, 1, I1, kc, 1, Q + (long long)rho * q_cs, q_rs, q_cs);
+      p = make_gemm(m, kc, rho, Q, q_rs, q_cs, G, kc, 1, Om, q_rs, q_cs, -1.0, 1.0);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
-      if (!last) TTK_TRY(copy_strided(m, kc, Q + (long long)rho * q_cs, q_rs, q_cs, Om, kc, 1, st));
-      return kOk;
-    };
-    // Om mixes residual directions of size ~1e-13 |Y| with rounding noise, so its
-    // first orthonormalisation amplifies the eps-sized leftovers along Q3 by
-    // kappa(Om): orthonormalise, project out again, and finish with a pass on
-    // the now well-conditioned block.
-    TTK_TRY(project_out());
-    TTK_TRY(chol_pass(false, false));
-    TTK_TRY(chol_pass(false, true));
-    TTK_TRY(project_out());
-    TTK_TRY(chol_pass(false, true));
-    TTK_TRY(chol_pass(true, true));
+    }
+    normalize_cols_kernel<<<kc, 256, 0, st>>>(m, kc, Om, q_rs, q_cs, 0x2545F4914F6CDD1Dull + (unsigned)l);
+    TTK_CHECK_LAUNCH();
+    // 4. joint CholeskyQR2 of [Q2 | Om] (in place through the Q1 scratch)
+    TTK_CHECK_CUDA(cudaMemsetAsync(status + 2, 0, 2 * sizeof(int), st));
+    TTK_TRY(gram_chol(Q, q_rs, q_cs, R1, I1, status + 2, 0, 0.0, 1e-28));
+    TTK_TRY(trsm_right_upper(m, l, Q, q_rs, q_cs, R1, Q1, l, 1, st));
+    TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 2, 1, 0.0, 1e-28));
+    p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+  } else {
+    // Q2 spans all of range(Y): one more CholeskyQR pass to working precision
+    TTK_CHECK_CUDA(cudaMemsetAsync(status + 2, 0, 2 * sizeof(int), st));
+    TTK_TRY(gram_chol(Q, q_rs, q_cs, R1, I1, status + 2, 1, 0.0, 1e-28));
+    p = make_gemm(m, l, l, Q, q_rs, q_cs, I1, l, 1, Q1, l, 1);
+    TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
+    TTK_TRY(copy_strided(m, l, Q1, l, 1, Q, q_rs, q_cs, st));
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (hs[2] & 1) return kOk;  // pass 3 / completion Cholesky broke down
+  TTK_SYNC(st);
+  if (hs[2] & 1) return kOk;  // joint Cholesky broke down: Householder fallback
   g_qr_last_path_set(2 + 100 * rho);
   if (R) {
-    // R = Q^T Y (l x l): exact to working precision because range(Q) covers range(Y)
+    // 5. R = Q^T Y (l x l): exact to working precision because range(Q) covers range(Y)
     p = make_gemm(l, l, m, Q, q_cs, q_rs, Y, y_rs, y_cs, R, l, 1);
     TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));
   }
@@ -2205,7 +2232,7 @@ static void qr_check_report(int m, int l, const std::vector<double>& hy, const d
 }
 
 int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
-            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint) {
   if (m <= 0 || l <= 0) return kOk;
   // CholeskyQR2 pays off only for tall inputs that need a multi-panel tree
   static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;  // 1: Householder only
@@ -2231,11 +2258,13 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
       double* tmp = nullptr;
       TTK_CHECK_CUDA(cudaMalloc(&tmp, 8 * (size_t)m * l));
       TTK_TRY(copy_strided(m, l, Y, y_rs, y_cs, tmp, l, 1, st));
-      TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+      TTK_SYNC(st);
       TTK_CHECK_CUDA(cudaMemcpy(hy.data(), tmp, 8 * (size_t)m * l, cudaMemcpyDeviceToHost));
       cudaFree(tmp);
     }
-    TTK_TRY(cholqr2(m, l, Y, y_rs, y_cs, Q, q_rs, q_cs, R, cws, cbytes, st, &ok));
+    int deficient = 0;
+    TTK_TRY(cholqr2(m, l, Y, y_rs, y_cs, Q, q_rs, q_cs, R, cws, cbytes, st, &ok, hint && *hint, &deficient));
+    if (hint) *hint = ok && deficient;
     if (ok && g_qr_check && R) qr_check_report(m, l, hy, Q, q_rs, q_cs, R, st);
     if (ok) return kOk;
   }

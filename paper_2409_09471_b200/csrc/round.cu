@@ -109,7 +109,7 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
   if (d == 1) {
     TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cores[0], sizeof(double) * core_elems(dims, ranks, 0),
                                    cudaMemcpyDeviceToDevice, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
     return kOk;
   }
   const size_t need = round_ws_bytes(d, dims, ranks);
@@ -162,17 +162,18 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
     sumsq_multi_kernel<<<d, 256, 0, st>>>(pdev, sdev, red);
     TTK_CHECK_LAUNCH();
     TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double) * d, cudaMemcpyDeviceToHost, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
     for (int k = 0; k < d; ++k) prod_norm *= std::sqrt(pin[k]);
   }
 
   // ---- right-to-left orthogonalisation (tt.py:321-334) ----
+  int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
   for (int k = d - 1; k >= 1; --k) {
     const double* ck = (k == d - 1) ? cores[k] : wk[k];
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = n * r1, kk = std::min(m, r0);
     // QR of C_k^T (m x r0): element (row=(i,b), col=a) at a*m + row
-    TTK_TRY(qr_auto(m, r0, ck, 1, m, wk[k], 1, m, tR, qws, qr_bytes, st));
+    TTK_TRY(qr_auto(m, r0, ck, 1, m, wk[k], 1, m, tR, qws, qr_bytes, st, &qr_hint));
     // new core k = Q^T reshaped (kk, n, r1): element (c, row) at c*m + row  -> written above
     // C_{k-1} <- C_{k-1} x_3 R^T : new[a,i,c] = sum_b C_{k-1}[a,i,b] R[c,b]
     // core k-1 is still the untouched input core at this point of the sweep
@@ -184,23 +185,24 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
   // ---- norm / zero test ----
   TTK_TRY(launch_sumsq(wk[0], (long long)r[0] * dims[0] * r[1], red, part, st));
   TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double), cudaMemcpyDeviceToHost, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  TTK_SYNC(st);
   const double nrm = std::sqrt(pin[0]);
   if (nrm == 0.0 || (zero_rel >= 0.0 && nrm <= zero_rel * prod_norm)) {
     for (int k = 0; k < d; ++k) TTK_CHECK_CUDA(cudaMemsetAsync(out[k], 0, sizeof(double) * dims[k], st));
     for (int k = 0; k <= d; ++k) out_ranks[k] = 1;
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
     return kOk;
   }
   const double budget = rel_tol * nrm / std::sqrt((double)(d - 1));
 
   // ---- left-to-right truncated SVD sweep (tt.py:358-367) ----
   const double* cur = wk[0];
+  qr_hint = 0;  // new sweep
   for (int k = 0; k < d - 1; ++k) {
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = r0 * n, kk = std::min(m, r1);
     // A = Q R (Q: m x kk in tq, R: kk x r1 in tR)
-    TTK_TRY(qr_auto(m, r1, cur, r1, 1, tq, kk, 1, tR, qws, qr_bytes, st));
+    TTK_TRY(qr_auto(m, r1, cur, r1, 1, tq, kk, 1, tR, qws, qr_bytes, st, &qr_hint));
     const bool vt = jacobi_fits_v(r1, kk);
     if (vt) {
       // Jacobi on R^T (converges in far fewer sweeps for graded spectra):
@@ -212,7 +214,7 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
     }
     TTK_TRY(truncation_rank_dev(tS, kk, budget, max_rank, rdev, st));
     TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, sizeof(int), cudaMemcpyDeviceToHost, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
     const int rk = *(int*)pin;
     // out_k = Q U[:, :rk]  (m x rk)
     TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], rk, 1, split_ws, st));
@@ -235,7 +237,7 @@ int ttk_tt_round(int d, const int* dims, const int* ranks, const double* const* 
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(out[d - 1], cur, sizeof(double) * (size_t)r[d - 1] * dims[d - 1],
                                  cudaMemcpyDeviceToDevice, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  TTK_SYNC(st);
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
   return kOk;
 }
@@ -271,7 +273,7 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
   for (int k = 0; k <= d; ++k) out_ranks[k] = ranks[k];
   if (d == 1) {
     TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cores[0], sizeof(double) * dims[0], cudaMemcpyDeviceToDevice, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
     return kOk;
   }
   const size_t need = ttk_tt_truncate_ws_bytes(d, dims, ranks);
@@ -305,21 +307,22 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
   // ||v|| = ||C_{d-1}||_F for a left-orthogonal TT
   TTK_TRY(launch_sumsq(cores[d - 1], (long long)r[d - 1] * dims[d - 1], red, part, st));
   TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double), cudaMemcpyDeviceToHost, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  TTK_SYNC(st);
   const double nrm = std::sqrt(pin[0]);
   if (nrm == 0.0) {
     for (int k = 0; k < d; ++k) TTK_CHECK_CUDA(cudaMemsetAsync(out[k], 0, sizeof(double) * dims[k], st));
     for (int k = 0; k <= d; ++k) out_ranks[k] = 1;
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
     return kOk;
   }
   const double budget = rel_tol * nrm / std::sqrt((double)(d - 1));
   const double* cur = cores[d - 1];
+  int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
   for (int k = d - 1; k >= 1; --k) {
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = n * r1, kk = std::min(m, r0);
     // C_k^T (m x r0) = Q R ; element (row=(i,b), col=a) of C_k^T at a*m + row
-    TTK_TRY(qr_auto(m, r0, cur, 1, m, tq, kk, 1, tR, qws, qrb, st));
+    TTK_TRY(qr_auto(m, r0, cur, 1, m, tq, kk, 1, tR, qws, qrb, st, &qr_hint));
     const bool vt = jacobi_fits_v(r0, kk);
     if (vt) {
       // Jacobi on R^T (r0 x kk): R^T V' = W = U' S; left vectors of R = V' (tU),
@@ -330,7 +333,7 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
     }
     TTK_TRY(truncation_rank_dev(tS, kk, budget, max_rank, rdev, st));
     TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, sizeof(int), cudaMemcpyDeviceToHost, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
     const int rk = *(int*)pin;
     // C_k <- (Q U_r)^T : out[k][c][row] = sum_j Q[row][j] U[j][c]
     TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_ws, st));
@@ -349,7 +352,7 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cur, sizeof(double) * (size_t)dims[0] * r[1],
                                  cudaMemcpyDeviceToDevice, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  TTK_SYNC(st);
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
   return kOk;
 }
@@ -429,13 +432,14 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
   // ---- left sweep ----
   const double* Z = X[0];  // (L_0 n_0 x R_1) = (n_0 x R_1)
   double* Zbuf[2] = {Z0, Z1};
+  int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
   for (int c = 1; c < d; ++c) {
     const int np = dims[c - 1];
     const int m = L[c - 1] * np, l = L[c], rc = R[c];
     // Y (m x l) = Z (m x R_c) W_c (R_c x l)
     TTK_TRY(gemm1(m, l, rc, Z, rc, 1, W[c], l, 1, Y, l, 1, split_ws, st));
     // Q (m x l) -> out core c-1, (L_{c-1}, n_{c-1}, L_c)
-    TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st));
+    TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st, &qr_hint));
     // M (l x R_c) = Q^T Z   (K = m, split over the long dimension)
     TTK_TRY(gemm1(l, rc, m, out[c - 1], 1, l, Z, rc, 1, Y, rc, 1, split_ws, st));
     // Z' (l x n_c R_{c+1}) = M X_c

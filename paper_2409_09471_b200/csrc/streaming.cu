@@ -158,7 +158,7 @@ int ttk_stream_recover_cores(int d, const int* dims, const int* lr, const int* r
   TTK_CHECK_LAUNCH();
   std::vector<double> hred(nl);
   TTK_CHECK_CUDA(cudaMemcpyAsync(hred.data(), red, sizeof(double) * nl, cudaMemcpyDeviceToHost, st));
-  TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+  TTK_SYNC(st);
   bool all_zero = true;
   for (int mu = 0; mu < d; ++mu) all_zero = all_zero && hred[mu] == 0.0;
   *is_zero = all_zero ? 1 : 0;
@@ -179,7 +179,7 @@ int ttk_stream_recover_cores(int d, const int* dims, const int* lr, const int* r
   std::vector<int> hk(d + 1, 1);
   if (d > 1) {
     TTK_CHECK_CUDA(cudaMemcpyAsync(hk.data() + 1, kept + 1, sizeof(int) * (d - 1), cudaMemcpyDeviceToHost, st));
-    TTK_CHECK_CUDA(cudaStreamSynchronize(st));
+    TTK_SYNC(st);
   }
   hk[0] = 1;
   hk[d] = 1;

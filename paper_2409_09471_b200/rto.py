@@ -54,6 +54,47 @@ def rto_flops(dims, in_ranks, ls) -> float:
     return f
 
 
+class CounterDRM:
+    """Gaussian TT-DRM generated on the device from a counter-based RNG
+    (csrc/drm.cu, ttk_drm_gaussian): entry (i, j, l) of core k depends only on
+    (seed, k, i, j, l) in the full index space, with variance 1/(R_{k-1} n_k R_k)
+    of the full ranks as tt_drm_new draws it.  ``block(ls)`` returns the
+    leading (l_{k-1} x n_k x l_k) blocks -- identical to slicing the full map --
+    so a solver whose sketch ranks grow never draws the cap-sized DRM.
+    ``cores`` materialises the full map (tests hand it to the CPU oracle)."""
+
+    def __init__(self, dims, ranks, seed=0, device=None):
+        self.dims = tuple(int(n) for n in dims)
+        d = len(self.dims)
+        ranks = list(ranks)
+        if len(ranks) != d - 1 or any(r < 1 for r in ranks):
+            raise ValueError("ranks must be d-1 positive integers")
+        self.ranks = tuple([1] + ranks + [1])
+        self.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+        self.device = torch.device(device) if device is not None else torch.device("cuda", 0)
+        _lib.require_cuda(torch.empty(0, device=self.device), "CounterDRM")
+
+    def block(self, ls):
+        L = [1] + [int(x) for x in ls] + [1]
+        if len(L) != len(self.ranks) or any(a > b for a, b in zip(L, self.ranks)):
+            raise ShapeMismatch(f"sketch ranks {L} exceed the DRM ranks {self.ranks}")
+        lib = _lib.load()
+        st = _lib.stream_ptr(self.device)
+        R = self.ranks
+        out = []
+        for k, n in enumerate(self.dims):
+            g = torch.empty((L[k], n, L[k + 1]), dtype=torch.float64, device=self.device)
+            scale = 1.0 / math.sqrt(float(R[k]) * n * R[k + 1])
+            _lib.check(lib.ttk_drm_gaussian(self.seed, k, n, R[k], R[k + 1], L[k], L[k + 1], scale,
+                                            g.data_ptr(), st))
+            out.append(g)
+        return out
+
+    @property
+    def cores(self):
+        return self.block(self.ranks[1:-1])
+
+
 def _drm_slices(drm_cores, ls, device):
     full = [1] + list(ls) + [1]
     out = []
@@ -67,16 +108,24 @@ def _drm_slices(drm_cores, ls, device):
 
 def rto_sweeps(v: TTVector, drm) -> TTVector:
     """Left-orthogonal TT with the DRM's ranks (clamped by rto_ranks)."""
-    if isinstance(drm, TTDRM):
-        drm = drm.cores
-    if tuple(int(g.shape[1]) for g in drm) != v.dims:
-        raise ShapeMismatch("DRM dims do not match the vector")
     d = v.d
     _lib.require_cuda(v.cores[0], "TT vector")
-    if d == 1:
-        return v.copy()
-    ls = rto_ranks(v.dims, v.ranks, [int(g.shape[2]) for g in drm[:-1]])
-    G = _drm_slices(drm, ls, v.device)
+    if isinstance(drm, CounterDRM):
+        if drm.dims != v.dims:
+            raise ShapeMismatch("DRM dims do not match the vector")
+        if d == 1:
+            return v.copy()
+        ls = rto_ranks(v.dims, v.ranks, list(drm.ranks[1:-1]))
+        G = drm.block(ls)
+    else:
+        if isinstance(drm, TTDRM):
+            drm = drm.cores
+        if tuple(int(g.shape[1]) for g in drm) != v.dims:
+            raise ShapeMismatch("DRM dims do not match the vector")
+        if d == 1:
+            return v.copy()
+        ls = rto_ranks(v.dims, v.ranks, [int(g.shape[2]) for g in drm[:-1]])
+        G = _drm_slices(drm, ls, v.device)
     lib = _lib.load()
     dev = v.device
     L = [1] + ls + [1]

@@ -20,7 +20,7 @@ import torch
 
 from . import _lib
 from .errors import ShapeMismatch
-from .rto import rto_ranks, rto_sweeps, tt_truncate_left_orth
+from .rto import CounterDRM, rto_ranks, rto_sweeps, tt_truncate_left_orth
 from .sketch import KhatriRaoSketch, kr_apply
 from .streaming import StreamFrame, combine_pairs, stream_recover, stream_sketch, tt_drm_new
 from .tt import (ZERO_REL, RoundSpec, TTOperator, TTVector, tt_combine, tt_dots, tt_matvec, tt_norm,
@@ -184,7 +184,9 @@ def solver_rto_drm(dims, cfg: SolverConfig, device=None):
     cap = cfg.rto_ell if cfg.rto_ell is not None else cfg.max_rank + cfg.rto_oversampling
     d = len(dims)
     ls = rto_ranks(list(dims), [1] + [10 ** 9] * (d - 1) + [1], cap)
-    return tt_drm_new(dims, ls, seed=cfg.seed + 2, device=device)
+    # generated on the device block by block as the sketch ranks grow (rto.CounterDRM):
+    # a host draw of the cap-sized map cost ~2.6 s per config-5 solve
+    return CounterDRM(dims, ls, seed=cfg.seed + 2, device=device)
 
 
 class _SketchedRun:
@@ -209,7 +211,7 @@ class _SketchedRun:
     def _round(self, v, spec):
         if self.cfg.rounding == "svd":
             return tt_round(v, spec, zero_rel=self.cfg.zero_rel)
-        return tt_truncate_left_orth(rto_sweeps(v, self.rto_drm.cores), spec)
+        return tt_truncate_left_orth(rto_sweeps(v, self.rto_drm), spec)
 
     def _rounded_norm(self, v):
         """||v|| of a rounded vector from the core carrying the norm: the last

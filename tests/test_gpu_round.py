@@ -242,3 +242,24 @@ def test_frame_create_matches_reference_draws(cuda):
     f = T.StreamFrame.create([3, 4, 3], [2, 2], oversampling=3, seed=6, device=cuda)
     for a, b in zip(f.left.cores + f.right.cores, cores(z, "ss_left") + cores(z, "ss_right")):
         assert np.array_equal(a.cpu().numpy(), b)
+
+
+def test_counter_drm_blocks_and_moments(cuda):
+    """Device TT-DRM: every leading block equals the same block of the full
+    map (the solver grows its sketch ranks without redrawing), entries are
+    N(0, 1/(R_{k-1} n R_k)) of the full ranks, and the map is deterministic."""
+    import math
+    dims = [6, 5, 7, 4]
+    full = T.CounterDRM(dims, [9, 11, 8], seed=123, device=cuda)
+    F = full.cores
+    blk = full.block([3, 5, 2])
+    L = [1, 3, 5, 2, 1]
+    for k in range(4):
+        assert torch.equal(blk[k], F[k][: L[k], :, : L[k + 1]].contiguous())
+    again = T.CounterDRM(dims, [9, 11, 8], seed=123, device=cuda).cores
+    assert all(torch.equal(a, b) for a, b in zip(F, again))
+    other = T.CounterDRM(dims, [9, 11, 8], seed=124, device=cuda).cores
+    assert not torch.equal(F[1], other[1])
+    big = T.CounterDRM([64, 64], [256], seed=7, device=cuda).cores[1]  # 256 x 64 x 1
+    z = (big * math.sqrt(256 * 64)).flatten().cpu().numpy()
+    assert abs(z.mean()) < 0.05 and abs(z.std() - 1.0) < 0.05

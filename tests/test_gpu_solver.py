@@ -74,7 +74,7 @@ def test_solver_config1_rto_vs_oracle(cuda):
     x, rep = T.tt_sgmres(a, b, None, cfg, s, T.make_solver_frame(b, cfg, seed=1))
     ocfg = {"maxit": cfg.maxit, "tol": cfg.tol, "ell": cfg.ell, "eta": cfg.eta, "max_rank": cfg.max_rank,
             "oversampling": cfg.oversampling, "seed": cfg.seed, "zero_rel": None}
-    drm = T.solver_rto_drm(b.dims, cfg, device="cpu").cores
+    drm = [g.cpu() for g in T.solver_rto_drm(b.dims, cfg, device=cuda).cores]
     ox, orep = O.sgmres(a_np, b_np, ocfg, f_np, frame=O.solver_frame(b_np, ocfg, seed=1), rounding="rto",
                         rto_drm=[g.numpy() for g in drm])
     assert rep.iterations == orep["iterations"]
@@ -107,3 +107,27 @@ def test_determinism(cuda):
         _, rep = T.tt_sgmres(a, b, None, cfg, s, frame)
         outs.append(rep.res_sketched)
     assert outs[0] == outs[1]
+
+
+def test_concurrent_rhs_equal_sequential(cuda):
+    """Independent right-hand sides solved concurrently on separate CUDA
+    streams (parallel.solve_rhs_sharded) give exactly the sequential reports."""
+    from paper_2409_09471_b200.parallel import solve_rhs_sharded
+    z = load("solver_small.npz")
+    a = T.TTOperator(cores(z, "sv_pde_op"), device=cuda)
+    base = T.TTVector(cores(z, "sv_pde_b"), device=cuda)
+
+    def solve_one(j):
+        b = T.tt_scale(base, 1.0 + 0.25 * j)
+        cfg = T.SolverConfig(maxit=12, tol=1e-9, ell=1, seed=19 + j, rounding="rto", zero_rel=None, max_rank=10)
+        s = T.kr_sketch_new(b.dims, cfg.sketch_rows, seed=20 + j, device=cuda)
+        frame = T.StreamFrame.create(b.dims, [8, 8], seed=21 + j, device=cuda)
+        _, rep = T.tt_sgmres(a, b, None, cfg, s, frame)
+        torch.cuda.current_stream(cuda).synchronize()
+        return {"iterations": rep.iterations, "res": list(rep.res_sketched), "ranks": list(rep.basis_rank)}
+
+    seq, _ = solve_rhs_sharded(4, 0, 1, solve_one, concurrency=1, device=cuda)
+    par, agg = solve_rhs_sharded(4, 0, 1, solve_one, concurrency=4, device=cuda)
+    assert agg["concurrency"] == 4
+    for x, y in zip(seq, par):
+        assert x["iterations"] == y["iterations"] and x["ranks"] == y["ranks"] and x["res"] == y["res"]
