@@ -157,6 +157,19 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
                    const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream);
 size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L);
 
+/* ---- TT containers (reference save_/load_vector, save_/load_operator,
+ * tt.py:451-520): magic "TTKVEC01" / "TTKOPR01", int64 LE header
+ * (vector: d, dims[d], ranks[d+1]; operator: d, row_dims[d], col_dims[d],
+ * ranks[d+1]), then row-major float64 LE cores.  Device transfers are staged
+ * through two pinned buffers (file I/O overlaps the copies).
+ * Errors: 2 (ValueError) for a bad magic, truncated file or bad header. */
+/* kind: 0 vector, 1 operator; header[0..] as laid out in the file (incl. d) */
+int ttk_io_read_header(const char* path, int* kind, int* d, long long* header, int cap);
+/* cores: d pointers (host if !to_device) sized from the header */
+int ttk_io_read_cores(const char* path, int to_device, double* const* cores, void* stream);
+int ttk_io_write(const char* path, int kind, int d, const long long* header, int from_device,
+                 const double* const* cores, void* stream);
+
 /* ---- counter-based Gaussian TT-DRM (the solver's randomized-rounding sketch;
  * no reference counterpart, SPEC.md:313 -- replaces the host draw of
  * streaming.py:38-53 for that one use).  Writes the leading r0 x n x r1 block of

@@ -57,4 +57,6 @@ from .tt import (
     tt_zero,
 )
 
+from .tt_io import load_operator, load_vector, read_header, save_operator, save_vector
+
 __version__ = "0.1.0"

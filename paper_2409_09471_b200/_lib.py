@@ -160,6 +160,11 @@ SIGNATURES.update({
 
 SIGNATURES.update({"ttk_debug_svd_sweeps": (c_int, [c_vp])})
 SIGNATURES.update({"ttk_debug_jacobi_profile": (c_int, [c_vp])})
+SIGNATURES.update({
+    "ttk_io_read_header": (c_int, [ctypes.c_char_p, P_int, P_int, ctypes.POINTER(ctypes.c_longlong), c_int]),
+    "ttk_io_read_cores": (c_int, [ctypes.c_char_p, c_int, P_vp, c_vp]),
+    "ttk_io_write": (c_int, [ctypes.c_char_p, c_int, c_int, ctypes.POINTER(ctypes.c_longlong), c_int, P_vp, c_vp]),
+})
 SIGNATURES.update({"ttk_debug_host_profile": (c_int, [ctypes.POINTER(ctypes.c_longlong)])})
 SIGNATURES.update({"ttk_drm_gaussian": (c_int, [ctypes.c_ulonglong, c_int, c_int, c_int, c_int, c_int, c_int,
                                                 c_double, c_vp, c_vp])})

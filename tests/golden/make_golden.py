@@ -282,10 +282,22 @@ def gen_solver_cfg1():
     np.savez_compressed(os.path.join(HERE, "solver_cfg1.npz"), **out)
 
 
+def gen_serial():
+    """TT containers written by the reference's save_vector / save_operator
+    (tt.py:451-520) on the shapes of its own round-trip tests
+    (test_tt.py:363-380), plus the cores for a bit-exact comparison."""
+    out = {}
+    v = rtt.tt_random([3, 5, 2], [2, 3], seed=30)
+    a = ttkrylov.TTOperator(random_operator([3, 4], [2, 5], [3], seed=31))
+    rtt.save_vector(os.path.join(HERE, "serial_vec.ttk"), v)
+    rtt.save_operator(os.path.join(HERE, "serial_op.ttk"), a)
+    cores_dict("vec", v.cores, out)
+    cores_dict("op", a.op_cores, out)
+    np.savez_compressed(os.path.join(HERE, "serial.npz"), **out)
+
+
 if __name__ == "__main__":
-    gen_tt_ops()
-    gen_sketch()
-    gen_streaming()
-    gen_solver_small()
-    gen_solver_cfg1()
+    which = sys.argv[1:] or ["tt_ops", "sketch", "streaming", "solver_small", "solver_cfg1", "serial"]
+    for name in which:
+        globals()["gen_" + name]()
     print("golden fixtures written to", HERE)

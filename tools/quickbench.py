@@ -66,4 +66,18 @@ if "concat" in which:
     del out
     best, med = timeit(lambda: T.tt_combine([vt] + ws, [1, -0.1, -0.2, -0.3]))
     res["concat_r300"] = {"ms": best, "med_ms": med, "bytes": tot + inb, "gbs": (tot + inb) / best / 1e6}
+if "io" in which:
+    # TT container I/O of the config-3 matvec output (1.13 GB) through pinned staging
+    import os, tempfile
+    d, n, r, rho = 32, 128, 64, 3
+    rr = [1] + [r * rho] * (d - 1) + [1]
+    v = T.tt_random([n] * d, rr[1:-1], seed=5, device=dev)
+    nbytes = sum(c.numel() for c in v.cores) * 8
+    path = os.path.join(tempfile.gettempdir(), "qb_io.ttk")
+    torch.cuda.synchronize(); t0 = time.perf_counter(); T.save_vector(path, v); t1 = time.perf_counter()
+    w = T.load_vector(path, device=dev); torch.cuda.synchronize(); t2 = time.perf_counter()
+    ok = all(torch.equal(a, b) for a, b in zip(v.cores, w.cores))
+    os.remove(path)
+    res["io_cfg3_matvec_output"] = {"gb": nbytes / 1e9, "save_gbs": nbytes / (t1 - t0) / 1e9,
+                                    "load_gbs": nbytes / (t2 - t1) / 1e9, "identical": ok}
 print(json.dumps(res, indent=1))
