@@ -1463,6 +1463,62 @@ __device__ void block_dmma(int M, int N, int K, const double* A, int a_rs, int a
   }
 }
 
+// Triangular variant of block_dmma for the near-identity series: only output
+// tiles with m-tile <= n-tile (upper triangle, lower tiles are left alone) and,
+// per tile, only the k range where both operands are nonzero:
+//   kind 0: C = F^T F with F upper  -> k < min(m, n) + 8  (k <= min(i, j))
+//   kind 1: C = A B with A, B upper -> k in [m-tile start, n-tile end)
+// rinv_out != nullptr: the R^{-1} epilogue of block_dmma (only c >= r written; the
+// strictly lower part of rinv_out is zeroed by the caller).
+__device__ void block_dmma_tri(int l, int kind, const double* A, int a_rs, int a_cs, const double* B, int b_rs,
+                               int b_cs, double* C, int ldc, double* rinv_out = nullptr,
+                               const double* rinv_f = nullptr, const double* rinv_p = nullptr) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int nt = (l + 7) >> 3;
+  const int tiles = nt * (nt + 1) / 2;
+  for (int tt = warp; tt < tiles; tt += nw) {
+    // tt -> (ti <= tj), row-major over the upper triangle
+    int ti = 0, rem = tt;
+    while (rem >= nt - ti) { rem -= nt - ti; ++ti; }
+    const int tj = ti + rem;
+    const int m0 = ti * 8, n0 = tj * 8;
+    const int m = m0 + fr, n = n0 + fr;
+    const int kb = (kind == 0) ? 0 : (m0 & ~3);
+    const int ke = min(l, (kind == 0) ? m0 + 8 : n0 + 8);
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    int k0 = kb;
+    for (; k0 + 8 <= ke; k0 += 8) {
+      const int ka = k0 + fk, kb2 = k0 + 4 + fk;
+      const double a0 = (m < l) ? A[m * a_rs + ka * a_cs] : 0.0;
+      const double b0 = (n < l) ? B[ka * b_rs + n * b_cs] : 0.0;
+      const double a1 = (m < l) ? A[m * a_rs + kb2 * a_cs] : 0.0;
+      const double b1 = (n < l) ? B[kb2 * b_rs + n * b_cs] : 0.0;
+      dmma_8x8x4(c0, a0, b0);
+      dmma_8x8x4(c1, a1, b1);
+    }
+    for (; k0 < ke; k0 += 4) {
+      const int k = k0 + fk;
+      const double a0 = (m < l && k < ke) ? A[m * a_rs + k * a_cs] : 0.0;
+      const double b0 = (n < l && k < ke) ? B[k * b_rs + n * b_cs] : 0.0;
+      dmma_8x8x4(c0, a0, b0);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cn = n0 + 2 * fk + h;
+      if (m < l && cn < l) {
+        const double v = c0[h] + c1[h];
+        if (rinv_out) {
+          if (cn >= m)
+            rinv_out[(size_t)m * l + cn] = (cn == m ? 1.0 : 0.0) - rinv_f[m * ldc + cn] + rinv_p[m * ldc + cn] - v;
+        } else {
+          C[m * ldc + cn] = v;
+        }
+      }
+    }
+  }
+}
+
 // Cholesky factor of a Gram matrix that is already the identity to within
 // tol (the second CholeskyQR pass of a well-conditioned block), by series:
 // with E = G - I, F1 = triu(E) - diag(E)/2 satisfies F1 + F1^T = E, and
@@ -1502,7 +1558,7 @@ __global__ void __launch_bounds__(1024, 1)
     if (tid == 0) *flag = 0;
     return;
   }
-  block_dmma(l, l, l, F, 1, ld, F, ld, 1, P, ld);  // P = F1^T F1
+  block_dmma_tri(l, 0, F, 1, ld, F, ld, 1, P, ld);  // P = F1^T F1 (upper tiles, k <= min(i, j))
   __syncthreads();
   for (int idx = tid; idx < l * l; idx += nt) {
     const int i = idx / l, c = idx - i * l;
@@ -1513,11 +1569,12 @@ __global__ void __launch_bounds__(1024, 1)
   for (int idx = tid; idx < l * l; idx += nt) {
     const int i = idx / l, c = idx - i * l;
     Rout[idx] = (c > i) ? F[i * ld + c] : (c == i ? 1.0 + F[i * ld + c] : 0.0);
+    if (c < i) Rinv[idx] = 0.0;
   }
-  block_dmma(l, l, l, F, ld, 1, F, ld, 1, P, ld);  // P = F2^2
+  block_dmma_tri(l, 1, F, ld, 1, F, ld, 1, P, ld);  // P = F2^2 (upper x upper)
   __syncthreads();
   // R^{-1} = I - F2 + F2^2 - F2^2 F2, the last product folded into the store
-  block_dmma(l, l, l, P, ld, 1, F, ld, 1, nullptr, ld, Rinv, F, P);
+  block_dmma_tri(l, 1, P, ld, 1, F, ld, 1, nullptr, ld, Rinv, F, P);
   if (tid == 0) *flag = 1;
 }
 
