@@ -1986,7 +1986,7 @@ __global__ void __launch_bounds__(kTrsmWarps * 32)
 // (block_dmma), and only the 16 x 16 diagonal solve is scalar: four threads
 // per row, each owning four columns, pivot value broadcast by shuffle.
 // Same backward-stable forward substitution, ~10x fewer instructions.
-constexpr int kTbRows = 64, kTbThreads = 256;
+constexpr int kTbRows = 32, kTbThreads = 128;
 
 __global__ void __launch_bounds__(kTbThreads)
     trsm_blocked_kernel(int m, int l, const double* Y, long long y_rs, long long y_cs,
@@ -1997,19 +1997,28 @@ __global__ void __launch_bounds__(kTbThreads)
   double* sY = sR + (size_t)l * ld;          // kTbRows x ld
   double* rinv = sY + (size_t)kTbRows * ld;  // l
   const int tid = threadIdx.x;
+  // R and the first Y tile staged asynchronously (one round of load latency)
   for (int e = tid; e < l * l; e += kTbThreads) {
     const int r = e / l, c = e - r * l;
-    sR[r * ld + c] = R[e];
+    cp_async8(sR + r * ld + c, R + e, true);
   }
-  for (int j = tid; j < l; j += kTbThreads) rinv[j] = 1.0 / R[(size_t)j * l + j];
   const int row = tid >> 2, g = tid & 3;
+  bool first = true;
   for (long long r0 = (long long)blockIdx.x * kTbRows; r0 < m; r0 += (long long)gridDim.x * kTbRows) {
     __syncthreads();
     for (int e = tid; e < kTbRows * l; e += kTbThreads) {
       const int r = e / l, c = e - r * l;
-      sY[r * ld + c] = (r0 + r < m) ? Y[(r0 + r) * y_rs + (long long)c * y_cs] : 0.0;
+      const bool ok = r0 + r < m;
+      cp_async8(sY + r * ld + c, ok ? Y + (r0 + r) * y_rs + (long long)c * y_cs : Y, ok);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
+    if (first) {
+      for (int j = tid; j < l; j += kTbThreads) rinv[j] = 1.0 / sR[j * ld + j];
+      __syncthreads();
+      first = false;
+    }
     for (int j0 = 0; j0 < l; j0 += 16) {
       const int bs = min(16, l - j0);
       if (j0 > 0) {
@@ -2063,7 +2072,7 @@ int trsm_right_upper(int m, int l, const double* Y, long long y_rs, long long y_
   }
   const int ld = ((l + 15) & ~15) + 4;
   const size_t smem = sizeof(double) * ((size_t)l * ld + (size_t)kTbRows * ld + l);
-  const int grid = (int)std::min<long long>((m + kTbRows - 1) / kTbRows, 2LL * kNumSMs);
+  const int grid = (int)std::min<long long>((m + kTbRows - 1) / kTbRows, 4LL * kNumSMs);
   trsm_blocked_kernel<<<grid, kTbThreads, smem, st>>>(m, l, Y, y_rs, y_cs, R, Q, q_rs, q_cs);
   TTK_CHECK_LAUNCH();
   return kOk;
