@@ -101,6 +101,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // 8-byte async global->shared copy; src_bytes = 0 zero-fills the destination
+// shared destination given as a 32-bit shared-window address
+__device__ __forceinline__ void cp_async8_s(uint32_t smem_dst, const void* gmem_src, bool valid) {
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_dst), "l"(gmem_src), "r"(sz));
+}
+
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src, bool valid) {
   int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem_dst)),

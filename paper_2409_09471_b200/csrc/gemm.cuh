@@ -94,14 +94,17 @@ __device__ __forceinline__ int pair_pos(int m) {
 // Per-thread load plan for one operand tile (E x BK elements, E = BM or BN):
 // each thread always copies the same (row, k) slots, so its source offsets
 // (32-bit element offsets from the operand base; the host checks that every
-// operand fits) and shared destinations are computed once per tile and only
-// advance by BK * ks per stage.  dst and k are packed into one word.
+// operand fits) and shared destinations (byte offsets within a stage) are
+// computed once per tile.  Per stage and element: one 64-bit add, one 32-bit
+// add and the cp.async; rows outside the problem and (on the last stage) k
+// beyond the slice are zero-filled through cp.async's src-size operand, so the
+// source pointer never needs a select.
 template <int E, int BK, int T, int NE, bool PAIR, int S>
 struct TileLoader {
   const double* base;
   int off[NE];
-  int dk[NE];      // (dst << 8) | k
-  unsigned valid;  // bit i: row in range and slot used
+  int dk[NE];      // (dst byte offset << 8) | k, -1 if the slot is unused
+  unsigned valid;  // bit i: row in range
   __device__ __forceinline__ void init(const double* b, const long long* rowoff, long long ks, int r0, int rows) {
     base = b;
     valid = 0;
@@ -114,17 +117,32 @@ struct TileLoader {
       const bool used = e < E * BK;
       const bool ok = used && (r0 + r < rows);
       off[i] = ok ? (int)(rowoff[r] + (long long)k * ks) : 0;
-      dk[i] = used ? (((k * S + pair_pos<PAIR>(r)) << 8) | k) : -1;  // -1: slot unused (no copy at all)
+      dk[i] = used ? ((((k * S + pair_pos<PAIR>(r)) * 8) << 8) | k) : -1;
       if (ok) valid |= 1u << i;
     }
   }
-  __device__ __forceinline__ void load(double* smem, long long koff, int kleft) const {
+  // full = every k of the stage lies inside the slice (all but the last stage)
+  template <bool FULL>
+  __device__ __forceinline__ void load(uint32_t smem_stage, long long koff, int kleft) const {
+    const double* gb = base + koff;
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       if ((i + 1) * T > E * BK && dk[i] < 0) continue;  // only the last slot can be unused
+      bool ok = (valid >> i) & 1u;
+      if constexpr (!FULL) ok = ok && ((dk[i] & 255) < kleft);
+      cp_async8_s(smem_stage + (uint32_t)(dk[i] >> 8), gb + off[i], ok);
+    }
+  }
+  // the per-element form (k bound tested on every stage, source selected):
+  // measured faster for the grouped tt_matvec launch (24.4 vs 22.5 TF/s, its
+  // L2-bound operand stream), slower on single large GEMMs
+  __device__ __forceinline__ void load_classic(uint32_t smem_stage, long long koff, int kleft) const {
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      if ((i + 1) * T > E * BK && dk[i] < 0) continue;
       const bool ok = ((valid >> i) & 1u) && ((dk[i] & 255) < kleft);
       const double* src = base + koff + off[i];
-      cp_async8(smem + (dk[i] >> 8), ok ? src : base, ok);  // !ok: zero-fill (row or k padding)
+      cp_async8_s(smem_stage + (uint32_t)(dk[i] >> 8), ok ? src : base, ok);
     }
   }
 };
@@ -202,12 +220,24 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, gemm_min_blocks<BM, BN
 
   const int klen = kend - kbeg;
   const int nk = (klen > 0) ? (klen + BK - 1) / BK : 0;
+  const uint32_t as0 = smem_u32(As), bs0 = smem_u32(Bs);
+  auto load_stage = [&](int kt, int buf) {
+    const uint32_t sa = as0 + (uint32_t)(buf * BK * Cfg::SA * 8), sb = bs0 + (uint32_t)(buf * BK * Cfg::SB * 8);
+    const int kleft = klen - kt * BK;
+    if constexpr (CAP > kSmallGroup) {
+      la.load_classic(sa, (long long)kt * BK * a_ks, kleft);
+      lb.load_classic(sb, (long long)kt * BK * b_ks, kleft);
+    } else if (kleft >= BK) {
+      la.template load<true>(sa, (long long)kt * BK * a_ks, kleft);
+      lb.template load<true>(sb, (long long)kt * BK * b_ks, kleft);
+    } else {
+      la.template load<false>(sa, (long long)kt * BK * a_ks, kleft);
+      lb.template load<false>(sb, (long long)kt * BK * b_ks, kleft);
+    }
+  };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) {
-      la.load(As + s * BK * Cfg::SA, (long long)s * BK * a_ks, klen - s * BK);
-      lb.load(Bs + s * BK * Cfg::SB, (long long)s * BK * b_ks, klen - s * BK);
-    }
+    if (s < nk) load_stage(s, s);
     cp_async_commit();
   }
 
@@ -217,11 +247,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, gemm_min_blocks<BM, BN
     __syncthreads();
     {
       const int nxt = kt + STAGES - 1;
-      if (nxt < nk) {
-        const int st = nxt % STAGES;
-        la.load(As + st * BK * Cfg::SA, (long long)nxt * BK * a_ks, klen - nxt * BK);
-        lb.load(Bs + st * BK * Cfg::SB, (long long)nxt * BK * b_ks, klen - nxt * BK);
-      }
+      if (nxt < nk) load_stage(nxt, nxt % STAGES);
       cp_async_commit();
     }
     const double* as = As + (kt % STAGES) * BK * Cfg::SA;
