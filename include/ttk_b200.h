@@ -130,8 +130,8 @@ int ttk_debug_svd_sweeps(int* dev_counter);
 /* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,
  * pull, rounds; 5 int64 per CTA, 8 CTAs) into dev_acc (NULL: off) */
 int ttk_debug_jacobi_profile(long long* dev_acc);
-/* diagnostics: the register Cholesky adds per-step clocks (step, thread-0 work,
- * owner publish + reciprocal) into dev_acc[3] (NULL: off) */
+/* diagnostics: the blocked Cholesky adds per-call phase clocks (load, diagonal
+ * blocks, panels, trailing updates, epilogue, call count) into dev_acc[6] (NULL: off) */
 int ttk_debug_chol_profile(long long* dev_acc);
 /* diagnostics: host synchronisation points (rank / path decisions) so far:
  * out[0] = count, out[1] = total wait in ns (timed only when TTK_HOST_PROF is set) */

@@ -465,7 +465,7 @@ int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* 
 // (round-robin tournament), one 16-lane group per pair.
 constexpr int kSvdThreads = 1024;
 __device__ int* g_svd_sweeps = nullptr;  // optional diagnostic sink (tests)
-__device__ long long* g_chol_prof = nullptr;  // diagnostics: per-step clocks of chol_inv_reg
+__device__ long long* g_chol_prof = nullptr;  // diagnostics: phase clocks of chol_blocked_kernel
 constexpr int kSvdGroup = 16;  // lanes per column pair
 
 template <int RPL>
@@ -1090,7 +1090,7 @@ int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V
   return jacobi_svd(k, l, B, U, S, V, (cudaStream_t)stream);
 }
 
-// diagnostics: chol_inv_reg per-step clocks (step total, thread-0 work, owner publish+divide)
+// diagnostics: chol_blocked_kernel phase clocks (load, diagonal blocks, panels, trailing, epilogue)
 int ttk_debug_chol_profile(long long* dev_acc) {
   TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_chol_prof, &dev_acc, sizeof(long long*)));
   return kOk;
@@ -1278,136 +1278,6 @@ __global__ void __launch_bounds__(1024, 1)
     int r = e / l, c = e - r * l;
     Rout[e] = (c > r) ? A[r * ld + c] * rsq[r] : (c == r ? dsq[r] : 0.0);
     Rinv[e] = (c >= r) ? X[c * ld + r] * rsq[c] : 0.0;
-  }
-  if (tid == 0 && bad) atomicOr(status, bad);
-}
-
-// Register-resident variant of chol_inv_kernel for l <= 96 (same elimination
-// of [G | I], same outputs and status bits).  kChW warps; warp w owns rows
-// w + kChW r (row-cyclic), lane t owns columns t + 32 q.  The finished pivot
-// row is published through a double-buffered shared row, the multiplier of
-// row i is one shuffle away (pivot-row column i lives in lane i & 31, slot
-// i >> 5), and the lane that finishes the next pivot forms its reciprocal.
-// One barrier per step.  Few fat warps: the step is issue-bound, so per-warp
-// overhead is what to minimise; column slots with nothing left to do (A part
-// left of the pivot, X part right of it) are skipped.
-constexpr int kChW = 8;
-
-template <int RW, int CPL>
-__global__ void __launch_bounds__(kChW * 32, 1)
-    chol_inv_reg_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
-                        double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
-                        double tiny_rel, const int* __restrict__ skip) {
-  if (skip && *skip) return;  // chol_near_identity_kernel already produced R, R^{-1}
-  extern __shared__ double sm[];  // epilogue staging: A (l x ld), X (l x ld)
-  const int ld = l + 1;
-  double* A = sm;
-  double* X = sm + (size_t)l * ld;
-  __shared__ double prow[2][2][32 * CPL];
-  __shared__ double pinv[kChW * RW];
-  __shared__ double dsq[kChW * RW], rsq[kChW * RW];
-  __shared__ double gmax_s, tr_s;
-  __shared__ int bad;
-  const int tid = threadIdx.x, w = tid >> 5, t = tid & 31;
-  if (tid == 0) bad = 0;
-  if (w == 0) {
-    double g = 0.0, tr = 0.0;
-    for (int i = t; i < l; i += 32) { const double v = G[(size_t)i * l + i]; g = fmax(g, v); tr += v; }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
-    tr = warp_sum(tr);
-    if (t == 0) { gmax_s = g; tr_s = tr; }
-  }
-  __syncthreads();
-  const double sh = shift_rel > 0.0 ? shift_rel * tr_s : 0.0;
-  const double tiny = gmax_s * tiny_rel + 1e-300;
-  double a[RW][CPL], x[RW][CPL];
-  int badl = 0;
-#pragma unroll
-  for (int r = 0; r < RW; ++r)
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int i = w + kChW * r, c = t + 32 * q;
-      double v = (i < l && c < l) ? G[(size_t)i * l + c] : 0.0;
-      if (check_identity && i < l && c < l && fabs(v - (i == c ? 1.0 : 0.0)) > 1e-3) badl |= 2;
-      if (i == c) v += sh;
-      a[r][q] = v;
-      x[r][q] = (i == c && i < l) ? 1.0 : 0.0;
-    }
-  if (badl) atomicOr(&bad, badl);
-  if (w == 0) {
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) { prow[0][0][t + 32 * q] = a[0][q]; prow[0][1][t + 32 * q] = x[0][q]; }
-    if (t == 0) {
-      const double p0 = a[0][0];
-      if (!(p0 > tiny)) { atomicOr(&bad, 1); pinv[0] = 1.0; } else { pinv[0] = 1.0 / p0; }
-    }
-  }
-  __syncthreads();
-  long long* const prof = (tid == 0) ? g_chol_prof : nullptr;
-  long long tp = prof ? clock64() : 0, acc_step = 0, acc_mid = 0;
-  for (int j = 0; j < l; ++j) {
-    const int buf = j & 1;
-    const int qa = j >> 5;          // first slot with A columns > j
-    const int qx = (j >> 5) + 1;    // slots with X columns <= j
-    double pa[CPL], px[CPL];
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      pa[q] = (q >= qa) ? prow[buf][0][t + 32 * q] : 0.0;
-      px[q] = (q < qx) ? prow[buf][1][t + 32 * q] : 0.0;
-    }
-    const double inv = pinv[j];
-#pragma unroll
-    for (int r = 0; r < RW; ++r) {
-      const int i = w + kChW * r;
-      if (i > j && i < l) {  // warp-uniform
-        const int src = ((kChW * r) & 31) + w;  // lane holding pivot-row column i
-        const double mlt = __shfl_sync(0xffffffffu, pa[(kChW * r) >> 5], src) * inv;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          if (q >= qa) a[r][q] -= mlt * pa[q];
-          if (q < qx) x[r][q] -= mlt * px[q];
-        }
-        if (i == j + 1) {
-#pragma unroll
-          for (int q = 0; q < CPL; ++q) {
-            prow[buf ^ 1][0][t + 32 * q] = a[r][q];
-            prow[buf ^ 1][1][t + 32 * q] = x[r][q];
-          }
-          if (t == src) {
-            const double pn = a[r][(kChW * r) >> 5];
-            if (!(pn > tiny)) { atomicOr(&bad, 1); pinv[i] = 1.0; } else { pinv[i] = 1.0 / pn; }
-          }
-        }
-      }
-    }
-    if (prof) acc_mid += clock64() - tp;
-    __syncthreads();
-    if (prof) { const long long tn = clock64(); acc_step += tn - tp; tp = tn; }
-  }
-  if (prof) {
-    atomicAdd((unsigned long long*)&prof[0], (unsigned long long)acc_step);
-    atomicAdd((unsigned long long*)&prof[1], (unsigned long long)acc_mid);
-  }
-#pragma unroll
-  for (int r = 0; r < RW; ++r)
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int i = w + kChW * r, c = t + 32 * q;
-      if (i < l && c < l) { A[(size_t)i * ld + c] = a[r][q]; X[(size_t)i * ld + c] = x[r][q]; }
-    }
-  __syncthreads();
-  for (int r = tid; r < l; r += blockDim.x) {
-    const double p = A[(size_t)r * ld + r];
-    const double d = sqrt(p > tiny ? p : 1.0);
-    dsq[r] = d;
-    rsq[r] = 1.0 / d;
-  }
-  __syncthreads();
-  for (int e = tid; e < l * l; e += blockDim.x) {
-    const int r = e / l, c = e - r * l;
-    Rout[e] = (c > r) ? A[(size_t)r * ld + c] * rsq[r] : (c == r ? dsq[r] : 0.0);
-    Rinv[e] = (c >= r) ? X[(size_t)c * ld + r] * rsq[c] : 0.0;
   }
   if (tid == 0 && bad) atomicOr(status, bad);
 }
@@ -1921,67 +1791,11 @@ size_t cholqr2_ws_bytes(int m, int l) {
 // returns kOk and *ok = 1 when the result was accepted
 // ---------------------------------------------------------------------------
 // Q = Y R^{-1} for an upper-triangular R (l x l, row-major) by forward
-// substitution, row by row.  Backward stable (Q R = Y + O(eps |Y|)), unlike a
-// GEMM with an explicit inverse whose error grows like eps kappa(R) ||Y||: the
-// first CholeskyQR pass of a rank-deficient / shifted Gram has kappa(R) up to
-// ~1e8 and the explicit inverse then loses 8 digits of the factorisation.
-// One warp solves two rows at once (independent chains interleaved); lane
-// owns columns lane + 32 q.  Rows are independent, so Q may alias Y.
-constexpr int kTrsmWarps = 16;
-
-template <int CPL>
-__global__ void __launch_bounds__(kTrsmWarps * 32)
-    trsm_rows_kernel(int m, int l, const double* Y, long long y_rs, long long y_cs,
-                     const double* __restrict__ R, double* Q, long long q_rs, long long q_cs) {
-  extern __shared__ double sR[];  // l x l (row-major) then rinv[l]
-  double* rinv = sR + (size_t)l * l;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < l * l; e += blockDim.x) sR[e] = R[e];
-  for (int j = tid; j < l; j += blockDim.x) rinv[j] = 1.0 / R[(size_t)j * l + j];
-  __syncthreads();
-  for (long long r0 = ((long long)blockIdx.x * kTrsmWarps + warp) * 2; r0 < m;
-       r0 += (long long)gridDim.x * kTrsmWarps * 2) {
-    const bool two = r0 + 1 < m;
-    double t0[CPL], t1[CPL];
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int c = lane + 32 * q;
-      t0[q] = (c < l) ? Y[r0 * y_rs + (long long)c * y_cs] : 0.0;
-      t1[q] = (c < l && two) ? Y[(r0 + 1) * y_rs + (long long)c * y_cs] : 0.0;
-    }
-#pragma unroll
-    for (int qb = 0; qb < CPL; ++qb) {
-      const int jend = min(32, l - 32 * qb);
-      for (int jj = 0; jj < jend; ++jj) {
-        const int j = 32 * qb + jj;
-        const double ri = rinv[j];
-        const double v0 = __shfl_sync(0xffffffffu, t0[qb], jj) * ri;
-        const double v1 = __shfl_sync(0xffffffffu, t1[qb], jj) * ri;
-        if (lane == jj) { t0[qb] = v0; t1[qb] = v1; }
-        const double* rj = sR + (size_t)j * l;
-#pragma unroll
-        for (int q = qb; q < CPL; ++q) {
-          const int c = lane + 32 * q;
-          if (c > j && c < l) {
-            const double rjc = rj[c];
-            t0[q] -= v0 * rjc;
-            t1[q] -= v1 * rjc;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int c = lane + 32 * q;
-      if (c < l) {
-        Q[r0 * q_rs + (long long)c * q_cs] = t0[q];
-        if (two) Q[(r0 + 1) * q_rs + (long long)c * q_cs] = t1[q];
-      }
-    }
-  }
-}
-
-// Blocked variant: a CTA owns 64 rows.  For every 16-column block J the
+// substitution: backward stable (Q R = Y + O(eps |Y|)), unlike a GEMM with an
+// explicit inverse whose error grows like eps kappa(R) ||Y|| -- the first
+// CholeskyQR pass of a rank-deficient / shifted Gram has kappa(R) up to ~1e8.
+// Rows are independent, so Q may alias Y.
+// Blocked form: a CTA owns kTbRows rows.  For every 16-column block J the
 // off-diagonal part Y_J -= Q_{<J} R_{<J,J} runs on the DMMA pipe
 // (block_dmma), and only the 16 x 16 diagonal solve is scalar: four threads
 // per row, each owning four columns, pivot value broadcast by shuffle.

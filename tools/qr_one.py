@@ -1,4 +1,4 @@
-"""One CholeskyQR2 (10240 x 80 Gaussian) for ncu: trsm_rows + chol_inv_reg + GEMMs."""
+"""One CholeskyQR2 (10240 x 80 Gaussian) for ncu: blocked Cholesky, near-identity series, TRSM, GEMMs."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
