@@ -70,6 +70,17 @@ size_t ttk_gemm_strided_ws_bytes(int batch, int M, int N, int K);
 int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
                const double* const* D, const double* const* C, double* const* G, void* stream);
 
+/* ---- mode_multiply (reference precond.py:189-200, exp-sum terms :266-273) --
+ * For each of nterms matrix lists sharing one TT X (ranks r[0..d], mode sizes
+ * n[k]): O_{t,k}[a, i, b] = s * sum_j M_{t,k}[i, j] * X_k[a, j, b], with
+ * s = alpha[t] on the last core (tt_scale convention) and 1 elsewhere
+ * (alpha NULL: all 1).  mats[t*d+k]: m[k] x n[k] row-major; out[t*d+k]:
+ * (r[k], m[k], r[k+1]).  Ranks are unchanged.  One grouped DMMA launch (per
+ * 96 products). */
+int ttk_mode_multiply(int nterms, int d, const int* n, const int* m, const int* r, const double* alpha,
+                      const double* const* mats, const double* const* X, double* const* out,
+                      void* stream);
+
 /* ---- TT-axpy / concatenation (reference tt_add + tt_scale, tt.py:254-282) --
  * out = sum_t coeff[t] * term_t as ONE block-diagonal concatenation: first core
  * concatenated along axis 2, last along axis 0 (scaled by coeff[t], the factor

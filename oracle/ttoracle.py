@@ -490,13 +490,15 @@ def solver_frame(b, cfg, seed):
     return frame_new([c.shape[1] for c in b], ranks, cfg.get("oversampling", 20), seed)
 
 
-def sgmres(op, b, cfg, factors, frame=None, rounding="svd", rto_drm=None):
+def sgmres(op, b, cfg, factors, frame=None, rounding="svd", rto_drm=None, precond=None):
     """TT-sGMRES with sketch-only basis memory (solvers.py:334-431, 450-480).
 
     cfg keys: maxit, tol, ell, eta, max_rank, oversampling, solution_rank,
     combine_mode ('explicit'|'stta'), seed, zero_rel.  rounding='svd' uses
     tt_round (TT-SVD); rounding='rto' uses rto_round with one DRM per solve
     (rto_drm, drawn at the maximal sketch-rank profile, leading slices reused).
+    precond: optional callable cores -> cores, the right preconditioner P^{-1}
+    of tt_spgmres (solvers.py:315-320, 462-463, 483-490).
     x0 is taken as zero.  Returns (x_cores, report_dict)."""
     maxit, tol, ell = cfg["maxit"], cfg["tol"], cfg["ell"]
     eta, max_rank = cfg.get("eta", 0.3), cfg.get("max_rank")
@@ -528,7 +530,10 @@ def sgmres(op, b, cfg, factors, frame=None, rounding="svd", rto_drm=None):
     wcols = []
     y = np.zeros(1)
     for k in range(1, maxit + 1):
-        vt = matvec(op, window[-1][1])
+        vt = window[-1][1]
+        if precond is not None:
+            vt = precond(vt)
+        vt = matvec(op, vt)
         norm_av = norm(vt)
         wcols.append(kr_apply(factors, vt))
         if mode == "explicit":
@@ -573,8 +578,35 @@ def sgmres(op, b, cfg, factors, frame=None, rounding="svd", rto_drm=None):
     comb = combine_pairs(ps, [float(c) for c in y])
     x = stream_recover(comb[0], comb[1], dims, tol, solution_rank([1] + [c.shape[2] for c in b], cfg),
                        zero_rel=zero_rel)
+    if precond is not None:
+        x = precond(x)
     rep["y"] = np.asarray(y)
     return x, rep
+
+
+# ---------------------------------------------------------------------------
+# exp-sum preconditioner apply (precond.py:189-200, 246-278)
+
+def mode_multiply(cores, mats):
+    """O_k[a, i, b] = sum_j M_k[i, j] C_k[a, j, b]; ranks unchanged (precond.py:189-200)."""
+    return [np.einsum("ij,ajb->aib", np.asarray(m, dtype=np.float64), c) for m, c in zip(mats, cores)]
+
+
+def expsum_apply(cores, exps, alpha, rel_tol, max_rank=None, accumulate="sequential", frame=None,
+                 zero_rel=ZERO_REL):
+    """sum_j alpha_j (x_i exp(-beta_j A_i)) v accumulated by rounded additions
+    (inner rounding without rank cap, final with cap) or in sketch space
+    against ``frame`` = (left, right) DRM cores (precond.py:246-278).
+    exps[j][k] = exp(-beta_j A_k)."""
+    terms = [scale(mode_multiply(cores, exps[j]), float(alpha[j])) for j in range(len(alpha))]
+    if accumulate == "sequential":
+        acc = terms[0]
+        for t in terms[1:]:
+            acc = tt_round(add(acc, t), rel_tol, None, zero_rel=zero_rel)
+        return tt_round(acc, rel_tol, max_rank, zero_rel=zero_rel)
+    left, right = frame
+    psi, omega = combine_pairs([stream_sketch(t, left, right) for t in terms], [1.0] * len(terms))
+    return stream_recover(psi, omega, [c.shape[1] for c in cores], rel_tol, max_rank, zero_rel=zero_rel)
 
 
 def true_residual(op, b, x, zero_rel=ZERO_REL):

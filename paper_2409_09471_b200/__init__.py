@@ -8,6 +8,14 @@ arithmetic runs in libttk_b200.so (C ABI: include/ttk_b200.h).
 """
 
 from .errors import DegenerateRecovery, ShapeMismatch, SizeLimit
+from .precond import (
+    ExpSumPreconditioner,
+    expsum_coeffs,
+    matrix_exp,
+    mode_multiply,
+    precond_apply,
+    spectral_interval,
+)
 from .rto import CounterDRM, rto_flops, rto_ranks, rto_sweeps, tt_round_rto, tt_truncate_left_orth
 from .sketch import KhatriRaoSketch, kr_apply, kr_apply_batch, kr_apply_device, kr_apply_rows, kr_sketch_new
 from .solvers import (
@@ -19,6 +27,7 @@ from .solvers import (
     solver_rto_drm,
     true_residual,
     tt_sgmres,
+    tt_spgmres,
 )
 from .streaming import (
     PINV_RCOND,

@@ -124,4 +124,45 @@ int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
                            /*allow_split=*/false);
 }
 
+// mode_multiply for nterms matrix lists sharing one TT (the exp-sum terms):
+// O_{t,k}[a, i, b] = s_{t,k} * sum_j M_{t,k}[i, j] * X_k[a, j, b], s = alpha[t] on
+// the last core (tt_scale's convention), 1 elsewhere.  Reference:
+// ttkrylov/precond.py:189-200 (tensordot over the mode index, transpose back)
+// and the term scaling precond.py:270-272 / tt.py:278-282.  Every (term, core)
+// product is one problem of a single grouped DMMA launch (rows (a,b), cols i).
+int ttk_mode_multiply(int nterms, int d, const int* n, const int* m, const int* r, const double* alpha,
+                      const double* const* mats, const double* const* X, double* const* out,
+                      void* stream) {
+  TTK_REQUIRE(nterms >= 0 && d >= 1, kInvalidValue, "need nterms >= 0 and d >= 1");
+  TTK_REQUIRE(r[0] == 1 && r[d] == 1, kShapeMismatch, "boundary ranks must equal 1");
+  std::vector<GemmProblem> probs;
+  probs.reserve((size_t)nterms * d);
+  for (int t = 0; t < nterms; ++t) {
+    for (int k = 0; k < d; ++k) {
+      const int r0 = r[k], r1 = r[k + 1], nk = n[k], mk = m[k];
+      TTK_REQUIRE(r0 >= 0 && r1 >= 0 && nk >= 1 && mk >= 1, kShapeMismatch, "bad shapes at core %d", k);
+      TTK_REQUIRE(mats[(size_t)t * d + k] != nullptr && out[(size_t)t * d + k] != nullptr, kInvalidValue,
+                  "null matrix or output at term %d core %d", t, k);
+      if (r0 == 0 || r1 == 0) continue;
+      GemmProblem p{};
+      p.M = r0 * r1;
+      p.N = mk;
+      p.K = nk;
+      p.A = X[k];  // A((a,b), j) = X[a, j, b]
+      p.a_mdiv = r1; p.a_ms1 = (long long)nk * r1; p.a_ms0 = 1; p.a_ks = r1;
+      p.B = mats[(size_t)t * d + k];  // B(j, i) = M[i, j]
+      p.b_ndiv = 1 << 30; p.b_ns1 = 0; p.b_ns0 = nk; p.b_ks = 1;
+      p.C = out[(size_t)t * d + k];  // C((a,b), i) = O[a, i, b]
+      p.c_mdiv = r1; p.c_ms1 = (long long)mk * r1; p.c_ms0 = 1;
+      p.c_ndiv = 1 << 30; p.c_ns1 = 0; p.c_ns0 = r1;
+      p.alpha = (alpha != nullptr && k == d - 1) ? alpha[t] : 1.0;
+      p.beta = 0.0; p.splits = 1;
+      probs.push_back(p);
+    }
+  }
+  if (probs.empty()) return kOk;
+  return gemm_group_launch(probs.data(), (int)probs.size(), nullptr, 0, (cudaStream_t)stream,
+                           /*allow_split=*/false);
+}
+
 }  // extern "C"

@@ -192,12 +192,13 @@ def solver_rto_drm(dims, cfg: SolverConfig, device=None):
 class _SketchedRun:
     """Explicit/STTA sketched GMRES with sketch-only basis memory (solvers.py:292-431)."""
 
-    def __init__(self, a, b, x0, cfg, sketch, frame):
+    def __init__(self, a, b, x0, cfg, sketch, frame, precond=None):
         if sketch.dims != b.dims:
             raise ShapeMismatch("sketch dims do not match the right-hand side")
         if a.col_dims != b.dims or a.row_dims != b.dims:
             raise ShapeMismatch("operator dims do not match the right-hand side")
         self.a, self.b, self.cfg, self.sketch, self.frame = a, b, cfg, sketch, frame
+        self.precond = precond
         self.x0 = None if _is_zero(x0) else x0
         self.report = SolveReport(seed=cfg.seed)
         self.device = b.device
@@ -246,7 +247,10 @@ class _SketchedRun:
         for k in range(1, cfg.maxit + 1):
             kk = k - 1
             tm.mark("matvec")
-            vt = tt_matvec(self.a, self.window[-1][1])
+            vt = self.window[-1][1]
+            if self.precond is not None:  # right preconditioning: A P^{-1} v (solvers.py:315-320)
+                vt = self.precond.apply_inverse(vt)
+            vt = tt_matvec(self.a, vt)
             tm.mark("orth")
             # one dot sweep: <vt, vt> and <vt, v_i> for the window (MGS
             # coefficients follow from the cached window Gram matrix)
@@ -336,7 +340,10 @@ class _SketchedRun:
             pairs.append(self.x0_pair)
             coeffs.append(1.0)
         spec = RoundSpec(self.cfg.tol, default_solution_rank(self.b, self.cfg))
-        return stream_recover(combine_pairs(pairs, coeffs), spec, zero_rel=self.cfg.zero_rel)
+        u = stream_recover(combine_pairs(pairs, coeffs), spec, zero_rel=self.cfg.zero_rel)
+        if self.precond is not None:  # x = P^{-1} u (solvers.py:462-463)
+            u = self.precond.apply_inverse(u)
+        return u
 
 
 def _trim_timer_tail(report, k_done):
@@ -354,3 +361,13 @@ def tt_sgmres(a: TTOperator, b: TTVector, x0, cfg: SolverConfig, sketch: KhatriR
     if frame is None:
         frame = make_solver_frame(b, cfg, seed=cfg.seed + 1)
     return _SketchedRun(a, b, x0, cfg, sketch, frame).run()
+
+
+def tt_spgmres(a: TTOperator, precond, b: TTVector, x0, cfg: SolverConfig, sketch: KhatriRaoSketch,
+               frame: StreamFrame | None = None):
+    """Right-preconditioned TT-sGMRES (solvers.py:483-490): the Krylov space is
+    built for A P^{-1} with P^{-1} an ExpSumPreconditioner (precond.py) applied
+    on the device; the returned solution is x = P^{-1} u."""
+    if frame is None:
+        frame = make_solver_frame(b, cfg, seed=cfg.seed + 1)
+    return _SketchedRun(a, b, x0, cfg, sketch, frame, precond=precond).run()

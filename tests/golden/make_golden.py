@@ -296,8 +296,111 @@ def gen_serial():
     np.savez_compressed(os.path.join(HERE, "serial.npz"), **out)
 
 
+def _lap(n):
+    # pkg/tests/test_precond.py:39-41 (positive definite orientation)
+    return -(-2.0 * np.eye(n) + np.diag(np.ones(n - 1), 1) + np.diag(np.ones(n - 1), -1))
+
+
+def _spgmres_case(name, op, b, p, cfg, sketch, out, frame=None):
+    x, rep = rsolvers.tt_spgmres(op, p, b, None, cfg, sketch, frame)
+    cores_dict(name + "_op", op.op_cores, out)
+    cores_dict(name + "_b", b.cores, out)
+    for k, f in enumerate(sketch.factors):
+        out[f"{name}_F__{k}"] = f
+    out[name + "_alpha"] = p.alpha
+    out[name + "_beta"] = p.beta
+    out[name + "_spec"] = np.array([p.spec.rel_tol, -1 if p.spec.max_rank is None else p.spec.max_rank])
+    out[name + "_res"] = np.array(rep.res_sketched)
+    out[name + "_ranks"] = np.array(rep.basis_rank)
+    out[name + "_iters"] = np.array(rep.iterations)
+    out[name + "_conv"] = np.array(rep.converged)
+    out[name + "_x"] = rtt.tt_to_dense(x)
+    out[name + "_true_res"] = np.array(rsolvers.true_residual(op, b, x))
+    out[name + "_cfg"] = np.array([cfg.maxit, cfg.tol, cfg.ell, cfg.eta,
+                                   -1 if cfg.max_rank is None else cfg.max_rank,
+                                   cfg.sketch_rows, cfg.oversampling,
+                                   -1 if cfg.solution_rank is None else cfg.solution_rank, cfg.seed])
+    if frame is not None:
+        cores_dict(name + "_left", frame.left.cores, out)
+        cores_dict(name + "_right", frame.right.cores, out)
+
+
+def gen_precond():
+    """Exp-sum preconditioner (precond.py) on the cases of pkg/tests/test_precond.py
+    and the preconditioned solver cases of test_solvers.py:255-285."""
+    from ttkrylov import precond as rp
+    from ttkrylov.problems import cd_factor_matrices
+    out = {}
+    # exp-sum coefficients (test_precond.py:83-112 intervals)
+    cases = [(0.5, 60.0, 12), (0.2, 30.0, 9), (3.0, 3.0, 1), (0.1, 10.0, 2)]
+    out["coef_cases"] = np.array(cases)
+    for i, c in enumerate(cases):
+        a, b, bound = rp.expsum_coeffs(*c)
+        out[f"coef{i}_alpha"], out[f"coef{i}_beta"], out[f"coef{i}_bound"] = a, b, np.array(bound)
+    # spectral intervals (test_precond.py:115-133) + a nonsymmetric set
+    rng = np.random.default_rng(42)
+    sets = [[np.eye(4)] * 3, [np.diag([1.0, 2.0, 3.0])], [_lap(8)] * 3,
+            [rng.standard_normal((6, 6)) + 6 * np.eye(6) for _ in range(3)]]
+    for i, fs in enumerate(sets):
+        out[f"int{i}_n"] = np.array(len(fs))
+        for k, f in enumerate(fs):
+            out[f"int{i}_f{k}"] = f
+        out[f"int{i}_val"] = np.array(rp.spectral_interval(fs))
+    out["int_count"] = np.array(len(sets))
+    # mode_multiply with rectangular matrices (mode sizes change)
+    v = rtt.tt_random([3, 4, 5], [2, 3], seed=40)
+    mats = [rng.standard_normal((5, 3)), rng.standard_normal((4, 4)), rng.standard_normal((2, 5))]
+    w = rp.mode_multiply(v, mats)
+    cores_dict("mm_in", v.cores, out)
+    cores_dict("mm_out", w.cores, out)
+    for k, m in enumerate(mats):
+        out[f"mm_mat{k}"] = m
+    # approximate inverse, sequential accumulation (test_precond.py:145-156)
+    factors = [_lap(6) for _ in range(3)]
+    p = rp.ExpSumPreconditioner.from_kron_sum(factors, 24, rtt.RoundSpec(1e-12))
+    x = rtt.tt_random([6, 6, 6], [2, 2], seed=5)
+    x = rtt.tt_scale(x, 1.0 / rtt.tt_norm(x))
+    qx = rtt.tt_matvec(ttkrylov.kron_sum_operator(factors), x)
+    got = rp.precond_apply(p, qx)
+    cores_dict("inv_x", x.cores, out)
+    cores_dict("inv_qx", qx.cores, out)
+    out["inv_alpha"], out["inv_beta"], out["inv_bound"] = p.alpha, p.beta, np.array(p.quad_bound)
+    out["inv_out"] = rtt.tt_to_dense(got)
+    out["inv_ranks"] = np.array(got.ranks)
+    # sequential vs stream accumulation (test_precond.py:182-191)
+    factors = [_lap(5) for _ in range(3)]
+    spec = rtt.RoundSpec(1e-10, max_rank=12)
+    seq = rp.ExpSumPreconditioner.from_kron_sum(factors, 10, spec, accumulate="sequential")
+    st = rp.ExpSumPreconditioner(factors, seq.alpha, seq.beta, spec, accumulate="stream")
+    v = rtt.tt_random([5, 5, 5], [2, 2], seed=10)
+    cores_dict("acc_v", v.cores, out)
+    out["acc_alpha"], out["acc_beta"] = seq.alpha, seq.beta
+    out["acc_seq"] = rtt.tt_to_dense(rp.precond_apply(seq, v))
+    out["acc_stream"] = rtt.tt_to_dense(rp.precond_apply(st, v))
+    # preconditioned solver: identity preconditioner (test_solvers.py:256-266)
+    op, rhs = convection_diffusion(ConvectionDiffusionSpec(d=3, n=5))
+    pid = rp.ExpSumPreconditioner([np.zeros((5, 5))] * 3, [1.0], [0.0], rtt.RoundSpec(1e-14))
+    cfg = rsolvers.SolverConfig(maxit=60, tol=1e-6, ell=1, seed=31, solution_rank=10)
+    s = ttkrylov.kr_sketch_new(rhs.dims, cfg.sketch_rows, seed=32)
+    frame = rstreaming.StreamFrame.create(rhs.dims, [10, 10], seed=33)
+    _spgmres_case("sp_id", op, rhs, pid, cfg, s, out, frame=frame)
+    x_u, rep_u = rsolvers.tt_sgmres(op, rhs, None, cfg, s, frame)
+    out["sp_id_plain_res"] = np.array(rep_u.res_sketched)
+    # exp-sum preconditioned convection-diffusion (test_solvers.py:268-285)
+    spec = ConvectionDiffusionSpec(d=3, n=16)
+    op, rhs = convection_diffusion(spec)
+    fac = cd_factor_matrices(spec)
+    p = rp.ExpSumPreconditioner.from_kron_sum(fac, 17, rtt.RoundSpec(1e-9, max_rank=30))
+    cfg = rsolvers.SolverConfig(maxit=20, tol=1e-9, ell=1, eta=0.1, seed=34, max_rank=30, solution_rank=15)
+    s = ttkrylov.kr_sketch_new(rhs.dims, cfg.sketch_rows, seed=35)
+    for k, f in enumerate(fac):
+        out[f"sp_pde_fac{k}"] = f
+    _spgmres_case("sp_pde", op, rhs, p, cfg, s, out)
+    np.savez_compressed(os.path.join(HERE, "precond.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tt_ops", "sketch", "streaming", "solver_small", "solver_cfg1", "serial"]
+    which = sys.argv[1:] or ["tt_ops", "sketch", "streaming", "solver_small", "solver_cfg1", "serial", "precond"]
     for name in which:
         globals()["gen_" + name]()
     print("golden fixtures written to", HERE)
