@@ -647,6 +647,18 @@ __global__ void __launch_bounds__(kSvdThreads, 1)
 //   right(s) -> right(s+1)  (s <= np-2),  right(np-1) -> left(np-1)
 // which is exactly the p/q index rotation of jacobi_svd_kernel.
 
+// 1/sqrt(p) for normal positive p without the library's slow-path CALL (a
+// call inside the unrolled pivot loop forces the register-resident block
+// to local memory): hardware approximation plus two Newton steps (~1 ulp).
+__device__ __forceinline__ double rsqrt_nr(double p) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+  const double h = 0.5 * p;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
 constexpr int kJcCluster = 8;
 constexpr int kJcMaxSlots = 8;   // pair slots per CTA (le <= 128)
 constexpr int kJcThreads = kJcMaxSlots * kSvdGroup;
@@ -821,10 +833,18 @@ __global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads,
       if (active && a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
         // same angle as tan = sign(d) w / (|d| + rho), division-free:
         //   c = (|d| + rho) / sqrt(q), s = sign(d) w / sqrt(q), q = 2 rho (|d| + rho)
-        const double dd = b - a, w = 2.0 * g;
-        const double rho = sqrt(dd * dd + w * w);
+        // (CALL-free square roots: the library sqrt/rsqrt put a slow-path
+        // CALL and its reconvergence barrier on every round's critical path).
+        // c and s depend only on w/dd, so both are first scaled by the exact
+        // power of two 2^-e(a+b): q below then stays a normal number (< 8) for
+        // any column norms, as the flush-to-zero approximation requires.
+        const long long ex = min((__double_as_longlong(a + b) >> 52) & 0x7ff, 2045LL);
+        const double sc = __longlong_as_double((2046LL - ex) << 52);
+        const double dd = (b - a) * sc, w = 2.0 * g * sc;
+        const double q = dd * dd + w * w;
+        const double rho = q * rsqrt_nr(q);
         const double sum = fabs(dd) + rho;
-        const double rq = rsqrt(2.0 * rho * sum);
+        const double rq = rsqrt_nr(2.0 * rho * sum);
         const double c = sum * rq, s = (dd >= 0.0 ? w : -w) * rq;
 #pragma unroll
         for (int i = 0; i < RPL; ++i) {
@@ -1457,17 +1477,6 @@ __global__ void __launch_bounds__(1024, 1)
 // blocked triangular inversion.  Same status bits as chol_inv_kernel.
 constexpr int kCbThreads = 512;
 
-// 1/sqrt(p) for normal positive p without the library's slow-path CALL (a
-// call inside the unrolled pivot loop forces the register-resident block
-// to local memory): hardware approximation plus two Newton steps (~1 ulp).
-__device__ __forceinline__ double rsqrt_nr(double p) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
-  const double h = 0.5 * p;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
-}
 
 // one pivot of the in-register 16 x 16 diagonal-block Cholesky (lane c owns
 // column c); compile-time recursion keeps every index of d[] static
