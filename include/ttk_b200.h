@@ -70,6 +70,18 @@ size_t ttk_gemm_strided_ws_bytes(int batch, int M, int N, int K);
 int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
                const double* const* D, const double* const* C, double* const* G, void* stream);
 
+/* ---- structure-aware tt_matvec (reference tt.py:302-314) --
+ * Same result and output layout as ttk_matvec for square operator cores whose
+ * blocks D_k[al, :, :, be] have half-bandwidth <= w (w in 0..2: zero / scaled
+ * identity / tridiagonal / pentadiagonal blocks).  band[k] holds
+ * band_k[((al*rho[k+1]+be)*n[k] + i)*(2w+1) + t] = D_k[al, i, i+t-w, be] (zero
+ * outside the matrix).  kinds (host, optional): per core rho[k]*rho[k+1] bytes
+ * (concatenated over k), 0 = zero block, 1 = diagonal block (only t = w
+ * nonzero), 2 = banded; NULL treats every block as banded.  An HBM write
+ * stream instead of a DMMA contraction. */
+int ttk_matvec_banded(int d, const int* rho, const int* n, const int* r, int w, const double* const* band,
+                      const unsigned char* kinds, const double* const* C, double* const* G, void* stream);
+
 /* ---- mode_multiply (reference precond.py:189-200, exp-sum terms :266-273) --
  * For each of nterms matrix lists sharing one TT X (ranks r[0..d], mode sizes
  * n[k]): O_{t,k}[a, i, b] = s * sum_j M_{t,k}[i, j] * X_k[a, j, b], with

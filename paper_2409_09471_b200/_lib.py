@@ -36,6 +36,7 @@ SIGNATURES = {
                                  c_vp, c_size, c_vp]),
     "ttk_gemm_strided_ws_bytes": (c_size, [c_int, c_int, c_int, c_int]),
     "ttk_matvec": (c_int, [c_int, P_int, P_int, P_int, P_int, P_vp, P_vp, P_vp, c_vp]),
+    "ttk_matvec_banded": (c_int, [c_int, P_int, P_int, P_int, c_int, P_vp, ctypes.c_char_p, P_vp, P_vp, c_vp]),
     "ttk_mode_multiply": (c_int, [c_int, c_int, P_int, P_int, P_int, P_double, P_vp, P_vp, P_vp, c_vp]),
     "ttk_tt_concat": (c_int, [c_int, c_int, P_double, P_int, P_int, P_vp, P_vp, c_vp]),
     "ttk_scale": (c_int, [c_vp, c_vp, c_ll, c_double, c_vp]),

@@ -140,6 +140,42 @@ class TTOperator:
     def copy(self) -> "TTOperator":
         return TTOperator([c.clone() for c in self.op_cores])
 
+    def band_tables(self, max_w: int = 2):
+        """(w, [band_k], kinds) for the structure-aware matvec, or None when a
+        core is not square or some block is wider than half-bandwidth max_w.
+        Built on the device once and cached: the cores must not be modified
+        afterwards.  band_k[al, be, i, t] = D_k[al, i, i+t-w, be] (zero outside
+        the matrix); kinds: bytes, per core and block 0 zero / 1 diagonal /
+        2 banded."""
+        key = ("_bands", max_w)
+        if getattr(self, "_band_key", None) == key:
+            return self._bands
+        res = None
+        if all(c.shape[1] == c.shape[2] for c in self.op_cores):
+            w = 0
+            for c in self.op_cores:
+                idx = (c != 0).any(dim=3).any(dim=0).nonzero()
+                if idx.numel():
+                    w = max(w, int((idx[:, 0] - idx[:, 1]).abs().max()))
+            if w <= max_w:
+                bands, kinds = [], []
+                for c in self.op_cores:
+                    rho0, n, _, rho1 = c.shape
+                    off = torch.arange(-w, w + 1, device=c.device)
+                    j = torch.arange(n, device=c.device)[:, None] + off[None, :]
+                    valid = (j >= 0) & (j < n)
+                    g = c.permute(0, 3, 1, 2)  # (rho0, rho1, i, j)
+                    bt = torch.gather(g, 3, j.clamp(0, n - 1).expand(rho0, rho1, n, 2 * w + 1))
+                    bt = (bt * valid).contiguous()
+                    bands.append(bt)
+                    nz = bt != 0                                # (rho0, rho1, n, 2w+1)
+                    any_nz = nz.any(dim=3).any(dim=2)
+                    off_diag = torch.cat([nz[..., :w], nz[..., w + 1:]], dim=3).any(dim=3).any(dim=2)
+                    kinds.append((any_nz.to(torch.uint8) + off_diag.to(torch.uint8)).flatten().cpu())
+                res = (w, bands, bytes(torch.cat(kinds).tolist()))
+        self._band_key, self._bands = key, res
+        return res
+
     def numpy(self):
         return [c.detach().cpu().numpy() for c in self.op_cores]
 
@@ -258,10 +294,14 @@ def _check_cuda_vec(v: TTVector, what="TT vector"):
     _lib.require_cuda(v.cores[0], what)
 
 
-def tt_matvec(a: TTOperator, v: TTVector, out=None) -> TTVector:
+def tt_matvec(a: TTOperator, v: TTVector, out=None, structured: bool = False) -> TTVector:
     """Apply the operator core by core; output ranks multiply, no rounding (tt.py:302-314).
 
-    ``out``: optional preallocated output cores (reused across calls)."""
+    ``out``: optional preallocated output cores (reused across calls).
+    ``structured``: use the banded kernel (``ttk_matvec_banded``) when every
+    operator block has half-bandwidth <= 2 (identity / tridiagonal operators,
+    SURVEY 8(f) #3); same result up to summation order, otherwise the dense
+    DMMA contraction (the default, the path the north star measures)."""
     if a.col_dims != v.dims:
         raise ShapeMismatch(f"operator col_dims {a.col_dims} do not match {v.dims}")
     _check_cuda_vec(v)
@@ -275,6 +315,12 @@ def tt_matvec(a: TTOperator, v: TTVector, out=None) -> TTVector:
         out = [torch.empty(sh, dtype=torch.float64, device=dev) for sh in shapes]
     elif [tuple(c.shape) for c in out] != shapes:
         raise ShapeMismatch("preallocated matvec output has the wrong shapes")
+    bt = a.band_tables() if structured else None
+    if bt is not None:
+        _lib.check(lib.ttk_matvec_banded(d, _lib.int_array(rho), _lib.int_array(n), _lib.int_array(r), bt[0],
+                                          _lib.ptr_array(bt[1]), bt[2], _lib.ptr_array(v.cores),
+                                          _lib.ptr_array(out), _lib.stream_ptr(dev)))
+        return TTVector(out)
     _lib.check(lib.ttk_matvec(d, _lib.int_array(rho), _lib.int_array(m), _lib.int_array(n),
                               _lib.int_array(r), _lib.ptr_array(a.op_cores), _lib.ptr_array(v.cores),
                               _lib.ptr_array(out), _lib.stream_ptr(dev)))

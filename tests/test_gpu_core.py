@@ -65,6 +65,58 @@ def test_matvec_config3_cores(cuda):
     assert_cores_close(lib_out, want, 1e-13)
 
 
+def _banded_op(rng, d, n, rho, w, kinds):
+    """Operator cores whose blocks are zero / scaled identity / random band-w matrices."""
+    full = [1] + [rho] * (d - 1) + [1]
+    out = []
+    for k in range(d):
+        c = np.zeros((full[k], n, n, full[k + 1]))
+        for al in range(full[k]):
+            for be in range(full[k + 1]):
+                kind = kinds[(k + al + be) % len(kinds)]
+                if kind == "eye":
+                    c[al, :, :, be] = rng.standard_normal() * np.eye(n)
+                elif kind == "band":
+                    m = rng.standard_normal((n, n))
+                    c[al, :, :, be] = np.triu(np.tril(m, w), -w)
+        out.append(c)
+    return out
+
+
+@pytest.mark.parametrize("d,n,rho,r,w", [(5, 16, 3, 12, 1), (4, 33, 2, 40, 2), (6, 8, 1, 5, 0),
+                                         (3, 128, 3, 64, 1), (4, 7, 2, 9, 2)])
+def test_matvec_structured_vs_dense_and_oracle(cuda, d, n, rho, r, w):
+    """Banded-block operators: the structure-aware kernel equals
+    the dense DMMA path and the oracle; config-3's explicit operator is banded."""
+    rng = np.random.default_rng(d * 100 + n + w)
+    opc = _banded_op(rng, d, n, rho, w, ["eye", "band", "zero", "band"])
+    xc = O.gaussian_tt([n] * d, [r] * (d - 1), rng, 1.0 / np.sqrt(n * r))
+    a, x = T.TTOperator(opc, device=cuda), T.TTVector(xc, device=cuda)
+    bt = a.band_tables()
+    assert bt is not None and bt[0] <= w
+    ys = T.tt_matvec(a, x, structured=True)
+    assert_cores_close(to_np(ys), O.matvec(opc, xc), 1e-13)
+    assert_cores_close(to_np(ys), to_np(T.tt_matvec(a, x)), 1e-13)
+
+
+def test_matvec_structured_config3_operator_and_fallback(cuda):
+    from paper_2409_09471_b200 import configs
+    opc = configs.config3_operator(d=6, n=32, seed=0)
+    rng = np.random.default_rng(1)
+    xc = O.gaussian_tt([32] * 6, [10] * 5, rng, 0.1)
+    a, x = T.TTOperator(opc, device=cuda), T.TTVector(xc, device=cuda)
+    assert a.band_tables()[0] == 1
+    assert_cores_close(to_np(T.tt_matvec(a, x, structured=True)), O.matvec(opc, xc), 1e-13)
+    # a dense block: band_tables() is None and structured=True takes the DMMA path
+    opc[2][0, :, :, 1] = rng.standard_normal((32, 32))
+    a2 = T.TTOperator(opc, device=cuda)
+    assert a2.band_tables() is None
+    assert_cores_close(to_np(T.tt_matvec(a2, x, structured=True)), O.matvec(opc, xc), 1e-13)
+    # rectangular cores are never banded
+    a3 = T.TTOperator([np.ones((1, 3, 4, 1))], device=cuda)
+    assert a3.band_tables() is None
+
+
 def test_add_scale_combine_golden(cuda, ops):
     a = T.TTVector(cores(ops, "add_a"), device=cuda)
     b = T.TTVector(cores(ops, "add_b"), device=cuda)
