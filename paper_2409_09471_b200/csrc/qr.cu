@@ -993,6 +993,203 @@ __global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Single-CTA variant for small factorisations (le <= 64, rows <= 64): the same
+// register-resident pair slots, tournament and rotation as the cluster kernel,
+// but every move stays in this CTA's shared memory (double-buffered inbox, one
+// barrier per round).  The cluster kernel's DSMEM handoff + mbarrier wait sets
+// a ~0.85-1.1 us per-round floor whatever the size; here a round costs the
+// reduction/rotation chain plus one CTA barrier, and the shared-memory traffic
+// (every moved column, C and V) grows with l^2 -- which is what keeps large
+// factorisations on the cluster.
+
+constexpr int kJlMaxSlots = 32;
+
+template <int RPL>
+__global__ void __launch_bounds__(kJlMaxSlots * kSvdGroup, 1)
+    jacobi_local_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
+                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
+                        int scaled_u) {
+  extern __shared__ __align__(16) double sm[];  // [2 bufs][np][2 sides][2 (C,V)][RPL/2][16] double2
+  __shared__ double nrm[kQrMaxCols + 2];
+  __shared__ double fin[kQrMaxCols + 2];
+  __shared__ int order[kQrMaxCols + 2];
+  __shared__ int flags[64];  // per-sweep "rotated" flag (never reset)
+  __shared__ int inid[2][kJlMaxSlots][2];
+  const int le = l + (l & 1), kk = k, np = le / 2;
+  const int tid = threadIdx.x, si = tid / kSvdGroup, gl = tid % kSvdGroup;
+  const bool active = si < np;
+  constexpr int box = RPL * kSvdGroup;
+  for (int c = tid >> 5; c < l; c += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int r = tid & 31; r < kk; r += 32) {
+      const double x = B[(long long)r * b_rs + (long long)c * b_cs];
+      s += x * x;
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) nrm[c] = s;
+  }
+  for (int i = tid; i < 64; i += blockDim.x) flags[i] = 0;
+  __syncthreads();
+  for (int c = tid; c < l; c += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < l; ++j) rank += (nrm[j] > nrm[c]) || (nrm[j] == nrm[c] && j < c);
+    order[rank] = c;
+  }
+  __syncthreads();
+  int idl = active ? si : 0, idr = active ? le - 1 - si : 0;
+  double x[RPL], y[RPL], vx[RPL], vy[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = gl + i * kSvdGroup;
+    const bool okl = active && r < kk && idl < l, okr = active && r < kk && idr < l;
+    x[i] = okl ? B[(long long)r * b_rs + (long long)order[idl] * b_cs] : 0.0;
+    y[i] = okr ? B[(long long)r * b_rs + (long long)order[idr] * b_cs] : 0.0;
+    vx[i] = (want_v && active && idl < l && r == order[idl]) ? 1.0 : 0.0;
+    vy[i] = (want_v && active && idr < l && r == order[idr]) ? 1.0 : 0.0;
+  }
+  const double tol = (double)max(kk, 1) * 1.1102230246251565e-16;
+  const double tol2 = tol * tol;
+  auto part = [&](int buf, int slot, int side, int cv) {
+    return reinterpret_cast<double2*>(sm + ((((size_t)buf * np + slot) * 2 + side) * 2 + cv) * box) + gl;
+  };
+  // moves (position v -> v-1 of the round-robin, as in the cluster kernel):
+  //   left(s) -> left(s-1) (s >= 2), left(1) -> right(0), right(s) -> right(s+1) (s <= np-2),
+  //   right(np-1) -> left(np-1) (stays in the slot), left(0) fixed
+  const bool send_l = active && si >= 1, send_r = active && si <= np - 2;
+  const int l_slot = si - 1, l_side = (si == 1) ? 1 : 0, r_slot = si + 1;
+  int sweep = 0, round = 0;
+  for (; sweep < 60; ++sweep) {
+    for (int rnd = 0; rnd < le - 1; ++rnd, ++round) {
+      double a = 0.0, b = 0.0, g = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; i += 2) {
+        a += x[i] * x[i]; b += y[i] * y[i]; g += x[i] * y[i];
+        if (i + 1 < RPL) { a2 += x[i + 1] * x[i + 1]; b2 += y[i + 1] * y[i + 1]; g2 += x[i + 1] * y[i + 1]; }
+      }
+      a += a2; b += b2; g += g2;
+#pragma unroll
+      for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        g += __shfl_xor_sync(0xffffffffu, g, o);
+      }
+      if (active && a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
+        const long long ex = min((__double_as_longlong(a + b) >> 52) & 0x7ff, 2045LL);
+        const double sc = __longlong_as_double((2046LL - ex) << 52);
+        const double dd = (b - a) * sc, w = 2.0 * g * sc;
+        const double q = dd * dd + w * w;
+        const double rho = q * rsqrt_nr(q);
+        const double sum = fabs(dd) + rho;
+        const double rq = rsqrt_nr(2.0 * rho * sum);
+        const double c = sum * rq, s = (dd >= 0.0 ? w : -w) * rq;
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const double xi = x[i], yi = y[i];
+          x[i] = c * xi - s * yi;
+          y[i] = s * xi + c * yi;
+        }
+        if (want_v) {
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const double xi = vx[i], yi = vy[i];
+            vx[i] = c * xi - s * yi;
+            vy[i] = s * xi + c * yi;
+          }
+        }
+        if (gl == 0) flags[sweep] = 1;
+      }
+      if (np > 1) {
+        const int buf = round & 1;
+        if (send_l) {
+          double2* pc = part(buf, l_slot, l_side, 0);
+#pragma unroll
+          for (int j = 0; j < RPL / 2; ++j) pc[j * kSvdGroup] = make_double2(x[2 * j], x[2 * j + 1]);
+          if (want_v) {
+            double2* pv = part(buf, l_slot, l_side, 1);
+#pragma unroll
+            for (int j = 0; j < RPL / 2; ++j) pv[j * kSvdGroup] = make_double2(vx[2 * j], vx[2 * j + 1]);
+          }
+          if (gl == 0) inid[buf][l_slot][l_side] = idl;
+        }
+        if (send_r) {
+          double2* pc = part(buf, r_slot, 1, 0);
+#pragma unroll
+          for (int j = 0; j < RPL / 2; ++j) pc[j * kSvdGroup] = make_double2(y[2 * j], y[2 * j + 1]);
+          if (want_v) {
+            double2* pv = part(buf, r_slot, 1, 1);
+#pragma unroll
+            for (int j = 0; j < RPL / 2; ++j) pv[j * kSvdGroup] = make_double2(vy[2 * j], vy[2 * j + 1]);
+          }
+          if (gl == 0) inid[buf][r_slot][1] = idr;
+        }
+        __syncthreads();
+        if (active) {
+          if (si >= 1) {
+            if (si == np - 1) {
+#pragma unroll
+              for (int i = 0; i < RPL; ++i) { x[i] = y[i]; vx[i] = vy[i]; }
+              idl = idr;
+            } else {
+              const double2* pc = part(buf, si, 0, 0);
+#pragma unroll
+              for (int j = 0; j < RPL / 2; ++j) { const double2 v2 = pc[j * kSvdGroup]; x[2 * j] = v2.x; x[2 * j + 1] = v2.y; }
+              if (want_v) {
+                const double2* pv = part(buf, si, 0, 1);
+#pragma unroll
+                for (int j = 0; j < RPL / 2; ++j) { const double2 v2 = pv[j * kSvdGroup]; vx[2 * j] = v2.x; vx[2 * j + 1] = v2.y; }
+              }
+              idl = inid[buf][si][0];
+            }
+          }
+          const double2* pc = part(buf, si, 1, 0);
+#pragma unroll
+          for (int j = 0; j < RPL / 2; ++j) { const double2 v2 = pc[j * kSvdGroup]; y[2 * j] = v2.x; y[2 * j + 1] = v2.y; }
+          if (want_v) {
+            const double2* pv = part(buf, si, 1, 1);
+#pragma unroll
+            for (int j = 0; j < RPL / 2; ++j) { const double2 v2 = pv[j * kSvdGroup]; vy[2 * j] = v2.x; vy[2 * j + 1] = v2.y; }
+          }
+          idr = inid[buf][si][1];
+        }
+      }
+    }
+    __syncthreads();  // every rotation flag of this sweep is visible
+    if (!flags[sweep]) break;
+  }
+  if (tid == 0 && g_svd_sweeps) *g_svd_sweeps = sweep + 1;
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) { a += x[i] * x[i]; b += y[i] * y[i]; }
+#pragma unroll
+  for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  a = sqrt(a); b = sqrt(b);
+  if (active && gl == 0) { fin[idl] = a; fin[idr] = b; }
+  __syncthreads();
+  if (!active) return;
+  const int kout = min(kk, l);
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const int id = side ? idr : idl;
+    const double nv2 = side ? b : a;
+    int rank = 0;
+    for (int j = 0; j < le; ++j) rank += (fin[j] > nv2) || (fin[j] == nv2 && j < id);
+    if (id >= l || rank >= kout) continue;
+    if (gl == 0) S[rank] = nv2;
+    const double inv = (scaled_u || nv2 <= 0.0) ? 1.0 : 1.0 / nv2;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = gl + i * kSvdGroup;
+      const double cv = side ? y[i] : x[i];
+      if (r < kk) U[(size_t)r * kout + rank] = scaled_u ? cv : (nv2 > 0.0 ? cv * inv : 0.0);
+      if (want_v && V && r < l) V[(size_t)r * kout + rank] = side ? vy[i] : vx[i];
+    }
+  }
+}
+
 int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs, double* U, double* S,
                   double* V, bool scaled_u, cudaStream_t st) {
   if (k <= 0 || l <= 0) return kOk;
@@ -1000,6 +1197,30 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
               "jacobi_svd: %d x %d exceeds %d", k, l, kQrMaxCols);
   const int le = l + (l & 1);
   static const bool single_cta = getenv("TTK_JACOBI_SINGLE") != nullptr;  // A/B switch
+  // largest (even) width for the single-CTA register kernel (tools/jac_ab.py, r01: local vs
+  // cluster 27 vs 54 us at 7x7, 77 vs 148 at 20, 205 vs 228 at 33, 435 vs 369 at 50 -- beyond
+  // ~40 its shared-memory traffic costs more than the cluster's handoff); env var: A/B
+  static const int local_max = getenv("TTK_JACOBI_LOCAL_MAX") ? atoi(getenv("TTK_JACOBI_LOCAL_MAX")) : 40;
+  if (!single_cta && le <= std::min(local_max, 2 * kJlMaxSlots) && std::max(k, le) <= 4 * kSvdGroup) {
+    static bool lattr = false;
+    if (!lattr) {
+      TTK_TRY(qr_set_smem((const void*)jacobi_local_kernel<2>, 128 * 1024));
+      TTK_TRY(qr_set_smem((const void*)jacobi_local_kernel<4>, 128 * 1024));
+      lattr = true;
+    }
+    const int np = le / 2;
+    const int threads = std::max(32, (np * kSvdGroup + 31) / 32 * 32);
+    const int want = V != nullptr;
+    if (std::max(k, le) <= 2 * kSvdGroup) {
+      const size_t jsm = sizeof(double) * 2 * np * 4 * 2 * kSvdGroup;
+      jacobi_local_kernel<2><<<1, threads, jsm, st>>>(k, l, B, b_rs, b_cs, U, S, V, want, scaled_u);
+    } else {
+      const size_t jsm = sizeof(double) * 2 * np * 4 * 4 * kSvdGroup;
+      jacobi_local_kernel<4><<<1, threads, jsm, st>>>(k, l, B, b_rs, b_cs, U, S, V, want, scaled_u);
+    }
+    TTK_CHECK_LAUNCH();
+    return kOk;
+  }
   if (!single_cta && le <= 2 * kJcCluster * kJcMaxSlots && k <= 8 * kSvdGroup) {
     static bool cattr = false;
     if (!cattr) {
