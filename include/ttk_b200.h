@@ -127,6 +127,14 @@ int ttk_kr_sketch(int d, const int* n, int s_lo, int s_hi, const double* const* 
                   const int* ranks, const double* const* cores, double* out, void* ws,
                   size_t ws_bytes, void* stream);
 size_t ttk_kr_sketch_ws_bytes(int d, const int* n, int s_lo, int s_hi, int nvec, const int* ranks);
+/* fused matvec -> sketch: out[j] = KR row j . vec(A x), A x
+ * never materialised.  Ft[k]: the operator-premultiplied factors
+ * Ft_k[j, al, i', be] = sum_i F_k[j, i] D_k[al, i, i', be]  (S x rho[k] x n[k] x
+ * rho[k+1], row-major; built once per (sketch, operator) pair, e.g. with
+ * ttk_gemm_strided); C: d cores of x with ranks r; out: S values. */
+int ttk_kr_sketch_matvec(int d, const int* n, int S, const double* const* Ft, const int* rho, const int* r,
+                         const double* const* C, double* out, void* ws, size_t ws_bytes, void* stream);
+size_t ttk_kr_sketch_matvec_ws_bytes(int d, int S, const int* rho, const int* r);
 /* same, forcing the fused (path 0) or two-phase (path 1) kernel; for tests */
 int ttk_kr_sketch_path(int path, int d, const int* n, int s_lo, int s_hi, const double* const* F,
                        int nvec, const int* ranks, const double* const* cores, double* out,

@@ -47,6 +47,8 @@ SIGNATURES = {
                               c_size, c_vp]),
     "ttk_kr_sketch_path": (c_int, [c_int, c_int, P_int, c_int, c_int, P_vp, c_int, P_int, P_vp, c_vp,
                                    c_vp, c_size, c_vp]),
+    "ttk_kr_sketch_matvec": (c_int, [c_int, P_int, c_int, P_vp, P_int, P_int, P_vp, c_vp, c_vp, c_size, c_vp]),
+    "ttk_kr_sketch_matvec_ws_bytes": (c_size, [c_int, c_int, P_int, P_int]),
     "ttk_kr_sketch_ws_bytes": (c_size, [c_int, P_int, c_int, c_int, c_int, P_int]),
 }
 

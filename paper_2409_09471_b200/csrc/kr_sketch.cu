@@ -391,6 +391,78 @@ int ttk_kr_sketch(int d, const int* n, int s_lo, int s_hi, const double* const* 
   return kr_two_phase(d, n, S, Fo.data(), nvec, ranks, cores, out, ws, ws_bytes, st);
 }
 
+// Fused matvec -> sketch: out[j] = (row j of the Khatri-Rao
+// product) . vec(A x) without materialising A x.  With the operator-premultiplied
+// factors Ft_k[j, al, i', be] = sum_i F_k[j, i] D_k[al, i, i', be] (S x rho_k x
+// n_k x rho_{k+1}, computed once per (sketch, operator) pair by the caller), phase
+// 1 forms M_k[j, (a*rho+al), (b*rho'+be)] = sum_i' Ft_k[j, al, i', be] C_k[a, i', b]
+// -- one grouped-GEMM problem per (core, al, be) writing straight into the merged
+// rank order of tt_matvec's output -- and phase 2 is the same per-row chain as the
+// two-phase sketch over ranks r_k * rho_k.  Same flops as sketching A x, minus
+// the write and re-read of A x.
+size_t ttk_kr_sketch_matvec_ws_bytes(int d, int S, const int* rho, const int* r) {
+  if (S <= 0 || d <= 0) return 0;
+  size_t tot = 0;
+  for (int k = 0; k < d; ++k) tot += (size_t)S * r[k] * rho[k] * r[k + 1] * rho[k + 1];
+  return tot * sizeof(double) + 4096;
+}
+
+int ttk_kr_sketch_matvec(int d, const int* n, int S, const double* const* Ft, const int* rho, const int* r,
+                         const double* const* C, double* out, void* ws, size_t ws_bytes, void* stream) {
+  TTK_REQUIRE(d >= 1 && d <= kKrMaxModes, kInvalidValue, "kr_sketch_matvec: d=%d out of range", d);
+  TTK_REQUIRE(S >= 0, kInvalidValue, "kr_sketch_matvec: negative row count");
+  TTK_REQUIRE(r[0] == 1 && r[d] == 1 && rho[0] == 1 && rho[d] == 1, kShapeMismatch,
+              "kr_sketch_matvec: boundary ranks must equal 1");
+  if (S == 0) return kOk;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int> R(d + 1);
+  for (int k = 0; k <= d; ++k) R[k] = r[k] * rho[k];
+  size_t melems = 0;
+  for (int k = 0; k < d; ++k) melems += (size_t)S * R[k] * R[k + 1];
+  Arena ar(ws, ws_bytes);
+  double* M = ar.take<double>(melems);
+  TTK_REQUIRE(M != nullptr, kWorkspace, "kr_sketch_matvec: workspace too small (%zu bytes needed)", ar.used);
+  std::vector<GemmProblem> probs;
+  std::vector<long long> moff(d);
+  long long off = 0;
+  int rmax = 1;
+  for (int k = 0; k < d; ++k) {
+    const int r0 = r[k], r1 = r[k + 1], p0 = rho[k], p1 = rho[k + 1], nk = n[k];
+    moff[k] = off;
+    rmax = std::max(rmax, std::max(R[k], R[k + 1]));
+    if (r0 > 0 && r1 > 0)
+      for (int al = 0; al < p0; ++al)
+        for (int be = 0; be < p1; ++be) {
+          GemmProblem p{};
+          p.M = S; p.N = r0 * r1; p.K = nk;
+          p.A = Ft[k] + (long long)al * nk * p1 + be;  // A(j, i') = Ft[j, al, i', be]
+          p.a_ms0 = (long long)p0 * nk * p1; p.a_ms1 = 0; p.a_mdiv = 1 << 30; p.a_ks = p1;
+          p.B = C[k];  // B(i', (a, b)) = C[a, i', b]
+          p.b_ndiv = r1; p.b_ns1 = (long long)nk * r1; p.b_ns0 = 1; p.b_ks = r1;
+          p.C = M + off + (long long)al * R[k + 1] + be;  // M_k[j, a*p0+al, b*p1+be]
+          p.c_mdiv = 1 << 30; p.c_ms0 = (long long)R[k] * R[k + 1]; p.c_ms1 = 0;
+          p.c_ndiv = r1; p.c_ns0 = p1; p.c_ns1 = (long long)p0 * R[k + 1];
+          p.alpha = 1.0; p.beta = 0.0; p.splits = 1;
+          probs.push_back(p);
+        }
+    off += (long long)S * R[k] * R[k + 1];
+  }
+  TTK_REQUIRE(d <= kKrMaxSlots, kInvalidValue, "kr_sketch_matvec: d too large");
+  TTK_TRY(gemm_group_launch(probs.data(), (int)probs.size(), nullptr, 0, st, false));
+  static thread_local KrChainParams CP;
+  CP.d = d; CP.S = S; CP.nvec = 1; CP.rmax = rmax; CP.M = M; CP.out = out;
+  for (int k = 0; k < d; ++k) CP.moff[k] = moff[k];
+  for (int k = 0; k <= d; ++k) CP.rank[k] = (short)R[k];
+  const int rows_per_cta = 4;
+  dim3 grid(ceil_div(S, rows_per_cta), 1);
+  const size_t smem = sizeof(double) * 2 * rmax * rows_per_cta;
+  if (smem > 48 * 1024)
+    TTK_CHECK_CUDA(cudaFuncSetAttribute(kr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kr_chain_kernel<<<grid, 32 * rows_per_cta, smem, st>>>(CP);
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
 // Force a path (testing): path 0 = fused, 1 = two-phase.
 int ttk_kr_sketch_path(int path, int d, const int* n, int s_lo, int s_hi, const double* const* F,
                        int nvec, const int* ranks, const double* const* cores, double* out,

@@ -7,7 +7,7 @@ import torch
 
 from . import _lib
 from .errors import ShapeMismatch
-from .tt import TTVector, default_device
+from .tt import TTOperator, TTVector, default_device
 
 
 class KhatriRaoSketch:
@@ -87,3 +87,52 @@ def kr_apply(s: KhatriRaoSketch, v: TTVector) -> np.ndarray:
     if s.dims != v.dims:
         raise ShapeMismatch(f"sketch dims {s.dims} do not match vector {v.dims}")
     return kr_apply_device(s, v).cpu().numpy()
+
+
+def _premultiplied_factors(s: KhatriRaoSketch, a: TTOperator):
+    """Ft_k[j, al, i', be] = sum_i F_k[j, i] D_k[al, i, i', be] for every core (one
+    batched DMMA GEMM per core); cached on the sketch for the last operator used."""
+    hit = getattr(s, "_ft_cache", None)
+    if hit is not None and hit[0] is a:
+        return hit[1]
+    lib = _lib.load()
+    dev = s.factors[0].device
+    fts = []
+    for F, D in zip(s.factors, a.op_cores):
+        p0, m, n, p1 = (int(x) for x in D.shape)
+        S = s.rows
+        ft = torch.empty((S, p0, n, p1), dtype=torch.float64, device=dev)
+        ws = _lib.workspace(max(int(lib.ttk_gemm_strided_ws_bytes(p0, S, n * p1, m)), 8), dev)
+        _lib.check(lib.ttk_gemm_strided(p0, S, n * p1, m, 1.0, F.data_ptr(), m, 1, 0, D.data_ptr(), n * p1, 1,
+                                        m * n * p1, 0.0, ft.data_ptr(), p0 * n * p1, 1, n * p1,
+                                        ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)))
+        fts.append(ft)
+    s._ft_cache = (a, fts)
+    return fts
+
+
+def kr_apply_matvec_device(s: KhatriRaoSketch, a: TTOperator, v: TTVector) -> torch.Tensor:
+    """Sketch of A v as a length-s device vector, without materialising A v
+    (SURVEY 8(f) #3): equal to kr_apply_device(s, tt_matvec(a, v)) up to rounding."""
+    if a.col_dims != v.dims:
+        raise ShapeMismatch(f"operator col_dims {a.col_dims} do not match {v.dims}")
+    if s.dims != a.row_dims:
+        raise ShapeMismatch(f"sketch dims {s.dims} do not match operator row_dims {a.row_dims}")
+    _lib.require_cuda(v.cores[0], "TT vector")
+    lib = _lib.load()
+    dev = s.factors[0].device
+    fts = _premultiplied_factors(s, a)
+    d = v.d
+    rho, r = list(a.ranks), list(v.ranks)
+    out = torch.empty(s.rows, dtype=torch.float64, device=dev)
+    ws = _lib.workspace(int(lib.ttk_kr_sketch_matvec_ws_bytes(d, s.rows, _lib.int_array(rho), _lib.int_array(r))),
+                        dev)
+    _lib.check(lib.ttk_kr_sketch_matvec(d, _lib.int_array(list(v.dims)), s.rows, _lib.ptr_array(fts),
+                                        _lib.int_array(rho), _lib.int_array(r), _lib.ptr_array(v.cores),
+                                        out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)))
+    return out
+
+
+def kr_apply_matvec(s: KhatriRaoSketch, a: TTOperator, v: TTVector) -> np.ndarray:
+    """kr_apply(s, tt_matvec(a, v)) as a host vector, A v never materialised."""
+    return kr_apply_matvec_device(s, a, v).cpu().numpy()

@@ -117,6 +117,31 @@ def test_matvec_structured_config3_operator_and_fallback(cuda):
     assert a3.band_tables() is None
 
 
+@pytest.mark.parametrize("d,n,m,rho,r,S", [(4, 16, 12, 2, 5, 40), (5, 32, 32, 3, 20, 120), (3, 7, 9, 1, 3, 11),
+                                            (6, 64, 64, 2, 40, 80)])
+def test_kr_apply_matvec_fused_vs_unfused(cuda, d, n, m, rho, r, S):
+    """Fused matvec -> sketch equals sketching the materialised
+    matvec output, and the oracle's sketch of the oracle matvec."""
+    rng = np.random.default_rng(d * 31 + n + S)
+    full = [1] + [rho] * (d - 1) + [1]
+    opc = [rng.standard_normal((full[k], m, n, full[k + 1])) for k in range(d)]
+    xc = O.gaussian_tt([n] * d, [r] * (d - 1), rng, 1.0 / np.sqrt(n * r))
+    fs = [rng.standard_normal((S, m)) / np.sqrt(m) for _ in range(d)]
+    a, x = T.TTOperator(opc, device=cuda), T.TTVector(xc, device=cuda)
+    sk = T.KhatriRaoSketch(fs, device=cuda)
+    got = T.kr_apply_matvec(sk, a, x)
+    want = T.kr_apply(sk, T.tt_matvec(a, x))
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() <= 1e-12 * scale
+    assert np.abs(got - O.kr_apply(fs, O.matvec(opc, xc))).max() <= 1e-12 * scale
+    # the cached premultiplied factors are reused for a second vector
+    x2 = T.TTVector(O.gaussian_tt([n] * d, [r] * (d - 1), rng, 1.0), device=cuda)
+    w2 = T.kr_apply(sk, T.tt_matvec(a, x2))
+    assert np.abs(T.kr_apply_matvec(sk, a, x2) - w2).max() <= 1e-12 * np.abs(w2).max()
+    with pytest.raises(T.ShapeMismatch):
+        T.kr_apply_matvec(T.KhatriRaoSketch([f[:, :5] for f in fs], device=cuda), a, x)
+
+
 def test_add_scale_combine_golden(cuda, ops):
     a = T.TTVector(cores(ops, "add_a"), device=cuda)
     b = T.TTVector(cores(ops, "add_b"), device=cuda)

@@ -54,6 +54,19 @@ if "matvec_banded" in which:
     res["matvec_banded_cfg3"] = {"w": w, "structured_ms": best_s, "structured_med_ms": med_s, "dense_ms": best_d,
                                  "dense_med_ms": med_d, "alg_bytes": alg, "gbs": alg / best_s / 1e6,
                                  "frac_hbm_6627": alg / best_s / 1e6 / 6627.0, "max_rel_diff_vs_dense": err}
+if "kr_matvec" in which:
+    # fused matvec -> sketch vs tt_matvec + kr_apply at config-5 scale (d=50, n=256, rho=2, r=100, s=120)
+    from paper_2409_09471_b200 import configs
+    C5 = configs.config5(0)
+    op = T.TTOperator(C5["op"], device=dev)
+    d, n = 50, 256
+    x = T.tt_random([n] * d, [100] * (d - 1), seed=3, device=dev)
+    sk = T.kr_sketch_new([n] * d, 120, seed=0, device=dev)
+    a1 = T.kr_apply_matvec_device(sk, op, x); a2 = T.kr_apply_device(sk, T.tt_matvec(op, x))
+    rel = float((a1 - a2).abs().max() / a2.abs().max())
+    bf, mf = timeit(lambda: [T.kr_apply_matvec_device(sk, op, x) for _ in range(5)], reps=5, warm=1)
+    bu, mu = timeit(lambda: [T.kr_apply_device(sk, T.tt_matvec(op, x)) for _ in range(5)], reps=5, warm=1)
+    res["kr_matvec_cfg5"] = {"fused_ms": bf / 5, "unfused_ms": bu / 5, "rel_diff": rel}
 if "kr" in which:
     d, n, r, s, B = 20, 64, 100, 512, 64
     rng = np.random.default_rng(0)
