@@ -1645,7 +1645,7 @@ __device__ __forceinline__ int near_id_ld(int l) { return ((l + 15) & ~15) + 4; 
 
 __global__ void __launch_bounds__(1024, 1)
     chol_near_identity_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
-                              double* __restrict__ Rinv, int* flag, double tol) {
+                              double* __restrict__ Rinv, int* flag, double tol, double first_order_max) {
   extern __shared__ double sm[];
   const int ld = near_id_ld(l);
   double* F = sm;
@@ -1667,6 +1667,19 @@ __global__ void __launch_bounds__(1024, 1)
   for (int i = 0; i < (nt >> 5); ++i) emax = fmax(emax, red[i]);
   if (!(emax <= tol)) {
     if (tid == 0) *flag = 0;
+    return;
+  }
+  if ((double)l * emax * emax <= first_order_max) {
+    // every second-order term (entries of F1^T F1, F1^2) is below l |E|^2 <= 1e-17:
+    // R = I + F1 and R^{-1} = I - F1 are exact to below an ulp of 1 (the usual
+    // case: a well-conditioned block leaves |E| ~ 1e-12 after the first pass)
+    for (int idx = tid; idx < l * l; idx += nt) {
+      const int i = idx / l, c = idx - i * l;
+      const double f = F[i * ld + c];
+      Rout[idx] = (c > i) ? f : (c == i ? 1.0 + f : 0.0);
+      Rinv[idx] = (c > i) ? -f : (c == i ? 1.0 - f : 0.0);
+    }
+    if (tid == 0) *flag = 1;
     return;
   }
   block_dmma_tri(l, 0, F, 1, ld, F, ld, 1, P, ld);  // P = F1^T F1 (upper tiles, k <= min(i, j))
@@ -1855,7 +1868,9 @@ int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status
   const int* skip = nullptr;
   if (near_id_flag && shift_rel == 0.0 && l <= kNearIdMax) {
     const size_t smem_n = sizeof(double) * 2 * (size_t)l * (((l + 15) & ~15) + 4);
-    chol_near_identity_kernel<<<1, 1024, smem_n, st>>>(l, G, R, Rinv, near_id_flag, 1e-7);
+    // first-order shortcut when l |E|^2 <= 1e-17; TTK_NEAR_ID_FIRST_ORDER=0 disables it (A/B)
+    static const double fo = getenv("TTK_NEAR_ID_FIRST_ORDER") ? atof(getenv("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
+    chol_near_identity_kernel<<<1, 1024, smem_n, st>>>(l, G, R, Rinv, near_id_flag, 1e-7, fo);
     TTK_CHECK_LAUNCH();
     skip = near_id_flag;
   }
@@ -2218,8 +2233,11 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, 0.0, 1e-15));
     TTK_TRY(trsm_right_upper(m, l, Y, y_rs, y_cs, R1, Q1, l, 1, st));  // Q1 = Y / R1 (backward stable)
     TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
-    TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    TTK_SYNC(st);
+    static const bool assume_fast = getenv("TTK_QR_ASSUME_FAST") != nullptr;  // diagnostics: cost of this sync
+    if (!assume_fast) {
+      TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      TTK_SYNC(st);
+    }
     if (hs[0] == 0 && hs[1] == 0) {
       p = make_gemm(m, l, l, Q1, l, 1, I2, l, 1, Q, q_rs, q_cs);
       TTK_TRY(gemm_group_launch(&p, 1, split, split_bytes, st));

@@ -359,17 +359,18 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
 
 // --------------------------------------------------------------------------
 size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L) {
-  size_t wsum = 0, tmax = 0, ymax = 0, zmax = 0, qr = 0;
+  size_t wsum = 0, tsum = 0, ymax = 0, zmax = 0, mmax = 0, qr = 0;
   for (int c = 1; c < d; ++c) wsum += align_up((size_t)R[c] * L[c] * 8, 256);
+  for (int c = 1; c + 1 < d; ++c) tsum += align_up((size_t)R[c] * dims[c] * L[c + 1] * 8, 256);
   for (int c = 1; c < d; ++c) {
-    tmax = std::max(tmax, (size_t)R[c] * dims[c] * L[c + 1]);
     size_t m = (size_t)L[c - 1] * dims[c - 1];
     ymax = std::max(ymax, m * L[c]);
-    zmax = std::max(zmax, (size_t)L[c] * dims[c] * R[c + 1]);
+    zmax = std::max(zmax, (size_t)L[c - 1] * dims[c - 1] * R[c]);
+    mmax = std::max(mmax, (size_t)L[c] * R[c]);
     qr = std::max(qr, qr_auto_ws_bytes((int)m, L[c]));
   }
-  return wsum + align_up(tmax * 8, 256) + align_up(ymax * 8, 256) + 2 * align_up(zmax * 8, 256) +
-         align_up(qr, 256) + kSplitKBytes + 65536;
+  return wsum + tsum + align_up(ymax * 8, 256) + 2 * align_up(zmax * 8, 256) + 2 * align_up(mmax * 8, 256) +
+         align_up(qr, 256) + 2 * kSplitKBytes + 65536;
 }
 
 // Randomize-then-orthogonalize sweeps.  X: d cores (R[k], n_k, R[k+1]); G: DRM
@@ -394,25 +395,28 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
   const size_t need = ttk_rto_ws_bytes(d, dims, R, L);
   TTK_REQUIRE(ws != nullptr && ws_bytes >= need, kWorkspace, "rto: workspace %zu < %zu", ws_bytes, need);
   Arena ar(ws, ws_bytes);
-  std::vector<double*> W(d + 1, nullptr);
+  std::vector<double*> W(d + 1, nullptr), Tk(d + 1, nullptr);
   for (int c = 1; c < d; ++c) W[c] = ar.take<double>((size_t)R[c] * L[c]);
-  size_t tmax = 0, ymax = 0, zmax = 0, qrb = 0;
+  // T_c = X_c W_{c+1} of the right sweep is kept: the left sweep's sketch of the
+  // next projected core is Y_{c+1} = M_c T_c (see below)
+  for (int c = 1; c + 1 < d; ++c) Tk[c] = ar.take<double>((size_t)R[c] * dims[c] * L[c + 1]);
+  size_t ymax = 0, zmax = 0, mmax = 0, qrb = 0;
   for (int c = 1; c < d; ++c) {
-    tmax = std::max(tmax, (size_t)R[c] * dims[c] * L[c + 1]);
     size_t m = (size_t)L[c - 1] * dims[c - 1];
     ymax = std::max(ymax, m * L[c]);
-    zmax = std::max(zmax, (size_t)L[c] * dims[c] * R[c + 1]);
+    zmax = std::max(zmax, (size_t)L[c - 1] * dims[c - 1] * R[c]);
+    mmax = std::max(mmax, (size_t)L[c] * R[c]);
     qrb = std::max(qrb, qr_auto_ws_bytes((int)m, L[c]));
   }
-  double* T = ar.take<double>(tmax);
   double* Y = ar.take<double>(ymax);
-  double* Z0 = ar.take<double>(zmax);
-  double* Z1 = ar.take<double>(zmax);
+  double* Zbuf[2] = {ar.take<double>(zmax), ar.take<double>(zmax)};
+  double* Mbuf[2] = {ar.take<double>(mmax), ar.take<double>(mmax)};
   size_t qoff = align_up(ar.used, 256);
   void* qws = (char*)ws + qoff;
   ar.used = qoff + qrb;
   void* split_ws = ar.take<char>(kSplitKBytes);
-  TTK_REQUIRE(split_ws != nullptr, kWorkspace, "rto: workspace too small");
+  void* split_side = ar.take<char>(kSplitKBytes);
+  TTK_REQUIRE(split_side != nullptr, kWorkspace, "rto: workspace too small");
 
   // ---- right sweep: W_c = sum_i X_c[:, i, :] W_{c+1} G_c[:, i, :]^T ----
   for (int c = d - 1; c >= 1; --c) {
@@ -421,33 +425,65 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
     if (c == d - 1) {
       Tin = X[c];  // (R_c, n, 1): W_d = [[1]]
     } else {
-      // T (R_c n x L_{c+1}) = X_c (R_c n x R_{c+1}) W_{c+1} (R_{c+1} x L_{c+1})
-      TTK_TRY(gemm1(rc * n, l1, r1, X[c], r1, 1, W[c + 1], l1, 1, T, l1, 1, split_ws, st));
-      Tin = T;
+      // T_c (R_c n x L_{c+1}) = X_c (R_c n x R_{c+1}) W_{c+1} (R_{c+1} x L_{c+1})
+      TTK_TRY(gemm1(rc * n, l1, r1, X[c], r1, 1, W[c + 1], l1, 1, Tk[c], l1, 1, split_ws, st));
+      Tin = Tk[c];
     }
     // W_c (R_c x L_c) = T (R_c x n L_{c+1}) G_c^T ; G_c viewed (L_c x n L_{c+1})
     const long long K = (long long)n * l1;
     TTK_TRY(gemm1(rc, lc, (int)K, Tin, K, 1, G[c], 1, K, W[c], lc, 1, split_ws, st));
   }
   // ---- left sweep ----
-  const double* Z = X[0];  // (L_0 n_0 x R_1) = (n_0 x R_1)
-  double* Zbuf[2] = {Z0, Z1};
+  // Step c orthogonalises the sketch Y_c of the projected core Z_{c-1}
+  // (L_{c-1} n_{c-1} x R_c), then M_c = Q_c^T Z_{c-1}.  Since Z_c = M_c X_c,
+  // the next sketch is Y_{c+1} = Z_c W_{c+1} = M_c T_c: only the small M_c is on
+  // the critical path; Z_c itself (needed for M_{c+1}) is formed on a side
+  // stream while Y_{c+1} is orthogonalised.
+  // (running the orthogonalisation on a high-priority stream was measured to
+  // make no difference: the step is bound by the QR chain's own latency)
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev_m = nullptr, ev_z = nullptr;
+  if (side == nullptr) {
+    TTK_CHECK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_m, cudaEventDisableTiming));
+    TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_z, cudaEventDisableTiming));
+  }
   int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
+  const double* Mprev = nullptr;
   for (int c = 1; c < d; ++c) {
     const int np = dims[c - 1];
     const int m = L[c - 1] * np, l = L[c], rc = R[c];
-    // Y (m x l) = Z (m x R_c) W_c (R_c x l)
-    TTK_TRY(gemm1(m, l, rc, Z, rc, 1, W[c], l, 1, Y, l, 1, split_ws, st));
+    const double* Z;
+    if (c == 1) {
+      Z = X[0];  // (n_0 x R_1)
+      // Y (m x l) = X_0 W_1
+      TTK_TRY(gemm1(m, l, rc, Z, rc, 1, W[c], l, 1, Y, l, 1, split_ws, st));
+    } else {
+      const int lp = L[c - 1], rp = R[c - 1];
+      // side: Z_{c-1} (L_{c-1} x n_{c-1} R_c) = M_{c-1} X_{c-1}
+      double* zdst = Zbuf[c & 1];
+      TTK_CHECK_CUDA(cudaEventRecord(ev_m, st));
+      TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_m, 0));
+      TTK_TRY(gemm1(lp, np * rc, rp, Mprev, rp, 1, X[c - 1], (long long)np * rc, 1, zdst, (long long)np * rc, 1,
+                    split_side, side));
+      TTK_CHECK_CUDA(cudaEventRecord(ev_z, side));
+      // main: Y (L_{c-1} x n_{c-1} L_c) = M_{c-1} (L_{c-1} x R_{c-1}) T_{c-1} (R_{c-1} x n_{c-1} L_c)
+      TTK_TRY(gemm1(lp, np * l, rp, Mprev, rp, 1, Tk[c - 1], (long long)np * l, 1, Y, (long long)np * l, 1,
+                    split_ws, st));
+      Z = zdst;
+    }
     // Q (m x l) -> out core c-1, (L_{c-1}, n_{c-1}, L_c)
     TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st, &qr_hint));
-    // M (l x R_c) = Q^T Z   (K = m, split over the long dimension)
-    TTK_TRY(gemm1(l, rc, m, out[c - 1], 1, l, Z, rc, 1, Y, rc, 1, split_ws, st));
-    // Z' (l x n_c R_{c+1}) = M X_c
-    const int n = dims[c], r1 = R[c + 1];
-    double* dst = (c == d - 1) ? out[d - 1] : Zbuf[c & 1];
-    TTK_TRY(gemm1(l, n * r1, rc, Y, rc, 1, X[c], (long long)n * r1, 1, dst, (long long)n * r1, 1,
-                  split_ws, st));
-    Z = dst;
+    if (c > 1) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_z, 0));
+    // M_c (l x R_c) = Q^T Z   (K = m, split over the long dimension)
+    double* Mc = Mbuf[c & 1];
+    TTK_TRY(gemm1(l, rc, m, out[c - 1], 1, l, Z, rc, 1, Mc, rc, 1, split_ws, st));
+    Mprev = Mc;
+  }
+  // last core: (L_{d-1} x n_{d-1}) = M_{d-1} X_{d-1}
+  {
+    const int c = d - 1, l = L[c], rc = R[c], n = dims[c];
+    TTK_TRY(gemm1(l, n, rc, Mprev, rc, 1, X[c], n, 1, out[d - 1], n, 1, split_ws, st));
   }
   return kOk;
 }
