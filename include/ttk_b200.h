@@ -164,6 +164,8 @@ int ttk_debug_jacobi_profile(long long* dev_acc);
 /* diagnostics: the blocked Cholesky adds per-call phase clocks (load, diagonal
  * blocks, panels, trailing updates, epilogue, call count) into dev_acc[6] (NULL: off) */
 int ttk_debug_chol_profile(long long* dev_acc);
+/* diagnostics: phase timestamps (%globaltimer, ns) of the fused CholeskyQR2 kernel into dev_ts[16]; NULL = off */
+int ttk_debug_fused_qr_profile(long long* dev_ts);
 /* diagnostics: host synchronisation points (rank / path decisions) so far:
  * out[0] = count, out[1] = total wait in ns (timed only when TTK_HOST_PROF is set) */
 int ttk_debug_host_profile(long long* out);

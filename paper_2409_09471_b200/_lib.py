@@ -49,6 +49,7 @@ SIGNATURES = {
                                    c_vp, c_size, c_vp]),
     "ttk_kr_sketch_matvec": (c_int, [c_int, P_int, c_int, P_vp, P_int, P_int, P_vp, c_vp, c_vp, c_size, c_vp]),
     "ttk_kr_sketch_matvec_ws_bytes": (c_size, [c_int, c_int, P_int, P_int]),
+    "ttk_debug_fused_qr_profile": (c_int, [c_vp]),
     "ttk_kr_sketch_ws_bytes": (c_size, [c_int, P_int, c_int, c_int, c_int, P_int]),
 }
 

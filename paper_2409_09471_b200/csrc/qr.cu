@@ -466,6 +466,7 @@ int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* 
 constexpr int kSvdThreads = 1024;
 __device__ int* g_svd_sweeps = nullptr;  // optional diagnostic sink (tests)
 __device__ long long* g_chol_prof = nullptr;  // diagnostics: phase clocks of chol_blocked_kernel
+__device__ long long* g_fq_prof = nullptr;  // fused CholeskyQR2 phase timestamps (diagnostics)
 constexpr int kSvdGroup = 16;  // lanes per column pair
 
 template <int RPL>
@@ -1332,6 +1333,11 @@ int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V
 }
 
 // diagnostics: chol_blocked_kernel phase clocks (load, diagonal blocks, panels, trailing, epilogue)
+int ttk_debug_fused_qr_profile(long long* dev_ts) {
+  TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_fq_prof, &dev_ts, sizeof(dev_ts)));
+  return kOk;
+}
+
 int ttk_debug_chol_profile(long long* dev_acc) {
   TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_chol_prof, &dev_acc, sizeof(long long*)));
   return kOk;
@@ -1643,10 +1649,11 @@ constexpr int kNearIdMax = kCholMaxCols;
 
 __device__ __forceinline__ int near_id_ld(int l) { return ((l + 15) & ~15) + 4; }
 
-__global__ void __launch_bounds__(1024, 1)
-    chol_near_identity_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
-                              double* __restrict__ Rinv, int* flag, double tol, double first_order_max) {
-  extern __shared__ double sm[];
+// body shared by chol_near_identity_kernel and the fused CholeskyQR2 kernel
+// (any block size that is a multiple of 32; sm: 2 l near_id_ld(l) doubles)
+__device__ void chol_near_identity_body(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                                        double* __restrict__ Rinv, int* flag, double tol, double first_order_max,
+                                        double* sm) {
   const int ld = near_id_ld(l);
   double* F = sm;
   double* P = F + (size_t)l * ld;
@@ -1702,6 +1709,13 @@ __global__ void __launch_bounds__(1024, 1)
   if (tid == 0) *flag = 1;
 }
 
+__global__ void __launch_bounds__(1024, 1)
+    chol_near_identity_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                              double* __restrict__ Rinv, int* flag, double tol, double first_order_max) {
+  extern __shared__ double sm[];
+  chol_near_identity_body(l, G, Rout, Rinv, flag, tol, first_order_max, sm);
+}
+
 // Blocked right-looking Cholesky (blocks of 16) of G + shift*trace(G) I for
 // l <= kCholMaxCols: warp 0 factors each 16 x 16 diagonal block in registers
 // (lane c owns column c; pivots by shuffle, rsqrt, no barrier inside), the
@@ -1737,12 +1751,11 @@ __device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, 
 
 __device__ __forceinline__ int cb_ld(int l) { return ((l + 15) & ~15) + 4; }
 
-__global__ void __launch_bounds__(kCbThreads, 1)
-    chol_blocked_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
-                        double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
-                        double tiny_rel, const int* __restrict__ skip) {
-  if (skip && *skip) return;  // chol_near_identity_kernel already produced R, R^{-1}
-  extern __shared__ double sm[];
+// body shared by chol_blocked_kernel and the fused CholeskyQR2 kernel (block
+// size kCbThreads; sm: 2 l cb_ld(l) + 256 ceil(l/16) doubles)
+__device__ void chol_blocked_body(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                                  double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
+                                  double tiny_rel, double* sm) {
   const int ld = cb_ld(l);
   double* A = sm;                       // l x ld
   double* X = A + (size_t)l * ld;       // l x ld (inverse)
@@ -1852,6 +1865,15 @@ __global__ void __launch_bounds__(kCbThreads, 1)
     atomicAdd((unsigned long long*)&prof[5], 1ull);
   }
   if (tid == 0 && bad) atomicOr(status, bad);
+}
+
+__global__ void __launch_bounds__(kCbThreads, 1)
+    chol_blocked_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
+                        double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
+                        double tiny_rel, const int* __restrict__ skip) {
+  if (skip && *skip) return;  // chol_near_identity_kernel already produced R, R^{-1}
+  extern __shared__ double sm[];
+  chol_blocked_body(l, G, Rout, Rinv, status, check_identity, shift_rel, tiny_rel, sm);
 }
 
 // R (upper) and R^{-1} of the Cholesky factor of G (+ shift): register kernel
@@ -2120,6 +2142,183 @@ __global__ void __launch_bounds__(kTbThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused fast-path CholeskyQR2: one cooperative kernel instead of the chain
+// Gram -> split-K reduce -> Cholesky -> TRSM -> Gram -> reduce -> near-identity
+// -> (Cholesky) -> Q GEMM -> R GEMM, each link a few microseconds of work behind
+// a launch.  CTAs 1..G-1 each keep one kFqRows-row tile of Y (then Q1) in shared
+// memory for the whole factorisation; the l x l Gram reductions are spread over
+// the grid; CTA 0 holds no tile and factors the two small Gram matrices between
+// grid barriers.  Same arithmetic as the unfused path (same Cholesky, TRSM,
+// near-identity and DMMA products), fixed reduction order.
+constexpr int kFqRows = 128, kFqThreads = 512, kFqMaxCols = 96;
+
+struct FqParams {
+  int m, l;
+  const double* Y;
+  long long y_rs, y_cs;
+  double* Q;      // row-major, ld q_rs
+  long long q_rs;
+  double* R;      // l x l or null
+  double* part;   // (grid - 1) x l x l partial Gram matrices
+  double* G;      // l x l reduced Gram
+  double* R1;
+  double* R2;
+  double* I2;     // R2^{-1}
+  int* status;    // [0] first pass, [1] second pass, [4] near-identity flag
+  double first_order_max;
+};
+
+__device__ __forceinline__ void fq_reduce(const double* part, int nparts, int ll, double* G) {
+  const int nthr = (gridDim.x - 1) * blockDim.x;
+  for (int e = (blockIdx.x - 1) * blockDim.x + threadIdx.x; e < ll; e += nthr) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * ll + e];
+    G[e] = s;
+  }
+}
+
+__device__ __forceinline__ void fq_mark(int i) {
+  if (g_fq_prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fq_prof[i] = (long long)t;
+  }
+}
+
+__global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __grid_constant__ FqParams P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  fq_mark(0);
+  extern __shared__ __align__(16) double fsm[];
+  const int l = P.l, ld = ((l + 15) & ~15) + 4, tid = threadIdx.x;
+  const bool fac = blockIdx.x == 0;  // the factorisation CTA
+  double* sY = fsm;                           // kFqRows x ld   (tile CTAs)
+  double* sR = sY + (size_t)kFqRows * ld;     // l x ld
+  double* rinv = sR + (size_t)l * ld;         // l
+  const long long r0 = (long long)(blockIdx.x - 1) * kFqRows;
+  const int rows = fac ? 0 : (int)(P.m - r0 < kFqRows ? P.m - r0 : kFqRows);
+  const int nparts = gridDim.x - 1, ll = l * l;
+  if (!fac) {
+    for (int e = tid; e < kFqRows * l; e += kFqThreads) {
+      const int r = e / l, c = e - r * l;
+      const bool ok = r < rows;
+      cp_async8(sY + r * ld + c, ok ? P.Y + (r0 + r) * P.y_rs + (long long)c * P.y_cs : P.Y, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // Gram partial of the tile (zero rows beyond m contribute nothing)
+    block_dmma(l, l, kFqRows, sY, 1, ld, sY, ld, 1, sR, ld);
+    __syncthreads();
+    double* mine = P.part + (size_t)(blockIdx.x - 1) * ll;
+    for (int e = tid; e < ll; e += kFqThreads) mine[e] = sR[(e / l) * ld + e % l];
+  }
+  grid.sync();
+  fq_mark(1);
+  if (!fac) fq_reduce(P.part, nparts, ll, P.G);
+  grid.sync();
+  fq_mark(2);
+  if (fac) chol_blocked_body(l, P.G, P.R1, nullptr, P.status, 0, 0.0, 1e-15, fsm);
+  grid.sync();
+  fq_mark(3);
+  if (!fac) {
+    // Q1 tile = Y tile R1^{-1}: blocked forward substitution (trsm_blocked_kernel's
+    // scheme, 4 threads per row), then the tile's partial of Q1^T Q1
+    for (int e = tid; e < ll; e += kFqThreads) sR[(e / l) * ld + e % l] = P.R1[e];
+    __syncthreads();
+    for (int j = tid; j < l; j += kFqThreads) rinv[j] = 1.0 / sR[j * ld + j];
+    __syncthreads();
+    const int row = tid >> 2, g = tid & 3;
+    for (int j0 = 0; j0 < l; j0 += 16) {
+      const int bs = min(16, l - j0);
+      if (j0 > 0) {
+        block_dmma(kFqRows, bs, j0, sY, ld, 1, sR + j0, ld, 1, sY + j0, ld, nullptr, nullptr, nullptr, true);
+        __syncthreads();
+      }
+      double t[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = g + 4 * k;
+        t[k] = (c < bs) ? sY[row * ld + j0 + c] : 0.0;
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        if (jj < bs) {
+          const int kj = jj >> 2;
+          double v = t[kj] * rinv[j0 + jj];
+          v = __shfl_sync(0xffffffffu, v, (threadIdx.x & ~3) | (jj & 3), 32);
+          if ((jj & 3) == g) t[kj] = v;
+          const double* rr = sR + (j0 + jj) * ld + j0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int c = g + 4 * k;
+            if (c > jj && c < bs) t[k] -= v * rr[c];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = g + 4 * k;
+        if (c < bs) sY[row * ld + j0 + c] = t[k];
+      }
+      __syncthreads();
+    }
+    if (row >= rows)  // padded rows stay zero (rinv scaling of zeros is zero; keep it exact)
+      for (int c = g; c < l; c += 4) sY[row * ld + c] = 0.0;
+    __syncthreads();
+    block_dmma(l, l, kFqRows, sY, 1, ld, sY, ld, 1, sR, ld);
+    __syncthreads();
+    double* mine = P.part + (size_t)(blockIdx.x - 1) * ll;
+    for (int e = tid; e < ll; e += kFqThreads) mine[e] = sR[(e / l) * ld + e % l];
+  }
+  grid.sync();
+  fq_mark(4);
+  if (!fac) fq_reduce(P.part, nparts, ll, P.G);
+  grid.sync();
+  fq_mark(5);
+  if (fac) {
+    chol_near_identity_body(l, P.G, P.R2, P.I2, P.status + 4, 1e-7, P.first_order_max, fsm);
+    __syncthreads();
+    if (!*(volatile int*)(P.status + 4))
+      chol_blocked_body(l, P.G, P.R2, P.I2, P.status + 1, 1, 0.0, 1e-28, fsm);
+    __syncthreads();
+    if (P.R) {  // R = R2 R1
+      double* a = fsm;
+      double* b = fsm + (size_t)l * ld;
+      for (int e = tid; e < ll; e += kFqThreads) {
+        a[(e / l) * ld + e % l] = P.R2[e];
+        b[(e / l) * ld + e % l] = P.R1[e];
+      }
+      __syncthreads();
+      block_dmma(l, l, l, a, ld, 1, b, ld, 1, P.R, l);
+    }
+  }
+  grid.sync();
+  fq_mark(6);
+  if (!fac) {
+    // Q tile = Q1 tile R2^{-1}
+    for (int e = tid; e < ll; e += kFqThreads) sR[(e / l) * ld + e % l] = P.I2[e];
+    __syncthreads();
+    block_dmma(rows, l, l, sY, ld, 1, sR, ld, 1, P.Q + r0 * P.q_rs, (int)P.q_rs);
+  }
+  grid.sync();
+  fq_mark(15);
+}
+
+size_t cholqr2_fused_smem(int l) {
+  const size_t ld = ((l + 15) & ~15) + 4;
+  const size_t tile = (size_t)kFqRows * ld + (size_t)l * ld + ((l + 1) & ~1);
+  const size_t fac = 2 * (size_t)l * ld + 256 * (size_t)((l + 15) / 16);
+  return sizeof(double) * std::max(tile, fac);
+}
+
+bool cholqr2_fused_fits(int m, int l, long long q_cs) {
+  static const bool off = getenv("TTK_QR_NO_FUSED") != nullptr;  // A/B
+  return !off && l <= kFqMaxCols && m >= l && q_cs == 1 && (m + kFqRows - 1) / kFqRows <= kNumSMs - 1 &&
+         cholqr2_fused_smem(l) <= 220 * 1024;
+}
+
 int trsm_right_upper(int m, int l, const double* Y, long long y_rs, long long y_cs, const double* R, double* Q,
                      long long q_rs, long long q_cs, cudaStream_t st) {
   if (m <= 0 || l <= 0) return kOk;
@@ -2227,7 +2426,40 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
   };
   int hs[4] = {0, 0, 0, 0};
   static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;
-  if (!robust_first || qr_mode == 2) {
+  bool fast_tried = false;
+  if ((!robust_first || qr_mode == 2) && cholqr2_fused_fits(m, l, q_cs)) {
+    // ---- fast path, fused into one cooperative kernel ----
+    static bool fattr = false;
+    if (!fattr) {
+      TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel, 220 * 1024));
+      fattr = true;
+    }
+    static const double fo = getenv("TTK_NEAR_ID_FIRST_ORDER") ? atof(getenv("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
+    TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 8 * sizeof(int), st));
+    FqParams fp{};
+    fp.m = m; fp.l = l; fp.Y = Y; fp.y_rs = y_rs; fp.y_cs = y_cs; fp.Q = Q; fp.q_rs = q_rs; fp.R = R;
+    fp.part = (double*)split; fp.G = G; fp.R1 = R1; fp.R2 = R2; fp.I2 = I2; fp.status = status;
+    fp.first_order_max = fo;
+    const int grid = 1 + (m + kFqRows - 1) / kFqRows;
+    void* args[] = {&fp};
+    const cudaError_t le = cudaLaunchCooperativeKernel((const void*)cholqr2_fused_kernel, dim3(grid),
+                                                       dim3(kFqThreads), args, cholqr2_fused_smem(l), st);
+    if (le == cudaSuccess) {
+      fast_tried = true;
+      TTK_CHECK_LAUNCH();
+      TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      TTK_SYNC(st);
+      if (hs[0] == 0 && hs[1] == 0) {
+        *ok = 1;
+        g_qr_last_path_set(1);
+        return kOk;
+      }
+      if (qr_mode == 2) return kOk;
+    } else {
+      (void)cudaGetLastError();  // cooperative launch refused (co-residency): unfused chain below
+    }
+  }
+  if (!fast_tried && (!robust_first || qr_mode == 2)) {
     // ---- fast path: CholeskyQR2, accepted for kappa(Y) <~ 3e7 ----
     TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(int), st));
     TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, 0.0, 1e-15));
