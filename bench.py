@@ -139,8 +139,9 @@ def load_peaks():
 def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=None):
     """The step's dominant kernel by time is the one-sided Jacobi SVD of the
     truncation (one per core, a sequential chain).  It runs on one 8-CTA
-    cluster (qr.cu jacobi_cluster_kernel): pair slots spread over 8 SMs,
-    columns register-resident, neighbour moves over DSMEM.  Time one l x l
+    cluster (qr.cu jacobi_block_kernel): pair slots spread over 8 SMs,
+    columns register-resident, block-ordered rounds (in-CTA moves through
+    shared memory, 15 DSMEM block moves per sweep).  Time one l x l
     instance live and report its algorithmic FLOPs against the fp64 peak of
     the 8 SMs it occupies; the bound is the per-round latency chain."""
     from paper_2409_09471_b200 import _lib
@@ -172,10 +173,10 @@ def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=No
     peak8 = 8 * 33.9e3 / 148  # GFLOP/s of 8 SMs, measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
     ach = flops / (ms * 1e-3) / 1e9
     rounds = sweeps * (l - 1)
-    out = {"kernel": "jacobi_cluster_kernel (8-CTA cluster, %dx%d, V accumulated)" % (l, l), "ms": ms,
+    out = {"kernel": "jacobi_block_kernel (8-CTA cluster, block-ordered, %dx%d, V accumulated)" % (l, l), "ms": ms,
            "sweeps": sweeps, "rounds": rounds, "us_per_round": ms * 1e3 / max(rounds, 1),
            "bound": "latency (sequential rotation rounds; per round: dot, 16-lane reduction, "
-                    "rotation, DSMEM neighbour exchange)",
+                    "rotation, in-CTA move; a DSMEM block move every bs rounds)",
            "achieved_gflops": ach, "peak_gflops_8_sms": peak8, "frac_of_8_sms": ach / peak8}
     if calls_per_step and step_ms:
         out["share_of_step_est"] = calls_per_step * ms / step_ms

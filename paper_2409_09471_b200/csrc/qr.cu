@@ -660,6 +660,18 @@ __device__ __forceinline__ double rsqrt_nr(double p) {
   return y;
 }
 
+// 1/sqrt(p) for the rotation formula (normal positive p): the fp64 hardware
+// seed is good to 2^-20 on B200 (tools/rsqrt_acc.cu), so one third-order
+// correction y (1 + e/2 + 3e^2/8), e = 1 - p y^2 (error ~0.3 e^3 < 2^-61)
+// replaces rsqrt_nr's two Newton steps: four dependent fp64 ops instead of six.
+__device__ __forceinline__ double rsqrt_rot(double p) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+  const double e = fma(-p * y, y, 1.0);
+  const double t = fma(e, 0.375, 0.5);
+  return fma(y * e, t, y);
+}
+
 constexpr int kJcCluster = 8;
 constexpr int kJcMaxSlots = 8;   // pair slots per CTA (le <= 128)
 constexpr int kJcThreads = kJcMaxSlots * kSvdGroup;
@@ -845,9 +857,9 @@ __global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads,
         const double sc = __longlong_as_double((2046LL - ex) << 52);
         const double dd = (b - a) * sc, w = 2.0 * g * sc;
         const double q = dd * dd + w * w;
-        const double rho = q * rsqrt_nr(q);
+        const double rho = q * rsqrt_rot(q);
         const double sum = fabs(dd) + rho;
-        const double rq = rsqrt_nr(2.0 * rho * sum);
+        const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
         const double c = sum * rq, s = (dd >= 0.0 ? w : -w) * rq;
 #pragma unroll
         for (int i = 0; i < RPL; ++i) {
@@ -1002,6 +1014,329 @@ __global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads,
 }
 
 // ---------------------------------------------------------------------------
+// Block-ordered cluster Jacobi.  Same rotations, stopping rule and outputs as
+// jacobi_cluster_kernel, different cyclic pair order: the le columns form 16
+// blocks of bs columns, CTA c holds two blocks P(c), Q(c) (slot a of the CTA
+// owns column a of each).  A sweep is
+//   block round 0  : round-robin over the CTA's own 2 bs columns (2 bs - 1 rounds;
+//                    covers every pair inside P(c) u Q(c));
+//   block rounds 1-14: bs rounds pairing P_a with Q_{a-t}: the Q block shifts by one
+//                    slot inside the CTA between rounds (all bs^2 cross pairs);
+//   after every block round the blocks move between CTAs by the circle method
+//   on 16 blocks (P(c) -> P(c-1), P(1) -> Q(0), Q(c) -> Q(c+1), Q(7) -> P(7)).
+// Every pair meets once per sweep, le - 1 rounds as before, but only 15 of
+// them end with a DSMEM handoff + mbarrier wait (the ~900-cycle part of the
+// plain kernel's round: r01 phase clocks rotate 666 / send 277 / wait 272 /
+// pull 320 at 80 x 80); the others exchange through this CTA's shared memory
+// with one barrier.
+constexpr int kJbCluster = 8;
+constexpr int kJbMaxSlots = 16;  // columns per block (8-CTA cluster: <= 8, l <= 128)
+
+template <int RPL, int CL = kJbCluster>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdGroup, 1)
+    jacobi_block_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
+                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
+                        int scaled_u, double skip2) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int c = (int)cl.block_rank();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double nrm[kQrMaxCols + 2];
+  __shared__ double fin[kQrMaxCols + 2];
+  __shared__ int order[kQrMaxCols + 2];
+  __shared__ int flags[64];
+  __shared__ int bigf[64];
+  __shared__ int bid[2][kJbMaxSlots][2];  // block-move inbox: column ids
+  __shared__ int lid[2][kJbMaxSlots][2];  // local-move inbox: column ids
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int bs = (l + 2 * CL - 1) / (2 * CL);
+  const int le = 2 * CL * bs, kk = k;
+  const int tid = threadIdx.x, a = tid / kSvdGroup, gl = tid % kSvdGroup;
+  const bool active = a < bs;
+  constexpr int box = RPL * kSvdGroup;
+  const int nv = want_v ? 2 : 1;
+  // [2 bufs][bs slots][2 sides][2 (C, V)][box], block inbox then local inbox
+  double* const lbox = sm + (size_t)2 * bs * 4 * box;
+  auto bslot = [&](int buf, int slot, int side, int cv) {
+    return sm + ((((size_t)buf * bs + slot) * 2 + side) * 2 + cv) * box + gl * 2;
+  };
+  auto lslot = [&](int buf, int slot, int side, int cv) {
+    return lbox + ((((size_t)buf * bs + slot) * 2 + side) * 2 + cv) * box + gl * 2;
+  };
+  const uint32_t msg_bytes = (uint32_t)(box * 8 * nv + 4);
+  // remote columns received per block move: new Q always, new P for 1 <= c <= CL-2
+  const uint32_t rx_bytes = (uint32_t)bs * msg_bytes * ((c >= 1 && c <= CL - 2) ? 2u : 1u);
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    jc_arm(bar0, rx_bytes);
+    jc_arm(bar0 + 8, rx_bytes);
+  }
+  // initial order: decreasing norm, ties by index (identical in every CTA)
+  for (int cc = tid >> 5; cc < l; cc += blockDim.x >> 5) {
+    double s = 0.0;
+    for (int r = tid & 31; r < kk; r += 32) {
+      double xv = B[(long long)r * b_rs + (long long)cc * b_cs];
+      s += xv * xv;
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) nrm[cc] = s;
+  }
+  for (int i = tid; i < 64; i += blockDim.x) { flags[i] = 0; bigf[i] = 0; }
+  __syncthreads();
+  for (int cc = tid; cc < l; cc += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < l; ++j) rank += (nrm[j] > nrm[cc]) || (nrm[j] == nrm[cc] && j < cc);
+    order[rank] = cc;
+  }
+  __syncthreads();
+  // positions: P slot a of CTA c = c bs + a, Q slot a = le - 1 - (c bs + a)
+  int idl = active ? c * bs + a : 0, idr = active ? le - 1 - (c * bs + a) : 0;
+  double x[RPL], y[RPL], vx[RPL], vy[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = gl + i * kSvdGroup;
+    const bool okl = active && r < kk && idl < l, okr = active && r < kk && idr < l;
+    x[i] = okl ? B[(long long)r * b_rs + (long long)order[idl] * b_cs] : 0.0;
+    y[i] = okr ? B[(long long)r * b_rs + (long long)order[idr] * b_cs] : 0.0;
+    vx[i] = (want_v && active && idl < l && r == order[idl]) ? 1.0 : 0.0;
+    vy[i] = (want_v && active && idr < l && r == order[idr]) ? 1.0 : 0.0;
+  }
+  const double tol = (double)max(kk, 1) * 1.1102230246251565e-16;
+  const double tol2 = tol * tol;
+  // block-move destinations (shared::cluster addresses, buffer 0)
+  const bool send_p = active && c >= 1;       // P(c) -> P(c-1) (c >= 2), P(1) -> Q(0)
+  const bool send_q = active && c <= CL - 2;  // Q(c) -> Q(c+1)
+  uint32_t p_c = 0, p_id = 0, p_bar = 0, q_c = 0, q_id = 0, q_bar = 0;
+  if (send_p) {
+    const int side = (c == 1) ? 1 : 0;
+    p_c = jc_map(bslot(0, a, side, 0), c - 1);
+    p_id = jc_map(&bid[0][a][side], c - 1);
+    p_bar = jc_map(&mbar[0], c - 1);
+  }
+  if (send_q) {
+    q_c = jc_map(bslot(0, a, 1, 0), c + 1);
+    q_id = jc_map(&bid[0][a][1], c + 1);
+    q_bar = jc_map(&mbar[0], c + 1);
+  }
+  const uint32_t bbuf_bytes = (uint32_t)(bs * 4 * box * 8);
+  const uint32_t bid_bytes = (uint32_t)(kJbMaxSlots * 2 * sizeof(int));
+  cl.sync();  // barriers initialised and armed in every CTA before the first remote store
+
+  auto put = [&](double* dst, const double* v) {  // one column part into an inbox slot
+    double2* p = reinterpret_cast<double2*>(dst);
+#pragma unroll
+    for (int j = 0; j < RPL / 2; ++j) p[j * kSvdGroup] = make_double2(v[2 * j], v[2 * j + 1]);
+  };
+  auto get = [&](const double* src, double* v) {
+    const double2* p = reinterpret_cast<const double2*>(src);
+#pragma unroll
+    for (int j = 0; j < RPL / 2; ++j) { double2 t = p[j * kSvdGroup]; v[2 * j] = t.x; v[2 * j + 1] = t.y; }
+  };
+
+  long long* const prof = (tid == 0) ? g_jc_prof : nullptr;
+  long long pt[4] = {0, 0, 0, 0}, tc = 0;
+  int sweep = 0, moves = 0, lr = 0;
+  for (; sweep < 60; ++sweep) {
+    for (int br = 0; br < 2 * CL - 1; ++br) {
+      const int nr = (br == 0) ? 2 * bs - 1 : bs;
+      for (int t = 0; t < nr; ++t, ++lr) {
+        // ---- rotate the pair (x, y) ----
+        if (prof) tc = clock64();
+        double ra = 0.0, rb = 0.0, rg = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; i += 2) {
+          ra += x[i] * x[i]; rb += y[i] * y[i]; rg += x[i] * y[i];
+          if (i + 1 < RPL) { a2 += x[i + 1] * x[i + 1]; b2 += y[i + 1] * y[i + 1]; g2 += x[i + 1] * y[i + 1]; }
+        }
+        ra += a2; rb += b2; rg += g2;
+#pragma unroll
+        for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
+          ra += __shfl_xor_sync(0xffffffffu, ra, o);
+          rb += __shfl_xor_sync(0xffffffffu, rb, o);
+          rg += __shfl_xor_sync(0xffffffffu, rg, o);
+        }
+        if (active && gl == 0 && rg * rg > skip2 * ra * rb) bigf[sweep] = 1;
+        if (active && ra > 0.0 && rb > 0.0 && rg * rg > tol2 * ra * rb) {
+          // jacobi_cluster_kernel's division- and CALL-free rotation
+          const long long ex = min((__double_as_longlong(ra + rb) >> 52) & 0x7ff, 2045LL);
+          const double sc = __longlong_as_double((2046LL - ex) << 52);
+          const double dd = (rb - ra) * sc, w = 2.0 * rg * sc;
+          const double q = dd * dd + w * w;
+          const double rho = q * rsqrt_rot(q);
+          const double sum = fabs(dd) + rho;
+          const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
+          const double cs = sum * rq, sn = (dd >= 0.0 ? w : -w) * rq;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const double xi = x[i], yi = y[i];
+            x[i] = cs * xi - sn * yi;
+            y[i] = sn * xi + cs * yi;
+          }
+          if (want_v) {
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              const double xi = vx[i], yi = vy[i];
+              vx[i] = cs * xi - sn * yi;
+              vy[i] = sn * xi + cs * yi;
+            }
+          }
+          if (gl == 0) flags[sweep] = 1;
+        }
+        // ---- local move through this CTA's shared memory ----
+        if (prof) { long long t = clock64(); pt[0] += t - tc; tc = t; }
+        const int buf = lr & 1;
+        if (br == 0) {
+          // round-robin over the CTA's 2 bs columns (circle method on bs slots):
+          // left(s) -> left(s-1) (s >= 2), left(1) -> right(0), right(s) -> right(s+1),
+          // right(bs-1) -> left(bs-1), left(0) fixed
+          if (active) {
+            if (a >= 1) {
+              const int ds = a - 1, side = (a == 1) ? 1 : 0;
+              put(lslot(buf, ds, side, 0), x);
+              if (want_v) put(lslot(buf, ds, side, 1), vx);
+              if (gl == 0) lid[buf][ds][side] = idl;
+            }
+            if (a <= bs - 2) {
+              put(lslot(buf, a + 1, 1, 0), y);
+              if (want_v) put(lslot(buf, a + 1, 1, 1), vy);
+              if (gl == 0) lid[buf][a + 1][1] = idr;
+            }
+          }
+          __syncthreads();
+          if (active) {
+            if (a >= 1) {
+              if (a == bs - 1) {
+#pragma unroll
+                for (int i = 0; i < RPL; ++i) { x[i] = y[i]; vx[i] = vy[i]; }
+                idl = idr;
+              } else {
+                get(lslot(buf, a, 0, 0), x);
+                if (want_v) get(lslot(buf, a, 0, 1), vx);
+                idl = lid[buf][a][0];
+              }
+            }
+            get(lslot(buf, a, 1, 0), y);
+            if (want_v) get(lslot(buf, a, 1, 1), vy);
+            idr = lid[buf][a][1];
+          }
+        } else {
+          // Q block shifts by one slot: Q_a -> slot a + 1 (mod bs)
+          if (active) {
+            const int ds = (a + 1 == bs) ? 0 : a + 1;
+            put(lslot(buf, ds, 1, 0), y);
+            if (want_v) put(lslot(buf, ds, 1, 1), vy);
+            if (gl == 0) lid[buf][ds][1] = idr;
+          }
+          __syncthreads();
+          if (active) {
+            get(lslot(buf, a, 1, 0), y);
+            if (want_v) get(lslot(buf, a, 1, 1), vy);
+            idr = lid[buf][a][1];
+          }
+        }
+        if (prof) { long long t = clock64(); pt[1] += t - tc; tc = t; }
+      }
+      // ---- block move between CTAs (DSMEM, completion on the receiver's mbarrier) ----
+      {
+        const int buf = moves & 1;
+        const uint32_t bo = buf * bbuf_bytes, io = buf * bid_bytes, mo = buf * 8;
+        if (send_p) {
+#pragma unroll
+          for (int j = 0; j < RPL; j += 2) jc_st_v2(p_c + bo + 128 * j, x[j], x[j + 1], p_bar + mo);
+          if (want_v) {
+#pragma unroll
+            for (int j = 0; j < RPL; j += 2) jc_st_v2(p_c + bo + box * 8 + 128 * j, vx[j], vx[j + 1], p_bar + mo);
+          }
+          if (gl == 0) jc_st_u32(p_id + io, (uint32_t)idl, p_bar + mo);
+        }
+        if (send_q) {
+#pragma unroll
+          for (int j = 0; j < RPL; j += 2) jc_st_v2(q_c + bo + 128 * j, y[j], y[j + 1], q_bar + mo);
+          if (want_v) {
+#pragma unroll
+            for (int j = 0; j < RPL; j += 2) jc_st_v2(q_c + bo + box * 8 + 128 * j, vy[j], vy[j + 1], q_bar + mo);
+          }
+          if (gl == 0) jc_st_u32(q_id + io, (uint32_t)idr, q_bar + mo);
+        }
+        jc_wait(bar0 + mo, (moves >> 1) & 1);
+        __syncthreads();  // every thread has seen the phase complete before it is re-armed
+        if (tid == 0) jc_arm(bar0 + mo, rx_bytes);  // for move + 2
+        if (active) {
+          if (c >= 1) {
+            if (c == CL - 1) {
+#pragma unroll
+              for (int i = 0; i < RPL; ++i) { x[i] = y[i]; vx[i] = vy[i]; }
+              idl = idr;
+            } else {
+              get(bslot(buf, a, 0, 0), x);
+              if (want_v) get(bslot(buf, a, 0, 1), vx);
+              idl = bid[buf][a][0];
+            }
+          }
+          get(bslot(buf, a, 1, 0), y);
+          if (want_v) get(bslot(buf, a, 1, 1), vy);
+          idr = bid[buf][a][1];
+        }
+        ++moves;
+        if (prof) { long long t = clock64(); pt[2] += t - tc; tc = t; }
+      }
+    }
+    // every rotation of this sweep is ordered before this cluster barrier
+    cl.sync();
+    int ch = 0, big = 0;
+#pragma unroll 1
+    for (int r = 0; r < CL; ++r) {
+      ch |= *cl.map_shared_rank(&flags[sweep], r);
+      big |= *cl.map_shared_rank(&bigf[sweep], r);
+    }
+    if (!ch || !big) break;
+  }
+  if (c == 0 && tid == 0 && g_svd_sweeps) *g_svd_sweeps = sweep + 1;
+  if (prof) {
+    for (int i = 0; i < 4; ++i) atomicAdd((unsigned long long*)&prof[c * 5 + i], (unsigned long long)pt[i]);
+    atomicAdd((unsigned long long*)&prof[c * 5 + 4], (unsigned long long)lr);
+  }
+  // final norms of every column, broadcast to every CTA
+  double na = 0.0, nb = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) { na += x[i] * x[i]; nb += y[i] * y[i]; }
+#pragma unroll
+  for (int o = kSvdGroup / 2; o > 0; o >>= 1) {
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  na = sqrt(na); nb = sqrt(nb);
+  if (active && gl == 0)
+    for (int r = 0; r < CL; ++r) {
+      *cl.map_shared_rank(&fin[idl], r) = na;
+      *cl.map_shared_rank(&fin[idr], r) = nb;
+    }
+  cl.sync();
+  if (!active) return;
+  const int kout = min(kk, l);
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const int id = side ? idr : idl;
+    const double nv2 = side ? nb : na;
+    int rank = 0;
+    for (int j = 0; j < le; ++j) rank += (fin[j] > nv2) || (fin[j] == nv2 && j < id);
+    if (id >= l || rank >= kout) continue;
+    if (gl == 0) S[rank] = nv2;
+    const double inv = (scaled_u || nv2 <= 0.0) ? 1.0 : 1.0 / nv2;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = gl + i * kSvdGroup;
+      const double cv = side ? y[i] : x[i];
+      if (r < kk) U[(size_t)r * kout + rank] = scaled_u ? cv : (nv2 > 0.0 ? cv * inv : 0.0);
+      if (want_v && V && r < l) V[(size_t)r * kout + rank] = side ? vy[i] : vx[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Single-CTA variant for small factorisations (le <= 64, rows <= 64): the same
 // register-resident pair slots, tournament and rotation as the cluster kernel,
 // but every move stays in this CTA's shared memory (double-buffered inbox, one
@@ -1089,9 +1424,9 @@ __global__ void __launch_bounds__(kJlMaxSlots * kSvdGroup, 1)
         const double sc = __longlong_as_double((2046LL - ex) << 52);
         const double dd = (b - a) * sc, w = 2.0 * g * sc;
         const double q = dd * dd + w * w;
-        const double rho = q * rsqrt_nr(q);
+        const double rho = q * rsqrt_rot(q);
         const double sum = fabs(dd) + rho;
-        const double rq = rsqrt_nr(2.0 * rho * sum);
+        const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
         const double c = sum * rq, s = (dd >= 0.0 ? w : -w) * rq;
 #pragma unroll
         for (int i = 0; i < RPL; ++i) {
@@ -1239,6 +1574,50 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
     TTK_CHECK_LAUNCH();
     return kOk;
   }
+  // block-ordered cluster kernel (2 CL - 1 DSMEM handoffs per sweep instead of
+  // le - 1); TTK_JACOBI_BLOCK=0 keeps the plain cluster kernel, =4 / =8 picks the
+  // cluster size (A/B)
+  static const int block_env = getenv("TTK_JACOBI_BLOCK") ? atoi(getenv("TTK_JACOBI_BLOCK")) : -1;
+  int block_cl = block_env;
+  if (block_cl < 0) {
+    // fewest padded columns (dummy columns cost whole rounds), 8 CTAs on ties:
+    // r01 (tools/jac_ab.py) 50 x 50: 4 CTAs (56 columns) 291 us vs 8 CTAs (64) 316;
+    // 80 x 80: 581 vs 529
+    const int le8 = 16 * ((l + 15) / 16), le4 = 8 * ((l + 7) / 8);
+    const int rows4 = std::max(k, le4), rpl4 = rows4 <= 4 * kSvdGroup ? 4 : rows4 <= 6 * kSvdGroup ? 6 : 8;
+    const bool fits4 = le4 / 8 <= kJbMaxSlots && sizeof(double) * 2 * (2 * (size_t)(le4 / 8) * 4 * rpl4 * kSvdGroup) <= 200 * 1024;
+    block_cl = (le4 < le8 && fits4) ? 4 : 8;
+  }
+  if (!single_cta && block_cl != 0 && l > 2 * block_cl && k <= 8 * kSvdGroup) {
+    const int bs = (l + 2 * block_cl - 1) / (2 * block_cl);
+    const int rows = std::max(k, 2 * block_cl * bs);
+    const int rpl = rows <= 4 * kSvdGroup ? 4 : rows <= 6 * kSvdGroup ? 6 : 8;
+    const size_t jsm = sizeof(double) * 2 * (2 * (size_t)bs * 4 * rpl * kSvdGroup);
+    if (bs <= kJbMaxSlots && jsm <= 200 * 1024) {
+      static bool battr = false;
+      if (!battr) {
+        TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<4, 8>, 200 * 1024));
+        TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<6, 8>, 200 * 1024));
+        TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<8, 8>, 200 * 1024));
+        TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<4, 4>, 200 * 1024));
+        TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<6, 4>, 200 * 1024));
+        TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<8, 4>, 200 * 1024));
+        battr = true;
+      }
+      const int threads = (bs * kSvdGroup + 31) / 32 * 32;
+      const int want = V != nullptr;
+#define TTK_JB_LAUNCH(R, C) \
+  jacobi_block_kernel<R, C><<<C, threads, jsm, st>>>(k, l, B, b_rs, b_cs, U, S, V, want, scaled_u, skip2)
+      if (block_cl == 4) {
+        if (rpl == 4) TTK_JB_LAUNCH(4, 4); else if (rpl == 6) TTK_JB_LAUNCH(6, 4); else TTK_JB_LAUNCH(8, 4);
+      } else {
+        if (rpl == 4) TTK_JB_LAUNCH(4, 8); else if (rpl == 6) TTK_JB_LAUNCH(6, 8); else TTK_JB_LAUNCH(8, 8);
+      }
+#undef TTK_JB_LAUNCH
+      TTK_CHECK_LAUNCH();
+      return kOk;
+    }
+  }
   if (!single_cta && le <= 2 * kJcCluster * kJcMaxSlots && k <= 8 * kSvdGroup) {
     static bool cattr = false;
     if (!cattr) {
@@ -1303,18 +1682,27 @@ int jacobi_svd(int k, int l, const double* B, double* U, double* S, double* V, c
 }
 
 __global__ void truncation_rank_kernel(const double* S, int n, double budget, int max_rank, int* r_out) {
-  if (threadIdx.x != 0) return;
   // tail[r] = sqrt(sum_{i>=r} S_i^2), accumulated from the smallest value as
-  // np.cumsum(sv[::-1]**2)[::-1] does (tt.py:207)
-  int r = n;
-  double acc = 0.0;
-  // find the smallest r with tail[r] <= budget: scan from the end
-  int best = n;
-  for (int i = n - 1; i >= 0; --i) {
-    acc += S[i] * S[i];
-    if (sqrt(fmax(acc, 0.0)) <= budget) best = i;
+  // np.cumsum(sv[::-1]**2)[::-1] does (tt.py:207): the running sums stay
+  // sequential with separately rounded squares (numpy's rounding), one
+  // thread; the square roots and the search for the smallest r with tail[r] <= budget run
+  // across the block (the serial form with sqrt in the loop took ~13 us)
+  __shared__ double acc[kQrMaxCols + 2];
+  __shared__ int best;
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+      a = __dadd_rn(a, __dmul_rn(S[i], S[i]));
+      acc[i] = a;
+    }
+    best = n;
   }
-  r = best;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (sqrt(fmax(acc[i], 0.0)) <= budget) atomicMin(&best, i);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int r = best;
   if (n == 0) r = 1;
   if (r < 1) r = 1;
   if (max_rank > 0 && r > max_rank) r = max_rank;
@@ -1323,7 +1711,8 @@ __global__ void truncation_rank_kernel(const double* S, int n, double budget, in
 
 int truncation_rank_dev(const double* S, int n, double budget, int max_rank, int* r_dev,
                         cudaStream_t st) {
-  truncation_rank_kernel<<<1, 32, 0, st>>>(S, n, budget, max_rank, r_dev);
+  TTK_REQUIRE(n <= kQrMaxCols, kInvalidValue, "truncation_rank: %d values exceed %d", n, kQrMaxCols);
+  truncation_rank_kernel<<<1, 128, 0, st>>>(S, n, budget, max_rank, r_dev);
   TTK_CHECK_LAUNCH();
   return kOk;
 }

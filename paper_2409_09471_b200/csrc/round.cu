@@ -261,8 +261,8 @@ size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks) {
     rmax = std::max(rmax, std::max(ranks[k], ranks[k + 1]));
     if (k > 0) qrws = std::max(qrws, qr_auto_ws_bytes(dims[k] * ranks[k + 1], ranks[k]));
   }
-  return sum + 3 * align_up(mx * 8, 256) + 5 * align_up((size_t)rmax * rmax * 8, 256) +
-         align_up(qrws, 256) + kSplitKBytes + 131072;
+  return sum + 4 * align_up(mx * 8, 256) + 6 * align_up((size_t)rmax * rmax * 8, 256) +
+         align_up(qrws, 256) + 2 * kSplitKBytes + 131072;
 }
 
 int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
@@ -288,9 +288,11 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
     if (k > 0) qrb = std::max(qrb, qr_auto_ws_bytes(dims[k] * ranks[k + 1], ranks[k]));
   }
   double* alt[2] = {ar.take<double>(mx), ar.take<double>(mx)};
-  double* tq = ar.take<double>(mx);
+  // Q and U double-buffered: the core's own product (Q U_r)^T runs on a side
+  // stream while the next core is factorised
+  double* tqb[2] = {ar.take<double>(mx), ar.take<double>(mx)};
   double* tR = ar.take<double>((size_t)rmax * rmax);
-  double* tU = ar.take<double>((size_t)rmax * rmax);
+  double* tUb[2] = {ar.take<double>((size_t)rmax * rmax), ar.take<double>((size_t)rmax * rmax)};
   double* tS = ar.take<double>((size_t)rmax + 8);
   double* tL = ar.take<double>((size_t)rmax * rmax);
   double* red = ar.take<double>(16);
@@ -300,7 +302,18 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
   void* qws = (char*)ws + qoff;
   ar.used = qoff + qrb;
   void* split_ws = ar.take<char>(kSplitKBytes);
-  TTK_REQUIRE(split_ws != nullptr, kWorkspace, "tt_truncate: workspace too small");
+  void* split_side = ar.take<char>(kSplitKBytes);
+  TTK_REQUIRE(split_side != nullptr, kWorkspace, "tt_truncate: workspace too small");
+  static thread_local cudaStream_t side = nullptr;
+  static thread_local cudaEvent_t ev_f[2] = {nullptr, nullptr}, ev_g[2] = {nullptr, nullptr};
+  if (side == nullptr) {
+    TTK_CHECK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_f[i], cudaEventDisableTiming));
+      TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_g[i], cudaEventDisableTiming));
+    }
+  }
+  bool g_pending[2] = {false, false};
   double* pin = (double*)g_pinned.get(64);
   TTK_REQUIRE(pin != nullptr, kCudaError, "tt_truncate: cannot allocate pinned scratch");
   std::vector<int> r(ranks, ranks + d + 1);
@@ -321,6 +334,10 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
   for (int k = d - 1; k >= 1; --k) {
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = n * r1, kk = std::min(m, r0);
+    double* const tq = tqb[k & 1];
+    double* const tU = tUb[k & 1];
+    // the side-stream product of core k + 2 read these buffers
+    if (g_pending[k & 1]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[k & 1], 0));
     // C_k^T (m x r0) = Q R ; element (row=(i,b), col=a) of C_k^T at a*m + row
     TTK_TRY(qr_auto(m, r0, cur, 1, m, tq, kk, 1, tR, qws, qrb, st, &qr_hint));
     const bool vt = jacobi_fits_v(r0, kk);
@@ -335,8 +352,13 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
     TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, sizeof(int), cudaMemcpyDeviceToHost, st));
     TTK_SYNC(st);
     const int rk = *(int*)pin;
-    // C_k <- (Q U_r)^T : out[k][c][row] = sum_j Q[row][j] U[j][c]
-    TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_ws, st));
+    // C_k <- (Q U_r)^T : out[k][c][row] = sum_j Q[row][j] U[j][c]  (side stream:
+    // only L feeds the next core)
+    TTK_CHECK_CUDA(cudaEventRecord(ev_f[k & 1], st));
+    TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_f[k & 1], 0));
+    TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_side, side));
+    TTK_CHECK_CUDA(cudaEventRecord(ev_g[k & 1], side));
+    g_pending[k & 1] = true;
     long long l_ld = kk;
     if (!vt) {
       // L = R^T U_r (r0 x rk)
@@ -352,6 +374,8 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cur, sizeof(double) * (size_t)dims[0] * r[1],
                                  cudaMemcpyDeviceToDevice, st));
+  for (int i = 0; i < 2; ++i)
+    if (g_pending[i]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[i], 0));
   TTK_SYNC(st);
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
   return kOk;
