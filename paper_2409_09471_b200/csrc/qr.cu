@@ -2060,6 +2060,28 @@ __device__ __forceinline__ int near_id_ld(int l) { return ((l + 15) & ~15) + 4; 
 
 // body shared by chol_near_identity_kernel and the fused CholeskyQR2 kernel
 // (any block size that is a multiple of 32; sm: 2 l near_id_ld(l) doubles)
+// Element-wise pass over an n-element global array written earlier in the same
+// kernel by other CTAs: U independent L2 loads in flight per thread (a plain
+// strided loop waits one L2 round trip, ~0.5 us, per element: 5-6 us for an
+// 80 x 80 matrix on 512 threads).  __ldcg: L2 only, never a stale L1 line.
+template <int U, typename F>
+__device__ __forceinline__ void for_each_l2(const double* __restrict__ src, int n, F&& f) {
+  const int nt = blockDim.x;
+  for (int e0 = threadIdx.x; e0 < n; e0 += U * nt) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nt;
+      v[u] = e < n ? __ldcg(src + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * nt;
+      if (e < n) f(e, v[u]);
+    }
+  }
+}
+
 __device__ void chol_near_identity_body(int l, const double* __restrict__ G, double* __restrict__ Rout,
                                         double* __restrict__ Rinv, int* flag, double tol, double first_order_max,
                                         double* sm) {
@@ -2069,12 +2091,11 @@ __device__ void chol_near_identity_body(int l, const double* __restrict__ G, dou
   __shared__ double red[32];
   const int tid = threadIdx.x, nt = blockDim.x;
   double e = 0.0;
-  for (int idx = tid; idx < l * l; idx += nt) {
+  for_each_l2<16>(G, l * l, [&](int idx, double g) {
     const int r = idx / l, c = idx - r * l;
-    const double g = G[idx];
     e = fmax(e, fabs(g - (r == c ? 1.0 : 0.0)));
     F[r * ld + c] = (c > r) ? g : (c == r ? 0.5 * (g - 1.0) : 0.0);
-  }
+  });
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, o));
   if ((tid & 31) == 0) red[tid >> 5] = e;
@@ -2144,7 +2165,7 @@ __device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, 
     double p = __shfl_sync(0xffffffffu, d[JJ], JJ);
     if (JJ < bs && !(p > tiny)) { badd = 1; p = 1.0; }
     if (JJ >= bs) p = 1.0;
-    const double inv = rsqrt_nr(p);
+    const double inv = rsqrt_rot(p);
     const double rrow = (c > JJ) ? d[JJ] * inv : (c == JJ ? p * inv : 0.0);
     d[JJ] = rrow;
     if (lane == JJ) invd[JJ] = inv;
@@ -2176,29 +2197,31 @@ __device__ void chol_blocked_body(int l, const double* __restrict__ G, double* _
   long long* const prof = (tid == 0) ? g_chol_prof : nullptr;
   long long t0 = prof ? clock64() : 0, ph[6] = {0, 0, 0, 0, 0, 0};
   if (tid == 0) bad = 0;
-  if (w == 0) {
-    double g = 0.0, tr = 0.0;
-    for (int i = lane; i < l; i += 32) { const double v = G[(size_t)i * l + i]; g = fmax(g, v); tr += v; }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
-    tr = warp_sum(tr);
-    if (lane == 0) { gmax_s = g; tr_s = tr; }
-  }
   __syncthreads();
-  const double sh = shift_rel > 0.0 ? shift_rel * tr_s : 0.0;
-  const double tiny = gmax_s * tiny_rel + 1e-300;
   {
     int badl = 0;
-    for (int e = tid; e < l * l; e += nt) {
+    for_each_l2<16>(G, l * l, [&](int e, double v) {
       const int r = e / l, c = e - r * l;
-      double v = G[e];
       if (check_identity && fabs(v - (r == c ? 1.0 : 0.0)) > 1e-3) badl |= 2;
-      if (r == c) v += sh;
       A[r * ld + c] = v;
-    }
+    });
     if (badl) atomicOr(&bad, badl);
   }
   __syncthreads();
+  if (w == 0) {
+    // diagonal statistics (same order as before: lane-strided max / sum, warp reduction)
+    double g = 0.0, tr = 0.0;
+    for (int i = lane; i < l; i += 32) { const double v = A[i * ld + i]; g = fmax(g, v); tr += v; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    tr = warp_sum(tr);
+    const double shw = shift_rel > 0.0 ? shift_rel * tr : 0.0;
+    if (shw != 0.0)
+      for (int i = lane; i < l; i += 32) A[i * ld + i] += shw;
+    if (lane == 0) { gmax_s = g; tr_s = tr; }
+  }
+  __syncthreads();
+  const double tiny = gmax_s * tiny_rel + 1e-300;
   if (prof) { long long t = clock64(); ph[0] += t - t0; t0 = t; }
   const int nb = (l + 15) >> 4;
   for (int kb = 0; kb < nb; ++kb) {
@@ -2579,11 +2602,32 @@ struct FqParams {
 };
 
 __device__ __forceinline__ void fq_reduce(const double* part, int nparts, int ll, double* G) {
-  const int nthr = (gridDim.x - 1) * blockDim.x;
-  for (int e = (blockIdx.x - 1) * blockDim.x + threadIdx.x; e < ll; e += nthr) {
+  // 8 lanes per element: lane j sums partials j, j + 8, ... (all loads in
+  // flight at once), then a fixed 3-level butterfly -- deterministic, and one
+  // L2 round trip instead of nparts dependent ones
+  const int lane8 = threadIdx.x & 7;
+  const int nthr = (gridDim.x - 1) * (blockDim.x >> 3);
+  const int ebase = (blockIdx.x - 1) * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  const int iters = (ll + nthr - 1) / nthr;  // uniform trip count: every lane reaches the shuffles
+  for (int it = 0; it < iters; ++it) {
+    const int e = ebase + it * nthr;
     double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * ll + e];
-    G[e] = s;
+    if (e < ll) {
+      double v[16];
+      for (int p0 = lane8; p0 < nparts; p0 += 8 * 16) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int pp = p0 + 8 * u;
+          v[u] = pp < nparts ? __ldcg(part + (size_t)pp * ll + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += v[u];
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (lane8 == 0 && e < ll) G[e] = s;
   }
 }
 
@@ -2634,7 +2678,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
   if (!fac) {
     // Q1 tile = Y tile R1^{-1}: blocked forward substitution (trsm_blocked_kernel's
     // scheme, 4 threads per row), then the tile's partial of Q1^T Q1
-    for (int e = tid; e < ll; e += kFqThreads) sR[(e / l) * ld + e % l] = P.R1[e];
+    for_each_l2<16>(P.R1, ll, [&](int e, double v) { sR[(e / l) * ld + e % l] = v; });
     __syncthreads();
     for (int j = tid; j < l; j += kFqThreads) rinv[j] = 1.0 / sR[j * ld + j];
     __syncthreads();
@@ -2696,8 +2740,8 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
       double* a = fsm;
       double* b = fsm + (size_t)l * ld;
       for (int e = tid; e < ll; e += kFqThreads) {
-        a[(e / l) * ld + e % l] = P.R2[e];
-        b[(e / l) * ld + e % l] = P.R1[e];
+        a[(e / l) * ld + e % l] = __ldcg(P.R2 + e);
+        b[(e / l) * ld + e % l] = __ldcg(P.R1 + e);
       }
       __syncthreads();
       block_dmma(l, l, l, a, ld, 1, b, ld, 1, P.R, l);
@@ -2707,7 +2751,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
   fq_mark(6);
   if (!fac) {
     // Q tile = Q1 tile R2^{-1}
-    for (int e = tid; e < ll; e += kFqThreads) sR[(e / l) * ld + e % l] = P.I2[e];
+    for_each_l2<16>(P.I2, ll, [&](int e, double v) { sR[(e / l) * ld + e % l] = v; });
     __syncthreads();
     block_dmma(rows, l, l, sY, ld, 1, sR, ld, 1, P.Q + r0 * P.q_rs, (int)P.q_rs);
   }
