@@ -696,11 +696,14 @@ __device__ __forceinline__ void jc_st_u32(uint32_t addr, uint32_t v, uint32_t ba
 __device__ __forceinline__ void jc_arm(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// CTA-scope acquire: the remote st.async data is tracked by this CTA's own
+// mbarrier (complete_tx), as for TMA multicast (a cluster-scope acquire adds an
+// L1 invalidation, CCTL.IVALL, to every wait; measured time-neutral in r01)
 __device__ __forceinline__ void jc_wait(uint32_t bar, uint32_t parity) {
   uint32_t done;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(bar), "r"(parity)
@@ -1029,6 +1032,12 @@ __global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads,
 // plain kernel's round: r01 phase clocks rotate 666 / send 277 / wait 272 /
 // pull 320 at 80 x 80); the others exchange through this CTA's shared memory
 // with one barrier.
+// diagnostics (TTK_JB_DIAG, fixed 9 sweeps): 1 = no rotations, 2 = also no local
+// moves, 3 = barrier only, 4 = stores + barrier.  r01, 80 x 80 on one box: 528 us
+// normal, 488 (1), 339 (2), 370 (3), 431 (4): dots + reduction ~465 cycles per
+// round, rotation ~110 (mostly hidden), local move ~400 (barrier ~90, stores
+// ~160, loads ~160), block moves ~230 per round on average
+__device__ int g_jb_diag = 0;
 constexpr int kJbCluster = 8;
 constexpr int kJbMaxSlots = 16;  // columns per block (8-CTA cluster: <= 8, l <= 128)
 
@@ -1053,6 +1062,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
   const int le = 2 * CL * bs, kk = k;
   const int tid = threadIdx.x, a = tid / kSvdGroup, gl = tid % kSvdGroup;
   const bool active = a < bs;
+  const int diag = g_jb_diag;  // diagnostics only (0 in production)
   constexpr int box = RPL * kSvdGroup;
   const int nv = want_v ? 2 : 1;
   // [2 bufs][bs slots][2 sides][2 (C, V)][box], block inbox then local inbox
@@ -1159,7 +1169,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
           rg += __shfl_xor_sync(0xffffffffu, rg, o);
         }
         if (active && gl == 0 && rg * rg > skip2 * ra * rb) bigf[sweep] = 1;
-        if (active && ra > 0.0 && rb > 0.0 && rg * rg > tol2 * ra * rb) {
+        if (active && ra > 0.0 && rb > 0.0 && rg * rg > tol2 * ra * rb && diag == 0) {
           // jacobi_cluster_kernel's division- and CALL-free rotation
           const long long ex = min((__double_as_longlong(ra + rb) >> 52) & 0x7ff, 2045LL);
           const double sc = __longlong_as_double((2046LL - ex) << 52);
@@ -1188,7 +1198,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
         // ---- local move through this CTA's shared memory ----
         if (prof) { long long t = clock64(); pt[0] += t - tc; tc = t; }
         const int buf = lr & 1;
-        if (br == 0) {
+        if (diag == 2) {
+        } else if (diag == 3) {
+          __syncthreads();
+        } else if (diag == 4) {
+          if (active) {
+            const int ds = (a + 1 == bs) ? 0 : a + 1;
+            put(lslot(buf, ds, 1, 0), y);
+            if (want_v) put(lslot(buf, ds, 1, 1), vy);
+          }
+          __syncthreads();
+        } else if (br == 0) {
           // round-robin over the CTA's 2 bs columns (circle method on bs slots):
           // left(s) -> left(s-1) (s >= 2), left(1) -> right(0), right(s) -> right(s+1),
           // right(bs-1) -> left(bs-1), left(0) fixed
@@ -1292,7 +1312,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
       ch |= *cl.map_shared_rank(&flags[sweep], r);
       big |= *cl.map_shared_rank(&bigf[sweep], r);
     }
-    if (!ch || !big) break;
+    if (diag ? sweep == 8 : (!ch || !big)) break;
   }
   if (c == 0 && tid == 0 && g_svd_sweeps) *g_svd_sweeps = sweep + 1;
   if (prof) {
@@ -1578,6 +1598,12 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   // le - 1); TTK_JACOBI_BLOCK=0 keeps the plain cluster kernel, =4 / =8 picks the
   // cluster size (A/B)
   static const int block_env = getenv("TTK_JACOBI_BLOCK") ? atoi(getenv("TTK_JACOBI_BLOCK")) : -1;
+  static const bool jb_diag_set = [] {
+    const int v = getenv("TTK_JB_DIAG") ? atoi(getenv("TTK_JB_DIAG")) : 0;
+    if (v) cudaMemcpyToSymbol(g_jb_diag, &v, sizeof(int));
+    return true;
+  }();
+  (void)jb_diag_set;
   int block_cl = block_env;
   if (block_cl < 0) {
     // fewest padded columns (dummy columns cost whole rounds), 8 CTAs on ties:
