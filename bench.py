@@ -276,9 +276,16 @@ def run_b200(args):
     x = T.TTVector(C["x"], device=dev)
     drm = [torch.as_tensor(g, device=dev) for g in C["drm"]]
 
+    # the step through the public API: tt_matvec_round_rto pipelines the same
+    # three calls (per-chunk matvec overlapping the event-gated RTO right sweep);
+    # BENCH_UNFUSED=1 times tt_matvec -> rto_sweeps -> tt_truncate_left_orth
+    unfused = os.environ.get("BENCH_UNFUSED") == "1"
+
     def step(op, x):
-        y = T.tt_matvec(op, x)
-        return T.tt_truncate_left_orth(T.rto_sweeps(y, drm), spec)
+        if unfused:
+            y = T.tt_matvec(op, x)
+            return T.tt_truncate_left_orth(T.rto_sweeps(y, drm), spec)
+        return T.tt_matvec_round_rto(op, x, spec, drm, device=dev)
 
     def barrier():
         if world > 1:
@@ -359,10 +366,15 @@ def run_b200(args):
     res_host = None
 
     def e2e_step():
-        a = T.TTOperator([t.to(dev, non_blocking=True) for t in host_op], device=dev)
-        v = T.TTVector([t.to(dev, non_blocking=True) for t in host_x], device=dev)
-        r = step(a, v)
-        return [c.to("cpu", non_blocking=True) for c in r.cores]
+        if unfused:
+            a = T.TTOperator([t.to(dev, non_blocking=True) for t in host_op], device=dev)
+            v = T.TTVector([t.to(dev, non_blocking=True) for t in host_x], device=dev)
+            r = step(a, v)
+            return [c.to("cpu", non_blocking=True) for c in r.cores]
+        # host (pinned) cores in, host cores out: uploads, contraction, rounding
+        # and the result download overlap inside the call
+        r = T.tt_matvec_round_rto(T.TTOperator(host_op), T.TTVector(host_x), spec, drm, device=dev)
+        return list(r.cores)
 
     for _ in range(2):
         res_host = e2e_step()

@@ -69,6 +69,11 @@ size_t ttk_gemm_strided_ws_bytes(int batch, int M, int N, int K);
  * One grouped launch over all d cores; G_k must hold r[k]*rho[k]*m[k]*r[k+1]*rho[k+1]. */
 int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
                const double* const* D, const double* const* C, double* const* G, void* stream);
+/* cores k0 <= k < k1 only (shapes are those of the full TT): lets a caller
+ * contract cores as their uploads land (tt_matvec_round_rto pipeline) */
+int ttk_matvec_range(int d, const int* rho, const int* m, const int* n, const int* r,
+                     const double* const* D, const double* const* C, double* const* G, int k0, int k1,
+                     void* stream);
 
 /* ---- structure-aware tt_matvec (reference tt.py:302-314) --
  * Same result and output layout as ttk_matvec for square operator cores whose
@@ -188,6 +193,12 @@ size_t ttk_tt_round_ws_bytes(int d, const int* dims, const int* ranks);
  * L[c-1] n_{c-1}); out: cores (L[k], n_k, L[k+1]), cores 0..d-2 left-orthonormal. */
 int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X, const int* L,
                    const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream);
+/* same, with ready[k] (cudaEvent_t, entries may be NULL) awaited on `stream`
+ * before core X[k] is first read: the right sweep starts on the last cores
+ * while earlier ones are still being produced */
+int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const* X, const int* L,
+                      const double* const* G, double* const* out, void* ws, size_t ws_bytes,
+                      void* const* ready, void* stream);
 size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L);
 
 /* ---- TT containers (reference save_/load_vector, save_/load_operator,
@@ -242,6 +253,13 @@ size_t ttk_stream_recover_ws_bytes(int d, const int* dims, const int* lr, const 
 int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
                     int max_rank, double* const* out, int* out_ranks, void* ws, size_t ws_bytes,
                     void* stream);
+/* same, and every result core is also copied to host_out[k] (pinned host
+ * memory, room for ranks[k]*dims[k]*ranks[k+1] doubles) as soon as it is
+ * final, overlapping the copies with the rest of the sweep; returns after all
+ * copies completed */
+int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
+                         int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
+                         size_t ws_bytes, void* stream);
 size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks);
 
 #ifdef __cplusplus

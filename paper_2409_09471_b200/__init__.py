@@ -16,7 +16,8 @@ from .precond import (
     precond_apply,
     spectral_interval,
 )
-from .rto import CounterDRM, rto_flops, rto_ranks, rto_sweeps, tt_round_rto, tt_truncate_left_orth
+from .rto import (CounterDRM, rto_flops, rto_ranks, rto_sweeps, tt_matvec_round_rto, tt_round_rto,
+                  tt_truncate_left_orth)
 from .sketch import (KhatriRaoSketch, kr_apply, kr_apply_batch, kr_apply_device, kr_apply_matvec,
                      kr_apply_matvec_device, kr_apply_rows, kr_sketch_new)
 from .solvers import (

@@ -36,6 +36,7 @@ SIGNATURES = {
                                  c_vp, c_size, c_vp]),
     "ttk_gemm_strided_ws_bytes": (c_size, [c_int, c_int, c_int, c_int]),
     "ttk_matvec": (c_int, [c_int, P_int, P_int, P_int, P_int, P_vp, P_vp, P_vp, c_vp]),
+    "ttk_matvec_range": (c_int, [c_int, P_int, P_int, P_int, P_int, P_vp, P_vp, P_vp, c_int, c_int, c_vp]),
     "ttk_matvec_banded": (c_int, [c_int, P_int, P_int, P_int, c_int, P_vp, ctypes.c_char_p, P_vp, P_vp, c_vp]),
     "ttk_mode_multiply": (c_int, [c_int, c_int, P_int, P_int, P_int, P_double, P_vp, P_vp, P_vp, c_vp]),
     "ttk_tt_concat": (c_int, [c_int, c_int, P_double, P_int, P_int, P_vp, P_vp, c_vp]),
@@ -145,6 +146,7 @@ SIGNATURES.update({
                              c_size, c_vp]),
     "ttk_tt_round_ws_bytes": (c_size, [c_int, P_int, P_int]),
     "ttk_rto_sweeps": (c_int, [c_int, P_int, P_int, P_vp, P_int, P_vp, P_vp, c_vp, c_size, c_vp]),
+    "ttk_rto_sweeps_ev": (c_int, [c_int, P_int, P_int, P_vp, P_int, P_vp, P_vp, c_vp, c_size, P_vp, c_vp]),
     "ttk_rto_ws_bytes": (c_size, [c_int, P_int, P_int, P_int]),
 })
 
@@ -160,6 +162,8 @@ SIGNATURES.update({
 
 SIGNATURES.update({
     "ttk_tt_truncate": (c_int, [c_int, P_int, P_int, P_vp, c_double, c_int, P_vp, P_int, c_vp, c_size, c_vp]),
+    "ttk_tt_truncate_host": (c_int, [c_int, P_int, P_int, P_vp, c_double, c_int, P_vp, P_int, P_vp, c_vp, c_size,
+                                     c_vp]),
     "ttk_tt_truncate_ws_bytes": (c_size, [c_int, P_int, P_int]),
 })
 

@@ -87,14 +87,16 @@ size_t ttk_gemm_strided_ws_bytes(int batch, int M, int N, int K) {
 // tt_matvec: G_k[(a*rho0+al), i, (b*rho1+be)] = sum_j D_k[al,i,j,be] * C_k[a,j,b]
 // Reference: ttkrylov/tt.py:302-314 (tensordot over j, transpose (0,2,3,1,4),
 // reshape to (r0*rho0, m, r1*rho1): vector-rank major, operator-rank minor).
-int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
-               const double* const* D, const double* const* C, double* const* G, void* stream) {
+int ttk_matvec_range(int d, const int* rho, const int* m, const int* n, const int* r,
+                     const double* const* D, const double* const* C, double* const* G, int k0, int k1,
+                     void* stream) {
   TTK_REQUIRE(d >= 1, kInvalidValue, "d must be >= 1");
   TTK_REQUIRE(rho[0] == 1 && rho[d] == 1 && r[0] == 1 && r[d] == 1, kShapeMismatch,
               "boundary ranks must equal 1");
+  TTK_REQUIRE(0 <= k0 && k0 <= k1 && k1 <= d, kInvalidValue, "core range [%d, %d) outside [0, %d)", k0, k1, d);
   std::vector<GemmProblem> probs;
   probs.reserve(64);
-  for (int k = 0; k < d; ++k) {
+  for (int k = k0; k < k1; ++k) {
     const int r0 = r[k], r1 = r[k + 1], p0 = rho[k], p1 = rho[k + 1];
     const int mk = m[k], nk = n[k];
     TTK_REQUIRE(r0 >= 0 && r1 >= 0 && p0 >= 1 && p1 >= 1 && mk >= 1 && nk >= 1, kShapeMismatch,
@@ -122,6 +124,11 @@ int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
   if (probs.empty()) return kOk;
   return gemm_group_launch(probs.data(), (int)probs.size(), nullptr, 0, (cudaStream_t)stream,
                            /*allow_split=*/false);
+}
+
+int ttk_matvec(int d, const int* rho, const int* m, const int* n, const int* r,
+               const double* const* D, const double* const* C, double* const* G, void* stream) {
+  return ttk_matvec_range(d, rho, m, n, r, D, C, G, 0, d, stream);
 }
 
 // mode_multiply for nterms matrix lists sharing one TT (the exp-sum terms):

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 namespace ttk {
@@ -265,14 +266,16 @@ size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks) {
          align_up(qrws, 256) + 2 * kSplitKBytes + 131072;
 }
 
-int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
-                    int max_rank, double* const* out, int* out_ranks, void* ws, size_t ws_bytes,
-                    void* stream) {
+int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
+                         int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
+                         size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   TTK_REQUIRE(d >= 1 && rel_tol >= 0.0, kInvalidValue, "tt_truncate: bad arguments");
   for (int k = 0; k <= d; ++k) out_ranks[k] = ranks[k];
   if (d == 1) {
     TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cores[0], sizeof(double) * dims[0], cudaMemcpyDeviceToDevice, st));
+    if (host_out)
+      TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[0], cores[0], sizeof(double) * dims[0], cudaMemcpyDeviceToHost, st));
     TTK_SYNC(st);
     return kOk;
   }
@@ -326,6 +329,8 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
     for (int k = 0; k < d; ++k) TTK_CHECK_CUDA(cudaMemsetAsync(out[k], 0, sizeof(double) * dims[k], st));
     for (int k = 0; k <= d; ++k) out_ranks[k] = 1;
     TTK_SYNC(st);
+    if (host_out)
+      for (int k = 0; k < d; ++k) memset(host_out[k], 0, sizeof(double) * dims[k]);
     return kOk;
   }
   const double budget = rel_tol * nrm / std::sqrt((double)(d - 1));
@@ -357,6 +362,11 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
     TTK_CHECK_CUDA(cudaEventRecord(ev_f[k & 1], st));
     TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_f[k & 1], 0));
     TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_side, side));
+    // core k is final: stream it to the caller's pinned host buffer behind the
+    // rest of the sweep (same side stream, so it also waits for the product)
+    if (host_out)
+      TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[k], out[k], sizeof(double) * (size_t)rk * m, cudaMemcpyDeviceToHost,
+                                     side));
     TTK_CHECK_CUDA(cudaEventRecord(ev_g[k & 1], side));
     g_pending[k & 1] = true;
     long long l_ld = kk;
@@ -374,11 +384,21 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
   }
   TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], cur, sizeof(double) * (size_t)dims[0] * r[1],
                                  cudaMemcpyDeviceToDevice, st));
+  if (host_out)
+    TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[0], cur, sizeof(double) * (size_t)dims[0] * r[1],
+                                   cudaMemcpyDeviceToHost, st));
   for (int i = 0; i < 2; ++i)
     if (g_pending[i]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[i], 0));
   TTK_SYNC(st);
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
   return kOk;
+}
+
+int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
+                    int max_rank, double* const* out, int* out_ranks, void* ws, size_t ws_bytes,
+                    void* stream) {
+  return ttk_tt_truncate_host(d, dims, ranks, cores, rel_tol, max_rank, out, out_ranks, nullptr, ws, ws_bytes,
+                              stream);
 }
 
 // --------------------------------------------------------------------------
@@ -401,13 +421,21 @@ size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L) {
 // cores (L[k], n_k, L[k+1]) with L[0] = L[d] = 1 and, for every cut c,
 // L[c] <= min(R[c], L[c-1] * n_{c-1}); out: d cores (L[k], n_k, L[k+1]).
 // Cores 0..d-2 of the result are left-orthonormal.
-int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X, const int* L,
-                   const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream) {
+int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const* X, const int* L,
+                      const double* const* G, double* const* out, void* ws, size_t ws_bytes,
+                      void* const* ready, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  // ready[c] (optional): event after which X[c] may be read -- lets the
+  // caller stream the matvec output in core by core (right to left)
+  auto wait_core = [&](int c) -> int {
+    if (ready && ready[c]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)ready[c], 0));
+    return kOk;
+  };
   TTK_REQUIRE(d >= 1, kInvalidValue, "rto: d must be >= 1");
   TTK_REQUIRE(R[0] == 1 && R[d] == 1 && L[0] == 1 && L[d] == 1, kShapeMismatch,
               "rto: boundary ranks must equal 1");
   if (d == 1) {
+    TTK_TRY(wait_core(0));
     TTK_CHECK_CUDA(cudaMemcpyAsync(out[0], X[0], sizeof(double) * dims[0], cudaMemcpyDeviceToDevice, st));
     return kOk;
   }
@@ -445,6 +473,7 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
   // ---- right sweep: W_c = sum_i X_c[:, i, :] W_{c+1} G_c[:, i, :]^T ----
   for (int c = d - 1; c >= 1; --c) {
     const int n = dims[c], rc = R[c], lc = L[c], l1 = L[c + 1], r1 = R[c + 1];
+    TTK_TRY(wait_core(c));
     const double* Tin;
     if (c == d - 1) {
       Tin = X[c];  // (R_c, n, 1): W_d = [[1]]
@@ -474,6 +503,7 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
   }
   int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
   const double* Mprev = nullptr;
+  TTK_TRY(wait_core(0));
   for (int c = 1; c < d; ++c) {
     const int np = dims[c - 1];
     const int m = L[c - 1] * np, l = L[c], rc = R[c];
@@ -510,6 +540,11 @@ int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X,
     TTK_TRY(gemm1(l, n, rc, Mprev, rc, 1, X[c], n, 1, out[d - 1], n, 1, split_ws, st));
   }
   return kOk;
+}
+
+int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X, const int* L,
+                   const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream) {
+  return ttk_rto_sweeps_ev(d, dims, R, X, L, G, out, ws, ws_bytes, nullptr, stream);
 }
 
 }  // extern "C"

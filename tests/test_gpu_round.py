@@ -263,3 +263,36 @@ def test_counter_drm_blocks_and_moments(cuda):
     big = T.CounterDRM([64, 64], [256], seed=7, device=cuda).cores[1]  # 256 x 64 x 1
     z = (big * math.sqrt(256 * 64)).flatten().cpu().numpy()
     assert abs(z.mean()) < 0.05 and abs(z.std() - 1.0) < 0.05
+
+
+@pytest.mark.parametrize("host,chunk", [(False, 1), (False, 4), (True, 3), (True, 100)])
+def test_matvec_round_rto_pipeline(cuda, host, chunk):
+    """tt_matvec_round_rto (per-core uploads, chunked matvec, event-gated RTO
+    sweeps, host-streamed truncation) == tt_matvec -> rto_sweeps ->
+    tt_truncate_left_orth, bit for bit, and == the oracle."""
+    rng = np.random.default_rng(5)
+    dims = [12, 10, 16, 9, 14, 11, 8]
+    d = len(dims)
+    opc = [rng.standard_normal((1 if k == 0 else 3, n, n, 1 if k == d - 1 else 3)) for k, n in enumerate(dims)]
+    x = O.tt_random(dims, [6, 9, 12, 10, 8, 5], seed=8)
+    drm = O.drm_new(dims, [14, 20, 24, 20, 16, 10], seed=2)
+    spec = T.RoundSpec(1e-9, 11)
+    dev_op, dev_x = T.TTOperator(opc, device=cuda), T.TTVector(x, device=cuda)
+    G = [torch.as_tensor(g, device=cuda) for g in drm]
+    ref = T.tt_truncate_left_orth(T.rto_sweeps(T.tt_matvec(dev_op, dev_x), G), spec)
+    if host:
+        a = T.TTOperator([torch.as_tensor(c).pin_memory() for c in opc])
+        v = T.TTVector([torch.as_tensor(c).pin_memory() for c in x])
+    else:
+        a, v = dev_op, dev_x
+    got = T.tt_matvec_round_rto(a, v, spec, G, chunk=chunk, device=cuda)
+    torch.cuda.synchronize()
+    assert got.device.type == ("cpu" if host else "cuda")
+    assert got.ranks == ref.ranks
+    for g, w in zip(got.cores, ref.cores):
+        assert torch.equal(g.cpu(), w.cpu())
+    y = O.matvec(opc, x)
+    ls = O.rto_ranks(dims, [1] + [c.shape[2] for c in y], [14, 20, 24, 20, 16, 10])
+    want = O.rto_round(y, O.slice_drm(drm, ls), 1e-9, 11)
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.rel_diff([c.cpu().numpy() for c in got.cores], want) <= 1e-10
