@@ -1357,6 +1357,312 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
 }
 
 // ---------------------------------------------------------------------------
+// One-warp-per-CTA block Jacobi (the truncation's SVD for 40 < l, rows <= 96).
+// The block kernel above spends ~400 of its
+// ~1300 cycles per round on the in-CTA move (shared-memory stores, a 3-warp
+// barrier, loads).  Here a CTA is ONE warp holding 4 pair slots of 8 lanes
+// (rows gl, gl + 8, ...; RPL per lane), so every in-CTA move is a register
+// shuffle inside the warp -- no shared memory, no barrier -- and the dot
+// products reduce over 3 shuffle levels instead of 4.  The cluster has
+// CL = le / 8 CTAs (10 for l = 80; sizes above 8 use the non-portable cluster
+// attribute, <= 16), each holding a P and a Q block of 4 columns; the sweep
+// order is the block kernel's (round-robin over the CTA's 8 columns, then
+// 2 CL - 2 block rounds of 4 cross rounds, blocks moving between CTAs by the
+// circle method over DSMEM between block rounds).
+// r01, same box, 80 x 80 with V: 512 us vs 546 us for the 16-lane block kernel
+// (50 x 50: 302 vs 305).  Phase clocks (80 x 80, per round): dots + 3-level
+// reduction ~230 cycles, rotation + apply ~475, shuffle move ~440, block moves
+// ~240 averaged -- the shuffles (40-80 SHFL.32 per lane per round) are not
+// cheaper than the shared-memory move, and an fp32 rotation angle (fp64
+// normalisation) measured time-neutral: the round is issue/latency bound
+// across the whole chain, not by one piece.
+constexpr int kJwSlots = 4, kJwLanes = 8;
+
+template <int RPL>
+__global__ void __launch_bounds__(32, 1)
+    jacobi_warp_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
+                       double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
+                       int scaled_u, double skip2) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int c = (int)cl.block_rank();
+  static_assert(RPL % 2 == 0, "RPL must be even");
+  constexpr int box = RPL * kJwLanes;  // doubles per column part
+  // block-move inbox: [2 bufs][4 slots][2 sides][2 (C, V)][box]
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double nrm[kQrMaxCols + 2];
+  __shared__ double fin[kQrMaxCols + 2];
+  __shared__ int order[kQrMaxCols + 2];
+  __shared__ int flags[64];
+  __shared__ int bigf[64];
+  __shared__ int bid[2][kJwSlots][2];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  const int le = 2 * kJwSlots * CL, kk = k;
+  const int lane = threadIdx.x, s = lane >> 3, gl = lane & 7;
+  const int nv = want_v ? 2 : 1;
+  auto bslot = [&](int buf, int slot, int side, int cv) {
+    return sm + ((((size_t)buf * kJwSlots + slot) * 2 + side) * 2 + cv) * box + gl * 2;
+  };
+  const uint32_t msg_bytes = (uint32_t)(box * 8 * nv + 4);
+  const uint32_t rx_bytes = (uint32_t)kJwSlots * msg_bytes * ((c >= 1 && c <= CL - 2) ? 2u : 1u);
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&mbar[0]);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    jc_arm(bar0, rx_bytes);
+    jc_arm(bar0 + 8, rx_bytes);
+  }
+  // column norms (lane-parallel over columns), ranking by decreasing norm
+  for (int cc = lane; cc < l; cc += 32) {
+    double s0 = 0.0, s1 = 0.0;
+    int r = 0;
+    for (; r + 1 < kk; r += 2) {
+      const double u0 = B[(long long)r * b_rs + (long long)cc * b_cs];
+      const double u1 = B[(long long)(r + 1) * b_rs + (long long)cc * b_cs];
+      s0 += u0 * u0;
+      s1 += u1 * u1;
+    }
+    if (r < kk) { const double u0 = B[(long long)r * b_rs + (long long)cc * b_cs]; s0 += u0 * u0; }
+    nrm[cc] = s0 + s1;
+  }
+  for (int i = lane; i < 64; i += 32) { flags[i] = 0; bigf[i] = 0; }
+  __syncwarp();
+  for (int cc = lane; cc < l; cc += 32) {
+    int rank = 0;
+    for (int j = 0; j < l; ++j) rank += (nrm[j] > nrm[cc]) || (nrm[j] == nrm[cc] && j < cc);
+    order[rank] = cc;
+  }
+  __syncwarp();
+  int idl = c * kJwSlots + s, idr = le - 1 - (c * kJwSlots + s);
+  double x[RPL], y[RPL], vx[RPL], vy[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = gl + i * kJwLanes;
+    const bool okl = r < kk && idl < l, okr = r < kk && idr < l;
+    x[i] = okl ? B[(long long)r * b_rs + (long long)order[idl] * b_cs] : 0.0;
+    y[i] = okr ? B[(long long)r * b_rs + (long long)order[idr] * b_cs] : 0.0;
+    vx[i] = (want_v && idl < l && r == order[idl]) ? 1.0 : 0.0;
+    vy[i] = (want_v && idr < l && r == order[idr]) ? 1.0 : 0.0;
+  }
+  const double tol = (double)max(kk, 1) * 1.1102230246251565e-16;
+  const double tol2 = tol * tol;
+  const bool send_p = c >= 1, send_q = c <= CL - 2;
+  uint32_t p_c = 0, p_id = 0, p_bar = 0, q_c = 0, q_id = 0, q_bar = 0;
+  if (send_p) {
+    const int side = (c == 1) ? 1 : 0;
+    p_c = jc_map(bslot(0, s, side, 0), c - 1);
+    p_id = jc_map(&bid[0][s][side], c - 1);
+    p_bar = jc_map(&mbar[0], c - 1);
+  }
+  if (send_q) {
+    q_c = jc_map(bslot(0, s, 1, 0), c + 1);
+    q_id = jc_map(&bid[0][s][1], c + 1);
+    q_bar = jc_map(&mbar[0], c + 1);
+  }
+  const uint32_t bbuf_bytes = (uint32_t)(kJwSlots * 4 * box * 8);
+  const uint32_t bid_bytes = (uint32_t)(kJwSlots * 2 * sizeof(int));
+  constexpr uint32_t pstride = 2u * kJwLanes * 8u;  // bytes between a lane's double2 pairs
+  cl.sync();  // barriers initialised and armed in every CTA before the first remote store
+
+  long long* const prof = (lane == 0) ? g_jc_prof : nullptr;
+  long long pt[4] = {0, 0, 0, 0}, tc = 0;
+  int lr = 0;
+  int sweep = 0, moves = 0;
+  for (; sweep < 60; ++sweep) {
+    int rot = 0, big = 0;
+    for (int br = 0; br < 2 * CL - 1; ++br) {
+      const int nr = (br == 0) ? 2 * kJwSlots - 1 : kJwSlots;
+      for (int t = 0; t < nr; ++t) {
+        // ---- rotate the pair (x, y): 8-lane dot products, 3 shuffle levels ----
+        if (prof) tc = clock64();
+        double ra0 = 0.0, rb0 = 0.0, rg0 = 0.0, ra1 = 0.0, rb1 = 0.0, rg1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < RPL; i += 2) {
+          ra0 = fma(x[i], x[i], ra0); rb0 = fma(y[i], y[i], rb0); rg0 = fma(x[i], y[i], rg0);
+          ra1 = fma(x[i + 1], x[i + 1], ra1); rb1 = fma(y[i + 1], y[i + 1], rb1); rg1 = fma(x[i + 1], y[i + 1], rg1);
+        }
+        double ra = ra0 + ra1, rb = rb0 + rb1, rg = rg0 + rg1;
+#pragma unroll
+        for (int o = kJwLanes / 2; o > 0; o >>= 1) {
+          ra += __shfl_xor_sync(0xffffffffu, ra, o);
+          rb += __shfl_xor_sync(0xffffffffu, rb, o);
+          rg += __shfl_xor_sync(0xffffffffu, rg, o);
+        }
+        if (prof) { long long t2 = clock64(); pt[3] += t2 - tc; }
+        if (rg * rg > skip2 * ra * rb) big = 1;
+        if (ra > 0.0 && rb > 0.0 && rg * rg > tol2 * ra * rb) {
+          rot = 1;
+          const long long ex = min((__double_as_longlong(ra + rb) >> 52) & 0x7ff, 2045LL);
+          const double sc = __longlong_as_double((2046LL - ex) << 52);
+          const double dd = (rb - ra) * sc, w = 2.0 * rg * sc;
+          const double q = dd * dd + w * w;
+          const double rho = q * rsqrt_rot(q);
+          const double sum = fabs(dd) + rho;
+          const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
+          const double cs = sum * rq, sn = (dd >= 0.0 ? w : -w) * rq;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const double xi = x[i], yi = y[i];
+            x[i] = cs * xi - sn * yi;
+            y[i] = sn * xi + cs * yi;
+          }
+          if (want_v) {
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              const double xi = vx[i], yi = vy[i];
+              vx[i] = cs * xi - sn * yi;
+              vy[i] = sn * xi + cs * yi;
+            }
+          }
+        }
+        // ---- in-CTA move: register shuffles inside the warp ----
+        if (prof) { long long t2 = clock64(); pt[0] += t2 - tc; tc = t2; }
+        if (br == 0) {
+          // circle method on the 4 slots: left(s) <- left(s+1) (s = 1, 2),
+          // left(3) <- right(3), left(0) fixed; right(0) <- left(1), right(s) <- right(s-1)
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const double tx = __shfl_down_sync(0xffffffffu, x[i], kJwLanes);
+            const double ty = __shfl_up_sync(0xffffffffu, y[i], kJwLanes);
+            const double nx = (s == 0) ? x[i] : (s == kJwSlots - 1 ? y[i] : tx);
+            y[i] = (s == 0) ? tx : ty;
+            x[i] = nx;
+          }
+          if (want_v) {
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) {
+              const double tx = __shfl_down_sync(0xffffffffu, vx[i], kJwLanes);
+              const double ty = __shfl_up_sync(0xffffffffu, vy[i], kJwLanes);
+              const double nx = (s == 0) ? vx[i] : (s == kJwSlots - 1 ? vy[i] : tx);
+              vy[i] = (s == 0) ? tx : ty;
+              vx[i] = nx;
+            }
+          }
+          const int tl = __shfl_down_sync(0xffffffffu, idl, kJwLanes);
+          const int tr = __shfl_up_sync(0xffffffffu, idr, kJwLanes);
+          const int nl = (s == 0) ? idl : (s == kJwSlots - 1 ? idr : tl);
+          idr = (s == 0) ? tl : tr;
+          idl = nl;
+        } else {
+          // the Q block shifts one slot: right(s) <- right(s-1 mod 4)
+          const int src = (lane + 32 - kJwLanes) & 31;
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) y[i] = __shfl_sync(0xffffffffu, y[i], src);
+          if (want_v) {
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) vy[i] = __shfl_sync(0xffffffffu, vy[i], src);
+          }
+          idr = __shfl_sync(0xffffffffu, idr, src);
+        }
+        if (prof) { long long t2 = clock64(); pt[1] += t2 - tc; tc = t2; }
+        ++lr;
+      }
+      // ---- block move between CTAs (DSMEM, completion on the receiver's mbarrier) ----
+      {
+        const int buf = moves & 1;
+        const uint32_t bo = buf * bbuf_bytes, io = buf * bid_bytes, mo = buf * 8;
+        if (send_p) {
+#pragma unroll
+          for (int j = 0; j < RPL; j += 2) jc_st_v2(p_c + bo + pstride * (j / 2), x[j], x[j + 1], p_bar + mo);
+          if (want_v) {
+#pragma unroll
+            for (int j = 0; j < RPL; j += 2)
+              jc_st_v2(p_c + bo + box * 8 + pstride * (j / 2), vx[j], vx[j + 1], p_bar + mo);
+          }
+          if (gl == 0) jc_st_u32(p_id + io, (uint32_t)idl, p_bar + mo);
+        }
+        if (send_q) {
+#pragma unroll
+          for (int j = 0; j < RPL; j += 2) jc_st_v2(q_c + bo + pstride * (j / 2), y[j], y[j + 1], q_bar + mo);
+          if (want_v) {
+#pragma unroll
+            for (int j = 0; j < RPL; j += 2)
+              jc_st_v2(q_c + bo + box * 8 + pstride * (j / 2), vy[j], vy[j + 1], q_bar + mo);
+          }
+          if (gl == 0) jc_st_u32(q_id + io, (uint32_t)idr, q_bar + mo);
+        }
+        jc_wait(bar0 + mo, (moves >> 1) & 1);
+        __syncwarp();
+        if (lane == 0) jc_arm(bar0 + mo, rx_bytes);  // for move + 2
+        auto get = [&](const double* src, double* v) {
+          const double2* p = reinterpret_cast<const double2*>(src);
+#pragma unroll
+          for (int j = 0; j < RPL / 2; ++j) { double2 t2 = p[j * kJwLanes]; v[2 * j] = t2.x; v[2 * j + 1] = t2.y; }
+        };
+        if (c >= 1) {
+          if (c == CL - 1) {
+#pragma unroll
+            for (int i = 0; i < RPL; ++i) { x[i] = y[i]; vx[i] = vy[i]; }
+            idl = idr;
+          } else {
+            get(bslot(buf, s, 0, 0), x);
+            if (want_v) get(bslot(buf, s, 0, 1), vx);
+            idl = bid[buf][s][0];
+          }
+        }
+        get(bslot(buf, s, 1, 0), y);
+        if (want_v) get(bslot(buf, s, 1, 1), vy);
+        idr = bid[buf][s][1];
+        ++moves;
+        if (prof) { long long t2 = clock64(); pt[2] += t2 - tc; tc = t2; }
+      }
+    }
+    if (__any_sync(0xffffffffu, rot) && lane == 0) flags[sweep] = 1;
+    if (__any_sync(0xffffffffu, big) && lane == 0) bigf[sweep] = 1;
+    // every rotation of this sweep is ordered before this cluster barrier
+    cl.sync();
+    int ch = 0, bg = 0;
+#pragma unroll 1
+    for (int r = 0; r < CL; ++r) {
+      ch |= *cl.map_shared_rank(&flags[sweep], r);
+      bg |= *cl.map_shared_rank(&bigf[sweep], r);
+    }
+    if (!ch || !bg) break;
+  }
+  if (c == 0 && lane == 0 && g_svd_sweeps) *g_svd_sweeps = sweep + 1;
+  if (prof && c < 8) {
+    for (int i = 0; i < 4; ++i) atomicAdd((unsigned long long*)&prof[c * 5 + i], (unsigned long long)pt[i]);
+    atomicAdd((unsigned long long*)&prof[c * 5 + 4], (unsigned long long)lr);
+  }
+  // final norms of every column, broadcast to every CTA
+  double na = 0.0, nb = 0.0;
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) { na += x[i] * x[i]; nb += y[i] * y[i]; }
+#pragma unroll
+  for (int o = kJwLanes / 2; o > 0; o >>= 1) {
+    na += __shfl_xor_sync(0xffffffffu, na, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+  }
+  na = sqrt(na); nb = sqrt(nb);
+  if (gl == 0)
+    for (int r = 0; r < CL; ++r) {
+      *cl.map_shared_rank(&fin[idl], r) = na;
+      *cl.map_shared_rank(&fin[idr], r) = nb;
+    }
+  cl.sync();
+  const int kout = min(kk, l);
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const int id = side ? idr : idl;
+    const double nv2 = side ? nb : na;
+    int rank = 0;
+    for (int j = 0; j < le; ++j) rank += (fin[j] > nv2) || (fin[j] == nv2 && j < id);
+    if (id >= l || rank >= kout) continue;
+    if (gl == 0) S[rank] = nv2;
+    const double inv = (scaled_u || nv2 <= 0.0) ? 1.0 : 1.0 / nv2;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = gl + i * kJwLanes;
+      const double cv = side ? y[i] : x[i];
+      if (r < kk) U[(size_t)r * kout + rank] = scaled_u ? cv : (nv2 > 0.0 ? cv * inv : 0.0);
+      if (want_v && V && r < l) V[(size_t)r * kout + rank] = side ? vy[i] : vx[i];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Single-CTA variant for small factorisations (le <= 64, rows <= 64): the same
 // register-resident pair slots, tournament and rotation as the cluster kernel,
 // but every move stays in this CTA's shared memory (double-buffered inbox, one
@@ -1591,6 +1897,49 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
       const size_t jsm = sizeof(double) * 2 * np * 4 * 4 * kSvdGroup;
       jacobi_local_kernel<4><<<1, threads, jsm, st>>>(k, l, B, b_rs, b_cs, U, S, V, want, scaled_u, skip2);
     }
+    TTK_CHECK_LAUNCH();
+    return kOk;
+  }
+  // one-warp-per-CTA block kernel (in-CTA moves are shuffles); TTK_JACOBI_WARP=0
+  // keeps the 16-lane block kernel below (A/B)
+  static const bool warp_off = getenv("TTK_JACOBI_WARP") && atoi(getenv("TTK_JACOBI_WARP")) == 0;
+  if (!single_cta && !warp_off && l > 2 * kJwSlots && std::max(k, l) <= 12 * kJwLanes &&
+      (l + 2 * kJwSlots - 1) / (2 * kJwSlots) <= 16) {
+    const int CL = (l + 2 * kJwSlots - 1) / (2 * kJwSlots);
+    const int rows = std::max(k, l);
+    const int rpl = ((rows + kJwLanes - 1) / kJwLanes + 1) & ~1;
+    static bool wattr = false;
+    if (!wattr) {
+      for (const void* fn : {(const void*)jacobi_warp_kernel<2>, (const void*)jacobi_warp_kernel<4>,
+                             (const void*)jacobi_warp_kernel<6>, (const void*)jacobi_warp_kernel<8>,
+                             (const void*)jacobi_warp_kernel<10>, (const void*)jacobi_warp_kernel<12>})
+        TTK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      wattr = true;
+    }
+    const size_t jsm = sizeof(double) * 2 * kJwSlots * 4 * (size_t)rpl * kJwLanes;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL, 1, 1);
+    cfg.blockDim = dim3(32, 1, 1);
+    cfg.dynamicSmemBytes = jsm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int want = V != nullptr;
+    cudaError_t e;
+    switch (rpl) {
+      case 2: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<2>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 4: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<4>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 6: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<6>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 8: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<8>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 10: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      default: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<12>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+    }
+    TTK_CHECK_CUDA(e);
     TTK_CHECK_LAUNCH();
     return kOk;
   }
