@@ -2959,6 +2959,7 @@ __global__ void __launch_bounds__(kTbThreads)
 // grid barriers.  Same arithmetic as the unfused path (same Cholesky, TRSM,
 // near-identity and DMMA products), fixed reduction order.
 constexpr int kFqRows = 128, kFqThreads = 512, kFqMaxCols = 96;
+constexpr int kFqTiles = 128;  // target tile CTAs (SMs left free for side-stream work)
 
 struct FqParams {
   int m, l;
@@ -2974,6 +2975,7 @@ struct FqParams {
   double* I2;     // R2^{-1}
   int* status;    // [0] first pass, [1] second pass, [4] near-identity flag
   double first_order_max;
+  int tr;         // rows per tile CTA
 };
 
 __device__ __forceinline__ void fq_reduce(const double* part, int nparts, int ll, double* G) {
@@ -3021,14 +3023,15 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
   extern __shared__ __align__(16) double fsm[];
   const int l = P.l, ld = ((l + 15) & ~15) + 4, tid = threadIdx.x;
   const bool fac = blockIdx.x == 0;  // the factorisation CTA
-  double* sY = fsm;                           // kFqRows x ld   (tile CTAs)
-  double* sR = sY + (size_t)kFqRows * ld;     // l x ld
+  const int tr = P.tr;                        // rows per tile (multiple of 8, <= kFqRows)
+  double* sY = fsm;                           // tr x ld   (tile CTAs)
+  double* sR = sY + (size_t)tr * ld;          // l x ld
   double* rinv = sR + (size_t)l * ld;         // l
-  const long long r0 = (long long)(blockIdx.x - 1) * kFqRows;
-  const int rows = fac ? 0 : (int)(P.m - r0 < kFqRows ? P.m - r0 : kFqRows);
+  const long long r0 = (long long)(blockIdx.x - 1) * tr;
+  const int rows = fac ? 0 : (int)(P.m - r0 < tr ? P.m - r0 : tr);
   const int nparts = gridDim.x - 1, ll = l * l;
   if (!fac) {
-    for (int e = tid; e < kFqRows * l; e += kFqThreads) {
+    for (int e = tid; e < tr * l; e += kFqThreads) {
       const int r = e / l, c = e - r * l;
       const bool ok = r < rows;
       cp_async8(sY + r * ld + c, ok ? P.Y + (r0 + r) * P.y_rs + (long long)c * P.y_cs : P.Y, ok);
@@ -3037,7 +3040,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
     cp_async_wait<0>();
     __syncthreads();
     // Gram partial of the tile (zero rows beyond m contribute nothing)
-    block_dmma(l, l, kFqRows, sY, 1, ld, sY, ld, 1, sR, ld);
+    block_dmma(l, l, tr, sY, 1, ld, sY, ld, 1, sR, ld);
     __syncthreads();
     double* mine = P.part + (size_t)(blockIdx.x - 1) * ll;
     for (int e = tid; e < ll; e += kFqThreads) mine[e] = sR[(e / l) * ld + e % l];
@@ -3061,41 +3064,43 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
     for (int j0 = 0; j0 < l; j0 += 16) {
       const int bs = min(16, l - j0);
       if (j0 > 0) {
-        block_dmma(kFqRows, bs, j0, sY, ld, 1, sR + j0, ld, 1, sY + j0, ld, nullptr, nullptr, nullptr, true);
+        block_dmma(tr, bs, j0, sY, ld, 1, sR + j0, ld, 1, sY + j0, ld, nullptr, nullptr, nullptr, true);
         __syncthreads();
       }
-      double t[4];
+      if (row < tr) {  // warp-uniform: a warp holds 8 rows and tr is a multiple of 8
+        double t[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = g + 4 * k;
-        t[k] = (c < bs) ? sY[row * ld + j0 + c] : 0.0;
-      }
+        for (int k = 0; k < 4; ++k) {
+          const int c = g + 4 * k;
+          t[k] = (c < bs) ? sY[row * ld + j0 + c] : 0.0;
+        }
 #pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        if (jj < bs) {
-          const int kj = jj >> 2;
-          double v = t[kj] * rinv[j0 + jj];
-          v = __shfl_sync(0xffffffffu, v, (threadIdx.x & ~3) | (jj & 3), 32);
-          if ((jj & 3) == g) t[kj] = v;
-          const double* rr = sR + (j0 + jj) * ld + j0;
+        for (int jj = 0; jj < 16; ++jj) {
+          if (jj < bs) {
+            const int kj = jj >> 2;
+            double v = t[kj] * rinv[j0 + jj];
+            v = __shfl_sync(0xffffffffu, v, (threadIdx.x & ~3) | (jj & 3), 32);
+            if ((jj & 3) == g) t[kj] = v;
+            const double* rr = sR + (j0 + jj) * ld + j0;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int c = g + 4 * k;
-            if (c > jj && c < bs) t[k] -= v * rr[c];
+            for (int k = 0; k < 4; ++k) {
+              const int c = g + 4 * k;
+              if (c > jj && c < bs) t[k] -= v * rr[c];
+            }
           }
         }
-      }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = g + 4 * k;
-        if (c < bs) sY[row * ld + j0 + c] = t[k];
+        for (int k = 0; k < 4; ++k) {
+          const int c = g + 4 * k;
+          if (c < bs) sY[row * ld + j0 + c] = t[k];
+        }
       }
       __syncthreads();
     }
-    if (row >= rows)  // padded rows stay zero (rinv scaling of zeros is zero; keep it exact)
+    if (row >= rows && row < tr)  // padded rows stay zero (rinv scaling of zeros is zero; keep it exact)
       for (int c = g; c < l; c += 4) sY[row * ld + c] = 0.0;
     __syncthreads();
-    block_dmma(l, l, kFqRows, sY, 1, ld, sY, ld, 1, sR, ld);
+    block_dmma(l, l, tr, sY, 1, ld, sY, ld, 1, sR, ld);
     __syncthreads();
     double* mine = P.part + (size_t)(blockIdx.x - 1) * ll;
     for (int e = tid; e < ll; e += kFqThreads) mine[e] = sR[(e / l) * ld + e % l];
@@ -3130,13 +3135,15 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
     __syncthreads();
     block_dmma(rows, l, l, sY, ld, 1, sR, ld, 1, P.Q + r0 * P.q_rs, (int)P.q_rs);
   }
-  grid.sync();
-  fq_mark(15);
+  if (g_fq_prof) {  // diagnostics only: the kernel's end orders the Q tiles
+    grid.sync();
+    fq_mark(15);
+  }
 }
 
-size_t cholqr2_fused_smem(int l) {
+size_t cholqr2_fused_smem(int l, int tr) {
   const size_t ld = ((l + 15) & ~15) + 4;
-  const size_t tile = (size_t)kFqRows * ld + (size_t)l * ld + ((l + 1) & ~1);
+  const size_t tile = (size_t)tr * ld + (size_t)l * ld + ((l + 1) & ~1);
   const size_t fac = 2 * (size_t)l * ld + 256 * (size_t)((l + 15) / 16);
   return sizeof(double) * std::max(tile, fac);
 }
@@ -3144,7 +3151,7 @@ size_t cholqr2_fused_smem(int l) {
 bool cholqr2_fused_fits(int m, int l, long long q_cs) {
   static const bool off = getenv("TTK_QR_NO_FUSED") != nullptr;  // A/B
   return !off && l <= kFqMaxCols && m >= l && q_cs == 1 && (m + kFqRows - 1) / kFqRows <= kNumSMs - 1 &&
-         cholqr2_fused_smem(l) <= 220 * 1024;
+         cholqr2_fused_smem(l, kFqRows) <= 220 * 1024;
 }
 
 int trsm_right_upper(int m, int l, const double* Y, long long y_rs, long long y_cs, const double* R, double* Q,
@@ -3268,10 +3275,17 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     fp.m = m; fp.l = l; fp.Y = Y; fp.y_rs = y_rs; fp.y_cs = y_cs; fp.Q = Q; fp.q_rs = q_rs; fp.R = R;
     fp.part = (double*)split; fp.G = G; fp.R1 = R1; fp.R2 = R2; fp.I2 = I2; fp.status = status;
     fp.first_order_max = fo;
-    const int grid = 1 + (m + kFqRows - 1) / kFqRows;
+    // tile rows: spread the tall dimension over up to kFqTiles CTAs (the tile
+    // phases are per-SM DMMA work: 10240 x 80 in 80-row tiles instead of 128);
+    // TTK_FQ_ROWS pins it (A/B)
+    static const int fq_rows = getenv("TTK_FQ_ROWS") ? atoi(getenv("TTK_FQ_ROWS")) : 0;
+    int trows = fq_rows > 0 ? fq_rows : (int)(((m + kFqTiles - 1) / kFqTiles + 7) & ~7);
+    trows = std::max(8, std::min(kFqRows, (trows + 7) & ~7));
+    fp.tr = trows;
+    const int grid = 1 + (m + trows - 1) / trows;
     void* args[] = {&fp};
     const cudaError_t le = cudaLaunchCooperativeKernel((const void*)cholqr2_fused_kernel, dim3(grid),
-                                                       dim3(kFqThreads), args, cholqr2_fused_smem(l), st);
+                                                       dim3(kFqThreads), args, cholqr2_fused_smem(l, trows), st);
     if (le == cudaSuccess) {
       fast_tried = true;
       TTK_CHECK_LAUNCH();
@@ -3424,7 +3438,9 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
   if (m <= 0 || l <= 0) return kOk;
   // CholeskyQR2 pays off only for tall inputs that need a multi-panel tree
   static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;  // 1: Householder only
-  if (qr_mode != 1 && l <= kCholMaxCols && m >= 4 * l && m > 512) {
+  // (r01: Householder 128 x 80 400 us vs 246, 256 x 40 235 vs 100, 512 x 100 1986 vs
+  // 140; only the smallest panels, e.g. 32 x 20 43 vs 76 us, stay on Householder)
+  if (qr_mode != 1 && l <= kCholMaxCols && ((m >= 4 * l && m > 512) || (m >= l && l >= 32))) {
     int ok = 0;
     const double* Y = A;
     long long y_rs = a_rs, y_cs = a_cs;
