@@ -139,11 +139,12 @@ def load_peaks():
 def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=None):
     """The step's dominant kernel by time is the one-sided Jacobi SVD of the
     truncation (one per core, a sequential chain).  It runs on one 8-CTA
-    cluster (qr.cu jacobi_block_kernel): pair slots spread over 8 SMs,
-    columns register-resident, block-ordered rounds (in-CTA moves through
-    shared memory, 15 DSMEM block moves per sweep).  Time one l x l
+    cluster (qr.cu jacobi_warp_kernel): one warp per CTA, l/8 CTAs (10 for
+    l = 80), 4 pair slots of 8 lanes per CTA, columns register-resident,
+    block-ordered rounds (in-CTA moves by warp shuffles, 2 l/8 - 1 DSMEM block
+    moves per sweep).  Time one l x l
     instance live and report its algorithmic FLOPs against the fp64 peak of
-    the 8 SMs it occupies; the bound is the per-round latency chain."""
+    the SMs it occupies; the bound is the per-round latency chain."""
     from paper_2409_09471_b200 import _lib
     lib = _lib.load()
     g = torch.Generator().manual_seed(0)
@@ -170,14 +171,16 @@ def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=No
     lib.ttk_debug_svd_sweeps(None)
     # per sweep l(l-1)/2 pairs x (3 dot FMAs + 2x2 rotation FMAs on C and on V) per row
     flops = sweeps * (l * (l - 1) / 2) * (6.0 * l + 12.0 * l)
-    peak8 = 8 * 33.9e3 / 148  # GFLOP/s of 8 SMs, measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
+    sms = (l + 7) // 8  # CTAs (one per SM) of the warp kernel's cluster
+    peak_sms = sms * 33.9e3 / 148  # GFLOP/s of those SMs: measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
     ach = flops / (ms * 1e-3) / 1e9
     rounds = sweeps * (l - 1)
-    out = {"kernel": "jacobi_block_kernel (8-CTA cluster, block-ordered, %dx%d, V accumulated)" % (l, l), "ms": ms,
+    out = {"kernel": "jacobi_warp_kernel (%d-CTA cluster, one warp per CTA, block-ordered, %dx%d, V accumulated)" % (sms, l, l), "ms": ms,
            "sweeps": sweeps, "rounds": rounds, "us_per_round": ms * 1e3 / max(rounds, 1),
            "bound": "latency (sequential rotation rounds; per round: dot, 16-lane reduction, "
                     "rotation, in-CTA move; a DSMEM block move every bs rounds)",
-           "achieved_gflops": ach, "peak_gflops_8_sms": peak8, "frac_of_8_sms": ach / peak8}
+           "achieved_gflops": ach, "sms": sms, "peak_gflops_of_its_sms": peak_sms,
+           "frac_of_its_sms": ach / peak_sms}
     if calls_per_step and step_ms:
         out["share_of_step_est"] = calls_per_step * ms / step_ms
         out["share_basis"] = "%d calls/step x this single-call time / ms_per_step" % calls_per_step
