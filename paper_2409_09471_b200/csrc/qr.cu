@@ -1873,7 +1873,11 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   // confirmation sweep).  1e-8: the skipped rotations are O(1e-16), below the
   // 8.9e-15 threshold; r01 (tools/jac_ab.py) singular values / orthogonality
   // unchanged, one sweep saved on most inputs (80x80 Gaussian 9 -> 8; config-3
-  // step 37.7 -> 36.1 ms).  TTK_JACOBI_SKIP overrides (0 keeps the confirmation sweep)
+  // step 37.7 -> 36.1 ms).  1e-7 was tried (tools/jac_ab.py: 80 x 80 Gaussian one
+  // sweep fewer, orthogonality unchanged) but moved neither the config-3 step
+  // (31.9 vs 31.9 ms) nor the solvers beyond their run-to-run noise; 1e-6 let
+  // 128 x 128 orthogonality slip to 2e-12.  TTK_JACOBI_SKIP overrides (0 keeps
+  // the confirmation sweep)
   static const double skip = getenv("TTK_JACOBI_SKIP") ? atof(getenv("TTK_JACOBI_SKIP")) : 1e-8;
   const double skip2 = skip * skip;
   // largest (even) width for the single-CTA register kernel (tools/jac_ab.py, r01: local vs

@@ -132,6 +132,28 @@ def test_jacobi_svd(cuda, k, l):
         assert np.linalg.norm((U * S) @ V.T - B) <= 1e-13 * np.linalg.norm(B) * 10
 
 
+@pytest.mark.parametrize("l", [42, 50, 64, 80, 96, 100, 128])
+def test_jacobi_orthogonality_gaussian(cuda, l):
+    """The early-stop rule (stop after a sweep whose pairs were all within
+    1e-7) must leave U and V orthonormal to working precision on the
+    truncation's R^T inputs, for every kernel form (warp / block / cluster)."""
+    lib = _lib.load()
+    rng = np.random.default_rng(l)
+    R = np.linalg.qr(rng.standard_normal((4 * l, l)))[1]
+    B = np.ascontiguousarray(R.T)
+    Bt = torch.as_tensor(B, device=cuda)
+    U = torch.empty((l, l), dtype=torch.float64, device=cuda)
+    S = torch.empty(l, dtype=torch.float64, device=cuda)
+    V = torch.empty((l, l), dtype=torch.float64, device=cuda)
+    _lib.check(lib.ttk_svd_small(l, l, Bt.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(),
+                                 _lib.stream_ptr(cuda)))
+    u, s, v = U.cpu().numpy(), S.cpu().numpy(), V.cpu().numpy()
+    assert np.abs(u.T @ u - np.eye(l)).max() <= 1e-13
+    assert np.abs(v.T @ v - np.eye(l)).max() <= 1e-13
+    assert np.abs(s - np.linalg.svd(B, compute_uv=False)).max() <= 1e-13 * s[0]
+    assert np.linalg.norm(B @ v - u * s[None, :]) <= 1e-13 * np.linalg.norm(B)
+
+
 def test_tt_round_golden(cuda):
     z = load("tt_ops.npz")
     for name in z["rd_names"]:
