@@ -2329,6 +2329,46 @@ __device__ void block_dmma(int M, int N, int K, const double* A, int a_rs, int a
                            const double* rinv_f = nullptr, const double* rinv_p = nullptr, bool sub = false) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
+  if (rinv_out == nullptr) {
+    // 16 x 16 output blocks per warp (2 x 2 DMMA tiles): each k-step loads two
+    // A and two B fragments for four DMMAs (the 8 x 8 form loads two per DMMA
+    // and is bound by shared-memory issue, not by the DMMA pipe)
+    const int tn = (N + 15) >> 4, tiles = ((M + 15) >> 4) * tn;
+    for (int tt = warp; tt < tiles; tt += nw) {
+      const int m0 = (tt / tn) * 16, n0 = (tt % tn) * 16;
+      const int ma = m0 + fr, mb = m0 + 8 + fr, na = n0 + fr, nb = n0 + 8 + fr;
+      const bool va = ma < M, vb = mb < M, wa = na < N, wb = nb < N;
+      double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
+#pragma unroll 2
+      for (int k0 = 0; k0 < K; k0 += 4) {
+        const int k = k0 + fk;
+        const bool kv = k < K;
+        const double a0 = (va && kv) ? A[ma * a_rs + k * a_cs] : 0.0;
+        const double a1 = (vb && kv) ? A[mb * a_rs + k * a_cs] : 0.0;
+        const double b0 = (wa && kv) ? B[k * b_rs + na * b_cs] : 0.0;
+        const double b1 = (wb && kv) ? B[k * b_rs + nb * b_cs] : 0.0;
+        dmma_8x8x4(c00, a0, b0);
+        dmma_8x8x4(c01, a0, b1);
+        dmma_8x8x4(c10, a1, b0);
+        dmma_8x8x4(c11, a1, b1);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cn0 = n0 + 2 * fk + h, cn1 = n0 + 8 + 2 * fk + h;
+        auto put = [&](int m, int cn, double v) {
+          if (m < M && cn < N) {
+            if (sub) C[m * ldc + cn] -= v;
+            else C[m * ldc + cn] = v;
+          }
+        };
+        put(ma, cn0, c00[h]);
+        put(ma, cn1, c01[h]);
+        put(mb, cn0, c10[h]);
+        put(mb, cn1, c11[h]);
+      }
+    }
+    return;
+  }
   const int tn = (N + 7) >> 3, tiles = ((M + 7) >> 3) * tn;
   for (int tt = warp; tt < tiles; tt += nw) {
     const int m0 = (tt / tn) * 8, n0 = (tt % tn) * 8;
