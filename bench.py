@@ -396,6 +396,37 @@ def run_b200(args):
         e2e_ms = float(t.item())
     d2h = sum(c.numel() * 8 for c in res_host)
 
+    # ---- independent problems in flight (serving-loop throughput; reported beside
+    # the single-problem headline, which stays the latency-bound chain) ----
+    def inflight(n, steps):
+        streams = [torch.cuda.Stream(dev) for _ in range(n)]
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ends = [torch.cuda.Event() for _ in range(n)]
+
+        def worker(i, k):
+            torch.cuda.set_device(dev)
+            streams[i].wait_event(g0)
+            with torch.cuda.stream(streams[i]):
+                for _ in range(k):
+                    step(op, x)
+            ends[i].record(streams[i])
+
+        def run(k):
+            g0.record(stream)
+            ths = [threading.Thread(target=worker, args=(i, k)) for i in range(n)]
+            [t.start() for t in ths]
+            [t.join() for t in ths]
+            for e in ends:
+                stream.wait_event(e)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            return g0.elapsed_time(g1)
+        run(1)  # warm-up: per-stream workspaces, per-thread side streams
+        ms_all = run(steps)
+        return {"problems_in_flight": n, "steps_each": steps, "value": flops * n * steps / (ms_all * 1e-3) / 1e9,
+                "unit": UNIT, "ms_per_problem_per_stream": ms_all / steps}
+    inflight_res = {str(n): inflight(n, max(2, args.steps // 2)) for n in (2, 4)} if world == 1 else None
+
     line = {"metric": METRIC, "value": flops * world / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -407,6 +438,7 @@ def run_b200(args):
             "e2e": {"value": flops * world / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": int(launches),
+            "inflight": inflight_res,
             "clocks": clocks.summary(),
             "breakdown": phases}
 
