@@ -99,6 +99,26 @@ def test_qr_auto_cholqr_paths(cuda, kind, trans):
     assert np.linalg.norm(Q @ R - A) <= 1e-14 * np.linalg.norm(A) + 1e-300
 
 
+@pytest.mark.parametrize("m,l", [(128, 80), (80, 80), (256, 40), (512, 100), (100, 64), (1000, 96)])
+@pytest.mark.parametrize("kind", ["gauss", "graded1e12", "dup"])
+def test_qr_auto_squarish(cuda, m, l, kind):
+    """Square-ish panels (m < 4 l) now take the CholeskyQR2 route with its
+    rank-robust / Householder fallbacks (qr_auto); same backward-stability bar."""
+    rng = np.random.default_rng(m + l)
+    if kind == "gauss":
+        A = rng.standard_normal((m, l))
+    elif kind == "graded1e12":
+        U, _ = np.linalg.qr(rng.standard_normal((m, l)))
+        V, _ = np.linalg.qr(rng.standard_normal((l, l)))
+        A = (U * np.logspace(0, -12, l)) @ V.T
+    else:
+        B = rng.standard_normal((m, l // 2))
+        A = np.concatenate([B, B[:, : l - l // 2]], axis=1)
+    Q, R = run_qr(A, cuda, auto=True)
+    assert np.abs(Q.T @ Q - np.eye(l)).max() <= 5e-14
+    assert np.linalg.norm(Q @ R - A) <= 1e-14 * np.linalg.norm(A)
+
+
 def test_tsqr_transposed_input(cuda):
     rng = np.random.default_rng(2)
     A = rng.standard_normal((4096, 37))
