@@ -5,7 +5,10 @@ applies the d=32, n=128, op-rank-3 anisotropic convection-diffusion TT
 operator to a rank-64 Gaussian TT (tt_matvec, output rank 192) and rounds the
 result with randomize-then-orthogonalize at sketch rank l=80 followed by TT-SVD
 truncation to rank 64.  value = (matvec + RTO-sweep FLOPs) / step time in
-GFLOP/s (the truncation is timed but not counted).
+GFLOP/s (the truncation is timed but not counted).  The step is the public
+tt_matvec_round_rto call; e2e runs it on pinned host cores (uploads and the
+result download overlap the compute), inflight runs 2 / 4 independent problems
+on separate streams.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--extras]
 
