@@ -338,3 +338,28 @@ def test_matvec_round_rto_pipeline(cuda, host, chunk):
     want = O.rto_round(y, O.slice_drm(drm, ls), 1e-9, 11)
     assert got.ranks == tuple([1] + [c.shape[2] for c in want])
     assert O.rel_diff([c.cpu().numpy() for c in got.cores], want) <= 1e-10
+
+
+@pytest.mark.parametrize("host", [False, True])
+@pytest.mark.parametrize("dims", [[9], [7, 11], [5, 6, 4]])
+def test_matvec_round_rto_pipeline_small(cuda, host, dims):
+    """Edge sizes of the pipelined call (d = 1 takes the copy branches)."""
+    rng = np.random.default_rng(len(dims))
+    d = len(dims)
+    opc = [rng.standard_normal((1 if k == 0 else 2, n, n, 1 if k == d - 1 else 2)) for k, n in enumerate(dims)]
+    x = O.tt_random(dims, [3] * (d - 1), seed=4) if d > 1 else [rng.standard_normal((1, dims[0], 1))]
+    drm = O.drm_new(dims, [4] * (d - 1), seed=6) if d > 1 else [rng.standard_normal((1, dims[0], 1))]
+    spec = T.RoundSpec(1e-10, 5)
+    G = [torch.as_tensor(g, device=cuda) for g in drm]
+    dev_op, dev_x = T.TTOperator(opc, device=cuda), T.TTVector(x, device=cuda)
+    ref = T.tt_truncate_left_orth(T.rto_sweeps(T.tt_matvec(dev_op, dev_x), G), spec)
+    if host:
+        a = T.TTOperator([torch.as_tensor(c).pin_memory() for c in opc])
+        v = T.TTVector([torch.as_tensor(c).pin_memory() for c in x])
+    else:
+        a, v = dev_op, dev_x
+    got = T.tt_matvec_round_rto(a, v, spec, G, device=cuda)
+    torch.cuda.synchronize()
+    assert got.ranks == ref.ranks
+    for g_, w in zip(got.cores, ref.cores):
+        assert torch.equal(g_.cpu(), w.cpu())
