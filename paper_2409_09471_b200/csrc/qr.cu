@@ -712,6 +712,7 @@ __device__ __forceinline__ void jc_wait(uint32_t bar, uint32_t parity) {
 }
 
 __device__ long long* g_jc_prof = nullptr;  // optional per-phase clock sink (diagnostics)
+static bool g_jc_prof_host = false;            // host mirror: launch the PROF kernel instances
 
 template <int RPL>
 __global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads, 1)
@@ -1378,7 +1379,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
 // across the whole chain, not by one piece.
 constexpr int kJwSlots = 4, kJwLanes = 8;
 
-template <int RPL>
+template <int RPL, bool PROF = false>
 __global__ void __launch_bounds__(32, 1)
     jacobi_warp_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
@@ -1466,7 +1467,8 @@ __global__ void __launch_bounds__(32, 1)
   constexpr uint32_t pstride = 2u * kJwLanes * 8u;  // bytes between a lane's double2 pairs
   cl.sync();  // barriers initialised and armed in every CTA before the first remote store
 
-  long long* const prof = (lane == 0) ? g_jc_prof : nullptr;
+  // phase clocks only in the PROF instance (the checks and clock reads cost ~2 % of a round)
+  long long* const prof = (PROF && lane == 0) ? g_jc_prof : nullptr;
   long long pt[4] = {0, 0, 0, 0}, tc = 0;
   int lr = 0;
   int sweep = 0, moves = 0;
@@ -1476,7 +1478,7 @@ __global__ void __launch_bounds__(32, 1)
       const int nr = (br == 0) ? 2 * kJwSlots - 1 : kJwSlots;
       for (int t = 0; t < nr; ++t) {
         // ---- rotate the pair (x, y): 8-lane dot products, 3 shuffle levels ----
-        if (prof) tc = clock64();
+        if (PROF && prof) tc = clock64();
         double ra0 = 0.0, rb0 = 0.0, rg0 = 0.0, ra1 = 0.0, rb1 = 0.0, rg1 = 0.0;
 #pragma unroll
         for (int i = 0; i < RPL; i += 2) {
@@ -1490,7 +1492,7 @@ __global__ void __launch_bounds__(32, 1)
           rb += __shfl_xor_sync(0xffffffffu, rb, o);
           rg += __shfl_xor_sync(0xffffffffu, rg, o);
         }
-        if (prof) { long long t2 = clock64(); pt[3] += t2 - tc; }
+        if (PROF && prof) { long long t2 = clock64(); pt[3] += t2 - tc; }
         if (rg * rg > skip2 * ra * rb) big = 1;
         if (ra > 0.0 && rb > 0.0 && rg * rg > tol2 * ra * rb) {
           rot = 1;
@@ -1518,7 +1520,7 @@ __global__ void __launch_bounds__(32, 1)
           }
         }
         // ---- in-CTA move: register shuffles inside the warp ----
-        if (prof) { long long t2 = clock64(); pt[0] += t2 - tc; tc = t2; }
+        if (PROF && prof) { long long t2 = clock64(); pt[0] += t2 - tc; tc = t2; }
         if (br == 0) {
           // circle method on the 4 slots: left(s) <- left(s+1) (s = 1, 2),
           // left(3) <- right(3), left(0) fixed; right(0) <- left(1), right(s) <- right(s-1)
@@ -1556,7 +1558,7 @@ __global__ void __launch_bounds__(32, 1)
           }
           idr = __shfl_sync(0xffffffffu, idr, src);
         }
-        if (prof) { long long t2 = clock64(); pt[1] += t2 - tc; tc = t2; }
+        if (PROF && prof) { long long t2 = clock64(); pt[1] += t2 - tc; tc = t2; }
         ++lr;
       }
       // ---- block move between CTAs (DSMEM, completion on the receiver's mbarrier) ----
@@ -1606,7 +1608,7 @@ __global__ void __launch_bounds__(32, 1)
         if (want_v) get(bslot(buf, s, 1, 1), vy);
         idr = bid[buf][s][1];
         ++moves;
-        if (prof) { long long t2 = clock64(); pt[2] += t2 - tc; tc = t2; }
+        if (PROF && prof) { long long t2 = clock64(); pt[2] += t2 - tc; tc = t2; }
       }
     }
     if (__any_sync(0xffffffffu, rot) && lane == 0) flags[sweep] = 1;
@@ -1622,7 +1624,7 @@ __global__ void __launch_bounds__(32, 1)
     if (!ch || !bg) break;
   }
   if (c == 0 && lane == 0 && g_svd_sweeps) *g_svd_sweeps = sweep + 1;
-  if (prof && c < 8) {
+  if (PROF && prof && c < 8) {
     for (int i = 0; i < 4; ++i) atomicAdd((unsigned long long*)&prof[c * 5 + i], (unsigned long long)pt[i]);
     atomicAdd((unsigned long long*)&prof[c * 5 + 4], (unsigned long long)lr);
   }
@@ -1916,7 +1918,10 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
     if (!wattr) {
       for (const void* fn : {(const void*)jacobi_warp_kernel<2>, (const void*)jacobi_warp_kernel<4>,
                              (const void*)jacobi_warp_kernel<6>, (const void*)jacobi_warp_kernel<8>,
-                             (const void*)jacobi_warp_kernel<10>, (const void*)jacobi_warp_kernel<12>})
+                             (const void*)jacobi_warp_kernel<10>, (const void*)jacobi_warp_kernel<12>,
+                             (const void*)jacobi_warp_kernel<2, true>, (const void*)jacobi_warp_kernel<4, true>,
+                             (const void*)jacobi_warp_kernel<6, true>, (const void*)jacobi_warp_kernel<8, true>,
+                             (const void*)jacobi_warp_kernel<10, true>, (const void*)jacobi_warp_kernel<12, true>})
         TTK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       wattr = true;
     }
@@ -1935,6 +1940,16 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
     cfg.numAttrs = 1;
     const int want = V != nullptr;
     cudaError_t e;
+    if (g_jc_prof_host) {
+    switch (rpl) {
+      case 2: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<2, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 4: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<4, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 6: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<6, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 8: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<8, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 10: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      default: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<12, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+    }
+    } else {
     switch (rpl) {
       case 2: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<2>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
       case 4: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<4>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
@@ -1942,6 +1957,7 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
       case 8: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<8>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
       case 10: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
       default: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<12>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+    }
     }
     TTK_CHECK_CUDA(e);
     TTK_CHECK_LAUNCH();
@@ -2135,6 +2151,7 @@ int ttk_debug_chol_profile(long long* dev_acc) {
 // rotate, send, wait, pull, rounds) into dev_acc (NULL: off)
 int ttk_debug_jacobi_profile(long long* dev_acc) {
   TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_jc_prof, &dev_acc, sizeof(long long*)));
+  g_jc_prof_host = dev_acc != nullptr;
   return kOk;
 }
 
