@@ -1504,18 +1504,21 @@ __global__ void __launch_bounds__(32, 1)
           const double sum = fabs(dd) + rho;
           const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
           const double cs = sum * rq, sn = (dd >= 0.0 ? w : -w) * rq;
+          // both products of the old x first, then each register overwritten by
+          // the FMA that consumes its old value (no temporaries to move back:
+          // the plain form cost ~40 register moves per round in SASS)
 #pragma unroll
           for (int i = 0; i < RPL; ++i) {
-            const double xi = x[i], yi = y[i];
-            x[i] = cs * xi - sn * yi;
-            y[i] = sn * xi + cs * yi;
+            const double cx = cs * x[i], sx = sn * x[i];
+            x[i] = fma(-sn, y[i], cx);
+            y[i] = fma(cs, y[i], sx);
           }
           if (want_v) {
 #pragma unroll
             for (int i = 0; i < RPL; ++i) {
-              const double xi = vx[i], yi = vy[i];
-              vx[i] = cs * xi - sn * yi;
-              vy[i] = sn * xi + cs * yi;
+              const double cx = cs * vx[i], sx = sn * vx[i];
+              vx[i] = fma(-sn, vy[i], cx);
+              vy[i] = fma(cs, vy[i], sx);
             }
           }
         }
