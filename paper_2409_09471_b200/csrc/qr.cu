@@ -866,17 +866,17 @@ __global__ void __cluster_dims__(kJcCluster, 1, 1) __launch_bounds__(kJcThreads,
         const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
         const double c = sum * rq, s = (dd >= 0.0 ? w : -w) * rq;
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const double xi = x[i], yi = y[i];
-          x[i] = c * xi - s * yi;
-          y[i] = s * xi + c * yi;
+        for (int i = 0; i < RPL; ++i) {  // old x consumed first: no register moves
+          const double cx = c * x[i], sx = s * x[i];
+          x[i] = fma(-s, y[i], cx);
+          y[i] = fma(c, y[i], sx);
         }
         if (want_v) {
 #pragma unroll
           for (int i = 0; i < RPL; ++i) {
-            const double xi = vx[i], yi = vy[i];
-            vx[i] = c * xi - s * yi;
-            vy[i] = s * xi + c * yi;
+            const double cx = c * vx[i], sx = s * vx[i];
+            vx[i] = fma(-s, vy[i], cx);
+            vy[i] = fma(c, vy[i], sx);
           }
         }
         if (gl == 0) flags[sweep] = 1;
@@ -1181,17 +1181,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
           const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
           const double cs = sum * rq, sn = (dd >= 0.0 ? w : -w) * rq;
 #pragma unroll
-          for (int i = 0; i < RPL; ++i) {
-            const double xi = x[i], yi = y[i];
-            x[i] = cs * xi - sn * yi;
-            y[i] = sn * xi + cs * yi;
+          for (int i = 0; i < RPL; ++i) {  // old x consumed first: no register moves
+            const double cx = cs * x[i], sx = sn * x[i];
+            x[i] = fma(-sn, y[i], cx);
+            y[i] = fma(cs, y[i], sx);
           }
           if (want_v) {
 #pragma unroll
             for (int i = 0; i < RPL; ++i) {
-              const double xi = vx[i], yi = vy[i];
-              vx[i] = cs * xi - sn * yi;
-              vy[i] = sn * xi + cs * yi;
+              const double cx = cs * vx[i], sx = sn * vx[i];
+              vx[i] = fma(-sn, vy[i], cx);
+              vy[i] = fma(cs, vy[i], sx);
             }
           }
           if (gl == 0) flags[sweep] = 1;
@@ -1760,17 +1760,17 @@ __global__ void __launch_bounds__(kJlMaxSlots * kSvdGroup, 1)
         const double rq = rsqrt_rot(fma(2.0 * rho, fabs(dd), 2.0 * q));  // 2 rho (|dd| + rho)
         const double c = sum * rq, s = (dd >= 0.0 ? w : -w) * rq;
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) {
-          const double xi = x[i], yi = y[i];
-          x[i] = c * xi - s * yi;
-          y[i] = s * xi + c * yi;
+        for (int i = 0; i < RPL; ++i) {  // old x consumed first: no register moves
+          const double cx = c * x[i], sx = s * x[i];
+          x[i] = fma(-s, y[i], cx);
+          y[i] = fma(c, y[i], sx);
         }
         if (want_v) {
 #pragma unroll
           for (int i = 0; i < RPL; ++i) {
-            const double xi = vx[i], yi = vy[i];
-            vx[i] = c * xi - s * yi;
-            vy[i] = s * xi + c * yi;
+            const double cx = c * vx[i], sx = s * vx[i];
+            vx[i] = fma(-s, vy[i], cx);
+            vy[i] = fma(c, vy[i], sx);
           }
         }
         if (gl == 0) flags[sweep] = 1;
