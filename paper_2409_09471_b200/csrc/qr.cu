@@ -1962,9 +1962,13 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
       default: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<12>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
     }
     }
-    TTK_CHECK_CUDA(e);
-    TTK_CHECK_LAUNCH();
-    return kOk;
+    if (e == cudaSuccess) {
+      TTK_CHECK_LAUNCH();
+      return kOk;
+    }
+    // a non-portable cluster of CL CTAs can be refused (e.g. a partitioned
+    // GPU): clear the error and take the portable 8-CTA block kernel below
+    (void)cudaGetLastError();
   }
   // block-ordered cluster kernel (2 CL - 1 DSMEM handoffs per sweep instead of
   // le - 1); TTK_JACOBI_BLOCK=0 keeps the plain cluster kernel, =4 / =8 picks the
