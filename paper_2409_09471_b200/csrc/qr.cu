@@ -2609,13 +2609,17 @@ __device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, 
     if (JJ < bs && !(p > tiny)) { badd = 1; p = 1.0; }
     if (JJ >= bs) p = 1.0;
     const double inv = rsqrt_rot(p);
-    const double rrow = (c > JJ) ? d[JJ] * inv : (c == JJ ? p * inv : 0.0);
+    // unconditional row and update: lanes c < JJ / entries below the diagonal
+    // only touch the strict lower triangle, which is never read again and is
+    // zeroed when the block is stored (the selects and predicates of the
+    // triangular form were ~half of this loop's instructions)
+    const double rrow = (lane == JJ ? p : d[JJ]) * inv;
     d[JJ] = rrow;
     if (lane == JJ) invd[JJ] = inv;
 #pragma unroll
     for (int rr = JJ + 1; rr < 16; ++rr) {
       const double rjr = __shfl_sync(0xffffffffu, rrow, rr);
-      if (c >= rr) d[rr] -= rjr * rrow;
+      d[rr] = fma(-rjr, rrow, d[rr]);
     }
     cb_diag_steps<JJ + 1>(d, c, lane, bs, tiny, badd, invd);
   }
