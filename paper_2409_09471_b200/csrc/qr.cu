@@ -2998,13 +2998,13 @@ __global__ void __launch_bounds__(kTbThreads)
           const int kj = jj >> 2;
           double v = t[kj] * rinv[j0 + jj];
           v = __shfl_sync(0xffffffffu, v, (threadIdx.x & ~3) | (jj & 3), 32);
-          if ((jj & 3) == g) t[kj] = v;
           const double* rr = sR + (j0 + jj) * ld + j0;
+          // unconditional update: R is zero below its diagonal (columns c < jj
+          // unchanged); the owner's own column (c == jj) is overwritten with v
+          // right after, and columns c >= bs are never stored
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int c = g + 4 * k;
-            if (c > jj && c < bs) t[k] -= v * rr[c];
-          }
+          for (int k = 0; k < 4; ++k) t[k] = fma(-v, rr[g + 4 * k], t[k]);
+          if ((jj & 3) == g) t[kj] = v;
         }
       }
 #pragma unroll
@@ -3152,13 +3152,13 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
             const int kj = jj >> 2;
             double v = t[kj] * rinv[j0 + jj];
             v = __shfl_sync(0xffffffffu, v, (threadIdx.x & ~3) | (jj & 3), 32);
-            if ((jj & 3) == g) t[kj] = v;
             const double* rr = sR + (j0 + jj) * ld + j0;
+            // unconditional update: R is zero below its diagonal (columns c < jj
+            // unchanged); the owner's own column (c == jj) is overwritten with v
+            // right after, and columns c >= bs are never stored
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int c = g + 4 * k;
-              if (c > jj && c < bs) t[k] -= v * rr[c];
-            }
+            for (int k = 0; k < 4; ++k) t[k] = fma(-v, rr[g + 4 * k], t[k]);
+            if ((jj & 3) == g) t[kj] = v;
           }
         }
 #pragma unroll
