@@ -1475,8 +1475,9 @@ __global__ void __launch_bounds__(32, 1)
   for (; sweep < 60; ++sweep) {
     int rot = 0, big = 0;
     for (int br = 0; br < 2 * CL - 1; ++br) {
-      const int nr = (br == 0) ? 2 * kJwSlots - 1 : kJwSlots;
-      for (int t = 0; t < nr; ++t) {
+      // one round (rotation + in-CTA move); the cross rounds run in a loop with a
+      // compile-time trip count, fully unrolled (no per-round loop / branch overhead)
+      auto round = [&](const bool tournament) {
         // ---- rotate the pair (x, y): 8-lane dot products, 3 shuffle levels ----
         if (PROF && prof) tc = clock64();
         double ra0 = 0.0, rb0 = 0.0, rg0 = 0.0, ra1 = 0.0, rb1 = 0.0, rg1 = 0.0;
@@ -1524,7 +1525,7 @@ __global__ void __launch_bounds__(32, 1)
         }
         // ---- in-CTA move: register shuffles inside the warp ----
         if (PROF && prof) { long long t2 = clock64(); pt[0] += t2 - tc; tc = t2; }
-        if (br == 0) {
+        if (tournament) {
           // circle method on the 4 slots: left(s) <- left(s+1) (s = 1, 2),
           // left(3) <- right(3), left(0) fixed; right(0) <- left(1), right(s) <- right(s-1)
 #pragma unroll
@@ -1563,6 +1564,12 @@ __global__ void __launch_bounds__(32, 1)
         }
         if (PROF && prof) { long long t2 = clock64(); pt[1] += t2 - tc; tc = t2; }
         ++lr;
+      };
+      if (br == 0) {
+        for (int t = 0; t < 2 * kJwSlots - 1; ++t) round(true);
+      } else {
+#pragma unroll
+        for (int t = 0; t < kJwSlots; ++t) round(false);
       }
       // ---- block move between CTAs (DSMEM, completion on the receiver's mbarrier) ----
       {
