@@ -1566,6 +1566,7 @@ __global__ void __launch_bounds__(32, 1)
         ++lr;
       };
       if (br == 0) {
+#pragma unroll
         for (int t = 0; t < 2 * kJwSlots - 1; ++t) round(true);
       } else {
 #pragma unroll
