@@ -1153,6 +1153,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
   for (; sweep < 60; ++sweep) {
     for (int br = 0; br < 2 * CL - 1; ++br) {
       const int nr = (br == 0) ? 2 * bs - 1 : bs;
+#pragma unroll 2
       for (int t = 0; t < nr; ++t, ++lr) {
         // ---- rotate the pair (x, y) ----
         if (prof) tc = clock64();
@@ -1743,6 +1744,7 @@ __global__ void __launch_bounds__(kJlMaxSlots * kSvdGroup, 1)
   const int l_slot = si - 1, l_side = (si == 1) ? 1 : 0, r_slot = si + 1;
   int sweep = 0, round = 0;
   for (; sweep < 60; ++sweep) {
+#pragma unroll 2
     for (int rnd = 0; rnd < le - 1; ++rnd, ++round) {
       double a = 0.0, b = 0.0, g = 0.0, a2 = 0.0, b2 = 0.0, g2 = 0.0;
 #pragma unroll
