@@ -1383,11 +1383,14 @@ constexpr int kJwSlots = 4, kJwLanes = 8;
 template <int RPL, bool PROF = false>
 __global__ void __launch_bounds__(32, 1)
     jacobi_warp_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
-                       double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
+                       double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v_arg,
                        int scaled_u, double skip2) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int CL = (int)cl.num_blocks();
+  // V is always accumulated by the truncation; a compile-time flag removes the
+  // per-round V branches (PROF instances keep the runtime form)
+  const bool want_v = PROF ? (want_v_arg != 0) : true;
   const int c = (int)cl.block_rank();
   static_assert(RPL % 2 == 0, "RPL must be even");
   constexpr int box = RPL * kJwLanes;  // doubles per column part
