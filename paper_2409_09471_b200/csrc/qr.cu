@@ -1045,8 +1045,12 @@ constexpr int kJbMaxSlots = 16;  // columns per block (8-CTA cluster: <= 8, l <=
 template <int RPL, int CL = kJbCluster>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdGroup, 1)
     jacobi_block_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
-                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
+                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v_arg,
                         int scaled_u, double skip2) {
+  // V accumulation is a compile-time constant (its runtime branches cost
+  // instructions every round); V stores stay guarded by V != nullptr
+  const bool want_v = true;
+  (void)want_v_arg;
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int c = (int)cl.block_rank();
@@ -1694,8 +1698,12 @@ constexpr int kJlMaxSlots = 32;
 template <int RPL>
 __global__ void __launch_bounds__(kJlMaxSlots * kSvdGroup, 1)
     jacobi_local_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
-                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v,
+                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v_arg,
                         int scaled_u, double skip2) {
+  // V accumulation is a compile-time constant (its runtime branches cost
+  // instructions every round); V stores stay guarded by V != nullptr
+  const bool want_v = true;
+  (void)want_v_arg;
   extern __shared__ __align__(16) double sm[];  // [2 bufs][np][2 sides][2 (C,V)][RPL/2][16] double2
   __shared__ double nrm[kQrMaxCols + 2];
   __shared__ double fin[kQrMaxCols + 2];
