@@ -3109,12 +3109,15 @@ __device__ __forceinline__ void fq_mark(int i) {
   }
 }
 
+// LC > 0: the column count as a compile-time constant (the RTO / truncation
+// width 80), so every l-bounded loop and block_dmma shape is specialised
+template <int LC>
 __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __grid_constant__ FqParams P) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   fq_mark(0);
   extern __shared__ __align__(16) double fsm[];
-  const int l = P.l, ld = ((l + 15) & ~15) + 4, tid = threadIdx.x;
+  const int l = LC > 0 ? LC : P.l, ld = ((l + 15) & ~15) + 4, tid = threadIdx.x;
   const bool fac = blockIdx.x == 0;  // the factorisation CTA
   const int tr = P.tr;                        // rows per tile (multiple of 8, <= kFqRows)
   double* sY = fsm;                           // tr x ld   (tile CTAs)
@@ -3359,7 +3362,8 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     // ---- fast path, fused into one cooperative kernel ----
     static bool fattr = false;
     if (!fattr) {
-      TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel, 220 * 1024));
+      TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel<0>, 220 * 1024));
+      TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel<80>, 220 * 1024));
       fattr = true;
     }
     static const double fo = getenv("TTK_NEAR_ID_FIRST_ORDER") ? atof(getenv("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
@@ -3377,7 +3381,9 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     fp.tr = trows;
     const int grid = 1 + (m + trows - 1) / trows;
     void* args[] = {&fp};
-    const cudaError_t le = cudaLaunchCooperativeKernel((const void*)cholqr2_fused_kernel, dim3(grid),
+    static const bool lc_off = getenv("TTK_FQ_LC") && atoi(getenv("TTK_FQ_LC")) == 0;  // A/B
+    const void* fq_fn = (l == 80 && !lc_off) ? (const void*)cholqr2_fused_kernel<80> : (const void*)cholqr2_fused_kernel<0>;
+    const cudaError_t le = cudaLaunchCooperativeKernel(fq_fn, dim3(grid),
                                                        dim3(kFqThreads), args, cholqr2_fused_smem(l, trows), st);
     if (le == cudaSuccess) {
       fast_tried = true;
