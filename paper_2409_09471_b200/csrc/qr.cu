@@ -1384,14 +1384,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
 // across the whole chain, not by one piece.
 constexpr int kJwSlots = 4, kJwLanes = 8;
 
-template <int RPL, bool PROF = false>
+template <int RPL, bool PROF = false, int LC = 0>
 __global__ void __launch_bounds__(32, 1)
-    jacobi_warp_kernel(int k, int l, const double* __restrict__ B, long long b_rs, long long b_cs,
+    jacobi_warp_kernel(int k, int l_arg, const double* __restrict__ B, long long b_rs, long long b_cs,
                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v_arg,
                        int scaled_u, double skip2) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
-  const int CL = (int)cl.num_blocks();
+  // LC > 0: the column count (and so the cluster size) as compile-time constants
+  const int l = LC > 0 ? LC : l_arg;
+  const int CL = LC > 0 ? LC / (2 * kJwSlots) : (int)cl.num_blocks();
   // V is always accumulated by the truncation; a compile-time flag removes the
   // per-round V branches (PROF instances keep the runtime form)
   const bool want_v = PROF ? (want_v_arg != 0) : true;
@@ -1964,7 +1966,17 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
     cfg.numAttrs = 1;
     const int want = V != nullptr;
     cudaError_t e;
-    if (g_jc_prof_host) {
+    static const bool jlc_off = getenv("TTK_JW_LC") && atoi(getenv("TTK_JW_LC")) == 0;  // A/B
+    if (!g_jc_prof_host && rpl == 10 && l == 80 && !jlc_off) {
+      static bool lcattr = false;
+      if (!lcattr) {
+        TTK_CHECK_CUDA(cudaFuncSetAttribute((const void*)jacobi_warp_kernel<10, false, 80>,
+                                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        lcattr = true;
+      }
+      e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, false, 80>, k, l, B, b_rs, b_cs, U, S, V, want,
+                             (int)scaled_u, skip2);
+    } else if (g_jc_prof_host) {
     switch (rpl) {
       case 2: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<2, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
       case 4: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<4, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
