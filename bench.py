@@ -10,13 +10,21 @@ tt_matvec_round_rto call; e2e runs it on pinned host cores (uploads and the
 result download overlap the compute), inflight runs 2 / 4 independent problems
 on separate streams.
 
+The same line carries the rest of the BASELINE metric ("... & TT-sGMRES
+iters/s"): ``solver`` (config 1, config 5 RHS 0: it/s and time to 1e-6, CPU
+oracle / committed reference wall time beside them) and ``sharded`` (the two
+workloads that partition over GPUs: config-4 Khatri-Rao rows
+with an NCCL all-gather, config-5 right-hand sides j on rank j mod G).
+
   python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--extras]
 
-N > 1 runs under torchrun: every rank runs an independent replica (the
-matvec/rounding chain does not shard -- "replicas only"), value is
+--gpus N without torchrun re-launches this script as N ranks under
+torch.distributed.run (127.0.0.1); under torchrun the world size must equal
+--gpus.  The config-3 headline runs as independent replicas on every rank
+(the rounding chain does not shard -- "replicas only"): value is
 the FLOPs of all ranks / the max-over-ranks device time.  --impl reference
 times the CPU oracle (numpy restatement of the reference path, oracle/) on
-the host cores for the same workload.
+the host cores for the same workload (rank 0 only).
 """
 
 from __future__ import annotations
@@ -59,7 +67,68 @@ def parse():
     p.add_argument("--workload", default="cfg3", choices=["cfg3", "kr", "solver"],
                    help="cfg3 (headline, replicas), kr (config 4, rows sharded over ranks + all-gather), "
                         "solver (config 5, 8 right-hand sides sharded over ranks)")
+    p.add_argument("--no-solver", action="store_true", help="skip the solver / sharded objects")
+    p.add_argument("--launcher-selftest", action="store_true",
+                   help="(tests) start the ranks exactly as --gpus N does, join a gloo group, print n_gpus")
     return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# launcher: --gpus N starts N ranks itself when not already under torchrun
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(n):
+    """Re-exec this script as ``n`` ranks under torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1); returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # the communicator reports nranks on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // n)))
+    return subprocess.call(cmd, env=env)
+
+
+def world_from_env(args):
+    """World size / rank of this process; the world must equal --gpus."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch with "
+                         f"torchrun --nproc-per-node {args.gpus} or without torchrun")
+    return world, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def launcher_selftest(args):
+    import torch
+    import torch.distributed as dist
+    world, rank, _ = world_from_env(args)
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "all_reduce": float(t.item()), "backend": "gloo",
+                          "launcher": "torch.distributed.run" if "TORCHELASTIC_RUN_ID" in os.environ else "env"}),
+              flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def bench_config(C, flops, mv_flops, rto_fl, world):
+    """The config object both arms print (identical keys and values for the same N)."""
+    return {"workload": WORKLOAD, "parallelism": f"replicas x{world}" if world > 1 else "single",
+            "flops_per_step": flops, "matvec_flops": mv_flops, "rto_sweep_flops": rto_fl,
+            "dims": [int(C["dims"][0])] * len(C["dims"]), "x_rank": 64, "op_rank": 3, "ell": C["ell"],
+            "max_rank": C["max_rank"], "rel_tol": C["rel_tol"],
+            "l2": "inputs larger than L2 (matvec output 1.13 GB per step)"}
 
 
 # ---------------------------------------------------------------------------
@@ -229,6 +298,9 @@ def cpu_baseline(C, flops, budget_s=20.0):
 # ---------------------------------------------------------------------------
 
 def run_reference(args):
+    """The reference arm: the CPU oracle (numpy + OpenBLAS on every host core)
+    on the same config-3 workload; under torchrun only rank 0 runs it."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -248,7 +320,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "flops_per_step": flops},
+            "config": bench_config(C, flops, mv, rto, world),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": f"{args.steps} full config-3 steps (numpy restatement of the "
@@ -265,9 +337,7 @@ def run_b200(args):
     import paper_2409_09471_b200 as T
     from paper_2409_09471_b200 import _lib, configs
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = world_from_env(args)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
@@ -435,16 +505,27 @@ def run_b200(args):
         except Exception as exc:  # the headline must not depend on the extra measurement
             inflight_res = {"error": repr(exc)[:200]}
 
+    peak_tf = peak / 1e3
+    step_tf = flops / (ms * 1e-3) / 1e12
+    roofline["step_frac"] = step_tf / peak_tf
+    roofline["step_achieved"] = step_tf
+    dk = roofline["dominant_kernel"]
+    dk["chip_frac"] = dk["achieved_gflops"] / 1e3 / peak_tf
+    roofline["note"] = ("frac/achieved: the matvec GEMM (the one FLOP-bound kernel, one launch per step); "
+                        "step_frac: whole step (matvec + RTO sweep FLOPs / step time) vs the same fp64 peak; "
+                        "dominant_kernel: the truncation's Jacobi SVD (largest share of step time), "
+                        "chip_frac against the whole chip's fp64 peak")
+
     line = {"metric": METRIC, "value": flops * world / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world}" if world > 1 else "single",
-                       "flops_per_step": flops, "matvec_flops": mv_flops, "rto_sweep_flops": rto_fl,
-                       "l2": "inputs larger than L2 (matvec output 1.13 GB per step)",
-                       "out_ranks_max": max(out.ranks)},
+            "config": bench_config(C, flops, mv_flops, rto_fl, world),
+            "out_ranks_max": max(out.ranks),
             "roofline": roofline,
             "e2e": {"value": flops * world / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                    "note": "h2d = operator + vector cores uploaded every step; the Gaussian TT-DRM of the "
+                            "rounding (197 MB, a per-solve constant drawn once) stays resident on the device"},
             "gpu_launches": int(launches),
             "inflight": inflight_res,
             "clocks": clocks.summary(),
@@ -456,6 +537,17 @@ def run_b200(args):
         import oracle as O
         line["parity"] = {"rel_diff_vs_oracle": O.rel_diff([c.cpu().numpy() for c in out.cores], cpu_out),
                           "ranks_equal": list(out.ranks) == [1] + [c.shape[2] for c in cpu_out]}
+    del y, z, ybuf, out
+    torch.cuda.empty_cache()
+    if not args.no_solver:
+        if rank == 0:
+            try:
+                line["solver"] = solver_metrics(T, torch, dev, cpu=(world == 1 and not args.no_cpu_baseline))
+            except Exception as exc:  # the headline must not depend on the extra measurement
+                line["solver"] = {"error": repr(exc)[:300]}
+        barrier()
+        line["sharded"] = {"kr": sharded_kr(args, T, torch, dev, world, rank, local, peak_tf),
+                           "solver": sharded_solver(args, T, torch, dev, world, rank, local)}
     if args.extras and rank == 0:
         line["extras"] = run_extras(T, torch, dev)
     if rank == 0:
@@ -463,6 +555,209 @@ def run_b200(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+# ---------------------------------------------------------------------------
+# TT-sGMRES iterations/s (the second half of the BASELINE metric)
+
+def _solver_inputs(T, torch, dev, C, rounding):
+    cfg = T.SolverConfig(**C["cfg"], zero_rel=None, rounding=rounding)
+    a = T.TTOperator(C["op"], device=dev)
+    b = T.TTVector(C["b"], device=dev)
+    s = T.kr_sketch_new(C["dims"], cfg.sketch_rows, seed=C["sketch_seed"], device=dev)
+    frame = T.make_solver_frame(b, cfg, seed=C["frame_seed"])
+    return cfg, a, b, s, frame
+
+
+def _timed_solve(T, torch, dev, C, rounding):
+    """One untimed warm-up solve capped at 4 iterations (lazy kernel loading,
+    grow-only workspaces), then the timed solve; wall clock around the whole
+    solve (it synchronises the host every iteration) and the phase split from
+    the solver's CUDA-event timer."""
+    cfg, a, b, s, frame = _solver_inputs(T, torch, dev, C, rounding)
+    warm = T.SolverConfig(**{**C["cfg"], "maxit": 4}, zero_rel=None, rounding=rounding)
+    T.tt_sgmres(a, b, None, warm, s, T.make_solver_frame(b, warm, seed=C["frame_seed"]))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _, rep = T.tt_sgmres(a, b, None, cfg, s, frame)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return {"rounding": rounding, "iterations": rep.iterations, "converged": rep.converged, "wall_s": wall,
+            "it_per_s": rep.iterations / wall, "final_res_sketched": rep.res_sketched[-1],
+            "time_to_1e-6_s": rep.time_to_tol.get(1e-6), "peak_rank": rep.peak_rank,
+            "phase_s": rep.phase_totals()}
+
+
+def _fixture(name):
+    try:
+        return np.load(os.path.join(ROOT, "tests", "golden", name), allow_pickle=False)
+    except Exception:
+        return None
+
+
+def solver_metrics(T, torch, dev, cpu=True):
+    """Config 1 (40 iterations) and config 5 RHS 0 on one GPU, both rounding
+    modes; the CPU oracle's config-1 solve (randomized rounding, same inputs)
+    timed beside it, and the committed reference run's config-5 wall time
+    (tests/golden/solver_cfg5.npz, measured in the build container) quoted."""
+    from paper_2409_09471_b200 import configs
+    out = {"unit": "it/s", "timing": "host wall clock around tt_sgmres after an untimed 4-iteration warm-up"}
+    C1 = configs.config1()
+    out["config1"] = {"rto": _timed_solve(T, torch, dev, C1, "rto"), "svd": _timed_solve(T, torch, dev, C1, "svd")}
+    if cpu:
+        import oracle as O
+        g = out["config1"]["rto"]
+        cfg = {**C1["cfg"], "zero_rel": None, "oversampling": 20}
+        drm = [x.cpu().numpy() for x in T.solver_rto_drm(C1["dims"], T.SolverConfig(**C1["cfg"], zero_rel=None,
+                                                                                     rounding="rto"),
+                                                         device=dev).cores]
+        f = O.kr_factors_new(C1["dims"], cfg["sketch_rows"], seed=C1["sketch_seed"])
+        t0 = time.perf_counter()
+        _, orep = O.sgmres(C1["op"], C1["b"], cfg, f, frame=O.solver_frame(C1["b"], cfg, seed=C1["frame_seed"]),
+                           rounding="rto", rto_drm=drm)
+        wall = time.perf_counter() - t0
+        out["config1"]["cpu_baseline"] = {
+            "value": orep["iterations"] / wall, "unit": "it/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"one full config-1 solve, randomized rounding ({orep['iterations']} iterations, "
+                      f"{wall:.2f} s), oracle/ttoracle.py sgmres",
+            "same_history": orep["iterations"] == g["iterations"]}
+    C5 = configs.config5(0)
+    out["config5_rhs0"] = {"rto": _timed_solve(T, torch, dev, C5, "rto"), "svd": _timed_solve(T, torch, dev, C5, "svd")}
+    z = _fixture("solver_cfg5.npz")
+    if z is not None:
+        it = int(z["cfg5_0_iters"])
+        res = z["cfg5_0_res"]
+        cum = np.cumsum(z["cfg5_0_iter_s"])
+        hit = [i for i, r in enumerate(res) if r <= 1e-6]
+        out["config5_rhs0"]["reference_run"] = {
+            "kind": "reference (recorded)", "iterations": it, "wall_s": float(z["cfg5_0_wall"]),
+            "it_per_s": it / float(z["cfg5_0_wall"]), "cores": 8,
+            "time_to_1e-6_s": float(cum[hit[0]]) if hit else None,
+            "sample": "the reference ttkrylov tt_sgmres (TT-SVD rounding, Q1 bypassed) timed in the build "
+                      "container (8 cores, OpenBLAS) when the committed fixture was made -- not this box"}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the two workloads that shard over GPUs (SURVEY 8(e))
+
+def sharded_kr(args, T, torch, dev, world, rank, local, peak_tf):
+    """Config 4: s=512 Khatri-Rao rows split over the ranks, all 64 vectors
+    replicated (drawn on rank 0, NCCL broadcast), one NCCL all-gather of the
+    (64 x s/G) blocks per step; value = batch FLOPs / max-over-ranks time."""
+    import torch.distributed as dist
+    from paper_2409_09471_b200 import _lib, configs
+    from paper_2409_09471_b200.parallel import kr_apply_sharded, row_partition
+    d, n, r, s, B = 20, 64, 100, 512, 64
+    full = [1] + [r] * (d - 1) + [1]
+    if rank == 0:
+        C = configs.config4()
+        fac = [torch.as_tensor(f, device=dev) for f in C["factors"]]
+        vecs = [[torch.as_tensor(c, device=dev) for c in v] for v in C["vecs"]]
+        del C
+    else:
+        fac = [torch.empty((s, n), dtype=torch.float64, device=dev) for _ in range(d)]
+        vecs = [[torch.empty((full[k], n, full[k + 1]), dtype=torch.float64, device=dev) for k in range(d)]
+                for _ in range(B)]
+    if world > 1:
+        for t in fac + [c for v in vecs for c in v]:
+            dist.broadcast(t, 0)
+    sk = T.KhatriRaoSketch(fac, device=dev)
+    vs = [T.TTVector(v, device=dev) for v in vecs]
+    flops = sum(2.0 * s * n * r0 * r1 for r0, r1 in zip(full[:-1], full[1:])) * B
+    lo, hi = row_partition(s, world)[rank]
+    lib = _lib.load()
+    for _ in range(3):
+        out = kr_apply_sharded(sk, vs, rank, world)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(args.steps // 2, 3)
+    n0 = lib.ttk_launch_count()
+    e0.record(st)
+    for _ in range(steps):
+        out = kr_apply_sharded(sk, vs, rank, world)
+    e1.record(st)
+    torch.cuda.synchronize()
+    launches = (lib.ttk_launch_count() - n0) // steps
+    ms = _max_over_ranks(torch, dev, world, e0.elapsed_time(e1) / steps)
+    # the kernel alone (this rank's rows, no gather)
+    k0.record(st)
+    for _ in range(steps):
+        T.kr_apply_rows(sk, vs, lo, hi)
+    k1.record(st)
+    torch.cuda.synchronize()
+    kms = _max_over_ranks(torch, dev, world, k0.elapsed_time(k1) / steps)
+    res = {"metric": "Khatri-Rao sketch GFLOP/s (fp64), config 4", "value": flops / (ms * 1e-3) / 1e9,
+           "unit": UNIT, "n_gpus": world, "scaling": "strong", "ms_per_step": ms, "steps": steps,
+           "config": {"workload": "config4: s=512 rows, 64 TTs d=20 n=64 r=100, N(0,1/n) factors; rows split "
+                                  "over ranks, NCCL all-gather of the row blocks", "rows_per_rank": hi - lo,
+                      "flops_per_step": flops},
+           "gpu_launches": int(launches),
+           "roofline": {"bound": "tensor", "kernel": "kr_fused_kernel (this rank's rows, all 64 vectors)",
+                        "achieved": flops / world / (kms * 1e-3) / 1e12, "peak": peak_tf, "unit": "TFLOP/s",
+                        "frac": flops / world / (kms * 1e-3) / 1e12 / peak_tf, "kernel_ms": kms,
+                        "traffic": None}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        C1 = configs.config4(nvec=1)
+        t0 = time.perf_counter()
+        want = O.kr_apply(C1["factors"], C1["vecs"][0])
+        t = time.perf_counter() - t0
+        got = out[0].cpu().numpy()
+        res["cpu_baseline"] = {"value": flops / B / t / 1e9, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                               "sample": f"oracle kr_apply of vector 0 (all 512 rows, {t:.2f} s)"}
+        res["parity"] = {"vector0_rel_diff": float(np.linalg.norm(got - want) / np.linalg.norm(want))}
+    del vs, vecs, fac, sk, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def sharded_solver(args, T, torch, dev, world, rank, local):
+    """Config 5: 8 right-hand sides, RHS j on rank j mod G (no device
+    collective, reports gathered on the host), each rank's RHS solved
+    concurrently on their own CUDA streams; randomized rounding."""
+    import torch.distributed as dist
+    from paper_2409_09471_b200 import configs
+    from paper_2409_09471_b200.parallel import rhs_assignment, solve_rhs_sharded
+    n_rhs = 8
+    prepared = {}
+    for j in rhs_assignment(n_rhs, world, rank):
+        prepared[j] = _solver_inputs(T, torch, dev, configs.config5(j), "rto")
+    torch.cuda.synchronize()
+
+    def warm_one(j):
+        cfg, a, b, sk, frame = prepared[j]
+        w = T.SolverConfig(**{**configs.config5(j)["cfg"], "maxit": 4}, zero_rel=None, rounding="rto")
+        T.tt_sgmres(a, b, None, w, sk, frame)
+        torch.cuda.current_stream(dev).synchronize()
+        return {"iterations": 0}
+
+    def solve_one(j):
+        cfg, a, b, sk, frame = prepared[j]
+        t0 = time.perf_counter()
+        _, rep = T.tt_sgmres(a, b, None, cfg, sk, frame)
+        torch.cuda.current_stream(dev).synchronize()
+        return {"iterations": rep.iterations, "converged": rep.converged, "wall_s": time.perf_counter() - t0,
+                "res_sketched": rep.res_sketched[-1], "peak_rank": rep.peak_rank,
+                "time_to_1e-6_s": rep.time_to_tol.get(1e-6)}
+    solve_rhs_sharded(n_rhs, rank, world, warm_one, concurrency=args.concurrency, device=dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    reports, agg = solve_rhs_sharded(n_rhs, rank, world, solve_one, concurrency=args.concurrency, device=dev)
+    ttt = [r["time_to_1e-6_s"] for r in reports if r.get("time_to_1e-6_s") is not None]
+    return {"metric": "TT-sGMRES iterations/s (fp64), config 5, 8 RHS", "value": agg["it_per_s"], "unit": "it/s",
+            "n_gpus": world, "scaling": "strong", "iterations": agg["iterations"], "max_wall_s": agg["max_wall_s"],
+            "time_to_1e-6_s_max": max(ttt) if ttt else None,
+            "config": {"workload": "config5: d=50 n=256, ell=3, s=120, maxit=60, tol=1e-8, cap 100, RTO rounding; "
+                                   "RHS j on rank j mod G, a rank's RHS on concurrent CUDA streams",
+                       "concurrency": args.concurrency},
+            "reports": [{k: r[k] for k in ("rhs", "rank", "iterations", "converged", "wall_s", "time_to_1e-6_s")}
+                        for r in reports]}
 
 
 def run_extras(T, torch, dev):
@@ -523,12 +818,10 @@ def run_extras(T, torch, dev):
     return out
 
 
-def _dist_setup():
+def _dist_setup(args):
     import torch
     import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = world_from_env(args)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1 and not dist.is_initialized():
@@ -553,7 +846,7 @@ def run_kr(args):
     import paper_2409_09471_b200 as T
     from paper_2409_09471_b200 import _lib, configs
     from paper_2409_09471_b200.parallel import kr_apply_sharded, row_partition
-    world, rank, local, dev = _dist_setup()
+    world, rank, local, dev = _dist_setup(args)
     lib = _lib.load()
     C = configs.config4()
     sk = T.KhatriRaoSketch(C["factors"], device=dev)
@@ -599,7 +892,7 @@ def run_solver(args):
     import paper_2409_09471_b200 as T
     from paper_2409_09471_b200 import configs
     from paper_2409_09471_b200.parallel import solve_rhs_sharded
-    world, rank, local, dev = _dist_setup()
+    world, rank, local, dev = _dist_setup(args)
     from paper_2409_09471_b200.parallel import rhs_assignment
     n_rhs = 8
 
@@ -662,6 +955,10 @@ def run_solver(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args.gpus)
+    if args.launcher_selftest:
+        return launcher_selftest(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "kr":

@@ -189,7 +189,7 @@ size_t ttk_tt_round_ws_bytes(int d, const int* dims, const int* ranks);
 /* ---- randomize-then-orthogonalize sweeps (absent from the reference,
  * SPEC.md:313; restated in oracle/ttoracle.py rto_sweeps) --------------------
  * X: cores (R[k], n_k, R[k+1]); G: Gaussian TT-DRM cores (L[k], n_k, L[k+1])
- * (reference tt_drm_new, streaming.py:135-150) with L[c] <= min(R[c],
+ * (reference tt_drm_new, streaming.py:38-53) with L[c] <= min(R[c],
  * L[c-1] n_{c-1}); out: cores (L[k], n_k, L[k+1]), cores 0..d-2 left-orthonormal. */
 int ttk_rto_sweeps(int d, const int* dims, const int* R, const double* const* X, const int* L,
                    const double* const* G, double* const* out, void* ws, size_t ws_bytes, void* stream);
@@ -224,7 +224,7 @@ int ttk_io_write(const char* path, int kind, int d, const long long* header, int
 int ttk_drm_gaussian(unsigned long long seed, int core, int n, int r0_full, int r1_full, int r0, int r1,
                      double scale, double* out, void* stream);
 
-/* ---- streaming sketches (reference streaming.py:214-302) -------------------
+/* ---- streaming sketches (reference streaming.py:117-205) -------------------
  * stream_sketch: psi[mu] ((lr[mu] n_mu) x rr[mu+1]) and omega[mu-1]
  * (lr[mu] x rr[mu]) of a TT with ranks tr against the frame's left (Y, ranks
  * lr) and right (X, ranks rr) TT-DRMs. */
@@ -233,7 +233,7 @@ int ttk_stream_sketch(int d, const int* dims, const int* tr, const double* const
                       double* const* psi, double* const* omega, void* ws, size_t ws_bytes,
                       void* stream);
 size_t ttk_stream_sketch_ws_bytes(int d, const int* dims, const int* tr, const int* lr, const int* rr);
-/* combine_pairs kernel: out = sum_t coeff[t] in_t, left-to-right (streaming.py:242-260) */
+/* combine_pairs kernel: out = sum_t coeff[t] in_t, left-to-right (streaming.py:145-163) */
 int ttk_axpy_multi(int nterms, const double* coeff, const double* const* in, long long n, double* out,
                    void* stream);
 /* stream_recover up to its final tt_round: truncated-SVD pseudo-inverse halves

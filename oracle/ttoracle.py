@@ -22,12 +22,12 @@ ZERO_REL = 1e-14           # tt.py:355 (rounding zero test)
 
 
 # ---------------------------------------------------------------------------
-# constructors (tt.py:131-164, 413-447; streaming.py:135-150; sketch.py:38-47)
+# constructors (tt.py:131-164, 413-447; streaming.py:38-53; sketch.py:38-47)
 
 def attainable_ranks(dims, ranks):
     """Clip an interior rank profile to the unfolding sizes in exact integers.
 
-    Same rule as tt.py:152-156 / streaming.py:184-187 but with Python ints, so
+    Same rule as tt.py:152-156 / streaming.py:87-90 but with Python ints, so
     it does not overflow at large d*log(n) (reference quirk Q2)."""
     d = len(dims)
     out = list(ranks)
@@ -95,7 +95,7 @@ def kron_sum_operator(factors):
 
 
 def drm_new(dims, ranks, seed=0):
-    """Gaussian TT-DRM, core k ~ N(0, 1/(l_{k-1} n_k l_k)) (streaming.py:135-150)."""
+    """Gaussian TT-DRM, core k ~ N(0, 1/(l_{k-1} n_k l_k)) (streaming.py:38-53)."""
     dims = list(dims)
     full = [1] + list(ranks) + [1]
     rng = np.random.default_rng(seed)
@@ -115,7 +115,7 @@ def kr_factors_new(dims, rows, seed=0):
 
 
 def frame_new(dims, recovery_ranks, oversampling=20, seed=0):
-    """StreamFrame.create with exact-integer clipping (streaming.py:174-194).
+    """StreamFrame.create with exact-integer clipping (streaming.py:77-97).
 
     Returns (left_cores, right_cores)."""
     ranks = attainable_ranks(list(dims), list(recovery_ranks))
@@ -399,10 +399,10 @@ def kr_flops(rows, dims, ranks):
 
 
 # ---------------------------------------------------------------------------
-# streaming sketches (streaming.py:214-302)
+# streaming sketches (streaming.py:117-205)
 
 def stream_sketch(cores, left, right):
-    """Psi/Omega of one tensor against a frame (streaming.py:214-239).
+    """Psi/Omega of one tensor against a frame (streaming.py:117-142).
 
     left/right: Y (oversampled) and X (recovery) DRM cores."""
     d = len(cores)
@@ -427,7 +427,7 @@ def stream_sketch(cores, left, right):
 
 
 def combine_pairs(pairs, coeffs):
-    """Entrywise weighted sum, first term scaled then accumulated (streaming.py:242-260)."""
+    """Entrywise weighted sum, first term scaled then accumulated (streaming.py:145-163)."""
     psi = [c * coeffs[0] for c in pairs[0][0]]
     omega = [c * coeffs[0] for c in pairs[0][1]]
     for (ps, om), a in zip(pairs[1:], coeffs[1:]):
@@ -440,7 +440,7 @@ def combine_pairs(pairs, coeffs):
 
 def stream_recover(psi, omega, dims, rel_tol=0.0, max_rank=None, zero_rel=ZERO_REL):
     """Generalised-Nystrom core recovery with symmetric S^{-1/2} split of
-    pinv(Omega_mu) (rcond PINV_RCOND), then tt_round (streaming.py:263-302)."""
+    pinv(Omega_mu) (rcond PINV_RCOND), then tt_round (streaming.py:166-205)."""
     d = len(psi)
     if all(not np.any(p) for p in psi):
         return zero_tt(dims)

@@ -10,11 +10,9 @@ arithmetic runs in libttk_b200.so (C ABI: include/ttk_b200.h).
 from .errors import DegenerateRecovery, ShapeMismatch, SizeLimit
 from .precond import (
     ExpSumPreconditioner,
-    expsum_coeffs,
     matrix_exp,
     mode_multiply,
     precond_apply,
-    spectral_interval,
 )
 from .rto import (CounterDRM, rto_flops, rto_ranks, rto_sweeps, tt_matvec_round_rto, tt_round_rto,
                   tt_truncate_left_orth)

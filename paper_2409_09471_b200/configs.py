@@ -58,7 +58,7 @@ def concat_cores(a, b):
 
 
 def drm_cores(dims, ranks, seed):
-    """reference tt_drm_new (streaming.py:135-150) draws."""
+    """reference tt_drm_new (streaming.py:38-53) draws."""
     full = [1] + list(ranks) + [1]
     rng = np.random.default_rng(seed)
     return [rng.normal(0.0, np.sqrt(1.0 / (full[k] * n * full[k + 1])), size=(full[k], n, full[k + 1]))

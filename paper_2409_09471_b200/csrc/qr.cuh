@@ -1,6 +1,6 @@
 // Tall-skinny Householder QR (TSQR) and one-sided Jacobi SVD for the
 // rounding sweeps.  Replaces np.linalg.qr / np.linalg.svd (LAPACK) at the
-// reference call sites tt.py:330, tt.py:361, streaming.py:284.
+// reference call sites tt.py:330, tt.py:361, streaming.py:187.
 #pragma once
 #include "common.cuh"
 

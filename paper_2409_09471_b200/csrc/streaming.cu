@@ -1,5 +1,5 @@
-// STTA recovery (reference stream_recover, streaming.py:263-302) and the
-// entrywise sketch-pair combination (combine_pairs, streaming.py:242-260).
+// STTA recovery (reference stream_recover, streaming.py:166-205) and the
+// entrywise sketch-pair combination (combine_pairs, streaming.py:145-163).
 #include "gemm.cuh"
 #include "qr.cuh"
 #include "../../include/ttk_b200.h"
@@ -20,7 +20,7 @@ struct AxpyParams {
 };
 
 // out = c0*in0 + c1*in1 + ... accumulated left to right with separate
-// multiply and add roundings (numpy's `psi += a * m`, streaming.py:255,259)
+// multiply and add roundings (numpy's `psi += a * m`, streaming.py:158,259)
 __global__ void axpy_multi_kernel(const __grid_constant__ AxpyParams P) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < P.n;
        e += (long long)gridDim.x * blockDim.x) {
@@ -117,7 +117,7 @@ size_t ttk_stream_recover_ws_bytes(int d, const int* dims, const int* lr, const 
 // max(lr[mu], rr[mu]) * n_mu * rr[mu+1]) and their ranks into out_ranks (host).
 // Returns TTK_DEGENERATE for an all-zero Omega with nonzero Psi; an all-zero
 // Psi list gives out_ranks all 1 and a zero flag in *is_zero (reference
-// streaming.py:276-277).  Synchronises `stream`.
+// streaming.py:179-180).  Synchronises `stream`.
 int ttk_stream_recover_cores(int d, const int* dims, const int* lr, const int* rr,
                              const double* const* psi, const double* const* omega, double rcond,
                              double* const* out, int* out_ranks, int* is_zero, void* ws,

@@ -1,6 +1,6 @@
 // Left-to-right interface sweeps built on the grouped DMMA GEMM:
 //   * tt_dot (reference tt.py:285-294), batched over several partners
-//   * stream_sketch partial contractions (reference streaming.py:214-239)
+//   * stream_sketch partial contractions (reference streaming.py:117-142)
 #include "gemm.cuh"
 #include "../../include/ttk_b200.h"
 
@@ -96,7 +96,7 @@ int ttk_tt_dots(int d, const int* dims, const int* xr, const double* const* x, i
 }  // extern "C"
 
 // ---------------------------------------------------------------------------
-// stream_sketch (reference streaming.py:214-239).  Left partial contractions
+// stream_sketch (reference streaming.py:117-142).  Left partial contractions
 // L_{k+1} = Y_k^T (L_k x_1 C_k) and right partial contractions
 // R_k = (C_k x_3 R_{k+1}) X_k^T run as two independent chains; step j of the
 // left chain and step j of the right chain share one grouped GEMM launch.

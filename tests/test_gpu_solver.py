@@ -35,9 +35,11 @@ def test_solver_small_golden(cuda, name):
     assert rep.iterations == int(z[f"{name}_iters"])
     assert rep.converged == bool(z[f"{name}_conv"])
     assert rep.basis_rank == list(z[f"{name}_ranks"])
-    np.testing.assert_allclose(rep.res_sketched, z[f"{name}_res"], rtol=1e-6)
+    # north star: final residual within 1e-8 relative; the whole history is held to the same bar
+    assert abs(rep.res_sketched[-1] - z[f"{name}_res"][-1]) <= 1e-8 * z[f"{name}_res"][-1]
+    np.testing.assert_allclose(rep.res_sketched, z[f"{name}_res"], rtol=1e-8)
     want = z[f"{name}_xprobe"]
-    assert np.linalg.norm(probe(x) - want) <= 1e-7 * np.linalg.norm(want)
+    assert np.linalg.norm(probe(x) - want) <= 1e-8 * np.linalg.norm(want)
     assert len(rep.times["round"]) == rep.iterations
 
 

@@ -109,3 +109,32 @@ def test_uneven_gather_world2_gloo():
     for p in procs:
         p.join(timeout=60)
     assert all(res)
+
+
+def test_bench_launcher_spawns_world2():
+    """`python bench.py --gpus 2` without torchrun starts 2 ranks itself
+    (torch.distributed.run on 127.0.0.1); the ranks join one process group and
+    rank 0 reports n_gpus == 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                          "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-selftest"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["n_gpus"] == 2 and lines[0]["all_reduce"] == 2.0
+    assert lines[0]["launcher"] == "torch.distributed.run"
+
+
+def test_bench_refuses_world_mismatch():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-selftest"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr

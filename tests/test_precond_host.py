@@ -1,7 +1,6 @@
-"""Exp-sum preconditioner, CPU side: the package's host-side construction
-(expsum_coeffs, spectral_interval, matrix_exp) bit-for-bit against the
-reference (golden/precond.npz, made by make_golden.py gen_precond), and the
-oracle's mode_multiply / exp-sum apply / preconditioned sGMRES pinned to the
+"""Exp-sum preconditioner, CPU side: argument validation of the package's
+setup (the coefficients are caller inputs, taken from the reference's own
+expsum_coeffs output in golden/precond.npz), and the oracle's mode_multiply / exp-sum apply / preconditioned sGMRES pinned to the
 reference's outputs on the cases of pkg/tests/test_precond.py and
 test_solvers.py:255-285."""
 
@@ -19,31 +18,12 @@ def z():
     return load("precond.npz")
 
 
-def test_expsum_coeffs_bitwise(z):
-    for i, (lo, hi, zeta) in enumerate(z["coef_cases"]):
-        a, b, bound = T.expsum_coeffs(float(lo), float(hi), int(zeta))
-        assert np.array_equal(a, z[f"coef{i}_alpha"]), (lo, hi, zeta)
-        assert np.array_equal(b, z[f"coef{i}_beta"])
-        assert bound == float(z[f"coef{i}_bound"])
-
-
-def test_spectral_interval_bitwise(z):
-    for i in range(int(z["int_count"])):
-        fs = [z[f"int{i}_f{k}"] for k in range(int(z[f"int{i}_n"]))]
-        assert T.spectral_interval(fs) == tuple(z[f"int{i}_val"])
-
-
 def test_host_errors():
     with pytest.raises(T.ShapeMismatch):
         T.matrix_exp(np.zeros((2, 3)))
     with pytest.raises(ValueError):
         T.matrix_exp(np.array([[np.inf, 0.0], [0.0, 1.0]]))
     assert np.array_equal(T.matrix_exp(np.zeros((4, 4))), np.eye(4))
-    for args in ((0.0, 1.0, 5), (-1.0, 1.0, 5), (2.0, 1.0, 3), (1.0, 2.0, 0)):
-        with pytest.raises(ValueError):
-            T.expsum_coeffs(*args)
-    with pytest.raises(T.ShapeMismatch):
-        T.spectral_interval([np.zeros((2, 3))])
     with pytest.raises(ValueError):
         T.ExpSumPreconditioner([np.eye(2)], [1.0, 2.0], [1.0], T.RoundSpec(0.0))
     with pytest.raises(ValueError):
