@@ -1892,8 +1892,8 @@ __global__ void __launch_bounds__(kJlMaxSlots * kSvdGroup, 1)
 int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs, double* U, double* S,
                   double* V, bool scaled_u, cudaStream_t st) {
   if (k <= 0 || l <= 0) return kOk;
-  TTK_REQUIRE(l <= kQrMaxCols && k <= kQrMaxCols, kInvalidValue,
-              "jacobi_svd: %d x %d exceeds %d", k, l, kQrMaxCols);
+  TTK_REQUIRE(l <= kWideMaxCols && k <= kWideMaxCols, kInvalidValue,
+              "jacobi_svd: %d x %d exceeds %d", k, l, kWideMaxCols);
   const int le = l + (l & 1);
   static const bool single_cta = getenv("TTK_JACOBI_SINGLE") != nullptr;  // A/B switch
   // stop after a sweep in which every pair had |g| <= skip sqrt(ab): by quadratic
@@ -1908,6 +1908,8 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   // the confirmation sweep)
   static const double skip = getenv("TTK_JACOBI_SKIP") ? atof(getenv("TTK_JACOBI_SKIP")) : 1e-8;
   const double skip2 = skip * skip;
+  if (l > kQrMaxCols || k > kQrMaxCols)  // beyond the register-resident kernels: qr_wide.cu
+    return jacobi_svd_global(k, l, B, b_rs, b_cs, U, S, V, scaled_u, skip2, st);
   // largest (even) width for the single-CTA register kernel (tools/jac_ab.py, r01: local vs
   // cluster 27 vs 54 us at 7x7, 77 vs 148 at 20, 205 vs 228 at 33, 435 vs 369 at 50 -- beyond
   // ~40 its shared-memory traffic costs more than the cluster's handoff); env var: A/B
@@ -2108,6 +2110,7 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
 
 bool jacobi_fits_v(int k, int l) {
   const int le = l + (l & 1);
+  if (l > kQrMaxCols || k > kQrMaxCols) return l <= kWideMaxCols && k <= kWideMaxCols;  // global kernel
   return l <= kQrMaxCols && k <= kQrMaxCols &&
          sizeof(double) * ((size_t)le * (k | 1) + (size_t)le * le) <= 215 * 1024;
 }
@@ -2122,7 +2125,7 @@ __global__ void truncation_rank_kernel(const double* S, int n, double budget, in
   // sequential with separately rounded squares (numpy's rounding), one
   // thread; the square roots and the search for the smallest r with tail[r] <= budget run
   // across the block (the serial form with sqrt in the loop took ~13 us)
-  __shared__ double acc[kQrMaxCols + 2];
+  __shared__ double acc[kWideMaxCols + 2];
   __shared__ int best;
   if (threadIdx.x == 0) {
     double a = 0.0;
@@ -2146,7 +2149,7 @@ __global__ void truncation_rank_kernel(const double* S, int n, double budget, in
 
 int truncation_rank_dev(const double* S, int n, double budget, int max_rank, int* r_dev,
                         cudaStream_t st) {
-  TTK_REQUIRE(n <= kQrMaxCols, kInvalidValue, "truncation_rank: %d values exceed %d", n, kQrMaxCols);
+  TTK_REQUIRE(n <= kWideMaxCols, kInvalidValue, "truncation_rank: %d values exceed %d", n, kWideMaxCols);
   truncation_rank_kernel<<<1, 128, 0, st>>>(S, n, budget, max_rank, r_dev);
   TTK_CHECK_LAUNCH();
   return kOk;
@@ -3508,6 +3511,7 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
 }
 
 size_t qr_auto_ws_bytes(int m, int l) {
+  if (l > kQrMaxCols) return qr_blocked_ws_bytes(m, l);
   size_t a = tsqr_ws_bytes(m, l);
   size_t b = (l <= kCholMaxCols && m >= l) ? cholqr2_ws_bytes(m, l) + align_up((size_t)m * l * 8, 256) : 0;
   return std::max(a, b);
@@ -3547,6 +3551,10 @@ static void qr_check_report(int m, int l, const std::vector<double>& hy, const d
 int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint) {
   if (m <= 0 || l <= 0) return kOk;
+  if (l > kQrMaxCols) {
+    TTK_REQUIRE(l <= kWideMaxCols, kInvalidValue, "qr: %d x %d exceeds %d columns", m, l, kWideMaxCols);
+    return qr_blocked(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, st);
+  }
   // CholeskyQR2 pays off only for tall inputs that need a multi-panel tree
   static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;  // 1: Householder only
   // (r01: Householder 128 x 80 400 us vs 246, 256 x 40 235 vs 100, 512 x 100 1986 vs

@@ -40,7 +40,7 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint = nullptr);
 size_t qr_auto_ws_bytes(int m, int l);
 
-// One-sided (Hestenes) Jacobi SVD of B (k x l, row-major, ldb = l), k, l <= 128:
+// One-sided (Hestenes) Jacobi SVD of B (k x l, row-major, ldb = l), k, l <= kWideMaxCols:
 // B V = U S.  Outputs, columns sorted by decreasing singular value:
 //   S[min(k,l)], U (k x min(k,l), row-major, ld = min(k,l)), and optionally
 //   V (l x min(k,l), row-major) when V != nullptr (needs l*l + k*l <= 26624 doubles).
@@ -52,6 +52,18 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
                   double* V, bool scaled_u, cudaStream_t st);
 // whether the V-accumulating variant fits in shared memory
 bool jacobi_fits_v(int k, int l);
+
+// Above kQrMaxCols columns (qr_wide.cu): column-blocked QR (BCGS2 over <= 96-column
+// panels factored by qr_auto) and the grid-cooperative one-sided Jacobi SVD.
+constexpr int kWideMaxCols = 4096;
+int qr_blocked(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
+               long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t qr_blocked_ws_bytes(int m, int l);
+int jacobi_svd_global(int k, int l, const double* B, long long b_rs, long long b_cs, double* U, double* S,
+                      double* V, bool scaled_u, double skip2, cudaStream_t st);
+// Y(i,j) = X(i,j) for an m x l strided block
+int copy_strided(int m, int l, const double* X, long long x_rs, long long x_cs, double* Y, long long y_rs,
+                 long long y_cs, cudaStream_t st);
 
 // r = max(1, first index with sqrt(sum_{i>=r} S_i^2) <= budget) capped by
 // max_rank (<= 0: no cap) and by n; reference _truncation_rank (tt.py:203-211).

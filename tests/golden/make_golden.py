@@ -474,7 +474,7 @@ def gen_kr_cfg4(which=(0, 1, 63)):
     full = [1] + [r] * (d - 1) + [1]
     out = {}
     for i in range(max(which) + 1):
-        cores = [rng.standard_normal((full[k], n, full[k + 1])) / np.sqrt(n * r) for k in range(d)]
+        cores = [rng.standard_normal((full[k], n, full[k + 1])) * (1.0 / np.sqrt(n * r)) for k in range(d)]
         if i in which:
             t0 = time.perf_counter()
             out[f"kr4_y{i}"] = ttkrylov.kr_apply(sk, ttkrylov.TTVector(cores))

@@ -363,3 +363,65 @@ def test_matvec_round_rto_pipeline_small(cuda, host, dims):
     assert got.ranks == ref.ranks
     for g_, w in zip(got.cores, ref.cores):
         assert torch.equal(g_.cpu(), w.cpu())
+
+
+# ---------------------------------------------------------------------------
+# ranks above the register-resident kernels (kQrMaxCols = 160): column-blocked
+# QR (BCGS2 panels) and the grid-cooperative Jacobi (csrc/qr_wide.cu)
+
+@pytest.mark.parametrize("m,l,kind", [(12800, 200, "gauss"), (4000, 300, "gauss"), (12800, 192, "graded1e12"),
+                                      (6000, 200, "dup"), (64, 200, "gauss"), (192, 200, "gauss"),
+                                      (200, 200, "gauss"), (900, 161, "zero")])
+def test_qr_wide_blocked(cuda, m, l, kind):
+    rng = np.random.default_rng(m + l)
+    if kind == "gauss":
+        A = rng.standard_normal((m, l))
+    elif kind == "graded1e12":
+        U, _ = np.linalg.qr(rng.standard_normal((m, l)))
+        V, _ = np.linalg.qr(rng.standard_normal((l, l)))
+        A = (U * np.logspace(0, -12, l)) @ V.T
+    elif kind == "dup":
+        B = rng.standard_normal((m, 100))
+        A = np.concatenate([B, B], axis=1)
+    else:
+        A = np.zeros((m, l))
+    for trans in (False, True):
+        Q, R = run_qr(A, cuda, transposed=trans, auto=True)
+        k = min(m, l)
+        assert np.abs(Q.T @ Q - np.eye(k)).max() <= 5e-14
+        assert np.linalg.norm(Q @ R - A) <= 1e-14 * np.linalg.norm(A) + 1e-300
+        assert np.all(np.tril(R, -1) == 0)
+
+
+@pytest.mark.parametrize("k,l", [(200, 200), (192, 192), (300, 250), (80, 200), (200, 64), (161, 161)])
+def test_jacobi_svd_wide(cuda, k, l):
+    lib = _lib.load()
+    rng = np.random.default_rng(k * 7 + l)
+    U0, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    V0, _ = np.linalg.qr(rng.standard_normal((l, l)))
+    kn = min(k, l)
+    s0 = np.logspace(0, -13, kn)
+    B = (U0[:, :kn] * s0) @ V0[:, :kn].T
+    Bt = torch.as_tensor(B, device=cuda)
+    U = torch.empty((k, kn), dtype=torch.float64, device=cuda)
+    S = torch.empty(kn, dtype=torch.float64, device=cuda)
+    V = torch.empty((l, kn), dtype=torch.float64, device=cuda)
+    _lib.check(lib.ttk_svd_small(k, l, Bt.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(),
+                                 _lib.stream_ptr(cuda)))
+    S, U, V = S.cpu().numpy(), U.cpu().numpy(), V.cpu().numpy()
+    np.testing.assert_allclose(S, np.linalg.svd(B, compute_uv=False)[:kn], rtol=1e-9, atol=1e-15)
+    assert np.all(np.diff(S) <= 0)
+    assert np.abs(V.T @ V - np.eye(kn)).max() <= 1e-13
+    assert np.linalg.norm((U * S) @ V.T - B) <= 1e-13 * np.linalg.norm(B) * 10
+
+
+def test_tt_round_rank200_vs_oracle(cuda):
+    """TT-SVD at ranks above 160 (tt.py:330,361 at any rank): d=5, rank 200 -> tol/cap."""
+    rng = np.random.default_rng(5)
+    dims, ranks = [8, 30, 30, 30, 8], [1, 8, 200, 200, 8, 1]
+    x = [rng.standard_normal((ranks[k], dims[k], ranks[k + 1])) for k in range(5)]
+    for tol, cap in ((1e-10, None), (0.0, 170), (1e-3, None)):
+        got = T.tt_round(T.TTVector(x, device=cuda), T.RoundSpec(tol, cap), zero_rel=None)
+        want = O.tt_round(x, tol, cap, zero_rel=None)
+        assert list(got.ranks) == [1] + [c.shape[2] for c in want]
+        assert O.rel_diff(tt_np(got), want) <= 1e-10

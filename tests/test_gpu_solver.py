@@ -10,6 +10,9 @@ from golden_io import cores, factors, load
 
 pytestmark = pytest.mark.gpu
 
+# absolute roundoff floor of a sketched residual (relative to ||S b||): ~45 ulp
+RES_FLOOR = 1e-14
+
 
 def cfg_from(z, name, **extra):
     c = z[f"{name}_cfg"]
@@ -35,11 +38,16 @@ def test_solver_small_golden(cuda, name):
     assert rep.iterations == int(z[f"{name}_iters"])
     assert rep.converged == bool(z[f"{name}_conv"])
     assert rep.basis_rank == list(z[f"{name}_ranks"])
-    # north star: final residual within 1e-8 relative; the whole history is held to the same bar
-    assert abs(rep.res_sketched[-1] - z[f"{name}_res"][-1]) <= 1e-8 * z[f"{name}_res"][-1]
-    np.testing.assert_allclose(rep.res_sketched, z[f"{name}_res"], rtol=1e-8)
-    want = z[f"{name}_xprobe"]
-    assert np.linalg.norm(probe(x) - want) <= 1e-8 * np.linalg.norm(want)
+    # north star: final residual within 1e-8 relative, above the roundoff floor.
+    # The sketched residual is relative to ||S b|| (= 1 at the start); the
+    # reference's own final residual moves by ~1e-16 absolute (2-4e-7 relative
+    # at 5e-10) when 1e-16 noise is injected into its roundings
+    # (tools/sensitivity_small.py, profiles/r02_solver_sensitivity_small.txt),
+    # so the bar is 1e-8 relative + FLOOR absolute.
+    want = z[f"{name}_res"]
+    assert np.all(np.abs(np.array(rep.res_sketched) - want) <= 1e-8 * want + RES_FLOOR)
+    wp = z[f"{name}_xprobe"]
+    assert np.linalg.norm(probe(x) - wp) <= 1e-8 * np.linalg.norm(wp)
     assert len(rep.times["round"]) == rep.iterations
 
 
@@ -81,8 +89,8 @@ def test_solver_config1_rto_vs_oracle(cuda):
                         rto_drm=[g.numpy() for g in drm])
     assert rep.iterations == orep["iterations"]
     assert rep.basis_rank == orep["basis_rank"]
-    assert abs(rep.res_sketched[-1] - orep["res_sketched"][-1]) <= 1e-8 * orep["res_sketched"][-1]
-    np.testing.assert_allclose(rep.res_sketched, orep["res_sketched"], rtol=1e-9)
+    assert abs(rep.res_sketched[-1] - orep["res_sketched"][-1]) <= 1e-8 * orep["res_sketched"][-1] + RES_FLOOR
+    np.testing.assert_allclose(rep.res_sketched, orep["res_sketched"], rtol=1e-9, atol=RES_FLOOR)
     assert O.rel_diff([c.cpu().numpy() for c in x.cores], ox) <= 1e-8
 
 
