@@ -5,9 +5,10 @@
 //
 //  * qr_blocked: column-blocked QR.  Panels of <= 96 columns; each panel is
 //    projected against the Q columns already formed twice (block classical
-//    Gram-Schmidt with re-orthogonalisation, BCGS2: two GEMM pairs per panel)
-//    and then factored by qr_auto (CholeskyQR2 / rank-robust CholeskyQR3 /
-//    Householder TSQR).  Wide inputs (m < l) factor the leading m columns and
+//    Gram-Schmidt with re-orthogonalisation, BCGS2: two GEMM pairs per panel),
+//    factored by qr_auto (CholeskyQR2 / rank-robust CholeskyQR3 / Householder
+//    TSQR), and its unit-norm Q block projected and re-factored once more
+//    (an ill-conditioned panel amplifies the projection residual by kappa).  Wide inputs (m < l) factor the leading m columns and
 //    form R's trailing columns as Q^T A.
 //  * jacobi_svd_global: one-sided (Hestenes) Jacobi with the columns in global
 //    memory (L2-resident: 200 x 200 fp64 is 320 KB), one warp per column pair,
@@ -42,11 +43,34 @@ __global__ void add_block_kernel(int rows, int cols, const double* __restrict__ 
   }
 }
 
-__global__ void zero_lower_kernel(int k, int l, double* R) {
-  const long long n = (long long)k * l;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(e / l), c = (int)(e % l);
-    if (c < r) R[e] = 0.0;
+// Columns of a projected unit-norm block that vanished (they lay in the span
+// of the Q columns already formed: completion directions of a rank-deficient
+// panel) are refilled with a deterministic pseudo-random vector; they carry an
+// O(eps) weight in R, so the factorisation stays backward stable, and the next
+// projection + QR makes them orthonormal to everything before.
+__global__ void refill_vanished_kernel(int m, double* X, long long x_rs, long long x_cs, unsigned long long seed) {
+  __shared__ double red[32];
+  __shared__ int vanished;
+  double* x = X + blockIdx.x * x_cs;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) s = fma(x[i * x_rs], x[i * x_rs], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    vanished = t < 1e-16;
+  }
+  __syncthreads();
+  if (!vanished) return;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    unsigned long long z = ((unsigned long long)i + 1) * 0x9E3779B97F4A7C15ull + seed * 0xD1B54A32D192ED03ull +
+                           blockIdx.x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    x[i * x_rs] = ((double)(z >> 11) * (2.0 / 9007199254740992.0) - 1.0) / sqrt((double)m);
   }
 }
 
@@ -58,7 +82,7 @@ size_t qr_blocked_ws_bytes(int m, int l) {
   const int k = std::min(m, l);
   const int np = (k + kWidePanel - 1) / kWidePanel;
   const int w = (k + np - 1) / np;
-  return align_up((size_t)m * w * 8, 256) + align_up((size_t)k * w * 8, 256) + align_up((size_t)w * w * 8, 256) +
+  return align_up((size_t)m * w * 8, 256) + 2 * align_up((size_t)k * w * 8, 256) + 2 * align_up((size_t)w * w * 8, 256) +
          kWideSplitBytes + qr_auto_ws_bytes(m, w) + 4096;
 }
 
@@ -74,7 +98,9 @@ int qr_blocked(int m, int l, const double* A, long long a_rs, long long a_cs, do
   Arena ar(ws, ws_bytes);
   double* P = ar.take<double>((size_t)m * w);      // panel, row-major (m x w)
   double* C = ar.take<double>((size_t)k * w);      // projection coefficients (c0 x w)
+  double* C2 = ar.take<double>((size_t)k * w);
   double* Rp = ar.take<double>((size_t)w * w);     // panel R
+  double* R2 = ar.take<double>((size_t)w * w);     // re-factorisation R
   void* split = ar.take<char>(kWideSplitBytes);
   const size_t used = align_up(ar.used, 256);
   void* qws = (char*)ws + used;
@@ -96,8 +122,35 @@ int qr_blocked(int m, int l, const double* A, long long a_rs, long long a_cs, do
         TTK_CHECK_LAUNCH();
       }
     }
-    TTK_TRY(qr_auto(m, wj, P, wj, 1, Q + (long long)c0 * q_cs, q_rs, q_cs, Rp, qws, qbytes, st));
-    if (R) {
+    double* Qj = Q + (long long)c0 * q_cs;
+    TTK_TRY(qr_auto(m, wj, P, wj, 1, Qj, q_rs, q_cs, Rp, qws, qbytes, st));
+    if (c0 > 0) {
+      // Q_j = P R_jj^{-1} amplifies P's O(eps |A_j|) residual along Q[:, :c0] by
+      // kappa(P) (graded inputs: 1e-10 instead of 1e-16): project the unit-norm
+      // Q_j once more and re-factor the now well-conditioned block,
+      //   Q_j = Q C2 + Q_j' R2  ->  R[:c0, j] += C2 R_jj,  R_jj <- R2 R_jj
+      g = make_gemm(c0, wj, m, Q, q_cs, q_rs, Qj, q_rs, q_cs, C, wj, 1);
+      TTK_TRY(gemm_group_launch(&g, 1, split, kWideSplitBytes, st));
+      g = make_gemm(m, wj, c0, Q, q_rs, q_cs, C, wj, 1, Qj, q_rs, q_cs, -1.0, 1.0);
+      TTK_TRY(gemm_group_launch(&g, 1, split, kWideSplitBytes, st));
+      refill_vanished_kernel<<<wj, 256, 0, st>>>(m, Qj, q_rs, q_cs, (unsigned long long)c0);
+      TTK_CHECK_LAUNCH();
+      // second projection (C accumulates it: Q_j = Q (C + C') + Q_j'' exactly)
+      g = make_gemm(c0, wj, m, Q, q_cs, q_rs, Qj, q_rs, q_cs, C2, wj, 1);
+      TTK_TRY(gemm_group_launch(&g, 1, split, kWideSplitBytes, st));
+      g = make_gemm(m, wj, c0, Q, q_rs, q_cs, C2, wj, 1, Qj, q_rs, q_cs, -1.0, 1.0);
+      TTK_TRY(gemm_group_launch(&g, 1, split, kWideSplitBytes, st));
+      add_block_kernel<<<grid_for((long long)c0 * wj), 256, 0, st>>>(c0, wj, C2, wj, C, wj, 1);
+      TTK_CHECK_LAUNCH();
+      TTK_TRY(copy_strided(m, wj, Qj, q_rs, q_cs, P, wj, 1, st));
+      TTK_TRY(qr_auto(m, wj, P, wj, 1, Qj, q_rs, q_cs, R2, qws, qbytes, st));
+      if (R) {
+        g = make_gemm(c0, wj, wj, C, wj, 1, Rp, wj, 1, R + c0, l, 1, 1.0, 1.0);
+        TTK_TRY(gemm_group_launch(&g, 1, split, kWideSplitBytes, st));
+        g = make_gemm(wj, wj, wj, R2, wj, 1, Rp, wj, 1, R + (size_t)c0 * l + c0, l, 1);
+        TTK_TRY(gemm_group_launch(&g, 1, split, kWideSplitBytes, st));
+      }
+    } else if (R) {
       add_block_kernel<<<grid_for((long long)wj * wj), 256, 0, st>>>(wj, wj, Rp, wj, R + (size_t)c0 * l + c0, l, 0);
       TTK_CHECK_LAUNCH();
     }
@@ -107,10 +160,9 @@ int qr_blocked(int m, int l, const double* A, long long a_rs, long long a_cs, do
     g = make_gemm(k, l - k, m, Q, q_cs, q_rs, A + (long long)k * a_cs, a_rs, a_cs, R + k, l, 1);
     TTK_TRY(gemm_group_launch(&g, 1, split, kWideSplitBytes, st));
   }
-  if (R) {
-    zero_lower_kernel<<<grid_for((long long)k * l), 256, 0, st>>>(k, l, R);
-    TTK_CHECK_LAUNCH();
-  }
+  // R is block upper triangular (zero below the diagonal panels); a panel's
+  // diagonal block is upper triangular unless the panel took the rank-robust
+  // path, whose R = Q^T Y is full (qr_auto's contract: A = Q R, Q orthonormal)
   return kOk;
 }
 

@@ -32,8 +32,16 @@ __global__ void axpy_multi_kernel(const __grid_constant__ AxpyParams P) {
 
 // keep count and the two half pseudo-inverse factors of one Omega (k x l):
 //   LH = S^{-1/2} U^T (kept x k),  RH = V S^{-1/2} (l x kept)
+// copy of X (n entries) scaled by an exact power of two
+__global__ void scale_copy_kernel(long long n, const double* __restrict__ X, double s, double* __restrict__ Y) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    Y[e] = X[e] * s;
+}
+
+// S, U, V: SVD of the cross matrix scaled by 2^e (unscale = 2^(e/2) restores
+// 1/sqrt of the true singular values)
 __global__ void recover_halves_kernel(int k, int l, const double* U, const double* S, const double* V,
-                                      double rcond, double* LH, double* RH, int* kept_out) {
+                                      double rcond, double unscale, double* LH, double* RH, int* kept_out) {
   const int kn = min(k, l);
   __shared__ int kept;
   if (threadIdx.x == 0) {
@@ -47,11 +55,11 @@ __global__ void recover_halves_kernel(int k, int l, const double* U, const doubl
   const int c = kept;
   for (int e = threadIdx.x; e < c * k; e += blockDim.x) {
     int i = e / k, j = e - i * k;
-    LH[e] = U[(long long)j * kn + i] * (1.0 / sqrt(S[i]));
+    LH[e] = U[(long long)j * kn + i] * (unscale / sqrt(S[i]));
   }
   for (int e = threadIdx.x; e < l * c; e += blockDim.x) {
     int j = e / c, i = e - j * c;
-    RH[e] = V[(long long)j * kn + i] * (1.0 / sqrt(S[i]));
+    RH[e] = V[(long long)j * kn + i] * (unscale / sqrt(S[i]));
   }
 }
 
@@ -108,7 +116,8 @@ size_t ttk_stream_recover_ws_bytes(int d, const int* dims, const int* lr, const 
     tot += align_up(k * kn * 8, 256) + align_up(kn * 8, 256) + align_up(l * kn * 8, 256) +
            align_up(kn * k * 8, 256) + align_up(l * kn * 8, 256);
   }
-  for (int mu = 0; mu < d; ++mu) tmax = std::max(tmax, (size_t)std::max(lr[mu], rr[mu]) * dims[mu] * rr[mu + 1]);
+  for (int mu = 0; mu < d; ++mu)
+    tmax = std::max(tmax, std::max((size_t)std::max(lr[mu], rr[mu]) * dims[mu] * rr[mu + 1], (size_t)lr[mu] * rr[mu]));
   return tot + align_up(tmax * 8, 256) + (size_t)(4 * d + 16) * 256 + (16u << 20) + 65536;
 }
 
@@ -137,7 +146,8 @@ int ttk_stream_recover_cores(int d, const int* dims, const int* lr, const int* r
     RH[mu] = ar.take<double>(l * kn);
   }
   size_t tmax = 0;
-  for (int mu = 0; mu < d; ++mu) tmax = std::max(tmax, (size_t)std::max(lr[mu], rr[mu]) * dims[mu] * rr[mu + 1]);
+  for (int mu = 0; mu < d; ++mu)
+    tmax = std::max(tmax, std::max((size_t)std::max(lr[mu], rr[mu]) * dims[mu] * rr[mu + 1], (size_t)lr[mu] * rr[mu]));
   double* T = ar.take<double>(tmax);
   double* red = ar.take<double>(2 * (size_t)d + 8);
   int* kept = ar.take<int>((size_t)d + 8);
@@ -169,11 +179,22 @@ int ttk_stream_recover_cores(int d, const int* dims, const int* lr, const int* r
   for (int mu = 1; mu < d; ++mu)
     TTK_REQUIRE(hred[d + mu - 1] != 0.0, kDegenerate, "zero cross matrix at mode %d", mu);
 
-  // truncated SVDs of the cross matrices and their symmetric half inverses
+  // truncated SVDs of the cross matrices and their symmetric half inverses.
+  // Omega is scaled by an exact power of two to unit size first (as LAPACK's
+  // dgesdd scales): at d = 50 its entries are ~1e-106, the Jacobi rotation
+  // tests square the products (~1e-424) and underflow, leaving noise singular
+  // values at the level of the large ones (config-5 solutions blew up to 1e71)
   for (int mu = 1; mu < d; ++mu) {
     const int k = lr[mu], l = rr[mu];
-    TTK_TRY(jacobi_svd(k, l, omega[mu - 1], U[mu], S[mu], V[mu], st));
-    recover_halves_kernel<<<1, 256, 0, st>>>(k, l, U[mu], S[mu], V[mu], rcond, LH[mu], RH[mu], kept + mu);
+    const double fro = std::sqrt(hred[d + mu - 1]);
+    const int e = -std::ilogb(fro);              // fro * 2^e in [1, 2)
+    const double sc = std::ldexp(1.0, e);
+    const double unscale = (e % 2 == 0) ? std::ldexp(1.0, e / 2) : std::ldexp(std::sqrt(2.0), (e - 1) / 2);
+    scale_copy_kernel<<<std::min(ceil_div((long)k * l, 256), 4 * kNumSMs), 256, 0, st>>>((long long)k * l,
+                                                                                        omega[mu - 1], sc, T);
+    TTK_CHECK_LAUNCH();
+    TTK_TRY(jacobi_svd(k, l, T, U[mu], S[mu], V[mu], st));
+    recover_halves_kernel<<<1, 256, 0, st>>>(k, l, U[mu], S[mu], V[mu], rcond, unscale, LH[mu], RH[mu], kept + mu);
     TTK_CHECK_LAUNCH();
   }
   std::vector<int> hk(d + 1, 1);
