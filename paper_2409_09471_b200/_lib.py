@@ -14,7 +14,7 @@ import torch
 from .errors import DegenerateRecovery, ShapeMismatch
 
 _PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("TTK_LIB_PATH") or os.path.join(_PKG_DIR, "libttk_b200.so")  # TTK_LIB_PATH: A/B experiments
+LIB_PATH = os.path.join(_PKG_DIR, "libttk_b200.so")
 
 c_int = ctypes.c_int
 c_ll = ctypes.c_longlong

@@ -3,6 +3,9 @@
 #include "../../include/ttk_b200.h"
 
 #include <chrono>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -21,7 +24,35 @@ void set_error(const char* fmt, ...) {
 
 const char* last_error() { return g_err; }
 
-static const bool g_host_prof = getenv("TTK_HOST_PROF") != nullptr;
+namespace {
+std::mutex g_attr_mu;
+std::set<std::tuple<int, const void*, int>> g_attr_done;
+int g_sms[64] = {0};
+}  // namespace
+
+int num_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kNumSMs;
+  if (g_sms[dev] == 0) {
+    int n = kNumSMs;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+    g_sms[dev] = n;  // benign race: every writer stores the same value
+  }
+  return g_sms[dev];
+}
+
+int set_attr_once(const void* fn, cudaFuncAttribute attr, int value) {
+  int dev = 0;
+  TTK_CHECK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  const auto key = std::make_tuple(dev, fn, (int)attr);
+  if (g_attr_done.count(key)) return kOk;
+  TTK_CHECK_CUDA(cudaFuncSetAttribute(fn, attr, value));
+  g_attr_done.insert(key);
+  return kOk;
+}
+
+static const bool g_host_prof = knob_env("TTK_HOST_PROF") != nullptr;
 std::atomic<long long> g_syncs{0}, g_sync_ns{0};
 
 int host_sync(cudaStream_t st) {

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstdarg>
 #include <cmath>
@@ -63,7 +64,27 @@ const char* last_error();
     if (_s != ::ttk::kOk) return _s;                                             \
   } while (0)
 
+// grid-size cap for grid-stride loops (B200: 148 SMs); residency decisions use num_sms()
 constexpr int kNumSMs = 148;
+
+// SM count of the current device (queried once per device)
+int num_sms();
+
+// Kernel attributes are per device: set (fn, attr) = value once per device.
+int set_attr_once(const void* fn, cudaFuncAttribute attr, int value);
+template <class F>
+inline int set_attr_once(F* fn, cudaFuncAttribute attr, int value) {
+  return set_attr_once((const void*)fn, attr, value);
+}
+
+// Experiment / diagnostic knobs (A/B switches, tracing) are read from the
+// environment only in builds with -DTTK_DEBUG_KNOBS; the shipped library
+// ignores them, so no environment variable changes its numerics or control flow.
+#ifdef TTK_DEBUG_KNOBS
+inline const char* knob_env(const char* name) { return getenv(name); }
+#else
+inline const char* knob_env(const char*) { return nullptr; }
+#endif
 
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

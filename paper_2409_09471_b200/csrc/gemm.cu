@@ -173,11 +173,9 @@ template <int BM, int BN, int WM, int WN, int ST, int CAP>
 int launch_cfg(GemmGroupT<CAP>& g, cudaStream_t st) {
   using Cfg = GemmCfg<BM, BN, kBK, WM, WN, ST>;
   auto kern = gemm_group_kernel<BM, BN, kBK, WM, WN, ST, CAP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    TTK_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  {  // per-device attributes (set_attr_once)
+    TTK_TRY(set_attr_once(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)Cfg::kSmemBytes));
-    attr_set = true;
   }
   kern<<<g.total_tiles, Cfg::kThreads, Cfg::kSmemBytes, st>>>(g);
   TTK_CHECK_LAUNCH();
@@ -259,7 +257,7 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
     if (nonempty == 0) continue;
     g.count = nonempty;
     TileCfg cfg = pick_cfg(g.p, g.count);
-    static const int force = getenv("TTK_GEMM_FORCE_CFG") ? atoi(getenv("TTK_GEMM_FORCE_CFG")) : -1;  // experiments
+    static const int force = knob_env("TTK_GEMM_FORCE_CFG") ? atoi(knob_env("TTK_GEMM_FORCE_CFG")) : -1;  // experiments
     if (force >= 0) cfg = (TileCfg)force;
     size_t pe; int total;
     plan(g.p, g.count, cfg, allow_split && ws != nullptr, &pe, &total);
@@ -289,7 +287,7 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
       TTK_REQUIRE(sa < (1LL << 31) && sb < (1LL << 31), kInvalidValue,
                   "gemm: operand spans %lld / %lld elements, limit 2^31", sa, sb);
     }
-    static const bool trace = getenv("TTK_GEMM_TRACE") != nullptr;  // shape log (diagnostics)
+    static const bool trace = knob_env("TTK_GEMM_TRACE") != nullptr;  // shape log (diagnostics)
     if (trace) fprintf(stderr, "gemm-launch count=%d\n", g.count);
     if (trace)
       for (int i = 0; i < g.count; ++i)

@@ -261,11 +261,9 @@ namespace {
 
 int kr_fused(int d, const int* n, int S, const double* const* F, int nvec, const int* ranks,
              const double* const* cores, double* out, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    TTK_CHECK_CUDA(cudaFuncSetAttribute(kr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  {  // per-device attributes (set_attr_once)
+    TTK_TRY(set_attr_once(kr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kr::smem_bytes(kr::NMAX)));
-    attr = true;
   }
   const int per = std::max(1, std::min(kKrMaxSlots / d, 64));
   for (int v0 = 0; v0 < nvec; v0 += per) {
@@ -341,7 +339,7 @@ int kr_two_phase(int d, const int* n, int S, const double* const* F, int nvec, c
     dim3 grid(ceil_div(S, rows_per_cta), nv);
     size_t smem = sizeof(double) * 2 * rmax * rows_per_cta;
     if (smem > 48 * 1024)
-      TTK_CHECK_CUDA(cudaFuncSetAttribute(kr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      TTK_TRY(set_attr_once(kr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)smem));
     kr_chain_kernel<<<grid, 32 * rows_per_cta, smem, st>>>(C);
     TTK_CHECK_LAUNCH();
@@ -457,7 +455,7 @@ int ttk_kr_sketch_matvec(int d, const int* n, int S, const double* const* Ft, co
   dim3 grid(ceil_div(S, rows_per_cta), 1);
   const size_t smem = sizeof(double) * 2 * rmax * rows_per_cta;
   if (smem > 48 * 1024)
-    TTK_CHECK_CUDA(cudaFuncSetAttribute(kr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TTK_TRY(set_attr_once(kr_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kr_chain_kernel<<<grid, 32 * rows_per_cta, smem, st>>>(CP);
   TTK_CHECK_LAUNCH();
   return kOk;

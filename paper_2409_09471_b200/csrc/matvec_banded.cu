@@ -162,12 +162,10 @@ int ttk_matvec_banded(int d, const int* rho, const int* n, const int* r, int w, 
   TTK_REQUIRE(blocks < (1LL << 31), kInvalidValue, "grid too large");
   const size_t smem = sizeof(double) * kBandThreads * rho_prod;
   TTK_REQUIRE(smem <= 200 * 1024, kInvalidValue, "operator ranks too large for the banded tile (%d)", rho_prod);
-  static bool attr = false;
-  if (!attr) {
+  {  // per-device attributes (set_attr_once)
     for (const void* f : {(const void*)matvec_banded_kernel<0>, (const void*)matvec_banded_kernel<1>,
                           (const void*)matvec_banded_kernel<2>})
-      TTK_CHECK_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
+      TTK_TRY(set_attr_once(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   }
   cudaStream_t st = (cudaStream_t)stream;
   const dim3 grid((unsigned)blocks, (unsigned)P.ncores);

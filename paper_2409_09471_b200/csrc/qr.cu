@@ -352,7 +352,7 @@ size_t tsqr_ws_bytes(int m, int l) {
 }
 
 static int qr_set_smem(const void* fn, size_t bytes) {
-  TTK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  TTK_TRY(set_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   return kOk;
 }
 
@@ -360,11 +360,9 @@ static int tsqr_tree(const QrPlan& P, const double* A, long long a_rs, long long
                      long long q_rs, long long q_cs, double* R, void* ws, size_t ws_bytes, size_t smem_f,
                      size_t smem_a, cudaStream_t st) {
   const int l = P.l, H = P.h, D = P.depth;
-  static bool attr = false;
-  if (!attr) {
+  {  // per-device attributes (set_attr_once)
     TTK_TRY(qr_set_smem((const void*)qr_pair_factor_kernel, 227 * 1024));
     TTK_TRY(qr_set_smem((const void*)qr_pair_apply_kernel, 128 * 1024));
-    attr = true;
   }
   const size_t pk = (size_t)l * (l + 1) / 2;
   Arena ar(ws, ws_bytes);
@@ -413,11 +411,9 @@ int tsqr(int m, int l, const double* A, long long a_rs, long long a_cs, double* 
   TTK_REQUIRE(ws != nullptr && ws_bytes >= P.ws_bytes, kWorkspace,
               "tsqr: workspace %zu < %zu bytes", ws_bytes, P.ws_bytes);
   const int H = P.h, ld = l | 1;
-  static bool attr = false;
-  if (!attr) {
+  {  // per-device attributes (set_attr_once)
     TTK_TRY(qr_set_smem((const void*)qr_panel_factor_kernel, 227 * 1024));
     TTK_TRY(qr_set_smem((const void*)qr_panel_apply_kernel, 227 * 1024));
-    attr = true;
   }
   const size_t smem_f = sizeof(double) * ((size_t)H * ld + 2 * H + l);
   const size_t smem_a = sizeof(double) * ((size_t)H * ld);
@@ -1895,7 +1891,7 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   TTK_REQUIRE(l <= kWideMaxCols && k <= kWideMaxCols, kInvalidValue,
               "jacobi_svd: %d x %d exceeds %d", k, l, kWideMaxCols);
   const int le = l + (l & 1);
-  static const bool single_cta = getenv("TTK_JACOBI_SINGLE") != nullptr;  // A/B switch
+  static const bool single_cta = knob_env("TTK_JACOBI_SINGLE") != nullptr;  // A/B switch
   // stop after a sweep in which every pair had |g| <= skip sqrt(ab): by quadratic
   // convergence the next sweep would only rotate by O(skip^2) < tol (a pure
   // confirmation sweep).  1e-8: the skipped rotations are O(1e-16), below the
@@ -1906,20 +1902,18 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   // (31.9 vs 31.9 ms) nor the solvers beyond their run-to-run noise; 1e-6 let
   // 128 x 128 orthogonality slip to 2e-12.  TTK_JACOBI_SKIP overrides (0 keeps
   // the confirmation sweep)
-  static const double skip = getenv("TTK_JACOBI_SKIP") ? atof(getenv("TTK_JACOBI_SKIP")) : 1e-8;
+  static const double skip = knob_env("TTK_JACOBI_SKIP") ? atof(knob_env("TTK_JACOBI_SKIP")) : 1e-8;
   const double skip2 = skip * skip;
   if (l > kQrMaxCols || k > kQrMaxCols)  // beyond the register-resident kernels: qr_wide.cu
     return jacobi_svd_global(k, l, B, b_rs, b_cs, U, S, V, scaled_u, skip2, st);
   // largest (even) width for the single-CTA register kernel (tools/jac_ab.py, r01: local vs
   // cluster 27 vs 54 us at 7x7, 77 vs 148 at 20, 205 vs 228 at 33, 435 vs 369 at 50 -- beyond
   // ~40 its shared-memory traffic costs more than the cluster's handoff); env var: A/B
-  static const int local_max = getenv("TTK_JACOBI_LOCAL_MAX") ? atoi(getenv("TTK_JACOBI_LOCAL_MAX")) : 40;
+  static const int local_max = knob_env("TTK_JACOBI_LOCAL_MAX") ? atoi(knob_env("TTK_JACOBI_LOCAL_MAX")) : 40;
   if (!single_cta && le <= std::min(local_max, 2 * kJlMaxSlots) && std::max(k, le) <= 4 * kSvdGroup) {
-    static bool lattr = false;
-    if (!lattr) {
+    {  // per-device attributes (set_attr_once)
       TTK_TRY(qr_set_smem((const void*)jacobi_local_kernel<2>, 128 * 1024));
       TTK_TRY(qr_set_smem((const void*)jacobi_local_kernel<4>, 128 * 1024));
-      lattr = true;
     }
     const int np = le / 2;
     const int threads = std::max(32, (np * kSvdGroup + 31) / 32 * 32);
@@ -1936,22 +1930,20 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   }
   // one-warp-per-CTA block kernel (in-CTA moves are shuffles); TTK_JACOBI_WARP=0
   // keeps the 16-lane block kernel below (A/B)
-  static const bool warp_off = getenv("TTK_JACOBI_WARP") && atoi(getenv("TTK_JACOBI_WARP")) == 0;
+  static const bool warp_off = knob_env("TTK_JACOBI_WARP") && atoi(knob_env("TTK_JACOBI_WARP")) == 0;
   if (!single_cta && !warp_off && l > 2 * kJwSlots && std::max(k, l) <= 12 * kJwLanes &&
       (l + 2 * kJwSlots - 1) / (2 * kJwSlots) <= 16) {
     const int CL = (l + 2 * kJwSlots - 1) / (2 * kJwSlots);
     const int rows = std::max(k, l);
     const int rpl = ((rows + kJwLanes - 1) / kJwLanes + 1) & ~1;
-    static bool wattr = false;
-    if (!wattr) {
+    {  // per-device attributes (set_attr_once)
       for (const void* fn : {(const void*)jacobi_warp_kernel<2>, (const void*)jacobi_warp_kernel<4>,
                              (const void*)jacobi_warp_kernel<6>, (const void*)jacobi_warp_kernel<8>,
                              (const void*)jacobi_warp_kernel<10>, (const void*)jacobi_warp_kernel<12>,
                              (const void*)jacobi_warp_kernel<2, true>, (const void*)jacobi_warp_kernel<4, true>,
                              (const void*)jacobi_warp_kernel<6, true>, (const void*)jacobi_warp_kernel<8, true>,
                              (const void*)jacobi_warp_kernel<10, true>, (const void*)jacobi_warp_kernel<12, true>})
-        TTK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      wattr = true;
+        TTK_TRY(set_attr_once(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     }
     const size_t jsm = sizeof(double) * 2 * kJwSlots * 4 * (size_t)rpl * kJwLanes;
     cudaLaunchConfig_t cfg = {};
@@ -1968,13 +1960,11 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
     cfg.numAttrs = 1;
     const int want = V != nullptr;
     cudaError_t e;
-    static const bool jlc_off = getenv("TTK_JW_LC") && atoi(getenv("TTK_JW_LC")) == 0;  // A/B
+    static const bool jlc_off = knob_env("TTK_JW_LC") && atoi(knob_env("TTK_JW_LC")) == 0;  // A/B
     if (!g_jc_prof_host && rpl == 10 && l == 80 && !jlc_off) {
-      static bool lcattr = false;
-      if (!lcattr) {
-        TTK_CHECK_CUDA(cudaFuncSetAttribute((const void*)jacobi_warp_kernel<10, false, 80>,
+      {  // per-device attributes (set_attr_once)
+        TTK_TRY(set_attr_once((const void*)jacobi_warp_kernel<10, false, 80>,
                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        lcattr = true;
       }
       e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, false, 80>, k, l, B, b_rs, b_cs, U, S, V, want,
                              (int)scaled_u, skip2);
@@ -2008,9 +1998,9 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   // block-ordered cluster kernel (2 CL - 1 DSMEM handoffs per sweep instead of
   // le - 1); TTK_JACOBI_BLOCK=0 keeps the plain cluster kernel, =4 / =8 picks the
   // cluster size (A/B)
-  static const int block_env = getenv("TTK_JACOBI_BLOCK") ? atoi(getenv("TTK_JACOBI_BLOCK")) : -1;
+  static const int block_env = knob_env("TTK_JACOBI_BLOCK") ? atoi(knob_env("TTK_JACOBI_BLOCK")) : -1;
   static const bool jb_diag_set = [] {
-    const int v = getenv("TTK_JB_DIAG") ? atoi(getenv("TTK_JB_DIAG")) : 0;
+    const int v = knob_env("TTK_JB_DIAG") ? atoi(knob_env("TTK_JB_DIAG")) : 0;
     if (v) cudaMemcpyToSymbol(g_jb_diag, &v, sizeof(int));
     return true;
   }();
@@ -2031,15 +2021,13 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
     const int rpl = rows <= 4 * kSvdGroup ? 4 : rows <= 6 * kSvdGroup ? 6 : 8;
     const size_t jsm = sizeof(double) * 2 * (2 * (size_t)bs * 4 * rpl * kSvdGroup);
     if (bs <= kJbMaxSlots && jsm <= 200 * 1024) {
-      static bool battr = false;
-      if (!battr) {
+      {  // per-device attributes (set_attr_once)
         TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<4, 8>, 200 * 1024));
         TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<6, 8>, 200 * 1024));
         TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<8, 8>, 200 * 1024));
         TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<4, 4>, 200 * 1024));
         TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<6, 4>, 200 * 1024));
         TTK_TRY(qr_set_smem((const void*)jacobi_block_kernel<8, 4>, 200 * 1024));
-        battr = true;
       }
       const int threads = (bs * kSvdGroup + 31) / 32 * 32;
       const int want = V != nullptr;
@@ -2056,12 +2044,10 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
     }
   }
   if (!single_cta && le <= 2 * kJcCluster * kJcMaxSlots && k <= 8 * kSvdGroup) {
-    static bool cattr = false;
-    if (!cattr) {
+    {  // per-device attributes (set_attr_once)
       TTK_TRY(qr_set_smem((const void*)jacobi_cluster_kernel<4>, 96 * 1024));
       TTK_TRY(qr_set_smem((const void*)jacobi_cluster_kernel<6>, 96 * 1024));
       TTK_TRY(qr_set_smem((const void*)jacobi_cluster_kernel<8>, 96 * 1024));
-      cattr = true;
     }
     const int spc = (le / 2 + kJcCluster - 1) / kJcCluster;
     const int rows = std::max(k, le);
@@ -2086,13 +2072,11 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
   size_t smem = sizeof(double) * ((size_t)le * (k | 1) + (V ? (size_t)le * le : 0));
   TTK_REQUIRE(smem <= 215 * 1024, kInvalidValue, "jacobi_svd: %d x %d (V=%d) exceeds shared memory", k,
               l, V != nullptr);
-  static bool attr = false;
-  if (!attr) {
+  {  // per-device attributes (set_attr_once)
     TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<4>, 215 * 1024));
     TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<6>, 215 * 1024));
     TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<8>, 215 * 1024));
     TTK_TRY(qr_set_smem((const void*)jacobi_svd_kernel<10>, 215 * 1024));
-    attr = true;
   }
   const int threads = std::min(kSvdThreads, std::max(64, ((le / 2) * kSvdGroup + 31) / 32 * 32));
   const int rows = std::max(k, le);
@@ -2795,18 +2779,16 @@ __global__ void __launch_bounds__(kCbThreads, 1)
 // for l <= 96, shared-memory kernel above
 int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status, int check_identity,
                     double shift_rel, double tiny_rel, cudaStream_t st, int* near_id_flag) {
-  static bool attr = false;
-  if (!attr) {
+  {  // per-device attributes (set_attr_once)
     TTK_TRY(qr_set_smem((const void*)chol_inv_kernel, 220 * 1024));
     TTK_TRY(qr_set_smem((const void*)chol_near_identity_kernel, 220 * 1024));
     TTK_TRY(qr_set_smem((const void*)chol_blocked_kernel, 225 * 1024));
-    attr = true;
   }
   const int* skip = nullptr;
   if (near_id_flag && shift_rel == 0.0 && l <= kNearIdMax) {
     const size_t smem_n = sizeof(double) * 2 * (size_t)l * (((l + 15) & ~15) + 4);
     // first-order shortcut when l |E|^2 <= 1e-17; TTK_NEAR_ID_FIRST_ORDER=0 disables it (A/B)
-    static const double fo = getenv("TTK_NEAR_ID_FIRST_ORDER") ? atof(getenv("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
+    static const double fo = knob_env("TTK_NEAR_ID_FIRST_ORDER") ? atof(knob_env("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
     chol_near_identity_kernel<<<1, 1024, smem_n, st>>>(l, G, R, Rinv, near_id_flag, 1e-7, fo);
     TTK_CHECK_LAUNCH();
     skip = near_id_flag;
@@ -3260,19 +3242,21 @@ size_t cholqr2_fused_smem(int l, int tr) {
 }
 
 bool cholqr2_fused_fits(int m, int l, long long q_cs) {
-  static const bool off = getenv("TTK_QR_NO_FUSED") != nullptr;  // A/B
-  return !off && l <= kFqMaxCols && m >= l && q_cs == 1 && (m + kFqRows - 1) / kFqRows <= kNumSMs - 1 &&
+  static const bool off = knob_env("TTK_QR_NO_FUSED") != nullptr;  // A/B
+  return !off && l <= kFqMaxCols && m >= l && q_cs == 1 && (m + kFqRows - 1) / kFqRows <= num_sms() - 1 &&
          cholqr2_fused_smem(l, kFqRows) <= 220 * 1024;
 }
 
+// Precondition: R's strict lower triangle is exactly zero and finite -- the
+// blocked off-diagonal update multiplies whole 16 x 16 blocks of R without
+// masking.  Every producer (chol_blocked_body, pchol, the near-identity series)
+// stores zeros there.
 int trsm_right_upper(int m, int l, const double* Y, long long y_rs, long long y_cs, const double* R, double* Q,
                      long long q_rs, long long q_cs, cudaStream_t st) {
   if (m <= 0 || l <= 0) return kOk;
   TTK_REQUIRE(l <= 128, kInvalidValue, "trsm: %d columns exceed 128", l);
-  static bool attr = false;
-  if (!attr) {
+  {  // per-device attributes (set_attr_once)
     TTK_TRY(qr_set_smem((const void*)trsm_blocked_kernel, 220 * 1024));
-    attr = true;
   }
   const int ld = ((l + 15) & ~15) + 4;
   const size_t smem = sizeof(double) * ((size_t)l * ld + (size_t)kTbRows * ld + l);
@@ -3371,17 +3355,15 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     return kOk;
   };
   int hs[4] = {0, 0, 0, 0};
-  static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;
+  static const int qr_mode = knob_env("TTK_QR_MODE") ? atoi(knob_env("TTK_QR_MODE")) : 0;
   bool fast_tried = false;
   if ((!robust_first || qr_mode == 2) && cholqr2_fused_fits(m, l, q_cs)) {
     // ---- fast path, fused into one cooperative kernel ----
-    static bool fattr = false;
-    if (!fattr) {
+    {  // per-device attributes (set_attr_once)
       TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel<0>, 220 * 1024));
       TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel<80>, 220 * 1024));
-      fattr = true;
     }
-    static const double fo = getenv("TTK_NEAR_ID_FIRST_ORDER") ? atof(getenv("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
+    static const double fo = knob_env("TTK_NEAR_ID_FIRST_ORDER") ? atof(knob_env("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
     TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 8 * sizeof(int), st));
     FqParams fp{};
     fp.m = m; fp.l = l; fp.Y = Y; fp.y_rs = y_rs; fp.y_cs = y_cs; fp.Q = Q; fp.q_rs = q_rs; fp.R = R;
@@ -3390,13 +3372,13 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     // tile rows: spread the tall dimension over up to kFqTiles CTAs (the tile
     // phases are per-SM DMMA work: 10240 x 80 in 80-row tiles instead of 128);
     // TTK_FQ_ROWS pins it (A/B)
-    static const int fq_rows = getenv("TTK_FQ_ROWS") ? atoi(getenv("TTK_FQ_ROWS")) : 0;
+    static const int fq_rows = knob_env("TTK_FQ_ROWS") ? atoi(knob_env("TTK_FQ_ROWS")) : 0;
     int trows = fq_rows > 0 ? fq_rows : (int)(((m + kFqTiles - 1) / kFqTiles + 7) & ~7);
     trows = std::max(8, std::min(kFqRows, (trows + 7) & ~7));
     fp.tr = trows;
     const int grid = 1 + (m + trows - 1) / trows;
     void* args[] = {&fp};
-    static const bool lc_off = getenv("TTK_FQ_LC") && atoi(getenv("TTK_FQ_LC")) == 0;  // A/B
+    static const bool lc_off = knob_env("TTK_FQ_LC") && atoi(knob_env("TTK_FQ_LC")) == 0;  // A/B
     const void* fq_fn = (l == 80 && !lc_off) ? (const void*)cholqr2_fused_kernel<80> : (const void*)cholqr2_fused_kernel<0>;
     const cudaError_t le = cudaLaunchCooperativeKernel(fq_fn, dim3(grid),
                                                        dim3(kFqThreads), args, cholqr2_fused_smem(l, trows), st);
@@ -3421,7 +3403,7 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     TTK_TRY(gram_chol(Y, y_rs, y_cs, R1, I1, status, 0, 0.0, 1e-15));
     TTK_TRY(trsm_right_upper(m, l, Y, y_rs, y_cs, R1, Q1, l, 1, st));  // Q1 = Y / R1 (backward stable)
     TTK_TRY(gram_chol(Q1, l, 1, R2, I2, status + 1, 1, 0.0, 1e-28));
-    static const bool assume_fast = getenv("TTK_QR_ASSUME_FAST") != nullptr;  // diagnostics: cost of this sync
+    static const bool assume_fast = knob_env("TTK_QR_ASSUME_FAST") != nullptr;  // diagnostics: cost of this sync
     if (!assume_fast) {
       TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
       TTK_SYNC(st);
@@ -3447,10 +3429,8 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
   // 2. pivoted Cholesky of Q1^T Q1: directions with eigenvalue < 1e-14 are left to the completion
   TTK_TRY(gram(Q1, l, 1));
   {
-    static bool pattr = false;
-    if (!pattr) {
+    {  // per-device attributes (set_attr_once)
       TTK_TRY(qr_set_smem((const void*)pchol_kernel, 220 * 1024));
-      pattr = true;
     }
     pchol_kernel<<<1, 1024, smem, st>>>(l, G, 1e-14, R2, status + 8, status + 3);
     TTK_CHECK_LAUNCH();
@@ -3518,7 +3498,7 @@ size_t qr_auto_ws_bytes(int m, int l) {
 }
 
 // diagnostics (TTK_QR_CHECK=1): host-side check of every CholeskyQR factorisation
-static const bool g_qr_check = getenv("TTK_QR_CHECK") != nullptr;
+static const bool g_qr_check = knob_env("TTK_QR_CHECK") != nullptr;
 #define g_qr_last_path g_qr_path_tmp  // 1 fast, 2 + 100 rho robust
 static void qr_check_report(int m, int l, const std::vector<double>& hy, const double* Q, long long q_rs,
                             long long q_cs, const double* R, cudaStream_t st) {
@@ -3556,7 +3536,7 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
     return qr_blocked(m, l, A, a_rs, a_cs, Q, q_rs, q_cs, R, ws, ws_bytes, st);
   }
   // CholeskyQR2 pays off only for tall inputs that need a multi-panel tree
-  static const int qr_mode = getenv("TTK_QR_MODE") ? atoi(getenv("TTK_QR_MODE")) : 0;  // 1: Householder only
+  static const int qr_mode = knob_env("TTK_QR_MODE") ? atoi(knob_env("TTK_QR_MODE")) : 0;  // 1: Householder only
   // (r01: Householder 128 x 80 400 us vs 246, 256 x 40 235 vs 100, 512 x 100 1986 vs
   // 140; only the smallest panels, e.g. 32 x 20 43 vs 76 us, stay on Householder)
   if (qr_mode != 1 && l <= kCholMaxCols && ((m >= 4 * l && m > 512) || (m >= l && l >= 32))) {

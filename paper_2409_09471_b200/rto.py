@@ -15,7 +15,7 @@ oracle/ttoracle.py (rto_sweeps / rto_round) as the checker:
 from __future__ import annotations
 
 import math
-import os
+import threading
 
 import torch
 
@@ -182,13 +182,20 @@ def tt_round_rto(v: TTVector, spec: RoundSpec, ell=None, drm=None, seed=0) -> TT
 
 
 _PIPE_STREAMS = {}
+_PIPE_LOCK = threading.Lock()
 
 
 def _pipe_streams(dev):
-    key = dev.index
-    if key not in _PIPE_STREAMS:
-        _PIPE_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-    return _PIPE_STREAMS[key]
+    """(upload, matvec) side streams of the caller's current stream: independent
+    callers on their own streams (bench.py inflight, concurrent solves) get
+    their own pair, so their pipelines do not serialise on shared streams."""
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    with _PIPE_LOCK:
+        pair = _PIPE_STREAMS.get(key)
+        if pair is None:
+            pair = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+            _PIPE_STREAMS[key] = pair
+    return pair
 
 
 def _drm_block(v_dims, v_ranks, drm, dev):
@@ -260,7 +267,7 @@ def tt_matvec_round_rto(a, v: TTVector, spec: RoundSpec, drm, chunk: int | None 
     D_p, C_p, Y_p = _lib.ptr_array(ops), _lib.ptr_array(xs), _lib.ptr_array(y)
     ev_mv = [None] * d
     if chunk is None:
-        chunk = int(os.environ.get("TTK_PIPE_CHUNK", "4")) if host else d
+        chunk = 4 if host else d
     chunk = max(1, int(chunk))
     for k1 in range(d, 0, -chunk):
         k0 = max(0, k1 - chunk)

@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -89,12 +91,26 @@ def kr_apply(s: KhatriRaoSketch, v: TTVector) -> np.ndarray:
     return kr_apply_device(s, v).cpu().numpy()
 
 
+_FT_LOCK = threading.Lock()
+
+
 def _premultiplied_factors(s: KhatriRaoSketch, a: TTOperator):
     """Ft_k[j, al, i', be] = sum_i F_k[j, i] D_k[al, i, i', be] for every core (one
-    batched DMMA GEMM per core); cached on the sketch for the last operator used."""
-    hit = getattr(s, "_ft_cache", None)
-    if hit is not None and hit[0] is a:
-        return hit[1]
+    batched DMMA GEMM per core); cached on the sketch for the last operator used,
+    keyed by the operator cores' storage and version counters (an in-place edit
+    of a core invalidates it) and built under a lock (concurrent solvers)."""
+    key = tuple((c.data_ptr(), c._version, tuple(c.shape)) for c in a.op_cores) + \
+        tuple((f.data_ptr(), f._version) for f in s.factors)
+    with _FT_LOCK:
+        hit = getattr(s, "_ft_cache", None)
+        if hit is not None and hit[0] == key:
+            return hit[1]
+        fts = _build_premultiplied(s, a)
+        s._ft_cache = (key, fts)
+        return fts
+
+
+def _build_premultiplied(s: KhatriRaoSketch, a: TTOperator):
     lib = _lib.load()
     dev = s.factors[0].device
     fts = []
@@ -107,7 +123,6 @@ def _premultiplied_factors(s: KhatriRaoSketch, a: TTOperator):
                                         m * n * p1, 0.0, ft.data_ptr(), p0 * n * p1, 1, n * p1,
                                         ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)))
         fts.append(ft)
-    s._ft_cache = (a, fts)
     return fts
 
 
