@@ -41,6 +41,29 @@ int num_sms() {
   return g_sms[dev];
 }
 
+int scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static bool pool_set[64] = {false};
+  int dev = 0;
+  TTK_CHECK_CUDA(cudaGetDevice(&dev));
+  if (dev >= 0 && dev < 64 && !pool_set[dev]) {
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    if (!pool_set[dev]) {
+      cudaMemPool_t pool;
+      TTK_CHECK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      unsigned long long thr = ~0ULL;
+      TTK_CHECK_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      pool_set[dev] = true;
+    }
+  }
+  TTK_CHECK_CUDA(cudaMallocAsync(p, bytes, st));
+  return kOk;
+}
+
+int scratch_free(void* p, cudaStream_t st) {
+  TTK_CHECK_CUDA(cudaFreeAsync(p, st));
+  return kOk;
+}
+
 int set_attr_once(const void* fn, cudaFuncAttribute attr, int value) {
   int dev = 0;
   TTK_CHECK_CUDA(cudaGetDevice(&dev));

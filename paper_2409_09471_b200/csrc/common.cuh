@@ -70,6 +70,12 @@ constexpr int kNumSMs = 148;
 // SM count of the current device (queried once per device)
 int num_sms();
 
+// Stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on the device's
+// default memory pool, whose release threshold is raised once per device so
+// freed blocks stay cached instead of going back to the driver at every sync)
+int scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+int scratch_free(void* p, cudaStream_t st);
+
 // Kernel attributes are per device: set (fn, attr) = value once per device.
 int set_attr_once(const void* fn, cudaFuncAttribute attr, int value);
 template <class F>

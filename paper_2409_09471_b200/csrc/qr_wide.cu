@@ -305,7 +305,7 @@ int jacobi_svd_global(int k, int l, const double* B, long long b_rs, long long b
   const size_t wb = V ? align_up((size_t)le * le * 8, 256) : 0;
   const size_t bytes = xb + wb + align_up((size_t)le * 8, 256) + align_up((size_t)le * 4, 256) + 256;
   char* buf = nullptr;
-  TTK_CHECK_CUDA(cudaMallocAsync((void**)&buf, bytes, st));
+  TTK_TRY(scratch_alloc((void**)&buf, bytes, st));
   JgParams p{};
   p.k = k; p.l = l; p.le = le; p.B = B; p.b_rs = b_rs; p.b_cs = b_cs;
   p.X = (double*)buf;
@@ -325,7 +325,7 @@ int jacobi_svd_global(int k, int l, const double* B, long long b_rs, long long b
   TTK_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_global_kernel, dim3(grid), dim3(kJgThreads), args,
                                              0, st));
   TTK_CHECK_LAUNCH();
-  TTK_CHECK_CUDA(cudaFreeAsync(buf, st));
+  TTK_TRY(scratch_free(buf, st));
   return kOk;
 }
 
