@@ -44,18 +44,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every csrc/*.cu into one shared library; returns its path."""
+def build(force: bool = False, verbose: bool = False, debug_knobs: bool = False, out: str | None = None) -> str:
+    """Compile every csrc/*.cu into one shared library; returns its path.
+    debug_knobs=True (experiments only) compiles the TTK_* environment knobs in
+    and writes the library to `out` (never the shipped path)."""
+    if debug_knobs:
+        if not out or os.path.abspath(out) == LIB_PATH:
+            raise ValueError("a debug-knob build needs its own output path")
+        return _compile(out, ["-DTTK_DEBUG_KNOBS"], os.path.join(PKG_DIR, "build_dbg"), verbose)
     if not force and not _stale():
         return LIB_PATH
+    return _compile(LIB_PATH, [], os.path.join(PKG_DIR, "build"), verbose)
+
+
+def _compile(lib_path, extra, tmp_dir, verbose):
     objs = []
     nvcc = _nvcc()
-    tmp_dir = os.path.join(PKG_DIR, "build")
     os.makedirs(tmp_dir, exist_ok=True)
     procs = []
     for src in sources():
         obj = os.path.join(tmp_dir, os.path.basename(src) + ".o")
-        cmd = [nvcc, *[f for f in NVCC_FLAGS if f != "-shared"], "-c", "-I", INCLUDE, "-o", obj, src]
+        cmd = [nvcc, *[f for f in NVCC_FLAGS if f != "-shared"], *extra, "-c", "-I", INCLUDE, "-o", obj, src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -70,12 +79,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp_lib = LIB_PATH + ".tmp"
+    tmp_lib = lib_path + ".tmp"
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
            "-o", tmp_lib, *objs]
     subprocess.run(cmd, check=True, capture_output=not verbose)
-    os.replace(tmp_lib, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp_lib, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
