@@ -1,6 +1,7 @@
+"""Jacobi with the rotation angle computed in fp32 and (c, s) renormalised in fp64: sweep counts and accuracy (numpy model)."""
 import numpy as np, sys
 sys.path.insert(0,'/tmp/jx')
-Bs = np.load('/tmp/jx/Bs.npy')
+Bs = np.load('/tmp/cfg3_Bs.npy')  # written by tools/jacobi_sweeps.py
 
 def jac(B, f32angle, skip=1e-8, maxsw=40):
     A = B.copy(); l = A.shape[1]; le = l; n1 = le - 1
