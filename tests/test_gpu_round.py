@@ -427,3 +427,48 @@ def test_tt_round_rank200_vs_oracle(cuda):
         want = O.tt_round(x, tol, cap, zero_rel=None)
         assert list(got.ranks) == [1] + [c.shape[2] for c in want]
         assert O.rel_diff(tt_np(got), want) <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# race detection by determinism (compute-sanitizer is closed on the GPU pool,
+# profiles/r02_sanitizer_refused.log): the kernels with cross-CTA hand-offs --
+# DSMEM st.async + mbarrier block moves (Jacobi cluster kernels), cooperative
+# grid barriers (fused CholeskyQR2) -- must give bit-identical results on every
+# run and when several run concurrently on separate streams; a missing
+# barrier / stale DSMEM read would show up as run-to-run differences.
+
+@pytest.mark.parametrize("l", [80, 50, 112])
+def test_jacobi_cluster_kernels_deterministic(cuda, l):
+    lib = _lib.load()
+    rng = np.random.default_rng(l)
+    B = torch.as_tensor(np.ascontiguousarray(np.linalg.qr(rng.standard_normal((10 * l, l)))[1].T), device=cuda)
+    outs = []
+    streams = [torch.cuda.Stream(cuda) for _ in range(4)]
+    for it in range(24):
+        st = streams[it % 4]
+        U = torch.empty((l, l), dtype=torch.float64, device=cuda)
+        S = torch.empty(l, dtype=torch.float64, device=cuda)
+        V = torch.empty((l, l), dtype=torch.float64, device=cuda)
+        with torch.cuda.stream(st):
+            _lib.check(lib.ttk_svd_small(l, l, B.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(), st.cuda_stream))
+        outs.append((U, S, V))
+    torch.cuda.synchronize()
+    for U, S, V in outs[1:]:
+        assert torch.equal(U, outs[0][0]) and torch.equal(S, outs[0][1]) and torch.equal(V, outs[0][2])
+
+
+def test_fused_cholqr2_deterministic(cuda):
+    lib = _lib.load()
+    m, l = 10240, 80
+    A = torch.as_tensor(np.random.default_rng(0).standard_normal((m, l)), device=cuda)
+    res = []
+    for it in range(16):
+        Q = torch.empty_like(A)
+        R = torch.empty((l, l), dtype=torch.float64, device=cuda)
+        ws = _lib.workspace(lib.ttk_qr_ws_bytes(m, l), cuda)
+        _lib.check(lib.ttk_qr_auto(m, l, A.data_ptr(), l, 1, Q.data_ptr(), l, 1, R.data_ptr(), ws.data_ptr(),
+                                   ws.numel(), _lib.stream_ptr(cuda)))
+        res.append((Q, R))
+    torch.cuda.synchronize()
+    for Q, R in res[1:]:
+        assert torch.equal(Q, res[0][0]) and torch.equal(R, res[0][1])
