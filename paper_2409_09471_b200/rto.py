@@ -229,6 +229,14 @@ def tt_matvec_round_rto(a, v: TTVector, spec: RoundSpec, drm, chunk: int | None 
     * with host inputs the result comes back in pinned host memory, each core
       copied as soon as the truncation finalises it (ttk_tt_truncate_host).
     Same arithmetic and result as the three calls in sequence."""
+    torch.cuda.nvtx.range_push("ttk/matvec_round_rto")
+    try:
+        return _matvec_round_rto(a, v, spec, drm, chunk, device)
+    finally:
+        torch.cuda.nvtx.range_pop()
+
+
+def _matvec_round_rto(a, v, spec, drm, chunk, device):
     if a.col_dims != v.dims:
         raise ShapeMismatch(f"operator col_dims {a.col_dims} do not match {v.dims}")
     host = v.device.type == "cpu"

@@ -108,19 +108,28 @@ class SolveReport:
 
 
 class _PhaseTimer:
-    """CUDA-event phase timer: events are recorded on the stream without host
-    syncs and resolved once at the end of the solve."""
+    """CUDA-event phase timer (the reference's _PhaseTimer, solvers.py:105-116,
+    with the same phase names): events are recorded on the stream without host
+    syncs and resolved once at the end of the solve; every phase is also an
+    NVTX range ("ttk/<phase>") for Nsight timelines."""
 
     def __init__(self, report, device):
         self.report = report
         self.device = device
         self.rows = []
         self.cur = []
+        self.open = False
 
     def mark(self, phase):
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(torch.cuda.current_stream(self.device))
         self.cur.append((phase, ev))
+        if self.open:
+            torch.cuda.nvtx.range_pop()
+            self.open = False
+        if phase is not None:
+            torch.cuda.nvtx.range_push("ttk/" + phase)
+            self.open = True
 
     def flush(self):
         self.rows.append(self.cur)
