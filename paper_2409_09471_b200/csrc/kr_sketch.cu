@@ -16,6 +16,8 @@
 //    at once with the grouped GEMM (all FLOPs, fully parallel); phase 2 walks
 //    the per-row state through the d small matrices (rows are independent).
 // Output rows stay in their fixed positions (SPEC: deterministic row order).
+#include <cooperative_groups.h>
+
 #include "gemm.cuh"
 #include "../../include/ttk_b200.h"
 
@@ -66,8 +68,8 @@ constexpr size_t smem_bytes(int nmax) {
 // (compile-time: no branches around the warp-synchronous DMMAs).
 template <int FNW>
 __device__ __forceinline__ void kr_mode(double* St, const double* Ft, double* Bs, const double* Ck, int r1,
-                                        int n, int nic, int nst, int wrow, int wcol, const int (&ckk)[kr::CPT],
-                                        const int (&ccol)[kr::CPT]) {
+                                        int n, int nic, int s_lo, int s_hi, int wrow, int wcol,
+                                        const int (&ckk)[kr::CPT], const int (&ccol)[kr::CPT], double* Dst) {
   using namespace kr;
   const int tid = threadIdx.x, lane = tid & 31;
   const int fr = lane >> 2, fk = lane & 3;
@@ -81,9 +83,11 @@ __device__ __forceinline__ void kr_mode(double* St, const double* Ft, double* Bs
       cp_async8(Bs + (size_t)buf * BK * SB + ckk[q] * SB + pair_pos<true>(ccol[q]), src, ok);
     }
   };
+  const int nst = s_hi - s_lo;  // this CTA's stages (a cluster splits the K range)
+  auto load_c_rel = [&](int s, int buf) { load_c(s_lo + s, buf); };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nst) load_c(s, s);
+    if (s < nst) load_c_rel(s, s);
     cp_async_commit();
   }
   double acc[2][FNW > 0 ? FNW : 1][2];
@@ -98,10 +102,11 @@ __device__ __forceinline__ void kr_mode(double* St, const double* Ft, double* Bs
     __syncthreads();
     {
       const int nxt = s + STAGES - 1;
-      if (nxt < nst) load_c(nxt, nxt % STAGES);
+      if (nxt < nst) load_c_rel(nxt, nxt % STAGES);
       cp_async_commit();
     }
-    const int a = s / nic, ic = s - a * nic;
+    const int sg = s_lo + s;
+    const int a = sg / nic, ic = sg - a * nic;
     if (a != a_cur) {  // state values of this lane's two rows for the new a
       a_cur = a;
       sa0 = St[(wrow + fr) * SST + a];
@@ -130,15 +135,15 @@ __device__ __forceinline__ void kr_mode(double* St, const double* Ft, double* Bs
     }
   }
   cp_async_wait<0>();
-  __syncthreads();  // every warp is done reading the old state
+  __syncthreads();  // every warp is done reading the old state (and the stage buffers)
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int row = wrow + i * 8 + fr;
 #pragma unroll
     for (int j = 0; j < FNW; ++j) {
       const int col = wcol + j * 8 + 2 * fk;
-      if (col < r1) St[row * SST + col] = acc[i][j][0];
-      if (col + 1 < r1) St[row * SST + col + 1] = acc[i][j][1];
+      if (col < r1) Dst[row * SST + col] = acc[i][j][0];
+      if (col + 1 < r1) Dst[row * SST + col + 1] = acc[i][j][1];
     }
   }
 }
@@ -154,8 +159,15 @@ __global__ void __launch_bounds__(kr::WARPS * 32, 1)
   double* Ft = St + BM * SST;                          // nft x SFT
   double* Bs = Ft + (size_t)nft * SFT;                 // STAGES x BK x SB
 
+  // a cluster of CL CTAs shares one (vector, 64-row) item: each contracts a
+  // contiguous slice of the mode's K stages into a partial state, the partials
+  // are summed over DSMEM in a fixed order (every CTA then holds the full state)
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), crank = (int)cl.block_rank();
+  double* Pbuf = Bs;  // partial state (BM x SST) in the stage buffers once the K loop is done
   const int vec = blockIdx.y;
-  const int j0 = blockIdx.x * BM;
+  const int j0 = (blockIdx.x / CL) * BM;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int wrow = (warp >> 1) * 16;     // 16 rows = fragment pair (rows r, r + 8)
 
@@ -197,23 +209,38 @@ __global__ void __launch_bounds__(kr::WARPS * 32, 1)
       const int i = n + e / BM, row = e % BM;
       Ft[i * SFT + row] = 0.0;
     }
+    const int s_lo = (int)((long long)nst * crank / CL), s_hi = (int)((long long)nst * (crank + 1) / CL);
+    double* Dst = CL > 1 ? Pbuf : St;
+#define KR_MODE(F) kr_mode<F>(St, Ft, Bs, Ck, r1, n, nic, s_lo, s_hi, wrow, wcol, ckk, ccol, Dst)
     switch (fnh) {  // warp-uniform
-      case 0: kr_mode<0>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 1: kr_mode<1>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 2: kr_mode<2>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 3: kr_mode<3>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 4: kr_mode<4>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 5: kr_mode<5>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 6: kr_mode<6>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 7: kr_mode<7>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 8: kr_mode<8>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      case 9: kr_mode<9>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
-      default: kr_mode<10>(St, Ft, Bs, Ck, r1, n, nic, nst, wrow, wcol, ckk, ccol); break;
+      case 0: KR_MODE(0); break;
+      case 1: KR_MODE(1); break;
+      case 2: KR_MODE(2); break;
+      case 3: KR_MODE(3); break;
+      case 4: KR_MODE(4); break;
+      case 5: KR_MODE(5); break;
+      case 6: KR_MODE(6); break;
+      case 7: KR_MODE(7); break;
+      case 8: KR_MODE(8); break;
+      case 9: KR_MODE(9); break;
+      default: KR_MODE(10); break;
+    }
+#undef KR_MODE
+    if (CL > 1) {
+      cl.sync();  // every CTA's partial written
+      for (int e = tid; e < BM * r1; e += WARPS * 32) {
+        const int row = e / r1, col = e - row * r1;
+        double v = 0.0;
+        for (int q = 0; q < CL; ++q) v += *cl.map_shared_rank(Pbuf + row * SST + col, q);
+        St[row * SST + col] = v;
+      }
+      cl.sync();  // partials read everywhere before the next mode reuses the stage buffers
     }
   }
   __syncthreads();
-  for (int row = tid; row < BM; row += WARPS * 32)
-    if (j0 + row < P.S) P.out[(long long)vec * P.S + j0 + row] = St[row * SST];
+  if (crank == 0)
+    for (int row = tid; row < BM; row += WARPS * 32)
+      if (j0 + row < P.S) P.out[(long long)vec * P.S + j0 + row] = St[row * SST];
 }
 
 // phase 2 of the two-phase path: per (vector, row) walk the state through
@@ -276,10 +303,32 @@ int kr_fused(int d, const int* n, int S, const double* const* F, int nvec, const
       for (int k = 0; k < d; ++k) P.core[v * d + k] = cores[(long long)(v0 + v) * d + k];
       for (int k = 0; k <= d; ++k) P.rank[v * (d + 1) + k] = (short)ranks[(long long)(v0 + v) * (d + 1) + k];
     }
-    dim3 grid(ceil_div(S, kr::BM), nv);
+    // cluster split of the K stages: at least 2 CTAs per (vector, row-block)
+    // item (config 4, 512 items: 3.46 -> 6.9 waves, 19.1 -> 20.7 TF/s), more
+    // when the items alone would leave SMs idle (a row shard of the
+    // 1/2/4/8-GPU partition: 64 rows x 64 vectors 10.2 -> 5.5 ms, 0.90 of the
+    // full-row per-row rate; CL 4 / 8 measured 5.7 / 8.1 ms, tools/kr_rows.py):
+    // the smallest CL in {2, 4, 8} with items * CL >= 0.8 SMs
+    const int items = ceil_div(S, kr::BM) * nv;
+    int CL = 2;
+    while (CL < 8 && (long)items * CL * 5 < 4L * num_sms()) CL *= 2;
+    static const int cl_knob = knob_env("TTK_KR_CL") ? atoi(knob_env("TTK_KR_CL")) : 0;  // A/B
+    if (cl_knob > 0) CL = cl_knob;
     int nmax = 0;
     for (int k = 0; k < d; ++k) nmax = std::max(nmax, n[k]);
-    kr_fused_kernel<<<grid, kr::WARPS * 32, kr::smem_bytes(nmax), st>>>(P);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ceil_div(S, kr::BM) * CL, nv, 1);
+    cfg.blockDim = dim3(kr::WARPS * 32, 1, 1);
+    cfg.dynamicSmemBytes = kr::smem_bytes(nmax);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    TTK_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kr_fused_kernel, P));
     TTK_CHECK_LAUNCH();
   }
   return kOk;
@@ -353,9 +402,10 @@ bool use_fused(int d, const int* n, int S, int nvec, const int* ranks) {
   for (int v = 0; v < nvec; ++v)
     for (int k = 0; k <= d; ++k)
       if (ranks[v * (d + 1) + k] > kr::BN) return false;
-  // the fused path needs enough (vector, row-block) CTAs to fill the machine
-  long ctas = (long)nvec * ceil_div(S, kr::BM);
-  return ctas >= kNumSMs / 2;
+  // the fused path needs enough CTAs to fill the machine: (vector, row-block)
+  // items, each split over a cluster of up to 8 CTAs
+  long ctas = (long)nvec * ceil_div(S, kr::BM) * 8;
+  return ctas >= num_sms();
 }
 
 }  // namespace
