@@ -161,19 +161,6 @@ int ttk_qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, d
 /* one-sided Jacobi SVD of B (k x l, row-major, k,l <= 128): B V = U S with
  * S[min(k,l)] descending, U (k x min(k,l)), V (l x min(k,l)) if V != NULL. */
 int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream);
-/* truncation eigensolver (replaces np.linalg.svd of the core unfolding at
- * tt.py:361 / the truncation step of tt.py:358-367 through the Gram G = C C^T,
- * n x n on the device, 6 <= n <= 128): two-sided cyclic Jacobi, then the
- * reference truncation rank (tt.py:203-211) with `budget` (absolute, on
- * singular values) and max_rank (<= 0: none).  S = sqrt(eigenvalues)
- * descending, T1 = U_r S_r^-1 and L = U_r S_r (n x r, ld ldo), U (n x n sorted
- * eigenvectors) if not NULL, info (device ints) = [r, certified, sweeps,
- * converged]; "certified" means the rank decision and the kept directions are
- * exact to the Gram's rounding error (callers use the SVD path otherwise). */
-int ttk_gram_eig(int n, const double* G, int ldg, double budget, int max_rank, double* S, double* T1,
-                 double* L, int ldo, double* U, int* info, void* stream);
-/* diagnostics: hand-off bisection mode of ttk_gram_eig (0 = normal) */
-int ttk_debug_gram_eig(int mode, int* host_trace);
 /* diagnostics: subsequent Jacobi SVDs store their sweep count in *dev_counter (NULL: off) */
 int ttk_debug_svd_sweeps(int* dev_counter);
 /* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,

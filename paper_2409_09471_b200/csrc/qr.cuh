@@ -65,13 +65,6 @@ int jacobi_svd_global(int k, int l, const double* B, long long b_rs, long long b
 int copy_strided(int m, int l, const double* X, long long x_rs, long long x_cs, double* Y, long long y_rs,
                  long long y_cs, cudaStream_t st);
 
-// Gram eigensolver for the truncation (eig_gram.cu): G (n x n, 6 <= n <= 128)
-// -> S, T1 = U_r S_r^-1, L = U_r S_r (ld ldo), optional sorted U, info = [r,
-// certified, sweeps, converged] on the device.
-bool gram_eig_supported(int n);
-int gram_eig(int n, const double* G, int ldg, double budget, int cap, double* S, double* T1, double* L, int ldo,
-             double* U, int* info, cudaStream_t st);
-
 // r = max(1, first index with sqrt(sum_{i>=r} S_i^2) <= budget) capped by
 // max_rank (<= 0: no cap) and by n; reference _truncation_rank (tt.py:203-211).
 int truncation_rank_dev(const double* S, int n, double budget, int max_rank, int* r_dev,
