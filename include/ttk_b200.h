@@ -249,7 +249,11 @@ size_t ttk_stream_recover_ws_bytes(int d, const int* dims, const int* lr, const 
 /* ---- truncation of a LEFT-orthogonal TT (the RTO output), right to left ------
  * TT-SVD without an orthogonalisation sweep; same budget rule
  * rel_tol*||v||/sqrt(d-1) and cap as tt_round (tt.py:357-364); output layout as
- * ttk_tt_round.  Oracle: oracle/ttoracle.py truncate_left_orth.  Synchronises. */
+ * ttk_tt_round.  Oracle: oracle/ttoracle.py truncate_left_orth.  Synchronises.
+ * Exact-rank roundings (rel_tol == 0) factor each unfolding through its Gram
+ * matrix (Cholesky, then the Jacobi SVD of R) when the kept singular values
+ * are >= sqrt(1e-3) of the largest; otherwise (and for rel_tol > 0) through
+ * the QR of C_k^T, as np.linalg.svd at tt.py:361. */
 int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
                     int max_rank, double* const* out, int* out_ranks, void* ws, size_t ws_bytes,
                     void* stream);
@@ -260,6 +264,8 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
 int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
                          int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
                          size_t ws_bytes, void* stream);
+/* diagnostics: cores truncated so far through the Gram path [0] and the QR path [1] */
+int ttk_debug_truncate_paths(long long* counts);
 size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks);
 
 #ifdef __cplusplus

@@ -65,6 +65,12 @@ int jacobi_svd_global(int k, int l, const double* B, long long b_rs, long long b
 int copy_strided(int m, int l, const double* X, long long x_rs, long long x_cs, double* Y, long long y_rs,
                  long long y_cs, cudaStream_t st);
 
+// Cholesky factor R (upper, l x l row-major) of G (+ shift_rel * trace), optional
+// R^{-1}; status bit set on a non-positive or tiny pivot (qr.cu)
+int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status, int check_identity,
+                    double shift_rel, double tiny_rel, cudaStream_t st, int* near_id_flag);
+constexpr int kCholBlockedMaxCols = 112;
+
 // r = max(1, first index with sqrt(sum_{i>=r} S_i^2) <= budget) capped by
 // max_rank (<= 0: no cap) and by n; reference _truncation_rank (tt.py:203-211).
 int truncation_rank_dev(const double* S, int n, double budget, int max_rank, int* r_dev,

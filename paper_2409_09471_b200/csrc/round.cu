@@ -11,6 +11,7 @@
 #include "../../include/ttk_b200.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -44,6 +45,16 @@ __global__ void sumsq_multi_kernel(const double* const* ptrs, const long long* s
   }
 }
 
+// T1[i][c] = L[i][c] / S[c]^2 (c < r): the right-factor map of the Gram truncation
+__global__ void scale_cols_inv_sq_kernel(int rows, int r, const double* __restrict__ L, int ld,
+                                         const double* __restrict__ S, double* __restrict__ T1) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * r; e += gridDim.x * blockDim.x) {
+    const int i = e / r, c = e - i * r;
+    const double s = S[c];
+    T1[i * ld + c] = L[i * ld + c] / (s * s);
+  }
+}
+
 struct PinnedScratch {
   void* p = nullptr;
   size_t cap = 0;
@@ -57,6 +68,9 @@ struct PinnedScratch {
   }
 };
 thread_local PinnedScratch g_pinned;
+
+// cores truncated by the Gram path / by the QR path (ttk_debug_truncate_paths)
+std::atomic<long long> g_trunc_gram{0}, g_trunc_qr{0};
 
 size_t core_elems(const int* dims, const int* ranks, int k) {
   return (size_t)ranks[k] * dims[k] * ranks[k + 1];
@@ -262,7 +276,7 @@ size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks) {
     rmax = std::max(rmax, std::max(ranks[k], ranks[k + 1]));
     if (k > 0) qrws = std::max(qrws, qr_auto_ws_bytes(dims[k] * ranks[k + 1], ranks[k]));
   }
-  return sum + 4 * align_up(mx * 8, 256) + 6 * align_up((size_t)rmax * rmax * 8, 256) +
+  return sum + 4 * align_up(mx * 8, 256) + 7 * align_up((size_t)rmax * rmax * 8, 256) +
          align_up(qrws, 256) + 2 * kSplitKBytes + 131072;
 }
 
@@ -298,6 +312,7 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
   double* tUb[2] = {ar.take<double>((size_t)rmax * rmax), ar.take<double>((size_t)rmax * rmax)};
   double* tS = ar.take<double>((size_t)rmax + 8);
   double* tL = ar.take<double>((size_t)rmax * rmax);
+  double* tG = ar.take<double>((size_t)rmax * rmax);
   double* red = ar.take<double>(16);
   double* part = ar.take<double>(256);
   int* rdev = ar.take<int>(8);
@@ -308,16 +323,22 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
   void* split_side = ar.take<char>(kSplitKBytes);
   TTK_REQUIRE(split_side != nullptr, kWorkspace, "tt_truncate: workspace too small");
   static thread_local cudaStream_t side = nullptr;
-  static thread_local cudaEvent_t ev_f[2] = {nullptr, nullptr}, ev_g[2] = {nullptr, nullptr};
+  static thread_local cudaEvent_t ev_f[2] = {nullptr, nullptr}, ev_g[2] = {nullptr, nullptr},
+                                  ev_r[2] = {nullptr, nullptr};
   if (side == nullptr) {
     TTK_CHECK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
       TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_f[i], cudaEventDisableTiming));
       TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_g[i], cudaEventDisableTiming));
+      TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_r[i], cudaEventDisableTiming));
     }
   }
   bool g_pending[2] = {false, false};
-  double* pin = (double*)g_pinned.get(64);
+  // Gram path: the side-stream product of core k reads C_k (alt[(k+1) & 1]),
+  // which the main stream overwrites at core k - 2 (its C_{k-3}) -- ev_r marks
+  // the end of that read (before the host copy, which must not gate the chain)
+  bool r_pending[2] = {false, false};
+  double* pin = (double*)g_pinned.get(sizeof(double) * ((size_t)rmax + 16));
   TTK_REQUIRE(pin != nullptr, kCudaError, "tt_truncate: cannot allocate pinned scratch");
   std::vector<int> r(ranks, ranks + d + 1);
   // ||v|| = ||C_{d-1}||_F for a left-orthogonal TT
@@ -336,6 +357,15 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
   const double budget = rel_tol * nrm / std::sqrt((double)(d - 1));
   const double* cur = cores[d - 1];
   int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
+  // Gram path (exact-rank roundings, rel_tol == 0): R from the Cholesky factor of
+  // G = C_k C_k^T instead of the QR of C_k^T (no Q: the new core is
+  // S_r^{-2} W_r^T C_k with W = R^T V), certified per core -- the Cholesky must
+  // succeed and the kept singular values stay >= sqrt(1e-3) of the largest, so
+  // the Gram's squared condition number costs at most ~1e3 eps; otherwise the
+  // core takes the QR path (and, after two failures in a row, so does the rest
+  // of the sweep: exactly rank-deficient unfoldings keep failing).
+  const bool gram_on = rel_tol == 0.0 && knob_env("TTK_TRUNC_NO_GRAM") == nullptr;
+  int gram_fails = 0;
   for (int k = d - 1; k >= 1; --k) {
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = n * r1, kk = std::min(m, r0);
@@ -343,6 +373,48 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
     double* const tU = tUb[k & 1];
     // the side-stream product of core k + 2 read these buffers
     if (g_pending[k & 1]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[k & 1], 0));
+    if (gram_on && gram_fails < 2 && m >= r0 && r0 >= 2 && r0 <= kCholBlockedMaxCols && jacobi_fits_v(r0, r0)) {
+      // G = C C^T (r0 x r0), C = cur (r0 x m, row-major)
+      TTK_TRY(gemm1(r0, r0, m, cur, m, 1, cur, 1, m, tG, r0, 1, split_ws, st));
+      TTK_CHECK_CUDA(cudaMemsetAsync(rdev + 2, 0, sizeof(int), st));
+      TTK_TRY(launch_chol_inv(r0, tG, tR, nullptr, rdev + 2, 0, 0.0, 1e-15, st, nullptr));
+      TTK_TRY(jacobi_svd_ex(r0, r0, tR, 1, r0, tL, tS, tU, true, st));
+      TTK_TRY(truncation_rank_dev(tS, r0, budget, max_rank, rdev, st));
+      TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+      TTK_CHECK_CUDA(cudaMemcpyAsync(pin + 2, tS, sizeof(double) * r0, cudaMemcpyDeviceToHost, st));
+      TTK_SYNC(st);
+      const int rk = ((int*)pin)[0], cstat = ((int*)pin)[2];
+      const double s0 = pin[2], sr = pin[2 + rk - 1];
+      if (cstat == 0 && s0 > 0.0 && sr * sr >= 1e-3 * s0 * s0) {
+        // core k <- T1^T C, T1 = W_r S_r^{-2} (side stream); L = W_r
+        scale_cols_inv_sq_kernel<<<ceil_div((long)r0 * rk, 256), 256, 0, st>>>(r0, rk, tL, r0, tS, tU);
+        TTK_CHECK_LAUNCH();
+        TTK_CHECK_CUDA(cudaEventRecord(ev_f[k & 1], st));
+        TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_f[k & 1], 0));
+        TTK_TRY(gemm1(m, rk, r0, cur, 1, m, tU, r0, 1, out[k], 1, m, split_side, side));
+        TTK_CHECK_CUDA(cudaEventRecord(ev_r[k & 1], side));
+        r_pending[k & 1] = true;
+        if (host_out)
+          TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[k], out[k], sizeof(double) * (size_t)rk * m,
+                                         cudaMemcpyDeviceToHost, side));
+        TTK_CHECK_CUDA(cudaEventRecord(ev_g[k & 1], side));
+        g_pending[k & 1] = true;
+        const int p0 = r[k - 1], pn = dims[k - 1];
+        double* dst = alt[k & 1];
+        if (r_pending[(k + 1) & 1]) {  // core k+1's side product read dst
+          TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_r[(k + 1) & 1], 0));
+          r_pending[(k + 1) & 1] = false;
+        }
+        TTK_TRY(gemm1(p0 * pn, rk, r0, cores[k - 1], r0, 1, tL, r0, 1, dst, rk, 1, split_ws, st));
+        cur = dst;
+        r[k] = rk;
+        g_trunc_gram.fetch_add(1, std::memory_order_relaxed);
+        gram_fails = 0;
+        continue;
+      }
+      ++gram_fails;
+    }
+    g_trunc_qr.fetch_add(1, std::memory_order_relaxed);
     // C_k^T (m x r0) = Q R ; element (row=(i,b), col=a) of C_k^T at a*m + row
     TTK_TRY(qr_auto(m, r0, cur, 1, m, tq, kk, 1, tR, qws, qrb, st, &qr_hint));
     const bool vt = jacobi_fits_v(r0, kk);
@@ -378,6 +450,10 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
     // C_{k-1} <- C_{k-1} x_3 L
     const int p0 = r[k - 1], pn = dims[k - 1];
     double* dst = alt[k & 1];
+    if (r_pending[(k + 1) & 1]) {  // core k+1's side product (Gram path) read dst
+      TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_r[(k + 1) & 1], 0));
+      r_pending[(k + 1) & 1] = false;
+    }
     TTK_TRY(gemm1(p0 * pn, rk, r0, cores[k - 1], r0, 1, tL, l_ld, 1, dst, rk, 1, split_ws, st));
     cur = dst;
     r[k] = rk;
@@ -391,6 +467,12 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
     if (g_pending[i]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[i], 0));
   TTK_SYNC(st);
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
+  return kOk;
+}
+
+int ttk_debug_truncate_paths(long long* counts) {
+  counts[0] = g_trunc_gram.load();
+  counts[1] = g_trunc_qr.load();
   return kOk;
 }
 

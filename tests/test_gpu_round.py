@@ -472,3 +472,46 @@ def test_fused_cholqr2_deterministic(cuda):
     torch.cuda.synchronize()
     for Q, R in res[1:]:
         assert torch.equal(Q, res[0][0]) and torch.equal(R, res[0][1])
+
+
+def _trunc_paths():
+    import ctypes
+    from paper_2409_09471_b200 import _lib
+    c = (ctypes.c_longlong * 2)()
+    _lib.load().ttk_debug_truncate_paths(ctypes.addressof(c))
+    return c[0], c[1]
+
+
+def test_truncate_gram_path_certified(cuda):
+    """Exact-rank truncation (rel_tol = 0, cap) of a generic left-orthogonal TT goes
+    through the Gram + Cholesky path on every core and matches the oracle's SVD path."""
+    dims = [12, 9, 16, 7, 11, 10]
+    x = O.tt_random(dims, [8, 14, 10, 9, 6], seed=5)
+    lo = O.rto_sweeps(x, O.drm_new(dims, [8, 14, 10, 9, 6], seed=6))  # sketch ranks = TT ranks: full rank
+    want = O.truncate_left_orth(lo, 0.0, 6)
+    g0, q0 = _trunc_paths()
+    got = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(0.0, 6))
+    g1, q1 = _trunc_paths()
+    assert (g1 - g0, q1 - q0) == (len(dims) - 1, 0)
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.rel_diff(tt_np(got), want) <= 1e-10
+    for c in got.cores[1:]:  # right-orthonormal cores, as the SVD path leaves them
+        u = c.cpu().numpy().reshape(c.shape[0], -1)
+        assert np.abs(u @ u.T - np.eye(u.shape[0])).max() <= 1e-12
+
+
+def test_truncate_gram_path_falls_back_on_rank_deficiency(cuda):
+    """rel_tol = 0 on a TT whose unfoldings are exactly rank deficient: the kept
+    singular values include ~1e-16 ones, the certificate fails and the cores go
+    through the QR path (the reference's behaviour: keep min(cap, l))."""
+    dims = [10, 12, 9, 11, 8]
+    y = O.tt_random(dims, [3, 4, 4, 3], seed=7)
+    x = O.add(y, O.scale(y, 0.5))  # nominal ranks 6, 8, 8, 6; true ranks 3, 4, 4, 3
+    lo = O.rto_sweeps(x, O.drm_new(dims, [8, 10, 10, 8], seed=8))
+    want = O.truncate_left_orth(lo, 0.0, 6)
+    g0, q0 = _trunc_paths()
+    got = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(0.0, 6))
+    g1, q1 = _trunc_paths()
+    assert q1 - q0 >= 1
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.diff_norm(tt_np(got), want) <= 1e-10 * O.norm(want)
