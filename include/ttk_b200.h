@@ -264,7 +264,8 @@ int ttk_tt_truncate(int d, const int* dims, const int* ranks, const double* cons
 int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
                          int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
                          size_t ws_bytes, void* stream);
-/* diagnostics: cores truncated so far through the Gram path [0] and the QR path [1] */
+/* diagnostics: cores truncated so far through the Gram path [0] and the QR path [1], and
+ * truncations redone through the QR path after a failed Gram certificate [2] */
 int ttk_debug_truncate_paths(long long* counts);
 size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks);
 

@@ -55,6 +55,17 @@ __global__ void scale_cols_inv_sq_kernel(int rows, int r, const double* __restri
   }
 }
 
+// certificate of one Gram-path core: Cholesky succeeded and the kept singular
+// values stay >= sqrt(1e-3) of the largest (so the rank is min(cap, r0), as the
+// reference's budget-0 rule gives, and the squared condition number costs <= ~1e3 eps)
+__global__ void gram_cert_kernel(const double* __restrict__ S, int rk, const int* __restrict__ cstat,
+                                 int* __restrict__ flag) {
+  if (threadIdx.x == 0) {
+    const double s0 = S[0], sr = S[rk - 1];
+    *flag = (*cstat == 0 && s0 > 0.0 && sr * sr >= 1e-3 * s0 * s0) ? 1 : 0;
+  }
+}
+
 struct PinnedScratch {
   void* p = nullptr;
   size_t cap = 0;
@@ -70,7 +81,7 @@ struct PinnedScratch {
 thread_local PinnedScratch g_pinned;
 
 // cores truncated by the Gram path / by the QR path (ttk_debug_truncate_paths)
-std::atomic<long long> g_trunc_gram{0}, g_trunc_qr{0};
+std::atomic<long long> g_trunc_gram{0}, g_trunc_qr{0}, g_trunc_redo{0};
 
 size_t core_elems(const int* dims, const int* ranks, int k) {
   return (size_t)ranks[k] * dims[k] * ranks[k + 1];
@@ -280,10 +291,9 @@ size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks) {
          align_up(qrws, 256) + 2 * kSplitKBytes + 131072;
 }
 
-int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
+static int truncate_impl(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
                          int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
-                         size_t ws_bytes, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+                         size_t ws_bytes, cudaStream_t st, bool allow_gram) {
   TTK_REQUIRE(d >= 1 && rel_tol >= 0.0, kInvalidValue, "tt_truncate: bad arguments");
   for (int k = 0; k <= d; ++k) out_ranks[k] = ranks[k];
   if (d == 1) {
@@ -316,6 +326,7 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
   double* red = ar.take<double>(16);
   double* part = ar.take<double>(256);
   int* rdev = ar.take<int>(8);
+  int* gflags = ar.take<int>((size_t)d + 8);
   size_t qoff = align_up(ar.used, 256);
   void* qws = (char*)ws + qoff;
   ar.used = qoff + qrb;
@@ -338,7 +349,7 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
   // which the main stream overwrites at core k - 2 (its C_{k-3}) -- ev_r marks
   // the end of that read (before the host copy, which must not gate the chain)
   bool r_pending[2] = {false, false};
-  double* pin = (double*)g_pinned.get(sizeof(double) * ((size_t)rmax + 16));
+  double* pin = (double*)g_pinned.get(sizeof(double) * ((size_t)std::max(rmax, d) + 16));
   TTK_REQUIRE(pin != nullptr, kCudaError, "tt_truncate: cannot allocate pinned scratch");
   std::vector<int> r(ranks, ranks + d + 1);
   // ||v|| = ||C_{d-1}||_F for a left-orthogonal TT
@@ -359,13 +370,13 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
   int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
   // Gram path (exact-rank roundings, rel_tol == 0): R from the Cholesky factor of
   // G = C_k C_k^T instead of the QR of C_k^T (no Q: the new core is
-  // S_r^{-2} W_r^T C_k with W = R^T V), certified per core -- the Cholesky must
-  // succeed and the kept singular values stay >= sqrt(1e-3) of the largest, so
-  // the Gram's squared condition number costs at most ~1e3 eps; otherwise the
-  // core takes the QR path (and, after two failures in a row, so does the rest
-  // of the sweep: exactly rank-deficient unfoldings keep failing).
-  const bool gram_on = rel_tol == 0.0 && knob_env("TTK_TRUNC_NO_GRAM") == nullptr;
-  int gram_fails = 0;
+  // S_r^{-2} W_r^T C_k with W = R^T V).  Its rank is min(cap, r0) whenever the
+  // core's certificate holds (gram_cert_kernel), so the sweep is enqueued with
+  // no host round trip per core and the certificates are checked once at the
+  // end; if any failed (e.g. an exactly rank-deficient unfolding) the whole
+  // truncation is redone through the QR path.
+  const bool gram_on = allow_gram && rel_tol == 0.0 && knob_env("TTK_TRUNC_NO_GRAM") == nullptr;
+  int ngram = 0;
   for (int k = d - 1; k >= 1; --k) {
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = n * r1, kk = std::min(m, r0);
@@ -373,19 +384,17 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
     double* const tU = tUb[k & 1];
     // the side-stream product of core k + 2 read these buffers
     if (g_pending[k & 1]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[k & 1], 0));
-    if (gram_on && gram_fails < 2 && m >= r0 && r0 >= 2 && r0 <= kCholBlockedMaxCols && jacobi_fits_v(r0, r0)) {
+    if (gram_on && m >= r0 && r0 >= 2 && r0 <= kCholBlockedMaxCols && jacobi_fits_v(r0, r0)) {
       // G = C C^T (r0 x r0), C = cur (r0 x m, row-major)
       TTK_TRY(gemm1(r0, r0, m, cur, m, 1, cur, 1, m, tG, r0, 1, split_ws, st));
       TTK_CHECK_CUDA(cudaMemsetAsync(rdev + 2, 0, sizeof(int), st));
       TTK_TRY(launch_chol_inv(r0, tG, tR, nullptr, rdev + 2, 0, 0.0, 1e-15, st, nullptr));
       TTK_TRY(jacobi_svd_ex(r0, r0, tR, 1, r0, tL, tS, tU, true, st));
-      TTK_TRY(truncation_rank_dev(tS, r0, budget, max_rank, rdev, st));
-      TTK_CHECK_CUDA(cudaMemcpyAsync(pin, rdev, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
-      TTK_CHECK_CUDA(cudaMemcpyAsync(pin + 2, tS, sizeof(double) * r0, cudaMemcpyDeviceToHost, st));
-      TTK_SYNC(st);
-      const int rk = ((int*)pin)[0], cstat = ((int*)pin)[2];
-      const double s0 = pin[2], sr = pin[2 + rk - 1];
-      if (cstat == 0 && s0 > 0.0 && sr * sr >= 1e-3 * s0 * s0) {
+      const int rk = std::min(max_rank > 0 ? max_rank : r0, r0);
+      gram_cert_kernel<<<1, 32, 0, st>>>(tS, rk, rdev + 2, gflags + ngram);
+      TTK_CHECK_LAUNCH();
+      ++ngram;
+      {
         // core k <- T1^T C, T1 = W_r S_r^{-2} (side stream); L = W_r
         scale_cols_inv_sq_kernel<<<ceil_div((long)r0 * rk, 256), 256, 0, st>>>(r0, rk, tL, r0, tS, tU);
         TTK_CHECK_LAUNCH();
@@ -409,10 +418,8 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
         cur = dst;
         r[k] = rk;
         g_trunc_gram.fetch_add(1, std::memory_order_relaxed);
-        gram_fails = 0;
         continue;
       }
-      ++gram_fails;
     }
     g_trunc_qr.fetch_add(1, std::memory_order_relaxed);
     // C_k^T (m x r0) = Q R ; element (row=(i,b), col=a) of C_k^T at a*m + row
@@ -465,14 +472,30 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
                                    cudaMemcpyDeviceToHost, st));
   for (int i = 0; i < 2; ++i)
     if (g_pending[i]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[i], 0));
+  int* hflags = reinterpret_cast<int*>(pin);
+  if (ngram > 0) TTK_CHECK_CUDA(cudaMemcpyAsync(hflags, gflags, sizeof(int) * ngram, cudaMemcpyDeviceToHost, st));
   TTK_SYNC(st);
+  for (int i = 0; i < ngram; ++i)
+    if (hflags[i] != 1) {
+      g_trunc_redo.fetch_add(1, std::memory_order_relaxed);
+      return truncate_impl(d, dims, ranks, cores, rel_tol, max_rank, out, out_ranks, host_out, ws, ws_bytes, st,
+                           false);
+    }
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
   return kOk;
+}
+
+int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
+                         int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
+                         size_t ws_bytes, void* stream) {
+  return truncate_impl(d, dims, ranks, cores, rel_tol, max_rank, out, out_ranks, host_out, ws, ws_bytes,
+                       (cudaStream_t)stream, true);
 }
 
 int ttk_debug_truncate_paths(long long* counts) {
   counts[0] = g_trunc_gram.load();
   counts[1] = g_trunc_qr.load();
+  counts[2] = g_trunc_redo.load();
   return kOk;
 }
 

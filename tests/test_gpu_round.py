@@ -477,9 +477,9 @@ def test_fused_cholqr2_deterministic(cuda):
 def _trunc_paths():
     import ctypes
     from paper_2409_09471_b200 import _lib
-    c = (ctypes.c_longlong * 2)()
+    c = (ctypes.c_longlong * 3)()
     _lib.load().ttk_debug_truncate_paths(ctypes.addressof(c))
-    return c[0], c[1]
+    return c[0], c[1], c[2]
 
 
 def test_truncate_gram_path_certified(cuda):
@@ -489,10 +489,10 @@ def test_truncate_gram_path_certified(cuda):
     x = O.tt_random(dims, [8, 14, 10, 9, 6], seed=5)
     lo = O.rto_sweeps(x, O.drm_new(dims, [8, 14, 10, 9, 6], seed=6))  # sketch ranks = TT ranks: full rank
     want = O.truncate_left_orth(lo, 0.0, 6)
-    g0, q0 = _trunc_paths()
+    g0, q0, x0 = _trunc_paths()
     got = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(0.0, 6))
-    g1, q1 = _trunc_paths()
-    assert (g1 - g0, q1 - q0) == (len(dims) - 1, 0)
+    g1, q1, x1 = _trunc_paths()
+    assert (g1 - g0, q1 - q0, x1 - x0) == (len(dims) - 1, 0, 0)
     assert got.ranks == tuple([1] + [c.shape[2] for c in want])
     assert O.rel_diff(tt_np(got), want) <= 1e-10
     for c in got.cores[1:]:  # right-orthonormal cores, as the SVD path leaves them
@@ -502,16 +502,16 @@ def test_truncate_gram_path_certified(cuda):
 
 def test_truncate_gram_path_falls_back_on_rank_deficiency(cuda):
     """rel_tol = 0 on a TT whose unfoldings are exactly rank deficient: the kept
-    singular values include ~1e-16 ones, the certificate fails and the cores go
-    through the QR path (the reference's behaviour: keep min(cap, l))."""
+    singular values include ~1e-16 ones, a certificate fails and the truncation
+    is redone through the QR path (the reference's behaviour: keep min(cap, l))."""
     dims = [10, 12, 9, 11, 8]
     y = O.tt_random(dims, [3, 4, 4, 3], seed=7)
     x = O.add(y, O.scale(y, 0.5))  # nominal ranks 6, 8, 8, 6; true ranks 3, 4, 4, 3
     lo = O.rto_sweeps(x, O.drm_new(dims, [8, 10, 10, 8], seed=8))
     want = O.truncate_left_orth(lo, 0.0, 6)
-    g0, q0 = _trunc_paths()
+    g0, q0, x0 = _trunc_paths()
     got = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(0.0, 6))
-    g1, q1 = _trunc_paths()
-    assert q1 - q0 >= 1
+    g1, q1, x1 = _trunc_paths()
+    assert x1 - x0 == 1 and q1 - q0 == len(dims) - 1
     assert got.ranks == tuple([1] + [c.shape[2] for c in want])
     assert O.diff_norm(tt_np(got), want) <= 1e-10 * O.norm(want)
