@@ -1380,7 +1380,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kJbMaxSlots * kSvdG
 // across the whole chain, not by one piece.
 constexpr int kJwSlots = 4, kJwLanes = 8;
 
-template <int RPL, bool PROF = false, int LC = 0>
+template <int RPL, bool PROF = false, int LC = 0, bool WV = true>
 __global__ void __launch_bounds__(32, 1)
     jacobi_warp_kernel(int k, int l_arg, const double* __restrict__ B, long long b_rs, long long b_cs,
                        double* __restrict__ U, double* __restrict__ S, double* __restrict__ V, int want_v_arg,
@@ -1390,9 +1390,11 @@ __global__ void __launch_bounds__(32, 1)
   // LC > 0: the column count (and so the cluster size) as compile-time constants
   const int l = LC > 0 ? LC : l_arg;
   const int CL = LC > 0 ? LC / (2 * kJwSlots) : (int)cl.num_blocks();
-  // V is always accumulated by the truncation; a compile-time flag removes the
-  // per-round V branches (PROF instances keep the runtime form)
-  const bool want_v = PROF ? (want_v_arg != 0) : true;
+  // V accumulation as a compile-time flag (no per-round V branches): the QR
+  // truncation path needs V (Q V_r), the Gram path only the rotated columns and
+  // S -- without V a round has half the rotation FMAs, shuffle moves and DSMEM
+  // block-move bytes.  PROF instances keep the runtime form.
+  const bool want_v = PROF ? (want_v_arg != 0) : WV;
   const int c = (int)cl.block_rank();
   static_assert(RPL % 2 == 0, "RPL must be even");
   constexpr int box = RPL * kJwLanes;  // doubles per column part
@@ -1942,7 +1944,13 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
                              (const void*)jacobi_warp_kernel<10>, (const void*)jacobi_warp_kernel<12>,
                              (const void*)jacobi_warp_kernel<2, true>, (const void*)jacobi_warp_kernel<4, true>,
                              (const void*)jacobi_warp_kernel<6, true>, (const void*)jacobi_warp_kernel<8, true>,
-                             (const void*)jacobi_warp_kernel<10, true>, (const void*)jacobi_warp_kernel<12, true>})
+                             (const void*)jacobi_warp_kernel<10, true>, (const void*)jacobi_warp_kernel<12, true>,
+                             (const void*)jacobi_warp_kernel<2, false, 0, false>,
+                             (const void*)jacobi_warp_kernel<4, false, 0, false>,
+                             (const void*)jacobi_warp_kernel<6, false, 0, false>,
+                             (const void*)jacobi_warp_kernel<8, false, 0, false>,
+                             (const void*)jacobi_warp_kernel<10, false, 0, false>,
+                             (const void*)jacobi_warp_kernel<12, false, 0, false>})
         TTK_TRY(set_attr_once(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     }
     const size_t jsm = sizeof(double) * 2 * kJwSlots * 4 * (size_t)rpl * kJwLanes;
@@ -1965,9 +1973,15 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
       {  // per-device attributes (set_attr_once)
         TTK_TRY(set_attr_once((const void*)jacobi_warp_kernel<10, false, 80>,
                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        TTK_TRY(set_attr_once((const void*)jacobi_warp_kernel<10, false, 80, false>,
+                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       }
-      e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, false, 80>, k, l, B, b_rs, b_cs, U, S, V, want,
-                             (int)scaled_u, skip2);
+      if (want)
+        e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, false, 80>, k, l, B, b_rs, b_cs, U, S, V, want,
+                               (int)scaled_u, skip2);
+      else
+        e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, false, 80, false>, k, l, B, b_rs, b_cs, U, S, V,
+                               want, (int)scaled_u, skip2);
     } else if (g_jc_prof_host) {
     switch (rpl) {
       case 2: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<2, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
@@ -1976,6 +1990,15 @@ int jacobi_svd_ex(int k, int l, const double* B, long long b_rs, long long b_cs,
       case 8: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<8, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
       case 10: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
       default: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<12, true>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+    }
+    } else if (!want) {
+    switch (rpl) {
+      case 2: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<2, false, 0, false>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 4: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<4, false, 0, false>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 6: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<6, false, 0, false>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 8: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<8, false, 0, false>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      case 10: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<10, false, 0, false>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
+      default: e = cudaLaunchKernelEx(&cfg, jacobi_warp_kernel<12, false, 0, false>, k, l, B, b_rs, b_cs, U, S, V, want, (int)scaled_u, skip2); break;
     }
     } else {
     switch (rpl) {

@@ -389,7 +389,7 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
       TTK_TRY(gemm1(r0, r0, m, cur, m, 1, cur, 1, m, tG, r0, 1, split_ws, st));
       TTK_CHECK_CUDA(cudaMemsetAsync(rdev + 2, 0, sizeof(int), st));
       TTK_TRY(launch_chol_inv(r0, tG, tR, nullptr, rdev + 2, 0, 0.0, 1e-15, st, nullptr));
-      TTK_TRY(jacobi_svd_ex(r0, r0, tR, 1, r0, tL, tS, tU, true, st));
+      TTK_TRY(jacobi_svd_ex(r0, r0, tR, 1, r0, tL, tS, nullptr, true, st));  // W and S only
       const int rk = std::min(max_rank > 0 ? max_rank : r0, r0);
       gram_cert_kernel<<<1, 32, 0, st>>>(tS, rk, rdev + 2, gflags + ngram);
       TTK_CHECK_LAUNCH();
