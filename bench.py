@@ -227,8 +227,9 @@ def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=No
     V = torch.empty((l, l), dtype=torch.float64, device=dev)
     cnt = torch.zeros(1, dtype=torch.int32, device=dev)
     lib.ttk_debug_svd_sweeps(cnt.data_ptr())
-    # the truncation runs Jacobi on R^T with V accumulated (qr.cu jacobi_svd_ex)
-    call = lambda: lib.ttk_svd_small(l, l, R.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(),
+    # the config-3 truncation (exact-rank Gram path, round.cu) runs the Jacobi on
+    # R^T of the Cholesky factor without V (only the rotated columns and S are used)
+    call = lambda: lib.ttk_svd_small(l, l, R.data_ptr(), U.data_ptr(), S.data_ptr(), None,
                                      _lib.stream_ptr(dev))
     call()
     torch.cuda.synchronize()
@@ -241,16 +242,16 @@ def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=No
     ms = a.elapsed_time(b) / 5
     sweeps = int(cnt.item())
     lib.ttk_debug_svd_sweeps(None)
-    # per sweep l(l-1)/2 pairs x (3 dot FMAs + 2x2 rotation FMAs on C and on V) per row
-    flops = sweeps * (l * (l - 1) / 2) * (6.0 * l + 12.0 * l)
+    # per sweep l(l-1)/2 pairs x (3 dot FMAs + the 2x2 rotation of the two columns) per row
+    flops = sweeps * (l * (l - 1) / 2) * (6.0 * l + 6.0 * l)
     sms = (l + 7) // 8  # CTAs (one per SM) of the warp kernel's cluster
     peak_sms = sms * 33.9e3 / 148  # GFLOP/s of those SMs: measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
     ach = flops / (ms * 1e-3) / 1e9
     rounds = sweeps * (l - 1)
-    out = {"kernel": "jacobi_warp_kernel (%d-CTA cluster, one warp per CTA, block-ordered, %dx%d, V accumulated)" % (sms, l, l), "ms": ms,
+    out = {"kernel": "jacobi_warp_kernel (%d-CTA cluster, one warp per CTA, block-ordered, %dx%d, no V)" % (sms, l, l), "ms": ms,
            "sweeps": sweeps, "rounds": rounds, "us_per_round": ms * 1e3 / max(rounds, 1),
-           "bound": "latency (sequential rotation rounds; per round: dot, 16-lane reduction, "
-                    "rotation, in-CTA move; a DSMEM block move every bs rounds)",
+           "bound": "latency (sequential rotation rounds; per round: dots, 8-lane reduction, "
+                    "rotation, in-CTA shuffle move; a DSMEM block move every 4 rounds)",
            "achieved_gflops": ach, "sms": sms, "peak_gflops_of_its_sms": peak_sms,
            "frac_of_its_sms": ach / peak_sms}
     if calls_per_step and step_ms:

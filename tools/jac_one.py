@@ -1,4 +1,4 @@
-"""One 80x80 Jacobi SVD with V accumulation (the truncation's configuration) for ncu."""
+"""One l x l Jacobi SVD for ncu: python tools/jac_one.py [l] [nov]  (nov: no V, the Gram truncation path)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -8,6 +8,7 @@ g = torch.Generator().manual_seed(0)
 R = torch.linalg.qr(torch.randn(10 * l, l, dtype=torch.float64, generator=g))[1].to(dev).contiguous()
 U = torch.empty((l, l), dtype=torch.float64, device=dev); S = torch.empty(l, dtype=torch.float64, device=dev)
 V = torch.empty((l, l), dtype=torch.float64, device=dev)
+vp = None if (len(sys.argv) > 2 and sys.argv[2] == "nov") else V.data_ptr()
 for _ in range(3):
-    lib.ttk_svd_small(l, l, R.data_ptr(), U.data_ptr(), S.data_ptr(), V.data_ptr(), _lib.stream_ptr(dev))
+    lib.ttk_svd_small(l, l, R.data_ptr(), U.data_ptr(), S.data_ptr(), vp, _lib.stream_ptr(dev))
 torch.cuda.synchronize(); print("ok")
