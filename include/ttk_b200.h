@@ -168,6 +168,8 @@ int ttk_debug_svd_sweeps(int* dev_counter);
 int ttk_debug_jacobi_profile(long long* dev_acc);
 /* diagnostics: the blocked Cholesky adds per-call phase clocks (load, diagonal
  * blocks, panels, trailing updates, epilogue, call count) into dev_acc[6] (NULL: off) */
+/* diagnostics: one blocked Cholesky R^T R = G (l x l, device; status: device int) */
+int ttk_debug_chol(int l, const double* G, double* R, int* status, void* stream);
 int ttk_debug_chol_profile(long long* dev_acc);
 /* diagnostics: phase timestamps (%globaltimer, ns) of the fused CholeskyQR2 kernel into dev_ts[16]; NULL = off */
 int ttk_debug_fused_qr_profile(long long* dev_ts);

@@ -179,6 +179,7 @@ SIGNATURES.update({"ttk_debug_host_profile": (c_int, [ctypes.POINTER(ctypes.c_lo
 SIGNATURES.update({"ttk_drm_gaussian": (c_int, [ctypes.c_ulonglong, c_int, c_int, c_int, c_int, c_int, c_int,
                                                 c_double, c_vp, c_vp])})
 SIGNATURES.update({"ttk_debug_chol_profile": (c_int, [c_vp])})
+SIGNATURES.update({"ttk_debug_chol": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp])})
 
 SIGNATURES.update({"ttk_qr_auto": (c_int, [c_int, c_int, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_vp, c_vp, c_size,
                                            c_vp])})

@@ -2227,6 +2227,12 @@ int ttk_debug_fused_qr_profile(long long* dev_ts) {
   return kOk;
 }
 
+// diagnostics: one Cholesky factorisation R^T R = G (l x l, device) through
+// launch_chol_inv (the truncation's Gram path); status: device int
+int ttk_debug_chol(int l, const double* G, double* R, int* status, void* stream) {
+  return launch_chol_inv(l, G, R, nullptr, status, 0, 0.0, 1e-15, (cudaStream_t)stream, nullptr);
+}
+
 int ttk_debug_chol_profile(long long* dev_acc) {
   TTK_CHECK_CUDA(cudaMemcpyToSymbol(g_chol_prof, &dev_acc, sizeof(long long*)));
   return kOk;
@@ -2681,7 +2687,7 @@ constexpr int kCbThreads = 512;
 // column c); compile-time recursion keeps every index of d[] static
 template <int JJ>
 __device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, int bs, double tiny, int& badd,
-                                              double* invd) {
+                                              double* invd, double (*rowb)[16]) {
   if constexpr (JJ < 16) {
     double p = __shfl_sync(0xffffffffu, d[JJ], JJ);
     if (JJ < bs && !(p > tiny)) { badd = 1; p = 1.0; }
@@ -2694,12 +2700,14 @@ __device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, 
     const double rrow = (lane == JJ ? p : d[JJ]) * inv;
     d[JJ] = rrow;
     if (lane == JJ) invd[JJ] = inv;
+    // row JJ of R broadcast through shared memory (double-buffered by pivot
+    // parity): one store per lane and 15 - JJ broadcast loads instead of
+    // 2 (15 - JJ) 32-bit shuffles per pivot
+    if (lane < 16) rowb[JJ & 1][lane] = rrow;
+    __syncwarp();
 #pragma unroll
-    for (int rr = JJ + 1; rr < 16; ++rr) {
-      const double rjr = __shfl_sync(0xffffffffu, rrow, rr);
-      d[rr] = fma(-rjr, rrow, d[rr]);
-    }
-    cb_diag_steps<JJ + 1>(d, c, lane, bs, tiny, badd, invd);
+    for (int rr = JJ + 1; rr < 16; ++rr) d[rr] = fma(-rowb[JJ & 1][rr], rrow, d[rr]);
+    cb_diag_steps<JJ + 1>(d, c, lane, bs, tiny, badd, invd, rowb);
   }
 }
 
@@ -2716,6 +2724,7 @@ __device__ void chol_blocked_body(int l, const double* __restrict__ G, double* _
   double* X = A + (size_t)l * ld;       // l x ld (inverse)
   double* Tb = X + (size_t)l * ld;      // 256 * nb
   __shared__ double invd[kCholMaxCols + 16];
+  __shared__ double rowb[2][16];  // pivot-row broadcast of the diagonal-block factorisation
   __shared__ double gmax_s, tr_s;
   __shared__ int bad;
   const int tid = threadIdx.x, nt = blockDim.x, w = tid >> 5, lane = tid & 31;
@@ -2759,7 +2768,7 @@ __device__ void chol_blocked_body(int l, const double* __restrict__ G, double* _
       for (int rr = 0; rr < 16; ++rr)
         d[rr] = (rr < bs && c < bs) ? A[(j0 + rr) * ld + j0 + c] : (rr == c ? 1.0 : 0.0);
       int badd = 0;
-      cb_diag_steps<0>(d, c, lane, bs, tiny, badd, invd + j0);
+      cb_diag_steps<0>(d, c, lane, bs, tiny, badd, invd + j0, rowb);
       if (lane < 16) {
 #pragma unroll
         for (int rr = 0; rr < 16; ++rr)
