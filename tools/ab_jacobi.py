@@ -19,6 +19,7 @@ for l in sizes:
     U = torch.empty((l, l), dtype=torch.float64, device=dev); S = torch.empty(l, dtype=torch.float64, device=dev)
     V = torch.empty((l, l), dtype=torch.float64, device=dev)
     res = {(nm, v): [] for nm in names for v in (0, 1)}
+    errs = {}
     for rep in range(5):
         for nm in names:
             for v in (0, 1):
@@ -31,6 +32,11 @@ for l in sizes:
                 for _ in range(10): call()
                 b.record(st); torch.cuda.synchronize()
                 res[(nm, v)].append(a.elapsed_time(b) / 10 * 1e3)
-    sl = np.linalg.svd(R, compute_uv=False)
-    print(f"{l}x{l}: " + "  ".join(f"{nm}{'+V' if v else ''} {np.median(t):.1f}" for (nm, v), t in res.items())
-          + f"  | S err {np.abs(np.sort(S.cpu().numpy())[::-1] - sl).max() / sl[0]:.1e}", flush=True)
+                if rep == 0:
+                    sl = np.linalg.svd(R, compute_uv=False)
+                    u = U.cpu().numpy(); sv = S.cpu().numpy()
+                    errs[(nm, v)] = (np.abs(sv - sl).max() / sl[0], np.abs(u.T @ u - np.eye(l)).max())
+    print(f"{l}x{l}: " + "  ".join(f"{nm}{'+V' if v else ''} {np.median(t):.1f}" for (nm, v), t in res.items()),
+          flush=True)
+    print("   errors (S rel, U orth): " + "  ".join(f"{nm}{'+V' if v else ''} {e[0]:.1e}/{e[1]:.1e}"
+                                                  for (nm, v), e in errs.items()), flush=True)
