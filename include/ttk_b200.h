@@ -161,6 +161,13 @@ int ttk_qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, d
 /* one-sided Jacobi SVD of B (k x l, row-major, k,l <= 128): B V = U S with
  * S[min(k,l)] descending, U (k x min(k,l)), V (l x min(k,l)) if V != NULL. */
 int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V, void* stream);
+/* C = alpha A B + beta C for row-major fp64 A (M x K, lda), B (K x N, ldb), C (M x N,
+ * ldc) on the TMA-staged DMMA kernel (cp.async.bulk.tensor tiles with the 128-byte
+ * swizzle, mbarrier ring): the plain skinny contractions of the RTO sweeps
+ * (tt.py's tensordot chains restated in oracle/ttoracle.py rto_sweeps).
+ * Requires 16-byte aligned bases, even leading dimensions and K >= 16. */
+int ttk_gemm_tma(int M, int N, int K, double alpha, const double* A, long long lda, const double* B, long long ldb,
+                 double beta, double* C, long long ldc, void* stream);
 /* diagnostics: subsequent Jacobi SVDs store their sweep count in *dev_counter (NULL: off) */
 int ttk_debug_svd_sweeps(int* dev_counter);
 /* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,

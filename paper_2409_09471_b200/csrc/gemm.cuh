@@ -337,6 +337,13 @@ struct GemmPlan {
 // split is needed; query with gemm_group_ws_bytes).
 int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, cudaStream_t st,
                       bool allow_split = true);
+
+// TMA-staged DMMA GEMM for plain row-major operands (gemm_tma.cu):
+// C = alpha A B + beta C, A (M x K, lda), B (K x N, ldb), C (M x N, ldc).
+// gemm_tma_ok: 16-byte aligned bases, even leading dimensions, K >= 16.
+bool gemm_tma_ok(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb);
+int gemm_tma(int M, int N, int K, double alpha, const double* A, long long lda, const double* B, long long ldb,
+             double beta, double* C, long long ldc, cudaStream_t st);
 size_t gemm_group_ws_bytes(const GemmProblem* probs, int count, bool allow_split = true);
 
 // Convenience: plain strided problem, C(m,n) = alpha*sum_k A(m,k)B(k,n) + beta*C

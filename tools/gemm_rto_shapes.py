@@ -32,8 +32,15 @@ for M, N, K in SHAPES:
     f = lambda: lib.ttk_gemm_strided(1, M, N, K, 1.0, A.data_ptr(), K, 1, 0, B.data_ptr(), N, 1, 0, 0.0,
                                      C.data_ptr(), N, 1, 0, ws.data_ptr(), ws.numel(), st)
     t = timed(f)
-    err = (C - A @ B).abs().max().item() / (A.abs().max().item() * B.abs().max().item() * K)
+    ref = A @ B
+    err = (C - ref).abs().max().item() / (A.abs().max().item() * B.abs().max().item() * K)
+    C.zero_()
+    g = lambda: lib.ttk_gemm_tma(M, N, K, 1.0, A.data_ptr(), K, B.data_ptr(), N, 0.0, C.data_ptr(), N, st)
+    _lib.check(g())
+    tt = timed(g)
+    err_t = (C - ref).abs().max().item() / (A.abs().max().item() * B.abs().max().item() * K)
     tc = timed(lambda: torch.mm(A, B, out=C))
     fl = 2.0 * M * N * K
-    print(f"M={M:6d} N={N:6d} K={K:6d}: ttk {t:7.1f} us {fl / t / 1e6:6.2f} TF/s | cuBLAS {tc:7.1f} us "
-          f"{fl / tc / 1e6:6.2f} TF/s | err {err:.1e}", flush=True)
+    print(f"M={M:6d} N={N:6d} K={K:6d}: ttk {t:7.1f} us {fl / t / 1e6:6.2f} TF/s | tma {tt:7.1f} us "
+          f"{fl / tt / 1e6:6.2f} TF/s | cuBLAS {tc:7.1f} us {fl / tc / 1e6:6.2f} TF/s | err {err:.1e} tma {err_t:.1e}",
+          flush=True)
