@@ -168,6 +168,14 @@ int ttk_svd_small(int k, int l, const double* B, double* U, double* S, double* V
  * Requires 16-byte aligned bases, even leading dimensions and K >= 16. */
 int ttk_gemm_tma(int M, int N, int K, double alpha, const double* A, long long lda, const double* B, long long ldb,
                  double beta, double* C, long long ldc, void* stream);
+/* general strided form: A(m,k) = A[m*a_ms + k*a_ks], B(k,n) = B[k*b_ks + n*b_ns],
+ * C(m,n) = C[m*c_ms + n*c_ns] with row-major operands or transposes of row-major
+ * operands (a column-major C is computed as the transposed problem); K is split
+ * over ws (ws_bytes) when the output tiles leave SMs idle.  Returns
+ * TTK_INVALID_VALUE without launching when the operands do not fit TMA. */
+int ttk_gemm_tma_strided(int M, int N, int K, double alpha, const double* A, long long a_ms, long long a_ks,
+                         const double* B, long long b_ks, long long b_ns, double beta, double* C, long long c_ms,
+                         long long c_ns, void* ws, size_t ws_bytes, void* stream);
 /* diagnostics: subsequent Jacobi SVDs store their sweep count in *dev_counter (NULL: off) */
 int ttk_debug_svd_sweeps(int* dev_counter);
 /* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,

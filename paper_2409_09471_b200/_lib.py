@@ -143,6 +143,8 @@ SIGNATURES.update({
     "ttk_qr_ws_bytes": (c_size, [c_int, c_int]),
     "ttk_svd_small": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "ttk_gemm_tma": (c_int, [c_int, c_int, c_int, c_double, c_vp, c_ll, c_vp, c_ll, c_double, c_vp, c_ll, c_vp]),
+    "ttk_gemm_tma_strided": (c_int, [c_int, c_int, c_int, c_double, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_double,
+                                     c_vp, c_ll, c_ll, c_vp, c_size, c_vp]),
     "ttk_tt_round": (c_int, [c_int, P_int, P_int, P_vp, c_double, c_int, c_double, P_vp, P_int, c_vp,
                              c_size, c_vp]),
     "ttk_tt_round_ws_bytes": (c_size, [c_int, P_int, P_int]),

@@ -342,6 +342,14 @@ int gemm_group_launch(GemmProblem* probs, int count, void* ws, size_t ws_bytes, 
 // C = alpha A B + beta C, A (M x K, lda), B (K x N, ldb), C (M x N, ldc).
 // gemm_tma_ok: 16-byte aligned bases, even leading dimensions, K >= 16.
 bool gemm_tma_ok(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb);
+// strided form (A(m,k) = A[m*a_ms + k*a_ks], ...): row-major operands or
+// transposes of row-major ones, column-major C as the transposed problem, K
+// split over ws when the tiles leave SMs idle (only with force_split_ok: the
+// grouped kernel's split-K is as fast); false = not taken, nothing launched
+bool gemm_tma_try(int M, int N, int K, double alpha, const double* A, long long a_ms, long long a_ks,
+                  const double* B, long long b_ks, long long b_ns, double beta, double* C, long long c_ms,
+                  long long c_ns, void* ws, size_t ws_bytes, cudaStream_t st, int* status,
+                  bool force_split_ok = false);
 int gemm_tma(int M, int N, int K, double alpha, const double* A, long long lda, const double* B, long long ldb,
              double beta, double* C, long long ldc, cudaStream_t st);
 size_t gemm_group_ws_bytes(const GemmProblem* probs, int count, bool allow_split = true);

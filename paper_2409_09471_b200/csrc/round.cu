@@ -25,10 +25,13 @@ constexpr size_t kSplitKBytes = 32u << 20;
 int gemm1(int M, int N, int K, const double* A, long long a_ms, long long a_ks, const double* B,
           long long b_ks, long long b_ns, double* C, long long c_ms, long long c_ns, void* split_ws,
           cudaStream_t st, double alpha = 1.0, double beta = 0.0) {
-  // plain row-major operands with a short K (the RTO sweeps' T = X W, Y = M T,
-  // Z = M X and the truncation's C_{k-1} W_r): the TMA-staged kernel
-  if (a_ks == 1 && b_ns == 1 && c_ns == 1 && K <= 1024 && gemm_tma_ok(M, N, K, A, a_ms, B, b_ks))
-    return gemm_tma(M, N, K, alpha, A, a_ms, B, b_ks, beta, C, c_ms, st);
+  // row-major operands or their transposes (every contraction of the RTO sweeps
+  // and of the truncation): the TMA-staged kernel, K split over split_ws when
+  // the tiles leave SMs idle; anything else: the grouped cp.async kernel
+  int status = kOk;
+  if (gemm_tma_try(M, N, K, alpha, A, a_ms, a_ks, B, b_ks, b_ns, beta, C, c_ms, c_ns, split_ws,
+                   split_ws ? kSplitKBytes : 0, st, &status))
+    return status;
   GemmProblem p = make_gemm(M, N, K, A, a_ms, a_ks, B, b_ks, b_ns, C, c_ms, c_ns, alpha, beta);
   return gemm_group_launch(&p, 1, split_ws, split_ws ? kSplitKBytes : 0, st);
 }
