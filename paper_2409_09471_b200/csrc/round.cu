@@ -342,9 +342,15 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
   TTK_REQUIRE(split_side != nullptr, kWorkspace, "tt_truncate: workspace too small");
   static thread_local cudaStream_t side = nullptr;
   static thread_local cudaEvent_t ev_f[2] = {nullptr, nullptr}, ev_g[2] = {nullptr, nullptr},
-                                  ev_r[2] = {nullptr, nullptr};
+                                  ev_r[2] = {nullptr, nullptr}, ev_d = nullptr;
+  // host copies of final cores run on their own stream, so that the chain's
+  // buffer-reuse waits (ev_g: the side product has read tq / tU) never wait
+  // on PCIe
+  static thread_local cudaStream_t d2h = nullptr;
   if (side == nullptr) {
     TTK_CHECK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    TTK_CHECK_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_d, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
       TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_f[i], cudaEventDisableTiming));
       TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_g[i], cudaEventDisableTiming));
@@ -410,11 +416,13 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
         TTK_TRY(gemm1(m, rk, r0, cur, 1, m, tU, r0, 1, out[k], 1, m, split_side, side));
         TTK_CHECK_CUDA(cudaEventRecord(ev_r[k & 1], side));
         r_pending[k & 1] = true;
-        if (host_out)
-          TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[k], out[k], sizeof(double) * (size_t)rk * m,
-                                         cudaMemcpyDeviceToHost, side));
         TTK_CHECK_CUDA(cudaEventRecord(ev_g[k & 1], side));
         g_pending[k & 1] = true;
+        if (host_out) {
+          TTK_CHECK_CUDA(cudaStreamWaitEvent(d2h, ev_g[k & 1], 0));
+          TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[k], out[k], sizeof(double) * (size_t)rk * m,
+                                         cudaMemcpyDeviceToHost, d2h));
+        }
         const int p0 = r[k - 1], pn = dims[k - 1];
         double* dst = alt[k & 1];
         if (r_pending[(k + 1) & 1]) {  // core k+1's side product read dst
@@ -448,13 +456,15 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
     TTK_CHECK_CUDA(cudaEventRecord(ev_f[k & 1], st));
     TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_f[k & 1], 0));
     TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_side, side));
-    // core k is final: stream it to the caller's pinned host buffer behind the
-    // rest of the sweep (same side stream, so it also waits for the product)
-    if (host_out)
-      TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[k], out[k], sizeof(double) * (size_t)rk * m, cudaMemcpyDeviceToHost,
-                                     side));
     TTK_CHECK_CUDA(cudaEventRecord(ev_g[k & 1], side));
     g_pending[k & 1] = true;
+    // core k is final: stream it to the caller's pinned host buffer behind the
+    // rest of the sweep (after the product, on the copy stream)
+    if (host_out) {
+      TTK_CHECK_CUDA(cudaStreamWaitEvent(d2h, ev_g[k & 1], 0));
+      TTK_CHECK_CUDA(cudaMemcpyAsync(host_out[k], out[k], sizeof(double) * (size_t)rk * m, cudaMemcpyDeviceToHost,
+                                     d2h));
+    }
     long long l_ld = kk;
     if (!vt) {
       // L = R^T U_r (r0 x rk)
@@ -479,6 +489,10 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
                                    cudaMemcpyDeviceToHost, st));
   for (int i = 0; i < 2; ++i)
     if (g_pending[i]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[i], 0));
+  if (host_out) {  // every host copy has landed before the call returns
+    TTK_CHECK_CUDA(cudaEventRecord(ev_d, d2h));
+    TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_d, 0));
+  }
   int* hflags = reinterpret_cast<int*>(pin);
   if (ngram > 0) TTK_CHECK_CUDA(cudaMemcpyAsync(hflags, gflags, sizeof(int) * ngram, cudaMemcpyDeviceToHost, st));
   TTK_SYNC(st);
