@@ -2609,6 +2609,15 @@ __device__ __forceinline__ void for_each_l2(const double* __restrict__ src, int 
   }
 }
 
+// Bound on l |E|^2 below which the second CholeskyQR pass uses the first-order
+// factor R = I + F1, R^{-1} = I - F1 (F1 = triu(E) - diag(E)/2): then
+// Q^T Q = R^{-T} (I + E) R^{-1} = I + O(l |E|^2), i.e. the dropped second-order
+// terms leave an orthogonality error of at most ~1e-15 -- the size of the
+// rounding of the Q product itself.  (r01 used 1e-17; the config-3 RTO
+// sketches, kappa up to ~600, sit between the two and paid ~19 us per
+// factorisation for three 80^3 products on one CTA.)
+constexpr double kNearIdFirstOrderMax = 1e-15;
+
 __device__ void chol_near_identity_body(int l, const double* __restrict__ G, double* __restrict__ Rout,
                                         double* __restrict__ Rinv, int* flag, double tol, double first_order_max,
                                         double* sm) {
@@ -2854,8 +2863,9 @@ int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status
   const int* skip = nullptr;
   if (near_id_flag && shift_rel == 0.0 && l <= kNearIdMax) {
     const size_t smem_n = sizeof(double) * 2 * (size_t)l * (((l + 15) & ~15) + 4);
-    // first-order shortcut when l |E|^2 <= 1e-17; TTK_NEAR_ID_FIRST_ORDER=0 disables it (A/B)
-    static const double fo = knob_env("TTK_NEAR_ID_FIRST_ORDER") ? atof(knob_env("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
+    // first-order shortcut when l |E|^2 <= kNearIdFirstOrderMax; TTK_NEAR_ID_FIRST_ORDER=0 disables it (A/B)
+    static const double fo = knob_env("TTK_NEAR_ID_FIRST_ORDER") ? atof(knob_env("TTK_NEAR_ID_FIRST_ORDER"))
+                                                                   : kNearIdFirstOrderMax;
     chol_near_identity_kernel<<<1, 1024, smem_n, st>>>(l, G, R, Rinv, near_id_flag, 1e-7, fo);
     TTK_CHECK_LAUNCH();
     skip = near_id_flag;
@@ -3165,6 +3175,49 @@ __device__ __forceinline__ void fq_reduce(const double* part, int nparts, int ll
   }
 }
 
+// The second Gram's reduction also emits the first-order second factor
+// elementwise -- R2^{-1} = I - F1 into I2 (and R2 = I + F1 when R is wanted),
+// F1 = triu(E) - diag(E)/2, E = G2 - I -- and max |E| into emax_bits (atomicMax
+// on the bit pattern of a nonnegative double): in the common case (l |E|^2
+// small, see kNearIdFirstOrderMax) CTA 0 has nothing left to factor.
+__device__ __forceinline__ void fq_reduce_nearid(const double* part, int nparts, int l, double* G, double* I2,
+                                                 double* R2, unsigned long long* emax_bits) {
+  const int ll = l * l;
+  const int lane8 = threadIdx.x & 7;
+  const int nthr = (gridDim.x - 1) * (blockDim.x >> 3);
+  const int ebase = (blockIdx.x - 1) * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  const int iters = (ll + nthr - 1) / nthr;
+  double em = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    const int e = ebase + it * nthr;
+    double s = 0.0;
+    if (e < ll) {
+      double v[16];
+      for (int p0 = lane8; p0 < nparts; p0 += 8 * 16) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int pp = p0 + 8 * u;
+          v[u] = pp < nparts ? __ldcg(part + (size_t)pp * ll + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += v[u];
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (lane8 == 0 && e < ll) {
+      const int r = e / l, c = e - r * l;
+      const double f = (c > r) ? s : (c == r ? 0.5 * (s - 1.0) : 0.0);
+      G[e] = s;
+      I2[e] = (c > r) ? -f : (c == r ? 1.0 - f : 0.0);
+      if (R2) R2[e] = (c > r) ? f : (c == r ? 1.0 + f : 0.0);
+      em = fmax(em, fabs(s - (r == c ? 1.0 : 0.0)));
+    }
+  }
+  if (lane8 == 0 && em > 0.0) atomicMax(emax_bits, (unsigned long long)__double_as_longlong(em));
+}
+
 __device__ __forceinline__ void fq_mark(int i) {
   if (g_fq_prof && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
@@ -3267,15 +3320,22 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
   }
   grid.sync();
   fq_mark(4);
-  if (!fac) fq_reduce(P.part, nparts, ll, P.G);
+  unsigned long long* emax_bits = reinterpret_cast<unsigned long long*>(P.status + 6);
+  if (!fac) fq_reduce_nearid(P.part, nparts, l, P.G, P.I2, P.R ? P.R2 : nullptr, emax_bits);
   grid.sync();
   fq_mark(5);
-  if (fac) {
+  // every CTA reads the same max |E| after the barrier: a uniform branch
+  const double emax = __longlong_as_double((long long)*(volatile unsigned long long*)emax_bits);
+  const bool first_order = (double)l * emax * emax <= P.first_order_max;
+  if (!first_order && fac) {
+    // second-order series or, beyond 1e-7, a full Cholesky of G2 (rare)
     chol_near_identity_body(l, P.G, P.R2, P.I2, P.status + 4, 1e-7, P.first_order_max, fsm);
     __syncthreads();
     if (!*(volatile int*)(P.status + 4))
       chol_blocked_body(l, P.G, P.R2, P.I2, P.status + 1, 1, 0.0, 1e-28, fsm);
     __syncthreads();
+  }
+  if (fac) {
     if (P.R) {  // R = R2 R1
       double* a = fsm;
       double* b = fsm + (size_t)l * ld;
@@ -3287,7 +3347,7 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
       block_dmma(l, l, l, a, ld, 1, b, ld, 1, P.R, l);
     }
   }
-  grid.sync();
+  if (!first_order) grid.sync();  // the Q phase reads the I2 CTA 0 just wrote
   fq_mark(6);
   if (!fac) {
     // Q tile = Q1 tile R2^{-1}
@@ -3430,7 +3490,8 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
       TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel<0>, 220 * 1024));
       TTK_TRY(qr_set_smem((const void*)cholqr2_fused_kernel<80>, 220 * 1024));
     }
-    static const double fo = knob_env("TTK_NEAR_ID_FIRST_ORDER") ? atof(knob_env("TTK_NEAR_ID_FIRST_ORDER")) : 1e-17;
+    static const double fo = knob_env("TTK_NEAR_ID_FIRST_ORDER") ? atof(knob_env("TTK_NEAR_ID_FIRST_ORDER"))
+                                                                   : kNearIdFirstOrderMax;
     TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 8 * sizeof(int), st));
     FqParams fp{};
     fp.m = m; fp.l = l; fp.Y = Y; fp.y_rs = y_rs; fp.y_cs = y_cs; fp.Q = Q; fp.q_rs = q_rs; fp.R = R;
