@@ -284,6 +284,9 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
 /* diagnostics: cores truncated so far through the Gram path [0] and the QR path [1], and
  * truncations redone through the QR path after a failed Gram certificate [2] */
 int ttk_debug_truncate_paths(long long* counts);
+/* the same plus [3] cores factored by the gap-certified subspace kernel and [4] truncations
+ * redone through the Jacobi Gram path after a failed subspace certificate; writes min(n, 5) */
+int ttk_debug_truncate_paths_ex(long long* counts, int n);
 size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks);
 
 #ifdef __cplusplus

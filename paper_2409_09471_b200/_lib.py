@@ -165,6 +165,7 @@ SIGNATURES.update({
 
 SIGNATURES.update({
     "ttk_debug_truncate_paths": (c_int, [c_vp]),
+    "ttk_debug_truncate_paths_ex": (c_int, [c_vp, c_int]),
     "ttk_tt_truncate": (c_int, [c_int, P_int, P_int, P_vp, c_double, c_int, P_vp, P_int, c_vp, c_size, c_vp]),
     "ttk_tt_truncate_host": (c_int, [c_int, P_int, P_int, P_vp, c_double, c_int, P_vp, P_int, P_vp, c_vp, c_size,
                                      c_vp]),

@@ -2721,7 +2721,70 @@ __device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, 
 }
 
 
-__device__ __forceinline__ int cb_ld(int l) { return ((l + 15) & ~15) + 4; }
+__host__ __device__ __forceinline__ int cb_ld(int l) { return ((l + 15) & ~15) + 4; }
+
+// Blocked right-looking Cholesky core on an l x l SPD matrix already in shared
+// memory (row stride ld = cb_ld(l)): on return the upper triangle of A holds R
+// (A = R^T R); the strict lower triangle is left unspecified.  *bad |= 1 on a
+// pivot <= tiny.  All threads of the CTA (a multiple of 32, >= 32); ph: optional
+// per-phase clock sink of thread 0 (chol_blocked_kernel diagnostics).
+__device__ void chol_blocked_core(int l, double* __restrict__ A, int ld, double tiny, int* bad, long long* ph,
+                                  long long& t0) {
+  __shared__ double invd[kCholMaxCols + 16];
+  __shared__ double rowb[2][16];  // pivot-row broadcast of the diagonal-block factorisation
+  const int tid = threadIdx.x, nt = blockDim.x, w = tid >> 5, lane = tid & 31;
+  const int nb = (l + 15) >> 4;
+  for (int kb = 0; kb < nb; ++kb) {
+    const int j0 = kb * 16, bs = min(16, l - j0);
+    if (w == 0) {
+      // diagonal block: lane c (< 16) owns column c (rows 0..15 of the block)
+      const int c = lane & 15;
+      double d[16];
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr)
+        d[rr] = (rr < bs && c < bs) ? A[(j0 + rr) * ld + j0 + c] : (rr == c ? 1.0 : 0.0);
+      int badd = 0;
+      cb_diag_steps<0>(d, c, lane, bs, tiny, badd, invd + j0, rowb);
+      if (lane < 16) {
+#pragma unroll
+        for (int rr = 0; rr < 16; ++rr)
+          if (rr < bs && c < bs) A[(j0 + rr) * ld + j0 + c] = (rr <= c) ? d[rr] : 0.0;
+      }
+      if (badd && lane == 0) atomicOr(bad, 1);
+    }
+    __syncthreads();
+    if (ph) { long long t = clock64(); ph[1] += t - t0; t0 = t; }
+    // panel: R_kJ = R_kk^{-T} A_kJ, one thread per column
+    for (int c = j0 + bs + tid; c < l; c += nt) {
+      double x[16];
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) x[jj] = (jj < bs) ? A[(j0 + jj) * ld + c] : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) {
+        if (jj < bs) {
+          x[jj] *= invd[j0 + jj];
+#pragma unroll
+          for (int kk = jj + 1; kk < 16; ++kk)
+            if (kk < bs) x[kk] -= A[(j0 + jj) * ld + j0 + kk] * x[jj];
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj)
+        if (jj < bs) A[(j0 + jj) * ld + c] = x[jj];
+    }
+    __syncthreads();
+    if (ph) { long long t = clock64(); ph[2] += t - t0; t0 = t; }
+    // trailing update (full square; only the upper triangle is used later)
+    const int rest = l - j0 - bs;
+    if (rest > 0) {
+      const double* P = A + (size_t)j0 * ld + j0 + bs;  // bs x rest panel
+      block_dmma(rest, rest, bs, P, 1, ld, P, ld, 1, A + (size_t)(j0 + bs) * ld + j0 + bs, ld, nullptr,
+                 nullptr, nullptr, true);
+    }
+    __syncthreads();
+    if (ph) { long long t = clock64(); ph[3] += t - t0; t0 = t; }
+  }
+}
 
 // body shared by chol_blocked_kernel and the fused CholeskyQR2 kernel (block
 // size kCbThreads; sm: 2 l cb_ld(l) + 256 ceil(l/16) doubles)
@@ -2732,8 +2795,6 @@ __device__ void chol_blocked_body(int l, const double* __restrict__ G, double* _
   double* A = sm;                       // l x ld
   double* X = A + (size_t)l * ld;       // l x ld (inverse)
   double* Tb = X + (size_t)l * ld;      // 256 * nb
-  __shared__ double invd[kCholMaxCols + 16];
-  __shared__ double rowb[2][16];  // pivot-row broadcast of the diagonal-block factorisation
   __shared__ double gmax_s, tr_s;
   __shared__ int bad;
   const int tid = threadIdx.x, nt = blockDim.x, w = tid >> 5, lane = tid & 31;
@@ -2766,57 +2827,7 @@ __device__ void chol_blocked_body(int l, const double* __restrict__ G, double* _
   __syncthreads();
   const double tiny = gmax_s * tiny_rel + 1e-300;
   if (prof) { long long t = clock64(); ph[0] += t - t0; t0 = t; }
-  const int nb = (l + 15) >> 4;
-  for (int kb = 0; kb < nb; ++kb) {
-    const int j0 = kb * 16, bs = min(16, l - j0);
-    if (w == 0) {
-      // diagonal block: lane c (< 16) owns column c (rows 0..15 of the block)
-      const int c = lane & 15;
-      double d[16];
-#pragma unroll
-      for (int rr = 0; rr < 16; ++rr)
-        d[rr] = (rr < bs && c < bs) ? A[(j0 + rr) * ld + j0 + c] : (rr == c ? 1.0 : 0.0);
-      int badd = 0;
-      cb_diag_steps<0>(d, c, lane, bs, tiny, badd, invd + j0, rowb);
-      if (lane < 16) {
-#pragma unroll
-        for (int rr = 0; rr < 16; ++rr)
-          if (rr < bs && c < bs) A[(j0 + rr) * ld + j0 + c] = (rr <= c) ? d[rr] : 0.0;
-      }
-      if (badd && lane == 0) atomicOr(&bad, 1);
-    }
-    __syncthreads();
-    if (prof) { long long t = clock64(); ph[1] += t - t0; t0 = t; }
-    // panel: R_kJ = R_kk^{-T} A_kJ, one thread per column
-    for (int c = j0 + bs + tid; c < l; c += nt) {
-      double x[16];
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) x[jj] = (jj < bs) ? A[(j0 + jj) * ld + c] : 0.0;
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        if (jj < bs) {
-          x[jj] *= invd[j0 + jj];
-#pragma unroll
-          for (int kk = jj + 1; kk < 16; ++kk)
-            if (kk < bs) x[kk] -= A[(j0 + jj) * ld + j0 + kk] * x[jj];
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj)
-        if (jj < bs) A[(j0 + jj) * ld + c] = x[jj];
-    }
-    __syncthreads();
-    if (prof) { long long t = clock64(); ph[2] += t - t0; t0 = t; }
-    // trailing update (full square; only the upper triangle is used later)
-    const int rest = l - j0 - bs;
-    if (rest > 0) {
-      const double* P = A + (size_t)j0 * ld + j0 + bs;  // bs x rest panel
-      block_dmma(rest, rest, bs, P, 1, ld, P, ld, 1, A + (size_t)(j0 + bs) * ld + j0 + bs, ld, nullptr,
-                 nullptr, nullptr, true);
-    }
-    __syncthreads();
-    if (prof) { long long t = clock64(); ph[3] += t - t0; t0 = t; }
-  }
+  chol_blocked_core(l, A, ld, tiny, &bad, prof ? ph : nullptr, t0);
   for (int e = tid; e < l * l; e += nt) {
     const int r = e / l, c = e - r * l;
     Rout[e] = (c >= r) ? A[r * ld + c] : 0.0;
@@ -2879,6 +2890,207 @@ int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status
     const size_t smem = sizeof(double) * (2 * (size_t)l * (l + 1) + 256 * (size_t)((l + 15) / 16));
     chol_inv_kernel<<<1, 1024, smem, st>>>(l, G, R, Rinv, status, check_identity, shift_rel, tiny_rel, skip);
   }
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
+// --------------------------------------------------------------------------
+// Gap-certified dominant-subspace factor for the exact-rank truncation.
+//
+// The truncation of core k (round.cu, Gram path) needs, for G = C C^T
+// (l x l, C the r0 x m unfolding), a left factor F (l x r) and the map M
+// (r x l) with Y = M C the new core: rows of Y orthonormal, F = C Y^T, so
+// that F Y = C P_Y is C projected onto the row space of Y.  The reference
+// (tt.py:358-367, np.linalg.svd) takes Y = V_r^T; any Y spanning the same
+// dominant row space gives the same rounded tensor (the cores differ by a
+// gauge).  When sigma_r / sigma_{r+1} is large -- the usual
+// regime of a rounding that discards noise; config 3 has 41..440 -- that
+// space is found with a few products instead of ~630 Jacobi rotation rounds:
+//   Q0 = orth(G[:, J])                J: the r largest diagonal entries
+//   repeat: Q = orth(G^2 Q)           (tail damped by (lambda_{r+1}/lambda_r)^2)
+//   B = Q^T G Q = R^T R,  M^T = Q R^{-1},  F = (G Q) R^{-1} = G M^T
+// so Y = M C has Y Y^T = R^{-T} B R^{-1} = I exactly (to the Cholesky's
+// rounding, kappa(B) = lambda_1 / lambda_r), whatever the accuracy of Q.
+// orth() is CholeskyQR on the DMMA pipe; every matrix lives in shared memory
+// of one CTA.  Certificate (flag = 1), else the caller redoes the sweep with
+// the Jacobi SVD: all Cholesky factorisations succeed; the tail
+// tau = tr(G) - tr(B) >= sum_{i>r} lambda_i is below half of the lower bound
+// lmin = 1 / ||R^{-1}||_F^2 <= lambda_min(B) (a clear gap); the Davis-Kahan
+// bound on the right-subspace angle, ||G Q - Q B||_F / (lmin - tau) *
+// sqrt(tau / lmin), is <= 1e-9 (the refinement repeats while it exceeds 1e-12,
+// at most kTsMaxIters times); and lmin >= 2e-6 ||B||_F (the Gram squares the
+// condition number, as for gram_cert_kernel).
+constexpr int kTsMaxL = 80, kTsMaxR = 64, kTsThreads = 512, kTsMaxIters = 3;
+
+__device__ __forceinline__ double ts_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];  // same order in every thread
+  return s;
+}
+
+// Cholesky of the r x r A (ld) in place and X = R^{-1} (ld); false on a tiny pivot
+__device__ bool ts_chol_inv(int r, double* A, double* X, double* Tb, int ld, int* bad, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double g = 0.0;
+  for (int i = tid; i < r; i += nt) g = fmax(g, A[i * ld + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = g;
+  if (tid == 0) *bad = 0;
+  __syncthreads();
+  double gm = 0.0;
+  for (int i = 0; i < (nt >> 5); ++i) gm = fmax(gm, red[i]);
+  long long t0 = 0;
+  chol_blocked_core(r, A, ld, gm * 1e-15 + 1e-300, bad, nullptr, t0);
+  for (int e = tid; e < r * ld; e += nt) {
+    const int i = e / ld, c = e - i * ld;
+    if (c < i) A[e] = 0.0;
+  }
+  __syncthreads();
+  const bool ok = (*bad == 0);
+  tri_inv_blocked(A, X, Tb, ld, r);
+  __syncthreads();
+  return ok;
+}
+
+__global__ void __launch_bounds__(kTsThreads, 1)
+    trunc_subspace_kernel(int l, int r, const double* __restrict__ G, double* __restrict__ F,
+                          double* __restrict__ Mt, int ldo, int* __restrict__ flag, double* __restrict__ info) {
+  extern __shared__ double sm[];
+  const int ldg = cb_ld(l), ldq = cb_ld(r);
+  double* Gs = sm;                                  // l x ldg
+  double* p[3] = {Gs + (size_t)l * ldg, Gs + (size_t)l * ldg + (size_t)l * ldq,
+                  Gs + (size_t)l * ldg + 2 * (size_t)l * ldq};  // l x ldq each
+  double* A = p[2] + (size_t)l * ldq;               // r x ldq
+  double* Tb = A + (size_t)r * ldq;                 // 256 * ceil(r/16)
+  __shared__ double red[32];
+  __shared__ int J[kTsMaxL];
+  __shared__ int bad;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double trg = 0.0;
+  for_each_l2<16>(G, l * l, [&](int e, double v) {
+    const int i = e / l, c = e - i * l;
+    Gs[i * ldg + c] = v;
+    if (i == c) trg += v;
+  });
+  trg = ts_block_sum(trg, red);  // (contains the barrier after the load)
+  // J: indices of the r largest diagonal entries (ties by index)
+  for (int i = tid; i < l; i += nt) {
+    const double di = Gs[i * ldg + i];
+    int rank = 0;
+    for (int j = 0; j < l; ++j) {
+      const double dj = Gs[j * ldg + j];
+      rank += (dj > di || (dj == di && j < i)) ? 1 : 0;
+    }
+    if (rank < r) J[rank] = i;
+  }
+  __syncthreads();
+  bool ok = true;
+  if (r < l) {
+    for (int e = tid; e < l * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      p[0][i * ldq + c] = Gs[i * ldg + J[c]];
+    }
+    __syncthreads();
+    // Q0 = orth(G[:, J]) -> p[1]; G Q0 -> p[0]
+    block_dmma(r, r, l, p[0], 1, ldq, p[0], ldq, 1, A, ldq);
+    __syncthreads();
+    ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red) && ok;
+    block_dmma(l, r, r, p[0], ldq, 1, p[2], ldq, 1, p[1], ldq);
+    __syncthreads();
+    block_dmma(l, r, l, Gs, ldg, 1, p[1], ldq, 1, p[0], ldq);
+    __syncthreads();
+  }
+  double bv = 0.0, taur = 0.0;
+  int it = 0;
+  for (;; ++it) {
+    if (r < l) {
+      // gq = p[0]: Z = G gq -> p[1]; Q = orth(Z) -> p[0]
+      block_dmma(l, r, l, Gs, ldg, 1, p[0], ldq, 1, p[1], ldq);
+      __syncthreads();
+      block_dmma(r, r, l, p[1], 1, ldq, p[1], ldq, 1, A, ldq);
+      __syncthreads();
+      ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red) && ok;
+      block_dmma(l, r, r, p[1], ldq, 1, p[2], ldq, 1, p[0], ldq);
+    } else {
+      // nothing is truncated: Q = I, B = G (only the gauge Y = R^{-T} C is computed)
+      for (int e = tid; e < l * ldq; e += nt) p[0][e] = (e / ldq == e % ldq) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    // gq = G Q -> p[1]; B = Q^T gq -> A; residual gq - Q B -> p[2]
+    block_dmma(l, r, l, Gs, ldg, 1, p[0], ldq, 1, p[1], ldq);
+    __syncthreads();
+    block_dmma(r, r, l, p[0], 1, ldq, p[1], ldq, 1, A, ldq);
+    for (int e = tid; e < l * ldq; e += nt) p[2][e] = p[1][e];
+    __syncthreads();
+    block_dmma(l, r, r, p[0], ldq, 1, A, ldq, 1, p[2], ldq, nullptr, nullptr, nullptr, true);
+    double trb = 0.0, bf = 0.0, rs = 0.0;
+    for (int e = tid; e < r * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      const double v = A[i * ldq + c];
+      bf += v * v;
+      if (i == c) trb += v;
+    }
+    __syncthreads();
+    for (int e = tid; e < l * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      const double v = p[2][i * ldq + c];
+      rs += v * v;
+    }
+    trb = ts_block_sum(trb, red);
+    bf = ts_block_sum(bf, red);
+    rs = ts_block_sum(rs, red);
+    ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red) && ok;
+    double xf = 0.0;
+    for (int e = tid; e < r * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      const double v = p[2][i * ldq + c];
+      xf += v * v;
+    }
+    xf = ts_block_sum(xf, red);
+    const double lmin = 1.0 / xf;
+    const double tau = fmax(trg - trb, 0.0) + 1e-12 * trg;
+    const double gap = lmin - tau;
+    bv = (gap > 0.0) ? sqrt(rs) / gap * sqrt(tau / lmin) : INFINITY;
+    taur = tau / lmin;
+    ok = ok && gap > 0.5 * lmin && lmin >= 2e-6 * sqrt(bf);
+    if (!ok || bv <= 1e-12 || it + 1 >= kTsMaxIters) break;
+    // continue from gq: swap so that gq sits in p[0]
+    double* t = p[0];
+    p[0] = p[1];
+    p[1] = t;
+  }
+  ok = ok && bv <= 1e-9;
+  if (tid == 0) {
+    *flag = ok ? 1 : 0;
+    if (info) { info[0] = bv; info[1] = taur; info[2] = it + 1; }
+  }
+  if (!ok) return;
+  // M^T = Q R^{-1}, F = (G Q) R^{-1}  (global, row stride ldo)
+  block_dmma(l, r, r, p[0], ldq, 1, p[2], ldq, 1, Mt, ldo);
+  block_dmma(l, r, r, p[1], ldq, 1, p[2], ldq, 1, F, ldo);
+}
+
+size_t trunc_subspace_smem(int l, int r) {
+  return sizeof(double) * ((size_t)l * cb_ld(l) + 3 * (size_t)l * cb_ld(r) + (size_t)r * cb_ld(r) +
+                           256 * (size_t)((r + 15) / 16));
+}
+
+bool trunc_subspace_fits(int l, int r) {
+  return l >= 2 && r >= 1 && r <= l && l <= kTsMaxL && r <= kTsMaxR && trunc_subspace_smem(l, r) <= 227 * 1024;
+}
+
+int launch_trunc_subspace(int l, int r, const double* G, double* F, double* Mt, int ldo, int* flag, double* info,
+                          cudaStream_t st) {
+  TTK_REQUIRE(trunc_subspace_fits(l, r), kInvalidValue, "trunc_subspace: l=%d r=%d outside the kernel", l, r);
+  TTK_TRY(qr_set_smem((const void*)trunc_subspace_kernel, (int)trunc_subspace_smem(kTsMaxL, kTsMaxR)));
+  trunc_subspace_kernel<<<1, kTsThreads, trunc_subspace_smem(l, r), st>>>(l, r, G, F, Mt, ldo, flag, info);
   TTK_CHECK_LAUNCH();
   return kOk;
 }

@@ -71,6 +71,12 @@ int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status
                     double shift_rel, double tiny_rel, cudaStream_t st, int* near_id_flag);
 constexpr int kCholBlockedMaxCols = 112;
 
+// gap-certified dominant-subspace factor of the exact-rank truncation (qr.cu):
+// F (l x r) and M^T (l x r), row stride ldo; *flag = 1 when certified
+bool trunc_subspace_fits(int l, int r);
+int launch_trunc_subspace(int l, int r, const double* G, double* F, double* Mt, int ldo, int* flag, double* info,
+                          cudaStream_t st);
+
 // r = max(1, first index with sqrt(sum_{i>=r} S_i^2) <= budget) capped by
 // max_rank (<= 0: no cap) and by n; reference _truncation_rank (tt.py:203-211).
 int truncation_rank_dev(const double* S, int n, double budget, int max_rank, int* r_dev,

@@ -14,6 +14,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <unordered_map>
 #include <vector>
 
 namespace ttk {
@@ -89,6 +90,24 @@ thread_local PinnedScratch g_pinned;
 
 // cores truncated by the Gram path / by the QR path (ttk_debug_truncate_paths)
 std::atomic<long long> g_trunc_gram{0}, g_trunc_qr{0}, g_trunc_redo{0};
+// cores factored by the gap-certified subspace kernel, and sweeps of it redone
+// through the Jacobi Gram path after a failed certificate
+std::atomic<long long> g_trunc_fast{0}, g_trunc_fast_redo{0};
+
+// Shapes whose subspace sweep failed its certificate skip the subspace kernel
+// for the next kFastSkip truncations of the same shape (a gap-free spectrum,
+// e.g. config 2, would otherwise pay a wasted sweep on every call).
+constexpr int kFastSkip = 16;
+uint64_t trunc_shape_key(int d, const int* dims, const int* ranks, int max_rank) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
+  mix((uint64_t)d);
+  mix((uint64_t)(uint32_t)max_rank);
+  for (int k = 0; k < d; ++k) mix((uint64_t)dims[k]);
+  for (int k = 0; k <= d; ++k) mix((uint64_t)ranks[k]);
+  return h;
+}
+thread_local std::unordered_map<uint64_t, int> g_fast_skip;
 
 size_t core_elems(const int* dims, const int* ranks, int k) {
   return (size_t)ranks[k] * dims[k] * ranks[k + 1];
@@ -300,7 +319,9 @@ size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks) {
 
 static int truncate_impl(int d, const int* dims, const int* ranks, const double* const* cores, double rel_tol,
                          int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
-                         size_t ws_bytes, cudaStream_t st, bool allow_gram) {
+                         size_t ws_bytes, cudaStream_t st, int mode) {
+  // mode 2: Gram path with the gap-certified subspace kernel where it fits,
+  // 1: Gram path with the Jacobi SVD, 0: QR path only
   TTK_REQUIRE(d >= 1 && rel_tol >= 0.0, kInvalidValue, "tt_truncate: bad arguments");
   for (int k = 0; k <= d; ++k) out_ranks[k] = ranks[k];
   if (d == 1) {
@@ -388,8 +409,17 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
   // no host round trip per core and the certificates are checked once at the
   // end; if any failed (e.g. an exactly rank-deficient unfolding) the whole
   // truncation is redone through the QR path.
-  const bool gram_on = allow_gram && rel_tol == 0.0 && knob_env("TTK_TRUNC_NO_GRAM") == nullptr;
-  int ngram = 0;
+  const bool gram_on = mode >= 1 && rel_tol == 0.0 && knob_env("TTK_TRUNC_NO_GRAM") == nullptr;
+  const uint64_t skey = trunc_shape_key(d, dims, ranks, max_rank);
+  bool fast_on = gram_on && mode >= 2 && knob_env("TTK_TRUNC_NO_FAST") == nullptr;
+  if (fast_on) {
+    auto it = g_fast_skip.find(skey);
+    if (it != g_fast_skip.end() && it->second > 0) {
+      --it->second;
+      fast_on = false;
+    }
+  }
+  int ngram = 0, nfast = 0;
   for (int k = d - 1; k >= 1; --k) {
     const int r0 = r[k], n = dims[k], r1 = r[k + 1];
     const int m = n * r1, kk = std::min(m, r0);
@@ -400,17 +430,25 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
     if (gram_on && m >= r0 && r0 >= 2 && r0 <= kCholBlockedMaxCols && jacobi_fits_v(r0, r0)) {
       // G = C C^T (r0 x r0), C = cur (r0 x m, row-major)
       TTK_TRY(gemm1(r0, r0, m, cur, m, 1, cur, 1, m, tG, r0, 1, split_ws, st));
-      TTK_CHECK_CUDA(cudaMemsetAsync(rdev + 2, 0, sizeof(int), st));
-      TTK_TRY(launch_chol_inv(r0, tG, tR, nullptr, rdev + 2, 0, 0.0, 1e-15, st, nullptr));
-      TTK_TRY(jacobi_svd_ex(r0, r0, tR, 1, r0, tL, tS, nullptr, true, st));  // W and S only
       const int rk = std::min(max_rank > 0 ? max_rank : r0, r0);
-      gram_cert_kernel<<<1, 32, 0, st>>>(tS, rk, rdev + 2, gflags + ngram);
-      TTK_CHECK_LAUNCH();
-      ++ngram;
-      {
-        // core k <- T1^T C, T1 = W_r S_r^{-2} (side stream); L = W_r
+      if (fast_on && trunc_subspace_fits(r0, rk)) {
+        // F = C Y^T -> tL, M^T -> tU (Y = M C), certificate -> gflags
+        TTK_TRY(launch_trunc_subspace(r0, rk, tG, tL, tU, r0, gflags + ngram, nullptr, st));
+        ++ngram;
+        ++nfast;
+      } else {
+        TTK_CHECK_CUDA(cudaMemsetAsync(rdev + 2, 0, sizeof(int), st));
+        TTK_TRY(launch_chol_inv(r0, tG, tR, nullptr, rdev + 2, 0, 0.0, 1e-15, st, nullptr));
+        TTK_TRY(jacobi_svd_ex(r0, r0, tR, 1, r0, tL, tS, nullptr, true, st));  // W and S only
+        gram_cert_kernel<<<1, 32, 0, st>>>(tS, rk, rdev + 2, gflags + ngram);
+        TTK_CHECK_LAUNCH();
+        ++ngram;
+        // T1 = W_r S_r^{-2}; L = W_r
         scale_cols_inv_sq_kernel<<<ceil_div((long)r0 * rk, 256), 256, 0, st>>>(r0, rk, tL, r0, tS, tU);
         TTK_CHECK_LAUNCH();
+      }
+      {
+        // core k <- T1^T C (side stream); C_{k-1} <- C_{k-1} L
         TTK_CHECK_CUDA(cudaEventRecord(ev_f[k & 1], st));
         TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_f[k & 1], 0));
         TTK_TRY(gemm1(m, rk, r0, cur, 1, m, tU, r0, 1, out[k], 1, m, split_side, side));
@@ -432,7 +470,6 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
         TTK_TRY(gemm1(p0 * pn, rk, r0, cores[k - 1], r0, 1, tL, r0, 1, dst, rk, 1, split_ws, st));
         cur = dst;
         r[k] = rk;
-        g_trunc_gram.fetch_add(1, std::memory_order_relaxed);
         continue;
       }
     }
@@ -498,10 +535,18 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
   TTK_SYNC(st);
   for (int i = 0; i < ngram; ++i)
     if (hflags[i] != 1) {
+      if (nfast > 0) {  // redo with the Jacobi SVD on every core; skip the subspace kernel for a while
+        g_trunc_fast_redo.fetch_add(1, std::memory_order_relaxed);
+        g_fast_skip[skey] = kFastSkip;
+        return truncate_impl(d, dims, ranks, cores, rel_tol, max_rank, out, out_ranks, host_out, ws, ws_bytes,
+                             st, 1);
+      }
       g_trunc_redo.fetch_add(1, std::memory_order_relaxed);
       return truncate_impl(d, dims, ranks, cores, rel_tol, max_rank, out, out_ranks, host_out, ws, ws_bytes, st,
-                           false);
+                           0);
     }
+  g_trunc_gram.fetch_add(ngram - nfast, std::memory_order_relaxed);
+  g_trunc_fast.fetch_add(nfast, std::memory_order_relaxed);
   for (int k = 0; k <= d; ++k) out_ranks[k] = r[k];
   return kOk;
 }
@@ -510,13 +555,20 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
                          int max_rank, double* const* out, int* out_ranks, double* const* host_out, void* ws,
                          size_t ws_bytes, void* stream) {
   return truncate_impl(d, dims, ranks, cores, rel_tol, max_rank, out, out_ranks, host_out, ws, ws_bytes,
-                       (cudaStream_t)stream, true);
+                       (cudaStream_t)stream, 2);
 }
 
 int ttk_debug_truncate_paths(long long* counts) {
   counts[0] = g_trunc_gram.load();
   counts[1] = g_trunc_qr.load();
   counts[2] = g_trunc_redo.load();
+  return kOk;
+}
+
+int ttk_debug_truncate_paths_ex(long long* counts, int n) {
+  const long long v[5] = {g_trunc_gram.load(), g_trunc_qr.load(), g_trunc_redo.load(), g_trunc_fast.load(),
+                          g_trunc_fast_redo.load()};
+  for (int i = 0; i < n && i < 5; ++i) counts[i] = v[i];
   return kOk;
 }
 

@@ -38,15 +38,26 @@ def _probe(x):
 def test_config3_full_size_vs_oracle(cuda):
     """The headline step at full size, device-resident and through the host
     pipeline, against oracle.matvec + oracle.rto_round on the same seeded inputs."""
+    import ctypes
+    from paper_2409_09471_b200 import _lib
     C = configs.config3()
     spec = T.RoundSpec(C["rel_tol"], C["max_rank"])
     drm = [torch.as_tensor(g, device=cuda) for g in C["drm"]]
+    c0 = (ctypes.c_longlong * 5)()
+    _lib.load().ttk_debug_truncate_paths_ex(ctypes.addressof(c0), 5)
     got = T.tt_matvec_round_rto(T.TTOperator(C["op"], device=cuda), T.TTVector(C["x"], device=cuda), spec, drm,
                                 device=cuda)
     y = O.matvec(C["op"], C["x"])
     want = O.rto_round(y, C["drm"], C["rel_tol"], C["max_rank"])
     assert list(got.ranks) == [1] + [c.shape[2] for c in want] == [1] + [64] * 31 + [1]
     assert O.rel_diff([c.cpu().numpy() for c in got.cores], want) <= 1e-10
+    # every core went through the gap-certified subspace kernel (sigma_64 / sigma_65 = 41..440)
+    c1 = (ctypes.c_longlong * 5)()
+    _lib.load().ttk_debug_truncate_paths_ex(ctypes.addressof(c1), 5)
+    assert (c1[3] - c0[3], c1[4] - c0[4], c1[0] - c0[0]) == (31, 0, 0)
+    for c in got.cores[1:]:  # right-orthonormal, as the reference's SVD leaves them
+        u = c.cpu().numpy().reshape(c.shape[0], -1)
+        assert np.abs(u @ u.T - np.eye(u.shape[0])).max() <= 1e-12
     # host (pinned) cores in and out: same kernels, bit-identical result
     host = T.tt_matvec_round_rto(T.TTOperator([torch.as_tensor(g).pin_memory() for g in C["op"]]),
                                  T.TTVector([torch.as_tensor(c).pin_memory() for c in C["x"]]), spec, drm,

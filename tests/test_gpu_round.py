@@ -500,6 +500,64 @@ def test_truncate_gram_path_certified(cuda):
         assert np.abs(u @ u.T - np.eye(u.shape[0])).max() <= 1e-12
 
 
+def _trunc_paths_ex():
+    import ctypes
+    from paper_2409_09471_b200 import _lib
+    c = (ctypes.c_longlong * 5)()
+    _lib.load().ttk_debug_truncate_paths_ex(ctypes.addressof(c), 5)
+    return np.array(list(c))
+
+
+def _gapped_left_orth(dims, r, s, eps, seed):
+    """Left-orthogonal TT (RTO output with exact range) whose unfoldings have a
+    gap ~1/eps after the first r singular values: A + eps B, rank r + s."""
+    a = O.tt_random(dims, [r] * (len(dims) - 1), seed=seed)
+    b = O.tt_random(dims, [s] * (len(dims) - 1), seed=seed + 1)
+    x = O.add(a, O.scale(b, eps))
+    return O.rto_sweeps(x, O.drm_new(dims, [r + s] * (len(dims) - 1), seed=seed + 2))
+
+
+@pytest.mark.parametrize("r,s,eps", [(6, 4, 1e-3), (20, 12, 1e-2), (64, 16, 1e-2)])
+def test_truncate_subspace_path_gapped(cuda, r, s, eps):
+    """Exact-rank truncation of a TT with a clear gap at the cap: every core takes
+    the gap-certified subspace kernel (no Jacobi SVD), the rounded TT matches the
+    oracle's SVD truncation to 1e-12 with equal ranks and right-orthonormal cores."""
+    dims = [10, 12, 9, 11, 8, 10] if r < 64 else [24, 16, 20, 16]
+    lo = _gapped_left_orth(dims, r, s, eps, seed=11)
+    want = O.truncate_left_orth(lo, 0.0, r)
+    c0 = _trunc_paths_ex()
+    got = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(0.0, r))
+    d = _trunc_paths_ex() - c0
+    # cores with n_k r_k < r_{k-1} (a rank-deficient Gram) take the QR path
+    assert d[3] >= 2 and d[3] + d[1] == len(dims) - 1 and d[4] == 0 and d[0] == 0
+    assert got.ranks == tuple([1] + [c.shape[2] for c in want])
+    assert O.rel_diff(tt_np(got), want) <= 1e-12
+    for c in got.cores[1:]:
+        u = c.cpu().numpy().reshape(c.shape[0], -1)
+        assert np.abs(u @ u.T - np.eye(u.shape[0])).max() <= 1e-13
+
+
+def test_truncate_subspace_certificate_rejects_flat_spectrum(cuda):
+    """No gap at the cap: the subspace certificate fails, the sweep is redone with the
+    Jacobi SVD (same result as the oracle), and the next call of the same shape goes
+    straight to the Jacobi path."""
+    dims = [12, 9, 16, 7, 11, 13]
+    x = O.tt_random(dims, [8, 14, 10, 9, 6], seed=5)
+    lo = O.rto_sweeps(x, O.drm_new(dims, [8, 14, 10, 9, 6], seed=6))
+    want = O.truncate_left_orth(lo, 0.0, 6)
+    # a shape no other test uses, so the skip hint starts clean
+    c0 = _trunc_paths_ex()
+    got = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(0.0, 6))
+    d1 = _trunc_paths_ex() - c0
+    assert d1[4] == 1 and d1[0] == len(dims) - 1 and d1[2] == 0
+    assert O.rel_diff(tt_np(got), want) <= 1e-10
+    got2 = T.tt_truncate_left_orth(T.TTVector(lo, device=cuda), T.RoundSpec(0.0, 6))
+    d2 = _trunc_paths_ex() - c0 - d1
+    assert d2[4] == 0 and d2[3] == 0 and d2[0] == len(dims) - 1
+    for a, b in zip(got.cores, got2.cores):
+        assert torch.equal(a, b)
+
+
 def test_truncate_gram_path_falls_back_on_rank_deficiency(cuda):
     """rel_tol = 0 on a TT whose unfoldings are exactly rank deficient: the kept
     singular values include ~1e-16 ones, a certificate fails and the truncation
