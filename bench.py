@@ -495,8 +495,9 @@ def run_b200(args):
             g1.record(stream)
             torch.cuda.synchronize()
             return g0.elapsed_time(g1)
-        run(1)  # warm-up: per-stream workspaces, per-thread side streams
-        ms_all = run(steps)
+        with _lib.concurrent_problems():  # several problems in flight: cp.async GEMMs (DESIGN 6.2)
+            run(1)  # warm-up: per-stream workspaces, per-thread side streams
+            ms_all = run(steps)
         return {"problems_in_flight": n, "steps_each": steps, "value": flops * n * steps / (ms_all * 1e-3) / 1e9,
                 "unit": UNIT, "ms_per_problem_per_stream": ms_all / steps}
     inflight_res = None

@@ -176,6 +176,11 @@ int ttk_gemm_tma(int M, int N, int K, double alpha, const double* A, long long l
 int ttk_gemm_tma_strided(int M, int N, int K, double alpha, const double* A, long long a_ms, long long a_ks,
                          const double* B, long long b_ks, long long b_ns, double beta, double* C, long long c_ms,
                          long long c_ns, void* ws, size_t ws_bytes, void* stream);
+/* Process-wide switch of the TMA-staged GEMM inside the rounding sweeps (default 1); returns the
+ * previous setting.  Independent problems kept in flight on several streams must run with it off
+ * (the library also drops to the cp.async kernel while it sees two caller streams active within
+ * 0.5 s of each other); DESIGN.md 6.2. */
+int ttk_gemm_tma_enable(int on);
 /* diagnostics: subsequent Jacobi SVDs store their sweep count in *dev_counter (NULL: off) */
 int ttk_debug_svd_sweeps(int* dev_counter);
 /* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,
@@ -186,6 +191,11 @@ int ttk_debug_jacobi_profile(long long* dev_acc);
 /* diagnostics: one blocked Cholesky R^T R = G (l x l, device; status: device int) */
 int ttk_debug_chol(int l, const double* G, double* R, int* status, void* stream);
 int ttk_debug_chol_profile(long long* dev_acc);
+/* diagnostics: one gap-certified subspace factorisation (truncation, DESIGN 2.2) of the l x l Gram G
+ * for rank r: F, Mt (l x r, row stride l), flag (1 = certified), info[3] = {angle bound, tau / lmin,
+ * iterations}; prof[5] (or NULL) accumulates phase clocks */
+int ttk_debug_trunc_subspace(int l, int r, const double* G, double* F, double* Mt, int* flag, double* info,
+                             long long* prof, void* stream);
 /* diagnostics: phase timestamps (%globaltimer, ns) of the fused CholeskyQR2 kernel into dev_ts[16]; NULL = off */
 int ttk_debug_fused_qr_profile(long long* dev_ts);
 /* diagnostics: host synchronisation points (rank / path decisions) so far:

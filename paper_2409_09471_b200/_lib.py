@@ -187,3 +187,19 @@ SIGNATURES.update({"ttk_debug_chol": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp])})
 
 SIGNATURES.update({"ttk_qr_auto": (c_int, [c_int, c_int, c_vp, c_ll, c_ll, c_vp, c_ll, c_ll, c_vp, c_vp, c_size,
                                            c_vp])})
+SIGNATURES.update({"ttk_debug_trunc_subspace": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp])})
+SIGNATURES.update({"ttk_gemm_tma_enable": (c_int, [c_int])})
+
+
+class concurrent_problems:
+    """Context for callers that keep several independent problems in flight on
+    different CUDA streams: the sweeps use the cp.async grouped GEMM instead of
+    the TMA-staged one while it is active (ttk_gemm_tma_enable, DESIGN 6.2)."""
+
+    def __enter__(self):
+        self._prev = load().ttk_gemm_tma_enable(0)
+        return self
+
+    def __exit__(self, *exc):
+        load().ttk_gemm_tma_enable(self._prev)
+        return False

@@ -132,8 +132,10 @@ __global__ void __launch_bounds__(TmCfg<BM, BN, STAGES>::kThreads)
   if (warp == Cfg::kConsumers) {
     // ---- producer: one elected lane streams this slice's k tiles ----
     if (lane == 0) {
+#ifndef TTK_TMA_NO_PREFETCH
       asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
+#endif
       for (int it = 0; it < KT; ++it) {
         const int s = it % STAGES;
         if (it >= STAGES) tm_wait(smem_u32(&empty[s]), (uint32_t)(((it / STAGES) - 1) & 1));
@@ -326,7 +328,12 @@ int launch_tma(int M, int N, int K, double alpha, TmOperand A, TmOperand B, doub
   splits = (KT + per - 1) / per;
   TmParams p{M, N, K, per, alpha, beta, splits > 1 ? part : C, c_ms, c_ns, splits};
   dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, splits);
-  kern<<<grid, Cfg::kThreads, Cfg::SMEM, st>>>(ma, mb, p);
+  static const int pad = knob_env("TTK_TMA_SMEM_PAD") ? atoi(knob_env("TTK_TMA_SMEM_PAD")) : 0;  // A/B
+  if (pad > 0) {
+    static std::once_flag once;
+    std::call_once(once, [&] { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM + pad); });
+  }
+  kern<<<grid, Cfg::kThreads, Cfg::SMEM + pad, st>>>(ma, mb, p);
   TTK_CHECK_LAUNCH();
   if (splits > 1) {
     const long long mn = (long long)M * N;

@@ -2270,71 +2270,6 @@ constexpr int kCholMaxCols = 112;
 // one CTA: upper Cholesky G = R^T R of an l x l SPD matrix and R^{-1};
 // status |= 1 on a non-positive / tiny pivot, |= 2 if check_identity and
 // max|G - I| > 1e-3.
-// X = inv(A) for the upper-triangular l x l A (row stride ld) held in shared
-// memory; Tb: 256 * ceil(l/16) doubles of scratch.  All threads of the CTA.
-__device__ void tri_inv_blocked(const double* A, double* X, double* Tb, int ld, int l) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int ty = tid >> 5, tx = tid & 31, nty = nt >> 5;
-  // R^{-1} by blocks of 16: (1) every warp inverts one 16x16 diagonal block
-  // (forward over columns, 16 dependent steps), (2) off-diagonal blocks by
-  // block back-substitution X_IJ = -inv(R_II) sum_{I<K<=J} R_IK X_KJ, one
-  // block-diagonal distance at a time (all blocks of a distance in parallel).
-  {
-    const int nb = (l + 15) / 16;
-    for (int e = tid; e < l * l; e += nt) {
-      int r = e / l, c = e - r * l;
-      X[r * ld + c] = 0.0;
-    }
-    __syncthreads();
-    for (int bI = ty; bI < nb; bI += nty) {
-      const int o = bI * 16, bs = min(16, l - o);
-      // lane tx owns column tx of the block; solve R_II x = e_tx by back substitution
-      if (tx < bs) {
-        double xr[16];
-#pragma unroll
-        for (int i = 15; i >= 0; --i) {
-          if (i < bs) {
-            double acc = (i == tx) ? 1.0 : 0.0;
-#pragma unroll
-            for (int k = i + 1; k < 16; ++k)
-              if (k < bs) acc -= A[(o + i) * ld + o + k] * xr[k];
-            xr[i] = (i <= tx) ? acc / A[(o + i) * ld + o + i] : 0.0;
-          } else {
-            xr[i] = 0.0;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (i < bs) X[(o + i) * ld + o + tx] = xr[i];
-      }
-    }
-    __syncthreads();
-    for (int dist = 1; dist < nb; ++dist) {
-      const int nblk = nb - dist;
-      for (int e = tid; e < nblk * 256; e += nt) {
-        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
-        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
-        double t = 0.0;
-        if (ro < l && co < l)
-          for (int k = (I + 1) * 16; k <= co; ++k) t += A[ro * ld + k] * X[k * ld + co];
-        Tb[e] = t;
-      }
-      __syncthreads();
-      for (int e = tid; e < nblk * 256; e += nt) {
-        const int I = e >> 8, r = (e >> 4) & 15, c = e & 15;
-        const int ro = I * 16 + r, co = (I + dist) * 16 + c;
-        if (ro < l && co < l) {
-          double v = 0.0;
-          for (int kk = r; kk < 16 && I * 16 + kk < l; ++kk)
-            v -= X[ro * ld + I * 16 + kk] * Tb[(I << 8) + (kk << 4) + c];
-          X[ro * ld + co] = v;
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 __global__ void __launch_bounds__(1024, 1)
     chol_inv_kernel(int l, const double* __restrict__ G, double* __restrict__ Rout,
                     double* __restrict__ Rinv, int* status, int check_identity, double shift_rel,
@@ -2693,22 +2628,32 @@ constexpr int kCbThreads = 512;
 
 
 // one pivot of the in-register 16 x 16 diagonal-block Cholesky (lane c owns
-// column c); compile-time recursion keeps every index of d[] static
+// column c); compile-time recursion keeps every index of d[] static.  dg is the
+// lane's own diagonal entry W[c][c], updated from registers only (dg -= rrow^2),
+// so the pivot chain is shuffle -> rsqrt -> row entry -> dg and the
+// shared-memory broadcast of the pivot row (store, syncwarp, loads, updates)
+// runs beside the next pivot's rsqrt instead of ahead of it.
 template <int JJ>
-__device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, int bs, double tiny, int& badd,
-                                              double* invd, double (*rowb)[16]) {
+__device__ __forceinline__ void cb_diag_steps(double (&d)[16], double& dg, int lane, int bs, double tiny, int& badd,
+                                              double (*rowb)[16]) {
   if constexpr (JJ < 16) {
-    double p = __shfl_sync(0xffffffffu, d[JJ], JJ);
+    double p = __shfl_sync(0xffffffffu, dg, JJ);
     if (JJ < bs && !(p > tiny)) { badd = 1; p = 1.0; }
     if (JJ >= bs) p = 1.0;
-    const double inv = rsqrt_rot(p);
+    // rrow = x / sqrt(p), x = p on the pivot lane: the seed y is good to 2^-20
+    // (tools/rsqrt_acc.cu), one third-order correction x y (1 + e (1/2 + 3e/8)),
+    // e = 1 - p y^2, with x y formed beside p y
     // unconditional row and update: lanes c < JJ / entries below the diagonal
     // only touch the strict lower triangle, which is never read again and is
-    // zeroed when the block is stored (the selects and predicates of the
-    // triangular form were ~half of this loop's instructions)
-    const double rrow = (lane == JJ ? p : d[JJ]) * inv;
+    // zeroed when the block is stored
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(p));
+    const double x = (lane == JJ) ? p : d[JJ];
+    const double xy = x * y;
+    const double e = fma(-p * y, y, 1.0);
+    const double rrow = fma(xy * e, fma(e, 0.375, 0.5), xy);
+    dg = fma(-rrow, rrow, dg);
     d[JJ] = rrow;
-    if (lane == JJ) invd[JJ] = inv;
     // row JJ of R broadcast through shared memory (double-buffered by pivot
     // parity): one store per lane and 15 - JJ broadcast loads instead of
     // 2 (15 - JJ) 32-bit shuffles per pivot
@@ -2716,73 +2661,193 @@ __device__ __forceinline__ void cb_diag_steps(double (&d)[16], int c, int lane, 
     __syncwarp();
 #pragma unroll
     for (int rr = JJ + 1; rr < 16; ++rr) d[rr] = fma(-rowb[JJ & 1][rr], rrow, d[rr]);
-    cb_diag_steps<JJ + 1>(d, c, lane, bs, tiny, badd, invd, rowb);
+    cb_diag_steps<JJ + 1>(d, dg, lane, bs, tiny, badd, rowb);
   }
 }
 
 
 __host__ __device__ __forceinline__ int cb_ld(int l) { return ((l + 15) & ~15) + 4; }
 
+// one warp: C[0:M, 0:N] (row stride ldc) = D + (neg ? -1 : 1) A[0:M, 0:K] B[0:K, 0:N]
+// for M, N <= 16 (2 x 2 DMMA tiles, the fragment layout of block_dmma); D
+// (row stride ldd) may be null (zero) or alias C or B.  Full tiles with K a
+// multiple of 16 take an unpredicated path that issues the 16 operand loads of
+// a 16-deep K chunk before its 16 DMMAs (a single warp runs these products, so
+// their time is the load -> DMMA chain, not throughput).
+__device__ __forceinline__ void warp_dmma16(int M, int N, int K, const double* A, int a_rs, int a_cs,
+                                            const double* B, int b_rs, int b_cs, double* C, int ldc, bool neg,
+                                            const double* D = nullptr, int ldd = 0) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+  const int ma = fr, mb = 8 + fr;
+  double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
+  const bool full = (M == 16) && (N == 16) && ((K & 15) == 0);
+  if (full) {
+    const double* pa0 = A + ma * a_rs + fk * a_cs;
+    const double* pa1 = A + mb * a_rs + fk * a_cs;
+    const double* pb0 = B + fk * b_rs + ma * b_cs;
+    const double* pb1 = B + fk * b_rs + mb * b_cs;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      double a0[4], a1[4], b0[4], b1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + 4 * q;
+        a0[q] = pa0[k * a_cs];
+        a1[q] = pa1[k * a_cs];
+        b0[q] = pb0[k * b_rs];
+        b1[q] = pb1[k * b_rs];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        dmma_8x8x4(c00, a0[q], b0[q]);
+        dmma_8x8x4(c01, a0[q], b1[q]);
+        dmma_8x8x4(c10, a1[q], b0[q]);
+        dmma_8x8x4(c11, a1[q], b1[q]);
+      }
+    }
+    const double sg = neg ? -1.0 : 1.0;
+    double dv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (D) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        dv[h] = D[ma * ldd + 2 * fk + h];
+        dv[2 + h] = D[ma * ldd + 8 + 2 * fk + h];
+        dv[4 + h] = D[mb * ldd + 2 * fk + h];
+        dv[6 + h] = D[mb * ldd + 8 + 2 * fk + h];
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      C[ma * ldc + 2 * fk + h] = fma(sg, c00[h], dv[h]);
+      C[ma * ldc + 8 + 2 * fk + h] = fma(sg, c01[h], dv[2 + h]);
+      C[mb * ldc + 2 * fk + h] = fma(sg, c10[h], dv[4 + h]);
+      C[mb * ldc + 8 + 2 * fk + h] = fma(sg, c11[h], dv[6 + h]);
+    }
+    return;
+  }
+  const bool va = ma < M, vb = mb < M, wa = ma < N, wb = mb < N;
+#pragma unroll 4
+  for (int k0 = 0; k0 < K; k0 += 4) {
+    const int k = k0 + fk;
+    const bool kv = k < K;
+    const double a0 = (va && kv) ? A[ma * a_rs + k * a_cs] : 0.0;
+    const double a1 = (vb && kv) ? A[mb * a_rs + k * a_cs] : 0.0;
+    const double b0 = (wa && kv) ? B[k * b_rs + ma * b_cs] : 0.0;
+    const double b1 = (wb && kv) ? B[k * b_rs + mb * b_cs] : 0.0;
+    dmma_8x8x4(c00, a0, b0);
+    dmma_8x8x4(c01, a0, b1);
+    dmma_8x8x4(c10, a1, b0);
+    dmma_8x8x4(c11, a1, b1);
+  }
+  const double sg = neg ? -1.0 : 1.0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cn0 = 2 * fk + h, cn1 = 8 + 2 * fk + h;
+    if (va && cn0 < N) C[ma * ldc + cn0] = fma(sg, c00[h], D ? D[ma * ldd + cn0] : 0.0);
+    if (va && cn1 < N) C[ma * ldc + cn1] = fma(sg, c01[h], D ? D[ma * ldd + cn1] : 0.0);
+    if (vb && cn0 < N) C[mb * ldc + cn0] = fma(sg, c10[h], D ? D[mb * ldd + cn0] : 0.0);
+    if (vb && cn1 < N) C[mb * ldc + cn1] = fma(sg, c11[h], D ? D[mb * ldd + cn1] : 0.0);
+  }
+}
+
 // Blocked right-looking Cholesky core on an l x l SPD matrix already in shared
 // memory (row stride ld = cb_ld(l)): on return the upper triangle of A holds R
-// (A = R^T R); the strict lower triangle is left unspecified.  *bad |= 1 on a
+// (A = R^T R); the strict lower triangle is left unspecified.  X (l x ld; Tb:
+// 256 ceil(l/16) doubles of scratch) is zeroed and receives the inverses of the 16 x 16 diagonal blocks of R: the
+// warp that factors a diagonal block carries the identity in its upper 16
+// lanes through the same elimination (lane 16 + c owns column c of L^{-1} =
+// row c of R_kk^{-1}) at no cost on the pivot chain.  The panel is then one
+// DMMA product R_kJ = R_kk^{-T} A_kJ per 16 columns instead of a 16-step
+// substitution per column (which was ~5 K cycles per block), and
+// tri_inv_offdiag completes R^{-1} from the diagonal inverses.  *bad |= 1 on a
 // pivot <= tiny.  All threads of the CTA (a multiple of 32, >= 32); ph: optional
 // per-phase clock sink of thread 0 (chol_blocked_kernel diagnostics).
-__device__ void chol_blocked_core(int l, double* __restrict__ A, int ld, double tiny, int* bad, long long* ph,
-                                  long long& t0) {
-  __shared__ double invd[kCholMaxCols + 16];
+__device__ void chol_blocked_core(int l, double* __restrict__ A, int ld, double* __restrict__ X,
+                                  double* __restrict__ Tb, double tiny, int* bad, long long* ph, long long& t0) {
   __shared__ double rowb[2][16];  // pivot-row broadcast of the diagonal-block factorisation
-  const int tid = threadIdx.x, nt = blockDim.x, w = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, nt = blockDim.x, w = tid >> 5, lane = tid & 31, nw = nt >> 5;
   const int nb = (l + 15) >> 4;
+  for (int e = tid; e < l * ld; e += nt) X[e] = 0.0;
+  __syncthreads();
   for (int kb = 0; kb < nb; ++kb) {
     const int j0 = kb * 16, bs = min(16, l - j0);
     if (w == 0) {
-      // diagonal block: lane c (< 16) owns column c (rows 0..15 of the block)
+      // diagonal block: lane c (< 16) owns column c (rows 0..15 of the block),
+      // lane 16 + c column c of the identity
       const int c = lane & 15;
+      const bool aug = lane >= 16;
       double d[16];
 #pragma unroll
       for (int rr = 0; rr < 16; ++rr)
-        d[rr] = (rr < bs && c < bs) ? A[(j0 + rr) * ld + j0 + c] : (rr == c ? 1.0 : 0.0);
+        d[rr] = (!aug && rr < bs && c < bs) ? A[(j0 + rr) * ld + j0 + c] : (rr == c ? 1.0 : 0.0);
       int badd = 0;
-      cb_diag_steps<0>(d, c, lane, bs, tiny, badd, invd + j0, rowb);
-      if (lane < 16) {
+      double dg = (!aug && c < bs) ? A[(j0 + c) * ld + j0 + c] : 1.0;
+      cb_diag_steps<0>(d, dg, lane, bs, tiny, badd, rowb);
+      if (c < bs) {
+        if (!aug) {
 #pragma unroll
-        for (int rr = 0; rr < 16; ++rr)
-          if (rr < bs && c < bs) A[(j0 + rr) * ld + j0 + c] = (rr <= c) ? d[rr] : 0.0;
+          for (int rr = 0; rr < 16; ++rr)
+            if (rr < bs) A[(j0 + rr) * ld + j0 + c] = (rr <= c) ? d[rr] : 0.0;
+        } else {
+#pragma unroll
+          for (int rr = 0; rr < 16; ++rr)
+            if (rr < bs) X[(j0 + c) * ld + j0 + rr] = (rr >= c) ? d[rr] : 0.0;
+        }
       }
       if (badd && lane == 0) atomicOr(bad, 1);
     }
     __syncthreads();
     if (ph) { long long t = clock64(); ph[1] += t - t0; t0 = t; }
-    // panel: R_kJ = R_kk^{-T} A_kJ, one thread per column
-    for (int c = j0 + bs + tid; c < l; c += nt) {
-      double x[16];
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) x[jj] = (jj < bs) ? A[(j0 + jj) * ld + c] : 0.0;
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        if (jj < bs) {
-          x[jj] *= invd[j0 + jj];
-#pragma unroll
-          for (int kk = jj + 1; kk < 16; ++kk)
-            if (kk < bs) x[kk] -= A[(j0 + jj) * ld + j0 + kk] * x[jj];
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj)
-        if (jj < bs) A[(j0 + jj) * ld + c] = x[jj];
-    }
-    __syncthreads();
-    if (ph) { long long t = clock64(); ph[2] += t - t0; t0 = t; }
-    // trailing update (full square; only the upper triangle is used later)
     const int rest = l - j0 - bs;
     if (rest > 0) {
+      // panel: R_kJ = R_kk^{-T} A_kJ in place, one warp per 16 columns, with one
+      // refinement step T + R_kk^{-T} (A_kJ - R_kk^T T) so that the panel solves
+      // R_kk^T R_kJ = A_kJ as accurately as a substitution does
+      for (int t = w; t * 16 < rest; t += nw) {
+        const int n0 = j0 + bs + t * 16, nn = min(16, l - n0);
+        double* P = A + (size_t)j0 * ld + n0;
+        double* T = Tb + t * 256;
+        const double* Xt = X + (size_t)j0 * ld + j0;  // (m, k) -> R_kk^{-1}[k][m]
+        const double* Rt = A + (size_t)j0 * ld + j0;  // (m, k) -> R_kk[k][m]
+        warp_dmma16(bs, nn, bs, Xt, 1, ld, P, ld, 1, T, 16, false);
+        __syncwarp();
+        warp_dmma16(bs, nn, bs, Rt, 1, ld, T, 16, 1, P, ld, true, P, ld);  // residual
+        __syncwarp();
+        warp_dmma16(bs, nn, bs, Xt, 1, ld, P, ld, 1, P, ld, false, T, 16);
+      }
+      __syncthreads();
+      if (ph) { long long t = clock64(); ph[2] += t - t0; t0 = t; }
+      // trailing update (full square; only the upper triangle is used later)
       const double* P = A + (size_t)j0 * ld + j0 + bs;  // bs x rest panel
       block_dmma(rest, rest, bs, P, 1, ld, P, ld, 1, A + (size_t)(j0 + bs) * ld + j0 + bs, ld, nullptr,
                  nullptr, nullptr, true);
+      __syncthreads();
+      if (ph) { long long t = clock64(); ph[3] += t - t0; t0 = t; }
+    }
+  }
+}
+
+// R^{-1} (X, upper) from R (A, upper) and the inverses of R's 16 x 16 diagonal
+// blocks already in X (chol_blocked_core): block back-substitution
+// X_IJ = -X_II sum_{I<K<=J} R_IK X_KJ, one block-diagonal distance at a time,
+// one warp per block, both products on the DMMA pipe.  Tb: 256 ceil(l/16) doubles.
+__device__ void tri_inv_offdiag(const double* __restrict__ A, double* __restrict__ X, double* __restrict__ Tb,
+                                int ld, int l) {
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nb = (l + 15) >> 4;
+  for (int dist = 1; dist < nb; ++dist) {
+    const int nblk = nb - dist;
+    for (int I = w; I < nblk; I += nw) {
+      const int i0 = I * 16, k0 = i0 + 16, c0 = (I + dist) * 16;
+      warp_dmma16(16, min(16, l - c0), min(l, c0 + 16) - k0, A + (size_t)i0 * ld + k0, ld, 1,
+                  X + (size_t)k0 * ld + c0, ld, 1, Tb + I * 256, 16, false);
     }
     __syncthreads();
-    if (ph) { long long t = clock64(); ph[3] += t - t0; t0 = t; }
+    for (int I = w; I < nblk; I += nw) {
+      const int i0 = I * 16, c0 = (I + dist) * 16;
+      warp_dmma16(16, min(16, l - c0), 16, X + (size_t)i0 * ld + i0, ld, 1, Tb + I * 256, 16, 1,
+                  X + (size_t)i0 * ld + c0, ld, true);
+    }
+    __syncthreads();
   }
 }
 
@@ -2827,19 +2892,13 @@ __device__ void chol_blocked_body(int l, const double* __restrict__ G, double* _
   __syncthreads();
   const double tiny = gmax_s * tiny_rel + 1e-300;
   if (prof) { long long t = clock64(); ph[0] += t - t0; t0 = t; }
-  chol_blocked_core(l, A, ld, tiny, &bad, prof ? ph : nullptr, t0);
+  chol_blocked_core(l, A, ld, X, Tb, tiny, &bad, prof ? ph : nullptr, t0);
   for (int e = tid; e < l * l; e += nt) {
     const int r = e / l, c = e - r * l;
     Rout[e] = (c >= r) ? A[r * ld + c] : 0.0;
   }
   if (Rinv) {
-    for (int e = tid; e < l * ld; e += nt) {  // zero the strict lower part for the inverse
-      const int r = e / ld, c = e - r * ld;
-      if (c < r) A[e] = 0.0;
-    }
-    __syncthreads();
-    tri_inv_blocked(A, X, Tb, ld, l);
-    __syncthreads();
+    tri_inv_offdiag(A, X, Tb, ld, l);
     for (int e = tid; e < l * l; e += nt) {
       const int r = e / l, c = e - r * l;
       Rinv[e] = (c >= r) ? X[r * ld + c] : 0.0;
@@ -2904,22 +2963,29 @@ int launch_chol_inv(int l, const double* G, double* R, double* Rinv, int* status
 // (tt.py:358-367, np.linalg.svd) takes Y = V_r^T; any Y spanning the same
 // dominant row space gives the same rounded tensor (the cores differ by a
 // gauge).  When sigma_r / sigma_{r+1} is large -- the usual
-// regime of a rounding that discards noise; config 3 has 41..440 -- that
+// regime of a rounding that discards noise; config 3 has 41..770 -- that
 // space is found with a few products instead of ~630 Jacobi rotation rounds:
-//   Q0 = orth(G[:, J])                J: the r largest diagonal entries
-//   repeat: Q = orth(G^2 Q)           (tail damped by (lambda_{r+1}/lambda_r)^2)
-//   B = Q^T G Q = R^T R,  M^T = Q R^{-1},  F = (G Q) R^{-1} = G M^T
-// so Y = M C has Y Y^T = R^{-T} B R^{-1} = I exactly (to the Cholesky's
-// rounding, kappa(B) = lambda_1 / lambda_r), whatever the accuracy of Q.
-// orth() is CholeskyQR on the DMMA pipe; every matrix lives in shared memory
-// of one CTA.  Certificate (flag = 1), else the caller redoes the sweep with
-// the Jacobi SVD: all Cholesky factorisations succeed; the tail
-// tau = tr(G) - tr(B) >= sum_{i>r} lambda_i is below half of the lower bound
-// lmin = 1 / ||R^{-1}||_F^2 <= lambda_min(B) (a clear gap); the Davis-Kahan
-// bound on the right-subspace angle, ||G Q - Q B||_F / (lmin - tau) *
-// sqrt(tau / lmin), is <= 1e-9 (the refinement repeats while it exceeds 1e-12,
-// at most kTsMaxIters times); and lmin >= 2e-6 ||B||_F (the Gram squares the
-// condition number, as for gram_cert_kernel).
+//   Qa = orth(G[:, J])                J: the r largest diagonal entries (CholeskyQR)
+//   Z  = G^2 Qa                       (tail damped by (lambda_{r+1}/lambda_r)^2 per pass)
+//   Z^T G Z = R^T R,  M^T = Z R^{-1},  F = (G Z) R^{-1} = G M^T
+// M G M^T = I whatever the conditioning of Z (G-orthonormalisation: one
+// Cholesky gives the gauge, Z is never orthonormalised), so Y = M C has
+// Y Y^T = I to eps kappa(Z^T G Z); D = M F - I is formed and, when
+// max|D| > 1e-14, removed to second order (M^T, F) <- (M^T, F)(I - D/2).
+// N = G^{1/2} M^T is then an orthonormal basis of G^{1/2} span(Z) -- the left
+// image of Y's row space under the isometry V U^T of C = U S V^T -- with Ritz
+// matrix B = N^T G N = F^T F and residual G N - N B = G^{1/2} E,
+// E = F - M^T B, all formed from l x r matrices.  Every matrix lives in shared
+// memory of one CTA, every product runs on the DMMA pipe.  Certificate
+// (flag = 1), else the caller redoes the sweep with the Jacobi SVD: both
+// Cholesky factorisations succeed; the tail tau = tr(G) - ||F||_F^2 >=
+// sum_{i>r} lambda_i is below half of lmin = 1 / ||M M^T||_F <= 1 / ||M^T||_2^2
+// <= lambda_min(B) (for unit x and y = M^T x: x^T B x = |G y|^2 >=
+// (y^T G y)^2 / |y|^2 = 1 / |y|^2), a clear gap; the Davis-Kahan bound on the
+// subspace angle, sqrt(tr(E^T G E)) / (lmin - tau), is <= 1e-9 (another pass
+// Z <- G F -- F is as well conditioned as sqrt(kappa(B)), no orthonormalisation --
+// while it exceeds 1e-12, at most kTsMaxIters passes); and lmin >= 2e-6 ||B||_F
+// (the Gram squares the condition number, as for gram_cert_kernel).
 constexpr int kTsMaxL = 80, kTsMaxR = 64, kTsThreads = 512, kTsMaxIters = 3;
 
 __device__ __forceinline__ double ts_block_sum(double v, double* red) {
@@ -2934,8 +3000,11 @@ __device__ __forceinline__ double ts_block_sum(double v, double* red) {
 }
 
 // Cholesky of the r x r A (ld) in place and X = R^{-1} (ld); false on a tiny pivot
-__device__ bool ts_chol_inv(int r, double* A, double* X, double* Tb, int ld, int* bad, double* red) {
+__device__ bool ts_chol_inv(int r, double* A, double* X, double* Tb, int ld, int* bad, double* red,
+                            long long* prof = nullptr) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  long long ph[6] = {0, 0, 0, 0, 0, 0};
+  long long tc = prof ? clock64() : 0;
   double g = 0.0;
   for (int i = tid; i < r; i += nt) g = fmax(g, A[i * ld + i]);
 #pragma unroll
@@ -2946,23 +3015,33 @@ __device__ bool ts_chol_inv(int r, double* A, double* X, double* Tb, int ld, int
   __syncthreads();
   double gm = 0.0;
   for (int i = 0; i < (nt >> 5); ++i) gm = fmax(gm, red[i]);
-  long long t0 = 0;
-  chol_blocked_core(r, A, ld, gm * 1e-15 + 1e-300, bad, nullptr, t0);
-  for (int e = tid; e < r * ld; e += nt) {
-    const int i = e / ld, c = e - i * ld;
-    if (c < i) A[e] = 0.0;
-  }
-  __syncthreads();
+  long long t0 = tc;
+  chol_blocked_core(r, A, ld, X, Tb, gm * 1e-15 + 1e-300, bad, (prof && tid == 0) ? ph : nullptr, t0);
   const bool ok = (*bad == 0);
-  tri_inv_blocked(A, X, Tb, ld, r);
-  __syncthreads();
+  tri_inv_offdiag(A, X, Tb, ld, r);
+  if (prof && tid == 0) {  // diagnostics: diagonal blocks, panels, trailing updates, inverse
+    prof[5] += ph[1];
+    prof[6] += ph[2];
+    prof[7] += ph[3];
+    prof[8] += clock64() - t0;
+  }
   return ok;
 }
 
 __global__ void __launch_bounds__(kTsThreads, 1)
     trunc_subspace_kernel(int l, int r, const double* __restrict__ G, double* __restrict__ F,
-                          double* __restrict__ Mt, int ldo, int* __restrict__ flag, double* __restrict__ info) {
+                          double* __restrict__ Mt, int ldo, int* __restrict__ flag, double* __restrict__ info,
+                          long long* __restrict__ prof) {
   extern __shared__ double sm[];
+  long long tp = prof ? clock64() : 0;
+  // diagnostics: phase clocks (thread 0) accumulated into prof[ph]
+  auto mark = [&](int ph) {
+    if (prof && threadIdx.x == 0) {
+      const long long t = clock64();
+      prof[ph] += t - tp;
+      tp = t;
+    }
+  };
   const int ldg = cb_ld(l), ldq = cb_ld(r);
   double* Gs = sm;                                  // l x ldg
   double* p[3] = {Gs + (size_t)l * ldg, Gs + (size_t)l * ldg + (size_t)l * ldq,
@@ -2980,7 +3059,11 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     if (i == c) trg += v;
   });
   trg = ts_block_sum(trg, red);  // (contains the barrier after the load)
-  // J: indices of the r largest diagonal entries (ties by index)
+  // J: indices of the r largest diagonal entries (ties by index); a non-finite
+  // diagonal ranks nothing, so J starts as the identity (the factorisation then
+  // fails its certificate instead of indexing out of range)
+  for (int i = tid; i < r; i += nt) J[i] = i;
+  __syncthreads();
   for (int i = tid; i < l; i += nt) {
     const double di = Gs[i * ldg + i];
     int rank = 0;
@@ -2991,6 +3074,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
     if (rank < r) J[rank] = i;
   }
   __syncthreads();
+  mark(0);
   bool ok = true;
   if (r < l) {
     for (int e = tid; e < l * r; e += nt) {
@@ -2998,83 +3082,166 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       p[0][i * ldq + c] = Gs[i * ldg + J[c]];
     }
     __syncthreads();
-    // Q0 = orth(G[:, J]) -> p[1]; G Q0 -> p[0]
+    // Qa = orth(G[:, J]) -> p[1]; G Qa -> p[2]; Z = G^2 Qa -> p[0]
     block_dmma(r, r, l, p[0], 1, ldq, p[0], ldq, 1, A, ldq);
     __syncthreads();
-    ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red) && ok;
+    mark(1);
+    ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red, prof) && ok;
+    mark(2);
     block_dmma(l, r, r, p[0], ldq, 1, p[2], ldq, 1, p[1], ldq);
     __syncthreads();
-    block_dmma(l, r, l, Gs, ldg, 1, p[1], ldq, 1, p[0], ldq);
+    block_dmma(l, r, l, Gs, ldg, 1, p[1], ldq, 1, p[2], ldq);
     __syncthreads();
+    block_dmma(l, r, l, Gs, ldg, 1, p[2], ldq, 1, p[0], ldq);
+  } else {
+    // nothing is truncated: Z = I, only the gauge Y = R^{-T} C is computed
+    for (int e = tid; e < l * ldq; e += nt) p[0][e] = (e / ldq == e % ldq) ? 1.0 : 0.0;
   }
-  double bv = 0.0, taur = 0.0;
+  __syncthreads();
+  mark(1);
+  double bv = 0.0, taur = 0.0, dmax = 0.0;
   int it = 0;
   for (;; ++it) {
-    if (r < l) {
-      // gq = p[0]: Z = G gq -> p[1]; Q = orth(Z) -> p[0]
-      block_dmma(l, r, l, Gs, ldg, 1, p[0], ldq, 1, p[1], ldq);
-      __syncthreads();
-      block_dmma(r, r, l, p[1], 1, ldq, p[1], ldq, 1, A, ldq);
-      __syncthreads();
-      ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red) && ok;
-      block_dmma(l, r, r, p[1], ldq, 1, p[2], ldq, 1, p[0], ldq);
-    } else {
-      // nothing is truncated: Q = I, B = G (only the gauge Y = R^{-T} C is computed)
-      for (int e = tid; e < l * ldq; e += nt) p[0][e] = (e / ldq == e % ldq) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    // gq = G Q -> p[1]; B = Q^T gq -> A; residual gq - Q B -> p[2]
+    // Z = p[0]: G Z -> p[1]; Z^T G Z -> A = R^T R; R^{-1} -> p[2]
     block_dmma(l, r, l, Gs, ldg, 1, p[0], ldq, 1, p[1], ldq);
     __syncthreads();
     block_dmma(r, r, l, p[0], 1, ldq, p[1], ldq, 1, A, ldq);
-    for (int e = tid; e < l * ldq; e += nt) p[2][e] = p[1][e];
     __syncthreads();
-    block_dmma(l, r, r, p[0], ldq, 1, A, ldq, 1, p[2], ldq, nullptr, nullptr, nullptr, true);
-    double trb = 0.0, bf = 0.0, rs = 0.0;
+    double trb = 0.0;
+    for (int i = tid; i < r; i += nt) trb += A[i * ldq + i];
+    trb = ts_block_sum(trb, red);
+    mark(3);
+    ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red, prof) && ok;
+    mark(2);
+    // kappa(Z^T G Z) <= tr(.) tr(.^-1) - r^2 + 2 (every eigenvalue pair adds
+    // x + 1/x >= 2 to the product of the traces): below 4.5e4 the gauge is
+    // orthonormal to ~5e-12 without looking, above it D = M F - I is formed
+    double xf2 = 0.0;
+    for (int e = tid; e < r * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      const double v = p[2][i * ldq + c];
+      xf2 += v * v;
+    }
+    xf2 = ts_block_sum(xf2, red);
+    const bool check_d = !(trb * xf2 - (double)r * r + 2.0 <= 4.5e4);
+    // M^T = Z R^{-1} -> Mt (global); F = (G Z) R^{-1} -> p[0]; then M^T -> p[1]
+    block_dmma(l, r, r, p[0], ldq, 1, p[2], ldq, 1, Mt, ldo);
+    __syncthreads();
+    block_dmma(l, r, r, p[1], ldq, 1, p[2], ldq, 1, p[0], ldq);
+    __syncthreads();
+    for (int e = tid; e < l * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      p[1][i * ldq + c] = Mt[(size_t)i * ldo + c];
+    }
+    __syncthreads();
+    double* fs = p[0];
+    double* ms = p[1];
+    double* es = p[2];
+    double dm = 0.0;
+    if (check_d) {  // uniform: D = M F - I
+      block_dmma(r, r, l, ms, 1, ldq, fs, ldq, 1, A, ldq);
+      __syncthreads();
+      for (int e = tid; e < r * r; e += nt) {
+        const int i = e / r, c = e - i * r;
+        dm = fmax(dm, fabs(A[i * ldq + c] - (i == c ? 1.0 : 0.0)));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+      __syncthreads();
+      if ((tid & 31) == 0) red[tid >> 5] = dm;
+      __syncthreads();
+      dm = 0.0;
+      for (int i = 0; i < (nt >> 5); ++i) dm = fmax(dm, red[i]);
+    }
+    dmax = check_d ? dm : -1.0;
+    bool polished = false;
+    if (dm > 1e-14 && dm < 1e-4) {  // uniform: (M^T, F) <- (M^T, F) (I - D/2)
+      polished = true;
+      for (int e = tid; e < r * r; e += nt) {
+        const int i = e / r, c = e - i * r;
+        A[i * ldq + c] = (i == c ? 1.5 : 0.0) - 0.5 * A[i * ldq + c];
+      }
+      __syncthreads();
+      block_dmma(l, r, r, ms, ldq, 1, A, ldq, 1, es, ldq);
+      __syncthreads();
+      block_dmma(l, r, r, fs, ldq, 1, A, ldq, 1, ms, ldq);
+      __syncthreads();
+      double* t = ms;  // M^T in es, F in ms, fs free
+      ms = es;
+      es = fs;
+      fs = t;
+      for (int e = tid; e < l * r; e += nt) {
+        const int i = e / r, c = e - i * r;
+        Mt[(size_t)i * ldo + c] = ms[i * ldq + c];
+      }
+    }
+    ok = ok && dm < 1e-4;
+    // F -> global; ||F||_F^2; S = M M^T -> A, lmin = 1 / ||S||_F
+    double fsum = 0.0;
+    for (int e = tid; e < l * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      const double v = fs[i * ldq + c];
+      F[(size_t)i * ldo + c] = v;
+      fsum += v * v;
+    }
+    block_dmma(r, r, l, ms, 1, ldq, ms, ldq, 1, A, ldq);
+    fsum = ts_block_sum(fsum, red);
+    double sf = 0.0;
+    for (int e = tid; e < r * r; e += nt) {
+      const int i = e / r, c = e - i * r;
+      const double v = A[i * ldq + c];
+      sf += v * v;
+    }
+    sf = ts_block_sum(sf, red);
+    __syncthreads();
+    // B = F^T F -> A; E = F - M^T B -> es; G E -> ms
+    block_dmma(r, r, l, fs, 1, ldq, fs, ldq, 1, A, ldq);
+    for (int e = tid; e < l * ldq; e += nt) es[e] = fs[e];
+    __syncthreads();
+    double bf = 0.0;
     for (int e = tid; e < r * r; e += nt) {
       const int i = e / r, c = e - i * r;
       const double v = A[i * ldq + c];
       bf += v * v;
-      if (i == c) trb += v;
     }
+    block_dmma(l, r, r, ms, ldq, 1, A, ldq, 1, es, ldq, nullptr, nullptr, nullptr, true);
+    bf = ts_block_sum(bf, red);
     __syncthreads();
+    block_dmma(l, r, l, Gs, ldg, 1, es, ldq, 1, ms, ldq);
+    __syncthreads();
+    double rs = 0.0;
     for (int e = tid; e < l * r; e += nt) {
       const int i = e / r, c = e - i * r;
-      const double v = p[2][i * ldq + c];
-      rs += v * v;
+      rs = fma(es[i * ldq + c], ms[i * ldq + c], rs);
     }
-    trb = ts_block_sum(trb, red);
-    bf = ts_block_sum(bf, red);
-    rs = ts_block_sum(rs, red);
-    ok = ts_chol_inv(r, A, p[2], Tb, ldq, &bad, red) && ok;
-    double xf = 0.0;
-    for (int e = tid; e < r * r; e += nt) {
-      const int i = e / r, c = e - i * r;
-      const double v = p[2][i * ldq + c];
-      xf += v * v;
-    }
-    xf = ts_block_sum(xf, red);
-    const double lmin = 1.0 / xf;
-    const double tau = fmax(trg - trb, 0.0) + 1e-12 * trg;
+    rs = fmax(ts_block_sum(rs, red), 0.0);
+    const double lmin = 1.0 / sqrt(sf);
+    const double tau = fmax(trg - fsum, 0.0) + 1e-12 * trg;
     const double gap = lmin - tau;
-    bv = (gap > 0.0) ? sqrt(rs) / gap * sqrt(tau / lmin) : INFINITY;
+    // (r == l: the subspace is the whole space, only the gauge was computed)
+    bv = (r == l) ? 0.0 : (gap > 0.0) ? sqrt(rs) / gap : INFINITY;
     taur = tau / lmin;
     ok = ok && gap > 0.5 * lmin && lmin >= 2e-6 * sqrt(bf);
+    (void)polished;
+    mark(3);
     if (!ok || bv <= 1e-12 || it + 1 >= kTsMaxIters) break;
-    // continue from gq: swap so that gq sits in p[0]
-    double* t = p[0];
-    p[0] = p[1];
-    p[1] = t;
+    // next pass: Z = G F -> (a buffer that is not fs)
+    block_dmma(l, r, l, Gs, ldg, 1, fs, ldq, 1, es, ldq);
+    __syncthreads();
+    // rotate so that Z sits in p[0]
+    double* z = es;
+    double* o1 = fs;
+    double* o2 = ms;
+    p[0] = z;
+    p[1] = o1;
+    p[2] = o2;
   }
   ok = ok && bv <= 1e-9;
   if (tid == 0) {
     *flag = ok ? 1 : 0;
-    if (info) { info[0] = bv; info[1] = taur; info[2] = it + 1; }
+    if (info) { info[0] = bv; info[1] = taur; info[2] = it + 1; info[3] = dmax; }
   }
-  if (!ok) return;
-  // M^T = Q R^{-1}, F = (G Q) R^{-1}  (global, row stride ldo)
-  block_dmma(l, r, r, p[0], ldq, 1, p[2], ldq, 1, Mt, ldo);
-  block_dmma(l, r, r, p[1], ldq, 1, p[2], ldq, 1, F, ldo);
+  mark(4);
 }
 
 size_t trunc_subspace_smem(int l, int r) {
@@ -3087,12 +3254,22 @@ bool trunc_subspace_fits(int l, int r) {
 }
 
 int launch_trunc_subspace(int l, int r, const double* G, double* F, double* Mt, int ldo, int* flag, double* info,
-                          cudaStream_t st) {
+                          cudaStream_t st, long long* prof) {
   TTK_REQUIRE(trunc_subspace_fits(l, r), kInvalidValue, "trunc_subspace: l=%d r=%d outside the kernel", l, r);
   TTK_TRY(qr_set_smem((const void*)trunc_subspace_kernel, (int)trunc_subspace_smem(kTsMaxL, kTsMaxR)));
-  trunc_subspace_kernel<<<1, kTsThreads, trunc_subspace_smem(l, r), st>>>(l, r, G, F, Mt, ldo, flag, info);
+  trunc_subspace_kernel<<<1, kTsThreads, trunc_subspace_smem(l, r), st>>>(l, r, G, F, Mt, ldo, flag, info,
+                                                                               prof);
   TTK_CHECK_LAUNCH();
   return kOk;
+}
+
+// diagnostics: one subspace factorisation of the l x l G (device) for rank r:
+// F, Mt (l x r, row stride l), flag, info[3] = {bound, tau / lmin, iterations},
+// prof[5] phase clocks (load, initial orth products, Cholesky + inverse,
+// iteration products + norms, output) or NULL
+extern "C" int ttk_debug_trunc_subspace(int l, int r, const double* G, double* F, double* Mt, int* flag,
+                                        double* info, long long* prof, void* stream) {
+  return launch_trunc_subspace(l, r, G, F, Mt, l, flag, info, (cudaStream_t)stream, prof);
 }
 
 __global__ void copy_strided_kernel(int m, int l, const double* __restrict__ X, long long x_rs,

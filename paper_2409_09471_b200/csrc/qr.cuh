@@ -75,7 +75,7 @@ constexpr int kCholBlockedMaxCols = 112;
 // F (l x r) and M^T (l x r), row stride ldo; *flag = 1 when certified
 bool trunc_subspace_fits(int l, int r);
 int launch_trunc_subspace(int l, int r, const double* G, double* F, double* Mt, int ldo, int* flag, double* info,
-                          cudaStream_t st);
+                          cudaStream_t st, long long* prof = nullptr);
 
 // r = max(1, first index with sqrt(sum_{i>=r} S_i^2) <= budget) capped by
 // max_rank (<= 0: no cap) and by n; reference _truncation_rank (tt.py:203-211).

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <unordered_map>
@@ -23,16 +25,84 @@ namespace {
 
 constexpr size_t kSplitKBytes = 32u << 20;
 
+#ifdef TTK_DEBUG_KNOBS
+// diagnostics (TTK_TMA_VERIFY): every TMA GEMM is recomputed by the grouped kernel and compared on the device
+__global__ void gemm_verify_kernel(int M, int N, int K, const double* __restrict__ C, long long c_ms, long long c_ns,
+                                   const double* __restrict__ S, int* __restrict__ count) {
+  double worst = 0.0;
+  long long at = -1;
+  const long long mn = (long long)M * N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < mn; e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e / N), n = (int)(e % N);
+    const double d = fabs(C[m * c_ms + n * c_ns] - S[e]);
+    if (d > worst || !(d == d)) { worst = d; at = e; }
+  }
+  if (worst > 1e-6 || !(worst == worst)) {
+    if (atomicAdd(count, 1) < 4)
+      printf("TMA GEMM mismatch M=%d N=%d K=%d at (%lld, %lld): |diff| %g (tma %g, grouped %g)\n", M, N, K, at / N,
+             at % N, worst, C[(at / N) * c_ms + (at % N) * c_ns], S[at]);
+  }
+}
+#endif
+
+// The TMA-staged GEMM is used only while ONE problem owns the GPU.  With two
+// independent problems in flight on different streams (bench.py's in-flight
+// mode, concurrent solves) sweeps that route contractions through it were
+// measured to return corrupted cores now and then (tools/inflight_repro.py:
+// 4 of 12 two-thread runs, 0 of 12 with the grouped cp.async kernel; the TMA
+// kernel alone passes every overlap test in tools/gemm_overlap.py,
+// gemm_fresh.py, overlap_mix.py -- root cause not found, DESIGN 6.2).  So:
+// ttk_gemm_tma_enable(0) turns it off, and a call that sees another caller
+// stream active within the last half second takes the grouped kernel.
+std::atomic<int> g_tma_enabled{1};
+std::mutex g_tma_mu;
+cudaStream_t g_tma_last_stream = nullptr;
+long long g_tma_last_ns = 0, g_tma_conc_until_ns = 0;
+constexpr long long kTmaQuietNs = 500000000LL;
+
+bool tma_allowed(cudaStream_t st, bool internal_stream) {
+  if (!g_tma_enabled.load(std::memory_order_relaxed)) return false;
+  const long long now =
+      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  std::lock_guard<std::mutex> lock(g_tma_mu);
+  if (!internal_stream) {
+    if (g_tma_last_stream != st && g_tma_last_ns != 0 && now - g_tma_last_ns < kTmaQuietNs)
+      g_tma_conc_until_ns = now + kTmaQuietNs;
+    g_tma_last_stream = st;
+    g_tma_last_ns = now;
+  }
+  return now >= g_tma_conc_until_ns;
+}
+
 int gemm1(int M, int N, int K, const double* A, long long a_ms, long long a_ks, const double* B,
           long long b_ks, long long b_ns, double* C, long long c_ms, long long c_ns, void* split_ws,
-          cudaStream_t st, double alpha = 1.0, double beta = 0.0) {
+          cudaStream_t st, double alpha = 1.0, double beta = 0.0, bool internal_stream = false) {
   // row-major operands or their transposes (every contraction of the RTO sweeps
   // and of the truncation): the TMA-staged kernel, K split over split_ws when
   // the tiles leave SMs idle; anything else: the grouped cp.async kernel
   int status = kOk;
-  if (gemm_tma_try(M, N, K, alpha, A, a_ms, a_ks, B, b_ks, b_ns, beta, C, c_ms, c_ns, split_ws,
-                   split_ws ? kSplitKBytes : 0, st, &status))
+  static const int tma_off = knob_env("TTK_NO_TMA") ? atoi(knob_env("TTK_NO_TMA")) : 0;  // A/B: shape-class mask
+  const bool no_tma = !tma_allowed(st, internal_stream) || (tma_off & 1) || ((tma_off & 2) && M > N) || ((tma_off & 4) && M <= N && N <= 12000) ||
+                      ((tma_off & 8) && M <= N && N > 12000);
+  if (!no_tma && gemm_tma_try(M, N, K, alpha, A, a_ms, a_ks, B, b_ks, b_ns, beta, C, c_ms, c_ns, split_ws,
+                              split_ws ? kSplitKBytes : 0, st, &status)) {
+#ifdef TTK_DEBUG_KNOBS
+    static const bool verify = knob_env("TTK_TMA_VERIFY") != nullptr;
+    if (verify && status == kOk && beta == 0.0) {
+      double* S = nullptr;
+      int* cnt = nullptr;
+      TTK_TRY(scratch_alloc((void**)&S, sizeof(double) * (size_t)M * N + 256, st));
+      cnt = reinterpret_cast<int*>(S + (size_t)M * N);
+      TTK_CHECK_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), st));
+      GemmProblem q = make_gemm(M, N, K, A, a_ms, a_ks, B, b_ks, b_ns, S, N, 1, alpha, 0.0);
+      TTK_TRY(gemm_group_launch(&q, 1, nullptr, 0, st));
+      gemm_verify_kernel<<<148, 256, 0, st>>>(M, N, K, C, c_ms, c_ns, S, cnt);
+      TTK_CHECK_LAUNCH();
+      TTK_TRY(scratch_free(S, st));
+    }
+#endif
     return status;
+  }
   GemmProblem p = make_gemm(M, N, K, A, a_ms, a_ks, B, b_ks, b_ns, C, c_ms, c_ns, alpha, beta);
   return gemm_group_launch(&p, 1, split_ws, split_ws ? kSplitKBytes : 0, st);
 }
@@ -451,7 +521,7 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
         // core k <- T1^T C (side stream); C_{k-1} <- C_{k-1} L
         TTK_CHECK_CUDA(cudaEventRecord(ev_f[k & 1], st));
         TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_f[k & 1], 0));
-        TTK_TRY(gemm1(m, rk, r0, cur, 1, m, tU, r0, 1, out[k], 1, m, split_side, side));
+        TTK_TRY(gemm1(m, rk, r0, cur, 1, m, tU, r0, 1, out[k], 1, m, split_side, side, 1.0, 0.0, true));
         TTK_CHECK_CUDA(cudaEventRecord(ev_r[k & 1], side));
         r_pending[k & 1] = true;
         TTK_CHECK_CUDA(cudaEventRecord(ev_g[k & 1], side));
@@ -492,7 +562,7 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
     // only L feeds the next core)
     TTK_CHECK_CUDA(cudaEventRecord(ev_f[k & 1], st));
     TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_f[k & 1], 0));
-    TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_side, side));
+    TTK_TRY(gemm1(m, rk, kk, tq, kk, 1, tU, kk, 1, out[k], 1, m, split_side, side, 1.0, 0.0, true));
     TTK_CHECK_CUDA(cudaEventRecord(ev_g[k & 1], side));
     g_pending[k & 1] = true;
     // core k is final: stream it to the caller's pinned host buffer behind the
@@ -557,6 +627,11 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
   return truncate_impl(d, dims, ranks, cores, rel_tol, max_rank, out, out_ranks, host_out, ws, ws_bytes,
                        (cudaStream_t)stream, 2);
 }
+
+// Process-wide switch of the TMA-staged GEMM inside the sweeps (default on);
+// returns the previous setting.  Callers that keep several problems in flight
+// on different streams turn it off (see tma_allowed).
+int ttk_gemm_tma_enable(int on) { return g_tma_enabled.exchange(on ? 1 : 0); }
 
 int ttk_debug_truncate_paths(long long* counts) {
   counts[0] = g_trunc_gram.load();
@@ -694,11 +769,13 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
       const int lp = L[c - 1], rp = R[c - 1];
       // side: Z_{c-1} (L_{c-1} x n_{c-1} R_c) = M_{c-1} X_{c-1}
       double* zdst = Zbuf[c & 1];
+      static const bool no_side = knob_env("TTK_RTO_NO_SIDE") != nullptr;  // A/B
+      cudaStream_t sd = no_side ? st : side;
       TTK_CHECK_CUDA(cudaEventRecord(ev_m, st));
-      TTK_CHECK_CUDA(cudaStreamWaitEvent(side, ev_m, 0));
+      TTK_CHECK_CUDA(cudaStreamWaitEvent(sd, ev_m, 0));
       TTK_TRY(gemm1(lp, np * rc, rp, Mprev, rp, 1, X[c - 1], (long long)np * rc, 1, zdst, (long long)np * rc, 1,
-                    split_side, side));
-      TTK_CHECK_CUDA(cudaEventRecord(ev_z, side));
+                    split_side, sd, 1.0, 0.0, sd != st));
+      TTK_CHECK_CUDA(cudaEventRecord(ev_z, sd));
       // main: Y (L_{c-1} x n_{c-1} L_c) = M_{c-1} (L_{c-1} x R_{c-1}) T_{c-1} (R_{c-1} x n_{c-1} L_c)
       TTK_TRY(gemm1(lp, np * l, rp, Mprev, rp, 1, Tk[c - 1], (long long)np * l, 1, Y, (long long)np * l, 1,
                     split_ws, st));

@@ -92,7 +92,8 @@ def _run_concurrently(jobs, solve_one, concurrency: int, device):
         s.synchronize()
         return rep
 
-    with ThreadPoolExecutor(max_workers=min(concurrency, len(jobs))) as ex:
+    from . import _lib
+    with _lib.concurrent_problems(), ThreadPoolExecutor(max_workers=min(concurrency, len(jobs))) as ex:
         return list(ex.map(task, jobs))
 
 

@@ -532,15 +532,13 @@ def test_truncate_subspace_path_gapped(cuda, r, s, eps):
     assert d[3] >= 2 and d[3] + d[1] == len(dims) - 1 and d[4] == 0 and d[0] == 0
     assert got.ranks == tuple([1] + [c.shape[2] for c in want])
     assert O.rel_diff(tt_np(got), want) <= 1e-12
-    # right-orthonormal cores: Y Y^T = R^-T B R^-1 is the identity to the Cholesky's
-    # rounding, eps * kappa(B) with kappa(B) = (sigma_1 / sigma_r)^2 of that unfolding
-    # (DESIGN 2.2); the represented tensor above is what parity is stated on
-    full = O.to_dense(lo)
-    for k, c in enumerate(got.cores[1:], start=1):
-        sv = np.linalg.svd(full.reshape(int(np.prod(dims[:k])), -1), compute_uv=False)
-        kappa = (sv[0] / sv[c.shape[0] - 1]) ** 2
+    # right-orthonormal cores: M G M^T = I to the Cholesky's rounding; the kernel
+    # looks at D = M F - I (and removes it to second order) unless its condition
+    # bound already keeps it below ~5e-12 (DESIGN 2.2); the represented tensor
+    # above is what parity is stated on
+    for c in got.cores[1:]:
         u = c.cpu().numpy().reshape(c.shape[0], -1)
-        assert np.abs(u @ u.T - np.eye(u.shape[0])).max() <= 1e-13 + 8 * np.finfo(float).eps * kappa
+        assert np.abs(u @ u.T - np.eye(u.shape[0])).max() <= 2e-11
 
 
 def test_truncate_subspace_certificate_rejects_flat_spectrum(cuda):
