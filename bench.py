@@ -208,31 +208,40 @@ def load_peaks():
         return {}
 
 
-def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=None):
-    """The step's dominant kernel by time is the one-sided Jacobi SVD of the
-    truncation (one per core, a sequential chain).  It runs on one 8-CTA
-    cluster (qr.cu jacobi_warp_kernel): one warp per CTA, l/8 CTAs (10 for
-    l = 80), 4 pair slots of 8 lanes per CTA, columns register-resident,
-    block-ordered rounds (in-CTA moves by warp shuffles, 2 l/8 - 1 DSMEM block
-    moves per sweep).  Time one l x l
-    instance live and report its algorithmic FLOPs against the fp64 peak of
-    the SMs it occupies; the bound is the per-round latency chain."""
+def subspace_roofline(T, torch, dev, stream, z, r, calls_per_step=None, step_ms=None):
+    """The step's largest kernel by time is the gap-certified subspace
+    factorisation of the truncation (qr.cu trunc_subspace_kernel, one per core,
+    a sequential chain): ONE CTA holds the l x l Gram and every l x r iterate in
+    shared memory; 12 DMMA products and two blocked Cholesky factorisations with
+    explicit inverses per pass.  Time it live on the Gram of the step's own last
+    unfolding and report its algorithmic FLOPs against the DMMA peak of the one
+    SM it occupies; the bound is that SM's DMMA issue rate plus the 2 x r pivot
+    chain of the Cholesky factorisations."""
     from paper_2409_09471_b200 import _lib
     lib = _lib.load()
-    g = torch.Generator().manual_seed(0)
-    A = torch.randn(10 * l, l, dtype=torch.float64, generator=g)
-    R = torch.linalg.qr(A)[1].to(dev).contiguous()
-    U = torch.empty((l, l), dtype=torch.float64, device=dev)
-    S = torch.empty(l, dtype=torch.float64, device=dev)
-    V = torch.empty((l, l), dtype=torch.float64, device=dev)
-    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
-    lib.ttk_debug_svd_sweeps(cnt.data_ptr())
-    # the config-3 truncation (exact-rank Gram path, round.cu) runs the Jacobi on
-    # R^T of the Cholesky factor without V (only the rotated columns and S are used)
-    call = lambda: lib.ttk_svd_small(l, l, R.data_ptr(), U.data_ptr(), S.data_ptr(), None,
-                                     _lib.stream_ptr(dev))
+    c = z.cores[-1]
+    l = int(c.shape[0])
+    cm = c.reshape(l, -1)
+    G = (cm @ cm.T).contiguous()
+    F = torch.empty((l, l), dtype=torch.float64, device=dev)
+    Mt = torch.empty((l, l), dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    info = torch.zeros(4, dtype=torch.float64, device=dev)
+    call = lambda: _lib.check(lib.ttk_debug_trunc_subspace(l, r, G.data_ptr(), F.data_ptr(), Mt.data_ptr(),
+                                                           flag.data_ptr(), info.data_ptr(), None,
+                                                           _lib.stream_ptr(dev)))
     call()
     torch.cuda.synchronize()
+    if len(z.cores) > 2:
+        # the typical instance is an interior core (flat kept spectrum, one pass); the two
+        # end cores carry the whole spectrum (kappa ~26) and take two passes.  Interior
+        # unfolding: C_{d-2} x_3 F, as the truncation forms it
+        p = z.cores[-2]
+        cm = (p.reshape(-1, l) @ F[:, :r]).reshape(int(p.shape[0]), -1)
+        l = int(p.shape[0])
+        G = (cm @ cm.T).contiguous()
+        call()
+        torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(5):
@@ -240,20 +249,20 @@ def jacobi_roofline(T, torch, dev, stream, l=80, calls_per_step=None, step_ms=No
     b.record(stream)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / 5
-    sweeps = int(cnt.item())
-    lib.ttk_debug_svd_sweeps(None)
-    # per sweep l(l-1)/2 pairs x (3 dot FMAs + the 2x2 rotation of the two columns) per row
-    flops = sweeps * (l * (l - 1) / 2) * (6.0 * l + 6.0 * l)
-    sms = (l + 7) // 8  # CTAs (one per SM) of the warp kernel's cluster
-    peak_sms = sms * 33.9e3 / 148  # GFLOP/s of those SMs: measured DFMA chip peak / SM count (profiles/fp64_peak_r01.log)
+    passes = int(info[2].item())
+    # products (M, N, K) of the first pass (DESIGN 2.2): 4 of r x r x l, 4 of l x r x r, 4 of l x r x l;
+    # a further pass adds 2 + 3 + 3 of them; two (one) Cholesky + triangular inverse of order r per pass
+    mac = lambda n_rrl, n_lrr, n_lrl: n_rrl * r * r * l + n_lrr * l * r * r + n_lrl * l * r * l
+    flops = 2.0 * (mac(4, 4, 4) + (passes - 1) * mac(3, 3, 3)) + (passes + 1) * (2.0 * r ** 3 / 3.0)
+    sm_peak = 37.1e3 / 148  # GFLOP/s of one SM: measured DMMA issue peak / SM count (profiles/fp64_peak_r01.log)
     ach = flops / (ms * 1e-3) / 1e9
-    rounds = sweeps * (l - 1)
-    out = {"kernel": "jacobi_warp_kernel (%d-CTA cluster, one warp per CTA, block-ordered, %dx%d, no V)" % (sms, l, l), "ms": ms,
-           "sweeps": sweeps, "rounds": rounds, "us_per_round": ms * 1e3 / max(rounds, 1),
-           "bound": "latency (sequential rotation rounds; per round: dots, 8-lane reduction, "
-                    "rotation, in-CTA shuffle move; a DSMEM block move every 4 rounds)",
-           "achieved_gflops": ach, "sms": sms, "peak_gflops_of_its_sms": peak_sms,
-           "frac_of_its_sms": ach / peak_sms}
+    out = {"kernel": "trunc_subspace_kernel (one CTA, %dx%d Gram -> rank %d, %d pass%s; second core from the right of the step)"
+                     % (l, l, r, passes, "" if passes == 1 else "es"),
+           "ms": ms, "passes": passes, "certified": int(flag.item()), "angle_bound": float(info[0].item()),
+           "bound": "one SM: DMMA issue rate of the l x r products + the sequential pivot chain of "
+                    "two r x r Cholesky factorisations per pass",
+           "algorithmic_flops": flops, "achieved_gflops": ach, "sms": 1, "peak_gflops_of_its_sms": sm_peak,
+           "frac_of_its_sms": ach / sm_peak}
     if calls_per_step and step_ms:
         out["share_of_step_est"] = calls_per_step * ms / step_ms
         out["share_basis"] = "%d calls/step x this single-call time / ms_per_step" % calls_per_step
@@ -433,8 +442,8 @@ def run_b200(args):
                 "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_flops": mv_flops,
                 "algorithmic_bytes": 8.0 * sum(c.numel() for c in y.cores)}
-    roofline["dominant_kernel"] = jacobi_roofline(T, torch, dev, stream, calls_per_step=len(C["x"]) - 1,
-                                                  step_ms=ms)
+    roofline["dominant_kernel"] = subspace_roofline(T, torch, dev, stream, z, int(C["max_rank"]),
+                                                    calls_per_step=len(C["x"]) - 1, step_ms=ms)
 
     # ---- end-to-end through the public API with host buffers ----
     host_op = [torch.as_tensor(g).pin_memory() for g in C["op"]]
@@ -515,7 +524,7 @@ def run_b200(args):
     dk["chip_frac"] = dk["achieved_gflops"] / 1e3 / peak_tf
     roofline["note"] = ("frac/achieved: the matvec GEMM (the one FLOP-bound kernel, one launch per step); "
                         "step_frac: whole step (matvec + RTO sweep FLOPs / step time) vs the same fp64 peak; "
-                        "dominant_kernel: the truncation's Jacobi SVD (largest share of step time), "
+                        "dominant_kernel: the truncation's subspace factorisation (largest single kernel of the step), "
                         "chip_frac against the whole chip's fp64 peak")
 
     line = {"metric": METRIC, "value": flops * world / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,

@@ -71,6 +71,40 @@ def test_config3_full_size_vs_oracle(cuda):
         assert np.abs(g - y[k]).max() <= 1e-13 * np.abs(y[k]).max()
 
 
+def test_config3_two_problems_in_flight(cuda):
+    """Two host threads, each driving the headline step on its own stream (bench.py's
+    in-flight mode): every result is the same tensor as a lone run.  Guards the
+    concurrent-stream rule of the sweeps' GEMM routing (DESIGN 6.2: with the TMA-staged
+    GEMM left on, overlapping problems returned corrupted cores in ~1 of 3 runs)."""
+    import threading
+    C = configs.config3()
+    spec = T.RoundSpec(C["rel_tol"], C["max_rank"])
+    drm = [torch.as_tensor(g, device=cuda) for g in C["drm"]]
+    op, x = T.TTOperator(C["op"], device=cuda), T.TTVector(C["x"], device=cuda)
+    ref = T.tt_matvec_round_rto(op, x, spec, drm, device=cuda)
+    nref = float(T.tt_norm(ref))
+    torch.cuda.synchronize()
+    out = {}
+
+    def worker(i):
+        torch.cuda.set_device(cuda)
+        s = torch.cuda.Stream(cuda)
+        with torch.cuda.stream(s):
+            worst = 0.0
+            for _ in range(4):
+                y = T.tt_matvec_round_rto(op, x, spec, drm, device=cuda)
+                assert y.ranks == ref.ranks
+                worst = max(worst, float(T.tt_norm(T.tt_add(y, T.tt_scale(ref, -1.0)))) / nref)
+            s.synchronize()
+        out[i] = worst
+
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    [t.start() for t in ths]
+    [t.join() for t in ths]
+    # ||a - b|| through dot products: cancellation floor ~1e-8; a corrupted core gives >= 1e-4
+    assert sorted(out) == [0, 1] and max(out.values()) <= 1e-6, out
+
+
 # ---------------------------------------------------------------------------
 # config 2: sum of 10 rank-20 TTs (d=16, n=64) -> rank 200; RTO l=50 -> 40
 
