@@ -295,7 +295,9 @@ int ttk_tt_truncate_host(int d, const int* dims, const int* ranks, const double*
  * truncations redone through the QR path after a failed Gram certificate [2] */
 int ttk_debug_truncate_paths(long long* counts);
 /* the same plus [3] cores factored by the gap-certified subspace kernel and [4] truncations
- * redone through the Jacobi Gram path after a failed subspace certificate; writes min(n, 5) */
+ * redone through the Jacobi Gram path after a failed subspace certificate, [5] RTO left sweeps
+ * accepted with the deferred CholeskyQR2 check, [6] RTO left sweeps redone with the per-core
+ * check; writes min(n, 7) */
 int ttk_debug_truncate_paths_ex(long long* counts, int n);
 size_t ttk_tt_truncate_ws_bytes(int d, const int* dims, const int* ranks);
 

@@ -3272,6 +3272,94 @@ extern "C" int ttk_debug_trunc_subspace(int l, int r, const double* G, double* F
   return launch_trunc_subspace(l, r, G, F, Mt, l, flag, info, (cudaStream_t)stream, prof);
 }
 
+// --------------------------------------------------------------------------
+// Gram matrix of a wide unfolding: G = C C^T for the row-major l x m C (l <= 96,
+// row stride m) -- the per-core Gram of the truncation (round.cu).  CTA b
+// stages columns [b kc, (b + 1) kc) of every row in shared memory once (kc a
+// multiple of 16, the tail zero-filled), forms the upper 16 x 16 tiles of its
+// l x l partial on DMMA (both operands of every tile come from the one staged
+// slab) and stores them; gram_wide_reduce_kernel sums the partials in a fixed
+// order (8 lanes per element, one L2 round trip) and mirrors the triangle.
+// Replaces the generic split-K GEMM + reduce for this shape (80 x 80 x 8192:
+// 19 + 4.6 us), which re-stages C for every 64 x 32 output tile.
+constexpr int kGwThreads = 256;
+
+__global__ void __launch_bounds__(kGwThreads)
+    gram_wide_partial_kernel(int l, long long m, int kc, const double* __restrict__ C, double* __restrict__ part) {
+  extern __shared__ double gw_sm[];
+  const int ld = kc + 4;  // kc is a multiple of 16: stride 4 mod 16 doubles
+  const long long c0 = (long long)blockIdx.x * kc;
+  const int cols = (int)min((long long)kc, m - c0);
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, nw = nt >> 5;
+  for (int e = tid; e < l * kc; e += nt) {
+    const int r = e / kc, c = e - r * kc;
+    const bool ok = c < cols;
+    cp_async8(gw_sm + r * ld + c, ok ? C + (long long)r * m + c0 + c : C, ok);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int tn = (l + 15) >> 4, tiles = tn * (tn + 1) / 2;
+  double* mine = part + (size_t)blockIdx.x * l * l;
+  for (int tt = warp; tt < tiles; tt += nw) {
+    int ti = 0, rem = tt;
+    while (rem >= tn - ti) { rem -= tn - ti; ++ti; }
+    const int tj = ti + rem;
+    const int i0 = ti * 16, j0 = tj * 16;
+    warp_dmma16(min(16, l - i0), min(16, l - j0), kc, gw_sm + (size_t)i0 * ld, ld, 1, gw_sm + (size_t)j0 * ld, 1, ld,
+                mine + (size_t)i0 * l + j0, l, false);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    gram_wide_reduce_kernel(int l, int nparts, const double* __restrict__ part, double* __restrict__ G) {
+  const int ll = l * l;
+  const int lane8 = threadIdx.x & 7;
+  const int e = blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  double s = 0.0;
+  if (e < ll) {
+    const int i = e / l, c = e - i * l;
+    // lower tiles mirror the stored upper ones
+    const int src = ((i >> 4) > (c >> 4)) ? c * l + i : e;
+    double v[16];
+    for (int p0 = lane8; p0 < nparts; p0 += 8 * 16) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int pp = p0 + 8 * u;
+        v[u] = pp < nparts ? __ldcg(part + (size_t)pp * ll + src) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  if (lane8 == 0 && e < ll) G[e] = s;
+}
+
+bool gram_wide_fits(int l, long long m, size_t ws_bytes) {
+  if (l < 16 || l > 96 || m < 1024) return false;
+  const long long per = (m + num_sms() - 1) / num_sms();
+  const int kc = (int)std::max<long long>(16, (per + 15) & ~15LL);
+  const long long nparts = (m + kc - 1) / kc;
+  return kc <= 256 && (size_t)nparts * l * l * sizeof(double) <= ws_bytes;
+}
+
+// G (l x l, row-major) = C C^T; ws: partials (gram_wide_fits checked by the caller)
+int gram_wide(int l, long long m, const double* C, double* G, void* ws, cudaStream_t st) {
+  const long long per = (m + num_sms() - 1) / num_sms();
+  const int kc = (int)std::max<long long>(16, (per + 15) & ~15LL);
+  const int nparts = (int)((m + kc - 1) / kc);
+  const size_t smem = sizeof(double) * (size_t)l * (kc + 4);
+  TTK_TRY(qr_set_smem((const void*)gram_wide_partial_kernel, (int)(sizeof(double) * 96 * (256 + 4))));
+  gram_wide_partial_kernel<<<nparts, kGwThreads, smem, st>>>(l, m, kc, C, reinterpret_cast<double*>(ws));
+  TTK_CHECK_LAUNCH();
+  gram_wide_reduce_kernel<<<(l * l + 31) / 32, 256, 0, st>>>(l, nparts, reinterpret_cast<const double*>(ws), G);
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
 __global__ void copy_strided_kernel(int m, int l, const double* __restrict__ X, long long x_rs,
                                     long long x_cs, double* __restrict__ Y, long long y_rs, long long y_cs) {
   const long long n = (long long)m * l;
@@ -3836,9 +3924,13 @@ __global__ void normalize_cols_kernel(int m, int n, double* X, long long x_rs, l
 //     5. R = Q^T Y (range(Q) covers range(Y) to working precision).
 //   *deficient is set to 1 when Y needed the robust path with rho < l, so a sweep
 //   can try it first on the next core (fewer launches, one host sync less).
+// defer_status (optional, 8 device ints, zeroed by the caller): the fused
+// kernel's acceptance flags go there and the host does NOT wait for them --
+// *ok = 1 optimistically; the caller checks [0] and [1] of every slot later
+// and redoes its sweep without deferral if one is nonzero.
 int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, double* Q, long long q_rs,
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* ok,
-            bool robust_first, int* deficient) {
+            bool robust_first, int* deficient, int* defer_status = nullptr) {
   *ok = 0;
   if (deficient) *deficient = 0;
   if (l > kCholMaxCols || m < l) return kOk;
@@ -3881,10 +3973,11 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     }
     static const double fo = knob_env("TTK_NEAR_ID_FIRST_ORDER") ? atof(knob_env("TTK_NEAR_ID_FIRST_ORDER"))
                                                                    : kNearIdFirstOrderMax;
-    TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 8 * sizeof(int), st));
+    int* const fstatus = defer_status ? defer_status : status;
+    if (!defer_status) TTK_CHECK_CUDA(cudaMemsetAsync(status, 0, 8 * sizeof(int), st));
     FqParams fp{};
     fp.m = m; fp.l = l; fp.Y = Y; fp.y_rs = y_rs; fp.y_cs = y_cs; fp.Q = Q; fp.q_rs = q_rs; fp.R = R;
-    fp.part = (double*)split; fp.G = G; fp.R1 = R1; fp.R2 = R2; fp.I2 = I2; fp.status = status;
+    fp.part = (double*)split; fp.G = G; fp.R1 = R1; fp.R2 = R2; fp.I2 = I2; fp.status = fstatus;
     fp.first_order_max = fo;
     // tile rows: spread the tall dimension over up to kFqTiles CTAs (the tile
     // phases are per-SM DMMA work: 10240 x 80 in 80-row tiles instead of 128);
@@ -3902,6 +3995,11 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
     if (le == cudaSuccess) {
       fast_tried = true;
       TTK_CHECK_LAUNCH();
+      if (defer_status) {  // flags checked by the caller after its sweep
+        *ok = 1;
+        g_qr_last_path_set(1);
+        return kOk;
+      }
       TTK_CHECK_CUDA(cudaMemcpyAsync(hs, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
       TTK_SYNC(st);
       if (hs[0] == 0 && hs[1] == 0) {
@@ -4046,7 +4144,7 @@ static void qr_check_report(int m, int l, const std::vector<double>& hy, const d
 }
 
 int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
-            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint) {
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint, int* defer_status) {
   if (m <= 0 || l <= 0) return kOk;
   if (l > kQrMaxCols) {
     TTK_REQUIRE(l <= kWideMaxCols, kInvalidValue, "qr: %d x %d exceeds %d columns", m, l, kWideMaxCols);
@@ -4083,7 +4181,8 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
       cudaFree(tmp);
     }
     int deficient = 0;
-    TTK_TRY(cholqr2(m, l, Y, y_rs, y_cs, Q, q_rs, q_cs, R, cws, cbytes, st, &ok, hint && *hint, &deficient));
+    TTK_TRY(cholqr2(m, l, Y, y_rs, y_cs, Q, q_rs, q_cs, R, cws, cbytes, st, &ok, hint && *hint, &deficient,
+                    defer_status));
     if (hint) *hint = ok && deficient;
     if (ok && g_qr_check && R) qr_check_report(m, l, hy, Q, q_rs, q_cs, R, st);
     if (ok) return kOk;

@@ -37,7 +37,8 @@ size_t tsqr_ws_bytes(int m, int l);
 // hint (in/out, optional): 1 = the previous factorisation of this sweep needed
 // the rank-robust path, try it first (one fast-path attempt and host sync less)
 int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
-            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint = nullptr);
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint = nullptr,
+            int* defer_status = nullptr);
 size_t qr_auto_ws_bytes(int m, int l);
 
 // One-sided (Hestenes) Jacobi SVD of B (k x l, row-major, ldb = l), k, l <= kWideMaxCols:
@@ -74,6 +75,9 @@ constexpr int kCholBlockedMaxCols = 112;
 // gap-certified dominant-subspace factor of the exact-rank truncation (qr.cu):
 // F (l x r) and M^T (l x r), row stride ldo; *flag = 1 when certified
 bool trunc_subspace_fits(int l, int r);
+// G = C C^T for a wide row-major C (l x m): staged-slab partials + fixed-order reduce
+bool gram_wide_fits(int l, long long m, size_t ws_bytes);
+int gram_wide(int l, long long m, const double* C, double* G, void* ws, cudaStream_t st);
 int launch_trunc_subspace(int l, int r, const double* G, double* F, double* Mt, int ldo, int* flag, double* info,
                           cudaStream_t st, long long* prof = nullptr);
 

@@ -163,6 +163,8 @@ std::atomic<long long> g_trunc_gram{0}, g_trunc_qr{0}, g_trunc_redo{0};
 // cores factored by the gap-certified subspace kernel, and sweeps of it redone
 // through the Jacobi Gram path after a failed certificate
 std::atomic<long long> g_trunc_fast{0}, g_trunc_fast_redo{0};
+// RTO left sweeps accepted with the deferred CholeskyQR2 check / redone with the per-core check
+std::atomic<long long> g_rto_deferred{0}, g_rto_defer_redo{0};
 
 // Shapes whose subspace sweep failed its certificate skip the subspace kernel
 // for the next kFastSkip truncations of the same shape (a gap-free spectrum,
@@ -499,7 +501,8 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
     if (g_pending[k & 1]) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_g[k & 1], 0));
     if (gram_on && m >= r0 && r0 >= 2 && r0 <= kCholBlockedMaxCols && jacobi_fits_v(r0, r0)) {
       // G = C C^T (r0 x r0), C = cur (r0 x m, row-major)
-      TTK_TRY(gemm1(r0, r0, m, cur, m, 1, cur, 1, m, tG, r0, 1, split_ws, st));
+      if (gram_wide_fits(r0, m, kSplitKBytes)) TTK_TRY(gram_wide(r0, m, cur, tG, split_ws, st));
+      else TTK_TRY(gemm1(r0, r0, m, cur, m, 1, cur, 1, m, tG, r0, 1, split_ws, st));
       const int rk = std::min(max_rank > 0 ? max_rank : r0, r0);
       if (fast_on && trunc_subspace_fits(r0, rk)) {
         // F = C Y^T -> tL, M^T -> tU (Y = M C), certificate -> gflags
@@ -641,9 +644,9 @@ int ttk_debug_truncate_paths(long long* counts) {
 }
 
 int ttk_debug_truncate_paths_ex(long long* counts, int n) {
-  const long long v[5] = {g_trunc_gram.load(), g_trunc_qr.load(), g_trunc_redo.load(), g_trunc_fast.load(),
-                          g_trunc_fast_redo.load()};
-  for (int i = 0; i < n && i < 5; ++i) counts[i] = v[i];
+  const long long v[7] = {g_trunc_gram.load(), g_trunc_qr.load(), g_trunc_redo.load(), g_trunc_fast.load(),
+                          g_trunc_fast_redo.load(), g_rto_deferred.load(), g_rto_defer_redo.load()};
+  for (int i = 0; i < n && i < 7; ++i) counts[i] = v[i];
   return kOk;
 }
 
@@ -667,8 +670,14 @@ size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L) {
     qr = std::max(qr, qr_auto_ws_bytes((int)m, L[c]));
   }
   return wsum + tsum + align_up(ymax * 8, 256) + 2 * align_up(zmax * 8, 256) + 2 * align_up(mmax * 8, 256) +
-         align_up(qr, 256) + 2 * kSplitKBytes + 65536;
+         align_up(qr, 256) + 2 * kSplitKBytes + 65536 + align_up((size_t)d * 8 * sizeof(int), 256);
 }
+
+// Left sweeps whose deferred CholeskyQR2 acceptance failed (rank-deficient or
+// ill-conditioned sketches, e.g. the solver's roundings) run the next kDeferSkip
+// sweeps of the same shape with the per-core host check instead.
+constexpr int kDeferSkip = 16;
+thread_local std::unordered_map<uint64_t, int> g_defer_skip;
 
 // Randomize-then-orthogonalize sweeps.  X: d cores (R[k], n_k, R[k+1]); G: DRM
 // cores (L[k], n_k, L[k+1]) with L[0] = L[d] = 1 and, for every cut c,
@@ -721,7 +730,8 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
   ar.used = qoff + qrb;
   void* split_ws = ar.take<char>(kSplitKBytes);
   void* split_side = ar.take<char>(kSplitKBytes);
-  TTK_REQUIRE(split_side != nullptr, kWorkspace, "rto: workspace too small");
+  int* qstat = ar.take<int>((size_t)d * 8);  // acceptance flags of the left sweep's factorisations
+  TTK_REQUIRE(split_side != nullptr && qstat != nullptr, kWorkspace, "rto: workspace too small");
 
   // ---- right sweep: W_c = sum_i X_c[:, i, :] W_{c+1} G_c[:, i, :]^T ----
   for (int c = d - 1; c >= 1; --c) {
@@ -754,9 +764,25 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
     TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_m, cudaEventDisableTiming));
     TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_z, cudaEventDisableTiming));
   }
+  // The CholeskyQR2 of every step is accepted on the device (flags in qstat) and
+  // the host looks at all of them once, after the sweep: a per-core wait cost
+  // ~30 us of host round trip per core (config 3: 0.9 ms of a 13.7 ms step).  If
+  // a factorisation was refused the sweep is redone with the per-core check, which
+  // takes the rank-robust path where needed.
+  const uint64_t dkey = trunc_shape_key(d, dims, R, L[d / 2]);
+  bool defer = knob_env("TTK_RTO_NO_DEFER") == nullptr;
+  if (defer) {
+    auto it = g_defer_skip.find(dkey);
+    if (it != g_defer_skip.end() && it->second > 0) {
+      --it->second;
+      defer = false;
+    }
+  }
+  TTK_TRY(wait_core(0));
+  for (int pass = 0; pass < 2; ++pass) {
+  if (defer) TTK_CHECK_CUDA(cudaMemsetAsync(qstat, 0, sizeof(int) * 8 * (size_t)d, st));
   int qr_hint = 0;  // per sweep: try the rank-robust QR first after it was needed
   const double* Mprev = nullptr;
-  TTK_TRY(wait_core(0));
   for (int c = 1; c < d; ++c) {
     const int np = dims[c - 1];
     const int m = L[c - 1] * np, l = L[c], rc = R[c];
@@ -782,7 +808,7 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
       Z = zdst;
     }
     // Q (m x l) -> out core c-1, (L_{c-1}, n_{c-1}, L_c)
-    TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st, &qr_hint));
+    TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st, &qr_hint, defer ? qstat + 8 * c : nullptr));
     if (c > 1) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_z, 0));
     // M_c (l x R_c) = Q^T Z   (K = m, split over the long dimension)
     double* Mc = Mbuf[c & 1];
@@ -793,6 +819,21 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
   {
     const int c = d - 1, l = L[c], rc = R[c], n = dims[c];
     TTK_TRY(gemm1(l, n, rc, Mprev, rc, 1, X[c], n, 1, out[d - 1], n, 1, split_ws, st));
+  }
+  if (!defer) break;
+  int* hq = reinterpret_cast<int*>(g_pinned.get(sizeof(int) * 8 * (size_t)d + 64));
+  TTK_REQUIRE(hq != nullptr, kCudaError, "rto: cannot allocate pinned scratch");
+  TTK_CHECK_CUDA(cudaMemcpyAsync(hq, qstat, sizeof(int) * 8 * (size_t)d, cudaMemcpyDeviceToHost, st));
+  TTK_SYNC(st);
+  bool refused = false;
+  for (int c = 1; c < d; ++c) refused = refused || hq[8 * c] != 0 || hq[8 * c + 1] != 0;
+  if (!refused) {
+    g_rto_deferred.fetch_add(1, std::memory_order_relaxed);
+    break;
+  }
+  g_rto_defer_redo.fetch_add(1, std::memory_order_relaxed);
+  g_defer_skip[dkey] = kDeferSkip;
+  defer = false;  // second pass: per-core acceptance
   }
   return kOk;
 }

@@ -500,12 +500,42 @@ def test_truncate_gram_path_certified(cuda):
         assert np.abs(u @ u.T - np.eye(u.shape[0])).max() <= 1e-12
 
 
-def _trunc_paths_ex():
+def _trunc_paths_ex(n=5):
     import ctypes
     from paper_2409_09471_b200 import _lib
-    c = (ctypes.c_longlong * 5)()
-    _lib.load().ttk_debug_truncate_paths_ex(ctypes.addressof(c), 5)
+    c = (ctypes.c_longlong * n)()
+    _lib.load().ttk_debug_truncate_paths_ex(ctypes.addressof(c), n)
     return np.array(list(c))
+
+
+def test_rto_sweeps_deferred_acceptance(cuda):
+    """The left sweep accepts its CholeskyQR2 factorisations on the device and checks the
+    flags once per sweep: a well-conditioned sweep takes no per-core host wait; a sweep with
+    exactly rank-deficient sketches is redone with the per-core check (rank-robust path), the
+    next sweeps of that shape skip the deferral, and both represent the input exactly."""
+    dims = [40, 36, 44, 40, 36]
+    x = O.tt_random(dims, [40, 48, 48, 40], seed=21)
+    drm = O.drm_new(dims, [34, 40, 40, 34], seed=22)
+    c0 = _trunc_paths_ex(7)
+    got = T.rto_sweeps(T.TTVector(x, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm])
+    d = _trunc_paths_ex(7) - c0
+    assert (d[5], d[6]) == (1, 0)
+    want = O.rto_sweeps(x, drm)
+    assert O.rel_diff(tt_np(got), want) <= 1e-10
+    # nominal ranks 2 x the true ranks: every sketch Gram is singular
+    y = O.tt_random(dims, [17, 20, 20, 17], seed=23)
+    z = O.add(y, O.scale(y, 0.5))
+    drm2 = O.drm_new(dims, [34, 40, 40, 34], seed=24)
+    c0 = _trunc_paths_ex(7)
+    got = T.rto_sweeps(T.TTVector(z, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm2])
+    d = _trunc_paths_ex(7) - c0
+    assert (d[5], d[6]) == (0, 1)
+    assert O.rel_diff(tt_np(got), z) <= 1e-10
+    got2 = T.rto_sweeps(T.TTVector(z, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm2])
+    d2 = _trunc_paths_ex(7) - c0 - d
+    assert (d2[5], d2[6]) == (0, 0)
+    for a, b in zip(got.cores, got2.cores):
+        assert torch.equal(a, b)
 
 
 def _gapped_left_orth(dims, r, s, eps, seed):
