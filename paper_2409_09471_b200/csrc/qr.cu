@@ -3930,7 +3930,7 @@ __global__ void normalize_cols_kernel(int m, int n, double* X, long long x_rs, l
 // and redoes its sweep without deferral if one is nonzero.
 int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, double* Q, long long q_rs,
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* ok,
-            bool robust_first, int* deficient, int* defer_status = nullptr) {
+            bool robust_first, int* deficient, int* defer_status = nullptr, int* fused_ok = nullptr) {
   *ok = 0;
   if (deficient) *deficient = 0;
   if (l > kCholMaxCols || m < l) return kOk;
@@ -4004,6 +4004,7 @@ int cholqr2(int m, int l, const double* Y, long long y_rs, long long y_cs, doubl
       TTK_SYNC(st);
       if (hs[0] == 0 && hs[1] == 0) {
         *ok = 1;
+        if (fused_ok) *fused_ok = 1;
         g_qr_last_path_set(1);
         return kOk;
       }
@@ -4144,7 +4145,9 @@ static void qr_check_report(int m, int l, const std::vector<double>& hy, const d
 }
 
 int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
-            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint, int* defer_status) {
+            long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint, int* defer_status,
+            int* fused_ok) {
+  if (fused_ok) *fused_ok = 0;
   if (m <= 0 || l <= 0) return kOk;
   if (l > kQrMaxCols) {
     TTK_REQUIRE(l <= kWideMaxCols, kInvalidValue, "qr: %d x %d exceeds %d columns", m, l, kWideMaxCols);
@@ -4182,7 +4185,7 @@ int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, doubl
     }
     int deficient = 0;
     TTK_TRY(cholqr2(m, l, Y, y_rs, y_cs, Q, q_rs, q_cs, R, cws, cbytes, st, &ok, hint && *hint, &deficient,
-                    defer_status));
+                    defer_status, fused_ok));
     if (hint) *hint = ok && deficient;
     if (ok && g_qr_check && R) qr_check_report(m, l, hy, Q, q_rs, q_cs, R, st);
     if (ok) return kOk;

@@ -38,7 +38,7 @@ size_t tsqr_ws_bytes(int m, int l);
 // the rank-robust path, try it first (one fast-path attempt and host sync less)
 int qr_auto(int m, int l, const double* A, long long a_rs, long long a_cs, double* Q, long long q_rs,
             long long q_cs, double* R, void* ws, size_t ws_bytes, cudaStream_t st, int* hint = nullptr,
-            int* defer_status = nullptr);
+            int* defer_status = nullptr, int* fused_ok = nullptr);
 size_t qr_auto_ws_bytes(int m, int l);
 
 // One-sided (Hestenes) Jacobi SVD of B (k x l, row-major, ldb = l), k, l <= kWideMaxCols:

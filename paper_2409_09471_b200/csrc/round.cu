@@ -673,11 +673,11 @@ size_t ttk_rto_ws_bytes(int d, const int* dims, const int* R, const int* L) {
          align_up(qr, 256) + 2 * kSplitKBytes + 65536 + align_up((size_t)d * 8 * sizeof(int), 256);
 }
 
-// Left sweeps whose deferred CholeskyQR2 acceptance failed (rank-deficient or
-// ill-conditioned sketches, e.g. the solver's roundings) run the next kDeferSkip
-// sweeps of the same shape with the per-core host check instead.
-constexpr int kDeferSkip = 16;
-thread_local std::unordered_map<uint64_t, int> g_defer_skip;
+// Shapes whose last left sweep had every factorisation accepted on the fused
+// fast path: only those defer the acceptance check (the solver's roundings --
+// rank-deficient sketches, a new shape every iteration -- never pay for a
+// wasted sweep); a refused deferred sweep takes the shape out again.
+thread_local std::unordered_map<uint64_t, bool> g_defer_ok;
 
 // Randomize-then-orthogonalize sweeps.  X: d cores (R[k], n_k, R[k+1]); G: DRM
 // cores (L[k], n_k, L[k+1]) with L[0] = L[d] = 1 and, for every cut c,
@@ -769,15 +769,13 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
   // ~30 us of host round trip per core (config 3: 0.9 ms of a 13.7 ms step).  If
   // a factorisation was refused the sweep is redone with the per-core check, which
   // takes the rank-robust path where needed.
-  const uint64_t dkey = trunc_shape_key(d, dims, R, L[d / 2]);
-  bool defer = knob_env("TTK_RTO_NO_DEFER") == nullptr;
-  if (defer) {
-    auto it = g_defer_skip.find(dkey);
-    if (it != g_defer_skip.end() && it->second > 0) {
-      --it->second;
-      defer = false;
-    }
+  const uint64_t dkey = trunc_shape_key(d, dims, R, 0) ^ (trunc_shape_key(d, dims, L, 1) * 0x9E3779B97F4A7C15ull);
+  bool defer = false;
+  if (knob_env("TTK_RTO_NO_DEFER") == nullptr) {
+    auto it = g_defer_ok.find(dkey);
+    defer = it != g_defer_ok.end() && it->second;
   }
+  bool all_fused = true;
   TTK_TRY(wait_core(0));
   for (int pass = 0; pass < 2; ++pass) {
   if (defer) TTK_CHECK_CUDA(cudaMemsetAsync(qstat, 0, sizeof(int) * 8 * (size_t)d, st));
@@ -808,7 +806,10 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
       Z = zdst;
     }
     // Q (m x l) -> out core c-1, (L_{c-1}, n_{c-1}, L_c)
-    TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st, &qr_hint, defer ? qstat + 8 * c : nullptr));
+    int fused_ok = 0;
+    TTK_TRY(qr_auto(m, l, Y, l, 1, out[c - 1], l, 1, nullptr, qws, qrb, st, &qr_hint, defer ? qstat + 8 * c : nullptr,
+                    &fused_ok));
+    all_fused = all_fused && fused_ok;
     if (c > 1) TTK_CHECK_CUDA(cudaStreamWaitEvent(st, ev_z, 0));
     // M_c (l x R_c) = Q^T Z   (K = m, split over the long dimension)
     double* Mc = Mbuf[c & 1];
@@ -820,7 +821,11 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
     const int c = d - 1, l = L[c], rc = R[c], n = dims[c];
     TTK_TRY(gemm1(l, n, rc, Mprev, rc, 1, X[c], n, 1, out[d - 1], n, 1, split_ws, st));
   }
-  if (!defer) break;
+  if (!defer) {
+    if (g_defer_ok.size() > 4096) g_defer_ok.clear();
+    g_defer_ok[dkey] = all_fused;
+    break;
+  }
   int* hq = reinterpret_cast<int*>(g_pinned.get(sizeof(int) * 8 * (size_t)d + 64));
   TTK_REQUIRE(hq != nullptr, kCudaError, "rto: cannot allocate pinned scratch");
   TTK_CHECK_CUDA(cudaMemcpyAsync(hq, qstat, sizeof(int) * 8 * (size_t)d, cudaMemcpyDeviceToHost, st));
@@ -832,8 +837,9 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
     break;
   }
   g_rto_defer_redo.fetch_add(1, std::memory_order_relaxed);
-  g_defer_skip[dkey] = kDeferSkip;
+  g_defer_ok[dkey] = false;
   defer = false;  // second pass: per-core acceptance
+  all_fused = true;
   }
   return kOk;
 }

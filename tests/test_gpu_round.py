@@ -509,31 +509,37 @@ def _trunc_paths_ex(n=5):
 
 
 def test_rto_sweeps_deferred_acceptance(cuda):
-    """The left sweep accepts its CholeskyQR2 factorisations on the device and checks the
-    flags once per sweep: a well-conditioned sweep takes no per-core host wait; a sweep with
-    exactly rank-deficient sketches is redone with the per-core check (rank-robust path), the
-    next sweeps of that shape skip the deferral, and both represent the input exactly."""
-    dims = [40, 36, 44, 40, 36]
+    """The left sweep of a shape whose last sweep stayed on the fused CholeskyQR2 fast path
+    accepts its factorisations on the device and checks the flags once per sweep (no per-core
+    host wait); a deferred sweep that meets exactly rank-deficient sketches is redone with the
+    per-core check (rank-robust path) and takes the shape out of the deferral again.  Every
+    result represents its input exactly."""
+    dims = [40, 36, 44, 40, 41]  # a shape no other test uses
     x = O.tt_random(dims, [40, 48, 48, 40], seed=21)
-    drm = O.drm_new(dims, [34, 40, 40, 34], seed=22)
+    drm = [torch.as_tensor(g, device=cuda) for g in O.drm_new(dims, [34, 40, 40, 34], seed=22)]
+    xv = T.TTVector(x, device=cuda)
     c0 = _trunc_paths_ex(7)
-    got = T.rto_sweeps(T.TTVector(x, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm])
-    d = _trunc_paths_ex(7) - c0
-    assert (d[5], d[6]) == (1, 0)
-    want = O.rto_sweeps(x, drm)
-    assert O.rel_diff(tt_np(got), want) <= 1e-10
-    # nominal ranks 2 x the true ranks: every sketch Gram is singular
-    y = O.tt_random(dims, [17, 20, 20, 17], seed=23)
+    first = T.rto_sweeps(xv, drm)
+    d1 = _trunc_paths_ex(7) - c0
+    assert (d1[5], d1[6]) == (0, 0)  # unknown shape: per-core check
+    got = T.rto_sweeps(xv, drm)
+    d2 = _trunc_paths_ex(7) - c0 - d1
+    assert (d2[5], d2[6]) == (1, 0)  # proven shape: deferred
+    for a, b in zip(first.cores, got.cores):
+        assert torch.equal(a, b)
+    assert O.rel_diff(tt_np(got), O.rto_sweeps(x, O.drm_new(dims, [34, 40, 40, 34], seed=22))) <= 1e-10
+    # same nominal shape, true ranks halved: every sketch Gram is singular
+    y = O.tt_random(dims, [20, 24, 24, 20], seed=23)
     z = O.add(y, O.scale(y, 0.5))
-    drm2 = O.drm_new(dims, [34, 40, 40, 34], seed=24)
+    zv = T.TTVector(z, device=cuda)
     c0 = _trunc_paths_ex(7)
-    got = T.rto_sweeps(T.TTVector(z, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm2])
-    d = _trunc_paths_ex(7) - c0
-    assert (d[5], d[6]) == (0, 1)
+    got = T.rto_sweeps(zv, drm)
+    d3 = _trunc_paths_ex(7) - c0
+    assert (d3[5], d3[6]) == (0, 1)  # refused, redone
     assert O.rel_diff(tt_np(got), z) <= 1e-10
-    got2 = T.rto_sweeps(T.TTVector(z, device=cuda), [torch.as_tensor(g, device=cuda) for g in drm2])
-    d2 = _trunc_paths_ex(7) - c0 - d
-    assert (d2[5], d2[6]) == (0, 0)
+    got2 = T.rto_sweeps(zv, drm)
+    d4 = _trunc_paths_ex(7) - c0 - d3
+    assert (d4[5], d4[6]) == (0, 0)  # back to the per-core check
     for a, b in zip(got.cores, got2.cores):
         assert torch.equal(a, b)
 
