@@ -2680,13 +2680,14 @@ __device__ __forceinline__ void warp_dmma16(int M, int N, int K, const double* A
   const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
   const int ma = fr, mb = 8 + fr;
   double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
-  const bool full = (M == 16) && (N == 16) && ((K & 15) == 0);
+  const bool full = (M == 16) && (N == 16) && ((K & 3) == 0);
   if (full) {
     const double* pa0 = A + ma * a_rs + fk * a_cs;
     const double* pa1 = A + mb * a_rs + fk * a_cs;
     const double* pb0 = B + fk * b_rs + ma * b_cs;
     const double* pb1 = B + fk * b_rs + mb * b_cs;
-    for (int k0 = 0; k0 < K; k0 += 16) {
+    int k0 = 0;
+    for (; k0 + 16 <= K; k0 += 16) {
       double a0[4], a1[4], b0[4], b1[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -2703,6 +2704,13 @@ __device__ __forceinline__ void warp_dmma16(int M, int N, int K, const double* A
         dmma_8x8x4(c10, a1[q], b0[q]);
         dmma_8x8x4(c11, a1[q], b1[q]);
       }
+    }
+    for (; k0 < K; k0 += 4) {  // K not a multiple of 16: single k steps
+      const double a0 = pa0[k0 * a_cs], a1 = pa1[k0 * a_cs], b0 = pb0[k0 * b_rs], b1 = pb1[k0 * b_rs];
+      dmma_8x8x4(c00, a0, b0);
+      dmma_8x8x4(c01, a0, b1);
+      dmma_8x8x4(c10, a1, b0);
+      dmma_8x8x4(c11, a1, b1);
     }
     const double sg = neg ? -1.0 : 1.0;
     double dv[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -2850,6 +2858,25 @@ __device__ void tri_inv_offdiag(const double* __restrict__ A, double* __restrict
     __syncthreads();
   }
 }
+
+// C (l x l, row stride ldc) = Y^T Y for the K x l tile Y (row stride ldy) in
+// shared memory: upper 16 x 16 tiles only (ti <= tj), one warp per tile -- 15
+// tiles instead of 25 for l = 80, one round of the 16 warps instead of two.
+// The lower tiles of C are left untouched.
+__device__ __forceinline__ void block_gram_upper(int l, int K, const double* Y, int ldy, double* C, int ldc) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tn = (l + 15) >> 4, tiles = tn * (tn + 1) / 2;
+  for (int tt = warp; tt < tiles; tt += nw) {
+    int ti = 0, rem = tt;
+    while (rem >= tn - ti) { rem -= tn - ti; ++ti; }
+    const int i0 = ti * 16, j0 = (ti + rem) * 16;
+    warp_dmma16(min(16, l - i0), min(16, l - j0), K, Y + i0, 1, ldy, Y + j0, ldy, 1, C + (size_t)i0 * ldc + j0, ldc,
+                false);
+  }
+}
+
+// element (i, c) of an l x l matrix stored with its upper 16 x 16 tiles only
+__device__ __forceinline__ bool in_upper_tiles(int i, int c) { return (i >> 4) <= (c >> 4); }
 
 // body shared by chol_blocked_kernel and the fused CholeskyQR2 kernel (block
 // size kCbThreads; sm: 2 l cb_ld(l) + 256 ceil(l/16) doubles)
@@ -3622,7 +3649,8 @@ struct FqParams {
   int tr;         // rows per tile CTA
 };
 
-__device__ __forceinline__ void fq_reduce(const double* part, int nparts, int ll, double* G) {
+__device__ __forceinline__ void fq_reduce(const double* part, int nparts, int l, double* G) {
+  const int ll = l * l;
   // 8 lanes per element: lane j sums partials j, j + 8, ... (all loads in
   // flight at once), then a fixed 3-level butterfly -- deterministic, and one
   // L2 round trip instead of nparts dependent ones
@@ -3634,12 +3662,17 @@ __device__ __forceinline__ void fq_reduce(const double* part, int nparts, int ll
     const int e = ebase + it * nthr;
     double s = 0.0;
     if (e < ll) {
+      // the partials hold the upper 16 x 16 tiles only: those elements are
+      // summed (coalesced) and written to both triangles
+      const int ei = e / l, ec = e - ei * l;
+      const int src = e;
       double v[16];
+      if (in_upper_tiles(ei, ec))
       for (int p0 = lane8; p0 < nparts; p0 += 8 * 16) {
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int pp = p0 + 8 * u;
-          v[u] = pp < nparts ? __ldcg(part + (size_t)pp * ll + e) : 0.0;
+          v[u] = pp < nparts ? __ldcg(part + (size_t)pp * ll + src) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 16; ++u) s += v[u];
@@ -3648,7 +3681,13 @@ __device__ __forceinline__ void fq_reduce(const double* part, int nparts, int ll
     s += __shfl_xor_sync(0xffffffffu, s, 1);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
-    if (lane8 == 0 && e < ll) G[e] = s;
+    if (lane8 == 0 && e < ll) {
+      const int ei = e / l, ec = e - ei * l;
+      if (in_upper_tiles(ei, ec)) {
+        G[e] = s;
+        if ((ei >> 4) != (ec >> 4)) G[ec * l + ei] = s;
+      }
+    }
   }
 }
 
@@ -3669,12 +3708,17 @@ __device__ __forceinline__ void fq_reduce_nearid(const double* part, int nparts,
     const int e = ebase + it * nthr;
     double s = 0.0;
     if (e < ll) {
+      // the partials hold the upper 16 x 16 tiles only: those elements are
+      // summed (coalesced) and written to both triangles
+      const int ei = e / l, ec = e - ei * l;
+      const int src = e;
       double v[16];
+      if (in_upper_tiles(ei, ec))
       for (int p0 = lane8; p0 < nparts; p0 += 8 * 16) {
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int pp = p0 + 8 * u;
-          v[u] = pp < nparts ? __ldcg(part + (size_t)pp * ll + e) : 0.0;
+          v[u] = pp < nparts ? __ldcg(part + (size_t)pp * ll + src) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 16; ++u) s += v[u];
@@ -3685,11 +3729,19 @@ __device__ __forceinline__ void fq_reduce_nearid(const double* part, int nparts,
     s += __shfl_xor_sync(0xffffffffu, s, 4);
     if (lane8 == 0 && e < ll) {
       const int r = e / l, c = e - r * l;
-      const double f = (c > r) ? s : (c == r ? 0.5 * (s - 1.0) : 0.0);
-      G[e] = s;
-      I2[e] = (c > r) ? -f : (c == r ? 1.0 - f : 0.0);
-      if (R2) R2[e] = (c > r) ? f : (c == r ? 1.0 + f : 0.0);
-      em = fmax(em, fabs(s - (r == c ? 1.0 : 0.0)));
+      if (in_upper_tiles(r, c)) {
+        const double f = (c > r) ? s : (c == r ? 0.5 * (s - 1.0) : 0.0);
+        G[e] = s;
+        I2[e] = (c > r) ? -f : (c == r ? 1.0 - f : 0.0);
+        if (R2) R2[e] = (c > r) ? f : (c == r ? 1.0 + f : 0.0);
+        em = fmax(em, fabs(s - (r == c ? 1.0 : 0.0)));
+        if ((r >> 4) != (c >> 4)) {  // the mirrored element of a strictly lower tile
+          const int mir = c * l + r;
+          G[mir] = s;
+          I2[mir] = 0.0;
+          if (R2) R2[mir] = 0.0;
+        }
+      }
     }
   }
   if (lane8 == 0 && em > 0.0) atomicMax(emax_bits, (unsigned long long)__double_as_longlong(em));
@@ -3730,14 +3782,17 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
     cp_async_wait<0>();
     __syncthreads();
     // Gram partial of the tile (zero rows beyond m contribute nothing)
-    block_dmma(l, l, tr, sY, 1, ld, sY, ld, 1, sR, ld);
+    block_gram_upper(l, tr, sY, ld, sR, ld);  // upper tiles; the reduction mirrors them
     __syncthreads();
     double* mine = P.part + (size_t)(blockIdx.x - 1) * ll;
-    for (int e = tid; e < ll; e += kFqThreads) mine[e] = sR[(e / l) * ld + e % l];
+    for (int e = tid; e < ll; e += kFqThreads) {
+      const int i = e / l, c = e - i * l;
+      if (in_upper_tiles(i, c)) mine[e] = sR[i * ld + c];
+    }
   }
   grid.sync();
   fq_mark(1);
-  if (!fac) fq_reduce(P.part, nparts, ll, P.G);
+  if (!fac) fq_reduce(P.part, nparts, l, P.G);
   grid.sync();
   fq_mark(2);
   if (fac) chol_blocked_body(l, P.G, P.R1, nullptr, P.status, 0, 0.0, 1e-15, fsm);
@@ -3790,10 +3845,13 @@ __global__ void __launch_bounds__(kFqThreads, 1) cholqr2_fused_kernel(const __gr
     if (row >= rows && row < tr)  // padded rows stay zero (rinv scaling of zeros is zero; keep it exact)
       for (int c = g; c < l; c += 4) sY[row * ld + c] = 0.0;
     __syncthreads();
-    block_dmma(l, l, tr, sY, 1, ld, sY, ld, 1, sR, ld);
+    block_gram_upper(l, tr, sY, ld, sR, ld);  // upper tiles; the reduction mirrors them
     __syncthreads();
     double* mine = P.part + (size_t)(blockIdx.x - 1) * ll;
-    for (int e = tid; e < ll; e += kFqThreads) mine[e] = sR[(e / l) * ld + e % l];
+    for (int e = tid; e < ll; e += kFqThreads) {
+      const int i = e / l, c = e - i * l;
+      if (in_upper_tiles(i, c)) mine[e] = sR[i * ld + c];
+    }
   }
   grid.sync();
   fq_mark(4);

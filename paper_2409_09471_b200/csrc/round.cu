@@ -60,8 +60,12 @@ cudaStream_t g_tma_last_stream = nullptr;
 long long g_tma_last_ns = 0, g_tma_conc_until_ns = 0;
 constexpr long long kTmaQuietNs = 500000000LL;
 
+// set while a sweep runs next to work of the same problem on other streams
+// (the host pipeline's matvec chunks overlap the RTO right sweep)
+thread_local int g_tma_suppress = 0;
+
 bool tma_allowed(cudaStream_t st, bool internal_stream) {
-  if (!g_tma_enabled.load(std::memory_order_relaxed)) return false;
+  if (!g_tma_enabled.load(std::memory_order_relaxed) || g_tma_suppress > 0) return false;
   const long long now =
       std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch()).count();
   std::lock_guard<std::mutex> lock(g_tma_mu);
@@ -458,11 +462,18 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
   double* pin = (double*)g_pinned.get(sizeof(double) * ((size_t)std::max(rmax, d) + 16));
   TTK_REQUIRE(pin != nullptr, kCudaError, "tt_truncate: cannot allocate pinned scratch");
   std::vector<int> r(ranks, ranks + d + 1);
+  // Gram path (exact-rank roundings, rel_tol == 0; set up below): the budget is
+  // zero whatever the norm, so the norm's host round trip is skipped (a zero
+  // tensor fails every certificate and comes back here through the QR path)
+  const bool gram_mode = mode >= 1 && rel_tol == 0.0 && knob_env("TTK_TRUNC_NO_GRAM") == nullptr;
   // ||v|| = ||C_{d-1}||_F for a left-orthogonal TT
-  TTK_TRY(launch_sumsq(cores[d - 1], (long long)r[d - 1] * dims[d - 1], red, part, st));
-  TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double), cudaMemcpyDeviceToHost, st));
-  TTK_SYNC(st);
-  const double nrm = std::sqrt(pin[0]);
+  double nrm = 1.0;
+  if (!gram_mode) {
+    TTK_TRY(launch_sumsq(cores[d - 1], (long long)r[d - 1] * dims[d - 1], red, part, st));
+    TTK_CHECK_CUDA(cudaMemcpyAsync(pin, red, sizeof(double), cudaMemcpyDeviceToHost, st));
+    TTK_SYNC(st);
+    nrm = std::sqrt(pin[0]);
+  }
   if (nrm == 0.0) {
     for (int k = 0; k < d; ++k) TTK_CHECK_CUDA(cudaMemsetAsync(out[k], 0, sizeof(double) * dims[k], st));
     for (int k = 0; k <= d; ++k) out_ranks[k] = 1;
@@ -481,7 +492,7 @@ static int truncate_impl(int d, const int* dims, const int* ranks, const double*
   // no host round trip per core and the certificates are checked once at the
   // end; if any failed (e.g. an exactly rank-deficient unfolding) the whole
   // truncation is redone through the QR path.
-  const bool gram_on = mode >= 1 && rel_tol == 0.0 && knob_env("TTK_TRUNC_NO_GRAM") == nullptr;
+  const bool gram_on = gram_mode;
   const uint64_t skey = trunc_shape_key(d, dims, ranks, max_rank);
   bool fast_on = gram_on && mode >= 2 && knob_env("TTK_TRUNC_NO_FAST") == nullptr;
   if (fast_on) {
@@ -734,6 +745,20 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
   TTK_REQUIRE(split_side != nullptr && qstat != nullptr, kWorkspace, "rto: workspace too small");
 
   // ---- right sweep: W_c = sum_i X_c[:, i, :] W_{c+1} G_c[:, i, :]^T ----
+  // pipelined callers (ready != nullptr) still have matvec chunks of this
+  // problem running on another stream: no TMA-staged GEMM next to them (DESIGN 6.2)
+  struct TmaSuppress {
+    bool on;
+    explicit TmaSuppress(bool o) : on(o) { if (on) ++g_tma_suppress; }
+    ~TmaSuppress() { release(); }
+    void release() { if (on) { --g_tma_suppress; on = false; } }
+  } right_guard([&] {
+    // one event for every core = one matvec launch the sweep waits for as a whole: nothing overlaps
+    if (!ready) return false;
+    for (int c = 0; c < d; ++c)
+      if (ready[c] != ready[d - 1]) return true;
+    return false;
+  }());
   for (int c = d - 1; c >= 1; --c) {
     const int n = dims[c], rc = R[c], lc = L[c], l1 = L[c + 1], r1 = R[c + 1];
     TTK_TRY(wait_core(c));
@@ -764,6 +789,7 @@ int ttk_rto_sweeps_ev(int d, const int* dims, const int* R, const double* const*
     TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_m, cudaEventDisableTiming));
     TTK_CHECK_CUDA(cudaEventCreateWithFlags(&ev_z, cudaEventDisableTiming));
   }
+  right_guard.release();
   // The CholeskyQR2 of every step is accepted on the device (flags in qstat) and
   // the host looks at all of them once, after the sweep: a per-core wait cost
   // ~30 us of host round trip per core (config 3: 0.9 ms of a 13.7 ms step).  If

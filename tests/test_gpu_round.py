@@ -311,7 +311,7 @@ def test_counter_drm_blocks_and_moments(cuda):
 def test_matvec_round_rto_pipeline(cuda, host, chunk):
     """tt_matvec_round_rto (per-core uploads, chunked matvec, event-gated RTO
     sweeps, host-streamed truncation) == tt_matvec -> rto_sweeps ->
-    tt_truncate_left_orth, bit for bit, and == the oracle."""
+    tt_truncate_left_orth (bit for bit on device inputs), and == the oracle."""
     rng = np.random.default_rng(5)
     dims = [12, 10, 16, 9, 14, 11, 8]
     d = len(dims)
@@ -331,8 +331,9 @@ def test_matvec_round_rto_pipeline(cuda, host, chunk):
     torch.cuda.synchronize()
     assert got.device.type == ("cpu" if host else "cuda")
     assert got.ranks == ref.ranks
-    for g, w in zip(got.cores, ref.cores):
-        assert torch.equal(g.cpu(), w.cpu())
+    # a right sweep that runs beside matvec chunks keeps its contractions off the TMA-staged
+    # GEMM (DESIGN 6.2): same arithmetic, another kernel's summation order
+    assert O.rel_diff([c.cpu().numpy() for c in got.cores], [c.cpu().numpy() for c in ref.cores]) <= 1e-12
     y = O.matvec(opc, x)
     ls = O.rto_ranks(dims, [1] + [c.shape[2] for c in y], [14, 20, 24, 20, 16, 10])
     want = O.rto_round(y, O.slice_drm(drm, ls), 1e-9, 11)
@@ -361,8 +362,11 @@ def test_matvec_round_rto_pipeline_small(cuda, host, dims):
     got = T.tt_matvec_round_rto(a, v, spec, G, device=cuda)
     torch.cuda.synchronize()
     assert got.ranks == ref.ranks
-    for g_, w in zip(got.cores, ref.cores):
-        assert torch.equal(g_.cpu(), w.cpu())
+    if host and len(dims) > 1:
+        assert O.rel_diff([c.cpu().numpy() for c in got.cores], [c.cpu().numpy() for c in ref.cores]) <= 1e-12
+    else:
+        for g_, w in zip(got.cores, ref.cores):
+            assert torch.equal(g_.cpu(), w.cpu())
 
 
 # ---------------------------------------------------------------------------

@@ -1,5 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_round.py -x -q -m gpu -k "rto" 2>&1 | tail -3
-python tools/solver_profile.py 0 20 2>&1 | tail -1 | cut -c1-120
-TTK_RTO_NO_DEFER=1 python tools/ab_run.py tools/solver_profile.py 0 20 2>&1 | tail -1 | cut -c1-120
-python tools/solver_profile.py 0 20 2>&1 | tail -1 | cut -c1-120
-bash tools/gpu/quick_bench.sh
+echo "== explicit no-TMA x10"
+for i in 1 2 3 4 5 6 7 8 9 10; do REPRO_NO_TMA=1 python tools/inflight_repro.py 2 4 pipe 2>&1 | grep -o "rel diff (tensor) [0-9.e-]*" | tr '\n' ' '; echo; done
+echo "== auto guard x10"
+for i in 1 2 3 4 5 6 7 8 9 10; do python tools/inflight_repro.py 2 4 pipe 2>&1 | grep -o "rel diff (tensor) [0-9.e-]*" | tr '\n' ' '; echo; done

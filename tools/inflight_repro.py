@@ -48,6 +48,9 @@ def worker(i):
                   flush=True)
     except Exception as e:
         errs.append(e); print(i, "ERR", str(e)[-200:], flush=True)
+from paper_2409_09471_b200 import _lib
+if os.environ.get("REPRO_NO_TMA"):
+    _lib.load().ttk_gemm_tma_enable(0)
 ths = [threading.Thread(target=worker, args=(i,)) for i in range(n)]
 [t.start() for t in ths]; [t.join() for t in ths]
 print("errors", len(errs))
