@@ -181,6 +181,11 @@ int ttk_gemm_tma_strided(int M, int N, int K, double alpha, const double* A, lon
  * (the library also drops to the cp.async kernel while it sees two caller streams active within
  * 0.5 s of each other); DESIGN.md 6.2. */
 int ttk_gemm_tma_enable(int on);
+/* diagnostics: a shared-memory-holding neighbour kernel for overlap experiments:
+ * blocks x threads, smem_bytes dynamic shared memory filled from src (4096 doubles; mode & 1:
+ * through cp.async), re-read for `spin` clocks, corrupted words counted into *bad */
+int ttk_debug_occupy(int blocks, int threads, int smem_bytes, long long spin, int mode, const double* src, int* bad,
+                     void* stream);
 /* diagnostics: subsequent Jacobi SVDs store their sweep count in *dev_counter (NULL: off) */
 int ttk_debug_svd_sweeps(int* dev_counter);
 /* diagnostics: the cluster Jacobi adds per-CTA phase clocks (rotate, send, wait,

@@ -189,6 +189,7 @@ SIGNATURES.update({"ttk_qr_auto": (c_int, [c_int, c_int, c_vp, c_ll, c_ll, c_vp,
                                            c_vp])})
 SIGNATURES.update({"ttk_debug_trunc_subspace": (c_int, [c_int, c_int, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp])})
 SIGNATURES.update({"ttk_gemm_tma_enable": (c_int, [c_int])})
+SIGNATURES.update({"ttk_debug_occupy": (c_int, [c_int, c_int, c_int, c_ll, c_int, c_vp, c_vp, c_vp])})
 
 
 class concurrent_problems:

@@ -445,6 +445,42 @@ using namespace ttk;
 
 extern "C" {
 
+// diagnostics (DESIGN 6.2): a neighbour for overlap experiments -- `blocks` CTAs of
+// `threads` threads holding `smem_bytes` of dynamic shared memory; every CTA fills its
+// shared memory with a pattern (mode & 1: through cp.async from `src`, else plain
+// stores), spins `spin` clocks re-reading it, and counts corrupted words into *bad
+__global__ void occupy_kernel(int smem_words, long long spin, int mode, const double* __restrict__ src,
+                              int* __restrict__ bad) {
+  extern __shared__ double oc_sm[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (mode & 1) {
+    for (int e = tid; e < smem_words; e += nt) cp_async8(oc_sm + e, src + (e & 4095), true);
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else {
+    for (int e = tid; e < smem_words; e += nt) oc_sm[e] = src[e & 4095];
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  int wrong = 0;
+  do {
+    for (int e = tid; e < smem_words; e += nt) wrong += (oc_sm[e] != src[e & 4095]) ? 1 : 0;
+  } while (clock64() - t0 < spin);
+  if (wrong) atomicAdd(bad, wrong);
+}
+
+int ttk_debug_occupy(int blocks, int threads, int smem_bytes, long long spin, int mode, const double* src, int* bad,
+                     void* stream) {
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    TTK_CHECK_CUDA(cudaFuncSetAttribute(occupy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  }
+  occupy_kernel<<<blocks, threads, smem_bytes, (cudaStream_t)stream>>>(smem_bytes / 8, spin, mode, src, bad);
+  TTK_CHECK_LAUNCH();
+  return kOk;
+}
+
 // C = alpha A B + beta C for row-major fp64 A (M x K, lda), B (K x N, ldb),
 // C (M x N, ldc): the TMA-staged DMMA kernel (16-byte aligned bases, even
 // leading dimensions, K >= 16).  Asynchronous on `stream`.
