@@ -2668,6 +2668,57 @@ __device__ __forceinline__ void cb_diag_steps(double (&d)[16], double& dg, int l
 
 __host__ __device__ __forceinline__ int cb_ld(int l) { return ((l + 15) & ~15) + 4; }
 
+// partial tiles of warp_dmma16 (M or N below 16, or K not a multiple of 4: the solver's
+// small ranks), out of line so that its registers do not weigh on the callers' pivot chains
+__device__ __noinline__ void warp_dmma16_partial(int M, int N, int K, const double* A, int a_rs, int a_cs,
+                                                 const double* B, int b_rs, int b_cs, double* C, int ldc, bool neg,
+                                                 const double* D, int ldd) {
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+  const int ma = fr, mb = 8 + fr;
+  double c00[2] = {0.0, 0.0}, c01[2] = {0.0, 0.0}, c10[2] = {0.0, 0.0}, c11[2] = {0.0, 0.0};
+  // partial tiles (the solver's small ranks): the same chunked schedule with clamped
+  // addresses and selects instead of predicated loads -- 16 loads in flight per chunk
+  const bool va = ma < M, vb = mb < M, wa = ma < N, wb = mb < N;
+  {
+    const double* pa0 = A + min(ma, M - 1) * a_rs;
+    const double* pa1 = A + min(mb, M - 1) * a_rs;
+    const double* pb0 = B + min(ma, N - 1) * b_cs;
+    const double* pb1 = B + min(mb, N - 1) * b_cs;
+    for (int k0 = 0; k0 < K; k0 += 16) {
+      double a0[4], a1[4], b0[4], b1[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + 4 * q + fk;
+        const int kc = min(k, K - 1);
+        const bool kv = k < K;
+        const double x0 = pa0[kc * a_cs], x1 = pa1[kc * a_cs], y0 = pb0[kc * b_rs], y1 = pb1[kc * b_rs];
+        a0[q] = (va && kv) ? x0 : 0.0;
+        a1[q] = (vb && kv) ? x1 : 0.0;
+        b0[q] = (wa && kv) ? y0 : 0.0;
+        b1[q] = (wb && kv) ? y1 : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (k0 + 4 * q < K) {  // warp-uniform
+          dmma_8x8x4(c00, a0[q], b0[q]);
+          dmma_8x8x4(c01, a0[q], b1[q]);
+          dmma_8x8x4(c10, a1[q], b0[q]);
+          dmma_8x8x4(c11, a1[q], b1[q]);
+        }
+      }
+    }
+  }
+  const double sg = neg ? -1.0 : 1.0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int cn0 = 2 * fk + h, cn1 = 8 + 2 * fk + h;
+    if (va && cn0 < N) C[ma * ldc + cn0] = fma(sg, c00[h], D ? D[ma * ldd + cn0] : 0.0);
+    if (va && cn1 < N) C[ma * ldc + cn1] = fma(sg, c01[h], D ? D[ma * ldd + cn1] : 0.0);
+    if (vb && cn0 < N) C[mb * ldc + cn0] = fma(sg, c10[h], D ? D[mb * ldd + cn0] : 0.0);
+    if (vb && cn1 < N) C[mb * ldc + cn1] = fma(sg, c11[h], D ? D[mb * ldd + cn1] : 0.0);
+  }
+}
+
 // one warp: C[0:M, 0:N] (row stride ldc) = D + (neg ? -1 : 1) A[0:M, 0:K] B[0:K, 0:N]
 // for M, N <= 16 (2 x 2 DMMA tiles, the fragment layout of block_dmma); D
 // (row stride ldd) may be null (zero) or alias C or B.  Full tiles with K a
@@ -2732,29 +2783,7 @@ __device__ __forceinline__ void warp_dmma16(int M, int N, int K, const double* A
     }
     return;
   }
-  const bool va = ma < M, vb = mb < M, wa = ma < N, wb = mb < N;
-#pragma unroll 4
-  for (int k0 = 0; k0 < K; k0 += 4) {
-    const int k = k0 + fk;
-    const bool kv = k < K;
-    const double a0 = (va && kv) ? A[ma * a_rs + k * a_cs] : 0.0;
-    const double a1 = (vb && kv) ? A[mb * a_rs + k * a_cs] : 0.0;
-    const double b0 = (wa && kv) ? B[k * b_rs + ma * b_cs] : 0.0;
-    const double b1 = (wb && kv) ? B[k * b_rs + mb * b_cs] : 0.0;
-    dmma_8x8x4(c00, a0, b0);
-    dmma_8x8x4(c01, a0, b1);
-    dmma_8x8x4(c10, a1, b0);
-    dmma_8x8x4(c11, a1, b1);
-  }
-  const double sg = neg ? -1.0 : 1.0;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int cn0 = 2 * fk + h, cn1 = 8 + 2 * fk + h;
-    if (va && cn0 < N) C[ma * ldc + cn0] = fma(sg, c00[h], D ? D[ma * ldd + cn0] : 0.0);
-    if (va && cn1 < N) C[ma * ldc + cn1] = fma(sg, c01[h], D ? D[ma * ldd + cn1] : 0.0);
-    if (vb && cn0 < N) C[mb * ldc + cn0] = fma(sg, c10[h], D ? D[mb * ldd + cn0] : 0.0);
-    if (vb && cn1 < N) C[mb * ldc + cn1] = fma(sg, c11[h], D ? D[mb * ldd + cn1] : 0.0);
-  }
+  warp_dmma16_partial(M, N, K, A, a_rs, a_cs, B, b_rs, b_cs, C, ldc, neg, D, ldd);
 }
 
 // Blocked right-looking Cholesky core on an l x l SPD matrix already in shared
