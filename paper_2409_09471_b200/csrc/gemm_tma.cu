@@ -206,10 +206,6 @@ __global__ void __launch_bounds__(TmCfg<BM, BN, STAGES>::kThreads)
       const int cur = kk & 1, nxt = cur ^ 1;
       if (kk < 3) {
         load_frags(nxt, s, kk + 1);
-        if (kk == 2) {  // the stage's last fragments are loaded: release it
-          __syncwarp();
-          if (lane == 0) tm_arrive(smem_u32(&empty[s]));
-        }
       } else if (it + 1 < KT) {
         const int s1 = (it + 1) % STAGES;
         tm_wait(smem_u32(&full[s1]), (uint32_t)(((it + 1) / STAGES) & 1));
@@ -219,6 +215,16 @@ __global__ void __launch_bounds__(TmCfg<BM, BN, STAGES>::kThreads)
       for (int fm = 0; fm < Cfg::FM; ++fm)
 #pragma unroll
         for (int fn = 0; fn < Cfg::FN; ++fn) dmma_8x8x4(acc[fm][fn], af[cur][fm], bf[cur][fn]);
+      if (kk == 3) {
+        // release the stage only after the DMMAs that consume its last fragments have been
+        // issued: their operands are then in registers, i.e. every shared-memory read of
+        // the stage has completed.  Releasing right after ISSUING those reads (one k step
+        // earlier) let the next TMA write overtake them whenever another kernel's traffic
+        // delayed this CTA's shared-memory pipeline: corrupted tiles next to any heavy
+        // neighbour (tools/overlap_tma_grouped.py, DESIGN 6.2)
+        __syncwarp();
+        if (lane == 0) tm_arrive(smem_u32(&empty[s]));
+      }
     }
   }
   // ---- epilogue ----
